@@ -1,0 +1,135 @@
+"""fp64 CPU oracle for the resampling layers (TEST INFRASTRUCTURE ONLY).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package.  The
+product path (``paper_1904_12228_b200``) never imports it and shares no code
+with it.  The arithmetic lives in ``oracle.c``; this module only marshals
+numpy float64 arrays through ctypes.
+
+Every function here follows the definitions cited in ``oracle.c``
+(PAPER.md:21-42 layers; PAPER.md:684, 2239-2241 VJP semantics; PAPER.md:700-707
+naive scatter adjoint).  Pins: ``tests/test_oracle_pins.py``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+CFLAGS = ["-O2", "-ffp-contract=off", "-fopenmp", "-shared", "-fPIC", "-std=c11"]
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c -> liboracle.so (gcc, fp64, no FMA contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        lib = ctypes.CDLL(build())
+        P = ctypes.c_void_p
+        I = ctypes.c_int
+        lib.oracle_stn_fwd.argtypes = [P, P, I, I, I, I, I, I, I, I, P]
+        lib.oracle_stn_bwd.argtypes = [P, P, P, I, I, I, I, I, I, I, I, P, P]
+        lib.oracle_warp_fwd.argtypes = [P, P, I, I, I, I, I, P]
+        lib.oracle_warp_bwd.argtypes = [P, P, P, I, I, I, I, I, P, P]
+        lib.oracle_bslice_fwd.argtypes = [P, P, P, I, I, I, I, I, I, P]
+        lib.oracle_bslice_bwd.argtypes = [P, P, P, P, I, I, I, I, I, I, P, P, P]
+        lib.oracle_set_threads.argtypes = [I]
+        lib.oracle_get_threads.restype = I
+        _lib = lib
+    return _lib
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def set_threads(n: int) -> None:
+    _load().oracle_set_threads(int(n))
+
+
+def get_threads() -> int:
+    return int(_load().oracle_get_threads())
+
+
+# ----------------------------------------------------------------------------- STN
+def stn_fwd(x, theta, Ho=None, Wo=None, align_corners=True, border=False):
+    x, theta = _f64(x), _f64(theta)
+    N, C, H, W = x.shape
+    Ho = H if Ho is None else Ho
+    Wo = W if Wo is None else Wo
+    y = np.empty((N, C, Ho, Wo), np.float64)
+    _load().oracle_stn_fwd(_p(x), _p(theta), N, C, H, W, Ho, Wo, int(align_corners),
+                           int(border), _p(y))
+    return y
+
+
+def stn_bwd(x, theta, dy, align_corners=True, border=False, need_dx=True, need_dtheta=True):
+    x, theta, dy = _f64(x), _f64(theta), _f64(dy)
+    N, C, H, W = x.shape
+    Ho, Wo = dy.shape[2:]
+    dx = np.empty_like(x) if need_dx else None
+    dth = np.empty((N, 2, 3), np.float64) if need_dtheta else None
+    _load().oracle_stn_bwd(_p(x), _p(theta), _p(dy), N, C, H, W, Ho, Wo, int(align_corners),
+                           int(border), _p(dx), _p(dth))
+    return dx, dth
+
+
+# ----------------------------------------------------------------------------- warp
+def warp_fwd(x, flow, border=False):
+    x, flow = _f64(x), _f64(flow)
+    N, C, H, W = x.shape
+    y = np.empty_like(x)
+    _load().oracle_warp_fwd(_p(x), _p(flow), N, C, H, W, int(border), _p(y))
+    return y
+
+
+def warp_bwd(x, flow, dy, border=False, need_dx=True, need_dflow=True):
+    x, flow, dy = _f64(x), _f64(flow), _f64(dy)
+    N, C, H, W = x.shape
+    dx = np.empty_like(x) if need_dx else None
+    df = np.empty_like(flow) if need_dflow else None
+    _load().oracle_warp_bwd(_p(x), _p(flow), _p(dy), N, C, H, W, int(border), _p(dx), _p(df))
+    return dx, df
+
+
+# ----------------------------------------------------------------------------- bslice
+def bslice_fwd(grid, guide, x):
+    grid, guide, x = _f64(grid), _f64(guide), _f64(x)
+    N, Q, D, Gh, Gw = grid.shape
+    assert Q == 12 and x.shape[1] == 3
+    H, W = guide.shape[1:]
+    y = np.empty_like(x)
+    _load().oracle_bslice_fwd(_p(grid), _p(guide), _p(x), N, H, W, D, Gh, Gw, _p(y))
+    return y
+
+
+def bslice_bwd(grid, guide, x, dy, need_dgrid=True, need_dguide=True, need_dx=True):
+    grid, guide, x, dy = _f64(grid), _f64(guide), _f64(x), _f64(dy)
+    N, Q, D, Gh, Gw = grid.shape
+    H, W = guide.shape[1:]
+    dgrid = np.empty_like(grid) if need_dgrid else None
+    dguide = np.empty_like(guide) if need_dguide else None
+    dx = np.empty_like(x) if need_dx else None
+    _load().oracle_bslice_bwd(_p(grid), _p(guide), _p(x), _p(dy), N, H, W, D, Gh, Gw,
+                              _p(dgrid), _p(dguide), _p(dx))
+    return dgrid, dguide, dx
