@@ -1,0 +1,504 @@
+#!/usr/bin/env python
+"""bench.py — fwd+bwd throughput of the three resampling layers on B200.
+
+Workload (BASELINE.json configs[4], the configuration the metric is quoted on):
+batch 64 at 1024 x 1024 through STN (C=16, theta as configs[1]), FlowNet warp
+(C=3, smooth flow) and bilateral slice-apply (grid 16x16x8, 12 coefficients).
+One STEP = stn_fwd + stn_bwd + warp_fwd + warp_bwd + bslice_fwd + bslice_bwd
+over the rank's shard of the batch (every sample's parameters are its own:
+batch sharding, no collective on the data path).  The global batch is fixed
+(64), so scaling is strong.
+
+value      = N*H*W pixel positions of the global batch / device time of a step
+             (max over ranks), in Mpix/s; each pixel position passes fwd+bwd
+             through all three layers.
+e2e        = the same step through the C ABI with pinned HOST buffers: the
+             library stages every input H2D and every output D2H on the stream.
+roofline   = the dominant call of the step: algorithmic bytes (DESIGN.md
+             "Algorithmic bytes") / its CUDA-event duration vs MEASURED_PEAKS.json.
+cpu_baseline = the fp64 oracle (oracle/) timed on the host cores on one sample of
+             each layer (rank 0, N=1 only).
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+BATCH, H, W = 64, 1024, 1024
+C_STN, C_WARP = 16, 3
+D, GH, GW = 8, 16, 16
+METRIC = "fwd+bwd Mpix/s per layer and % HBM roofline at 1/2/4/8 B200"
+UNIT = "Mpix/s"
+
+# algorithmic bytes per pixel position (compulsory traffic only)
+BYTES = {
+    ("stn", "fwd"): lambda C: 8 * C, ("stn", "bwd"): lambda C: 12 * C,
+    ("warp", "fwd"): lambda C: 8 + 8 * C, ("warp", "bwd"): lambda C: 16 + 12 * C,
+    ("bslice", "fwd"): lambda C: 28, ("bslice", "bwd"): lambda C: 44,
+}
+
+
+def peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            v = float(json.load(f)["hbm_gbs"])
+        return v, "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- distributed
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(world, vals):
+    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
+def shard(world, rank, batch=BATCH):
+    per = batch // world
+    assert per * world == batch, "global batch must divide the GPU count"
+    return rank * per, per
+
+
+# --------------------------------------------------------------------------- workload
+def make_inputs(n0, nb, dev):
+    import synth
+
+    s = synth.stn_inputs(nb, C_STN, H, W, cfg=5, device=dev, n0=n0)
+    w = synth.warp_inputs(nb, C_WARP, H, W, cfg=5, device=dev, flow="smooth", n0=n0)
+    b = synth.bslice_inputs(nb, H, W, D, GH, GW, cfg=5, device=dev, n0=n0)
+    return s, w, b
+
+
+def alloc_outputs(s, w, b, host=False):
+    def e(ref):
+        if host:
+            return torch.empty(ref.shape, dtype=torch.float32, pin_memory=True)
+        return torch.empty_like(ref)
+
+    nb = s["x"].shape[0]
+    return {
+        "stn_y": e(s["dy"]), "stn_dx": e(s["x"]), "stn_dth": e(s["theta"]),
+        "warp_y": e(w["dy"]), "warp_dx": e(w["x"]), "warp_df": e(w["flow"]),
+        "bs_y": e(b["dy"]), "bs_dgr": e(b["grid"]), "bs_dgd": e(b["guide"]), "bs_dx": e(b["x"]),
+        "_nb": nb,
+    }
+
+
+def step_calls(rs, s, w, b, o):
+    """The six C-ABI calls of one step, as (name, thunk)."""
+    return [
+        ("stn_fwd", lambda: rs.stn_fwd(s["x"], s["theta"], out=o["stn_y"])),
+        ("stn_bwd", lambda: rs.stn_bwd(s["x"], s["theta"], s["dy"], out=(o["stn_dx"], o["stn_dth"]))),
+        ("warp_fwd", lambda: rs.warp_fwd(w["x"], w["flow"], out=o["warp_y"])),
+        ("warp_bwd", lambda: rs.warp_bwd(w["x"], w["flow"], w["dy"], out=(o["warp_dx"], o["warp_df"]))),
+        ("bslice_fwd", lambda: rs.bslice_fwd(b["grid"], b["guide"], b["x"], out=o["bs_y"])),
+        ("bslice_bwd", lambda: rs.bslice_bwd(b["grid"], b["guide"], b["x"], b["dy"],
+                                             out=(o["bs_dgr"], o["bs_dgd"], o["bs_dx"]))),
+    ]
+
+
+CALL_BYTES = {
+    "stn_fwd": BYTES[("stn", "fwd")](C_STN), "stn_bwd": BYTES[("stn", "bwd")](C_STN),
+    "warp_fwd": BYTES[("warp", "fwd")](C_WARP), "warp_bwd": BYTES[("warp", "bwd")](C_WARP),
+    "bslice_fwd": BYTES[("bslice", "fwd")](0), "bslice_bwd": BYTES[("bslice", "bwd")](0),
+}
+
+
+# --------------------------------------------------------------------------- paper shapes
+def flush_l2(buf):
+    buf.add_(1.0)
+
+
+def paper_shapes(rs, peak):
+    """configs[1..3] (+ the paper's 32x32x8 grid), each call timed alone after an L2 flush."""
+    import synth
+
+    dev = torch.device("cuda")
+    fl = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 2x L2
+    out = {}
+    cases = [
+        ("stn_4x16x512x512", "stn", C_STN, synth.stn_inputs(4, 16, 512, 512, cfg=2, device=dev)),
+        ("warp_8x3x384x512_smooth", "warp", 3, synth.warp_inputs(8, 3, 384, 512, cfg=3, device=dev)),
+        ("warp_8x3x384x512_stress", "warp", 3,
+         synth.warp_inputs(8, 3, 384, 512, cfg=3, device=dev, flow="stress")),
+        ("bslice_4x1024x1024_g16x16x8", "bslice", 3,
+         synth.bslice_inputs(4, 1024, 1024, 8, 16, 16, cfg=4, device=dev)),
+        ("bslice_4x1024x1024_g32x32x8", "bslice", 3,
+         synth.bslice_inputs(4, 1024, 1024, 8, 32, 32, cfg=4, device=dev)),
+    ]
+    for name, layer, C, i in cases:
+        if layer == "stn":
+            o = (torch.empty_like(i["x"]), torch.empty_like(i["theta"]))
+            y = torch.empty_like(i["dy"])
+            fwd = lambda: rs.stn_fwd(i["x"], i["theta"], out=y)  # noqa: E731
+            bwd = lambda: rs.stn_bwd(i["x"], i["theta"], i["dy"], out=o)  # noqa: E731
+            P = i["x"].shape[0] * 512 * 512
+        elif layer == "warp":
+            o = (torch.empty_like(i["x"]), torch.empty_like(i["flow"]))
+            y = torch.empty_like(i["x"])
+            fwd = lambda: rs.warp_fwd(i["x"], i["flow"], out=y)  # noqa: E731
+            bwd = lambda: rs.warp_bwd(i["x"], i["flow"], i["dy"], out=o)  # noqa: E731
+            P = 8 * 384 * 512
+        else:
+            o = (torch.empty_like(i["grid"]), torch.empty_like(i["guide"]), torch.empty_like(i["x"]))
+            y = torch.empty_like(i["x"])
+            fwd = lambda: rs.bslice_fwd(i["grid"], i["guide"], i["x"], out=y)  # noqa: E731
+            bwd = lambda: rs.bslice_bwd(i["grid"], i["guide"], i["x"], i["dy"], out=o)  # noqa: E731
+            P = 4 * 1024 * 1024
+        times = {"fwd": [], "bwd": []}
+        for rep in range(25):
+            for kind, fn in (("fwd", fwd), ("bwd", bwd)):
+                flush_l2(fl)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                fn()
+                e1.record()
+                torch.cuda.synchronize()
+                if rep >= 5:
+                    times[kind].append(e0.elapsed_time(e1) * 1e-3)
+        tf, tb = statistics.median(times["fwd"]), statistics.median(times["bwd"])
+        bf, bb = BYTES[(layer, "fwd")](C) * P, BYTES[(layer, "bwd")](C) * P
+        out[name] = {
+            "fwd_us": round(tf * 1e6, 2), "bwd_us": round(tb * 1e6, 2),
+            "fwd_bwd_mpix_s": round(P / (tf + tb) / 1e6, 1),
+            "bwd_mpix_s": round(P / tb / 1e6, 1),
+            "fwd_roofline_frac": round(bf / tf / 1e9 / peak, 3),
+            "bwd_roofline_frac": round(bb / tb / 1e9 / peak, 3),
+        }
+    del fl
+    return {"l2": "flushed (256 MB write) before every call; median of 20", "cases": out}
+
+
+# --------------------------------------------------------------------------- cpu baseline
+def cpu_baseline(s, w, b, budget_s=12.0):
+    """The fp64 oracle as it stands on sample 0 of each layer, repeated while under budget."""
+    import oracle
+
+    sub = lambda d: {k: v[:1].double().cpu().numpy() for k, v in d.items()}  # noqa: E731
+    S, Wp, B = sub(s), sub(w), sub(b)
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        oracle.stn_fwd(S["x"], S["theta"])
+        oracle.stn_bwd(S["x"], S["theta"], S["dy"])
+        oracle.warp_fwd(Wp["x"], Wp["flow"])
+        oracle.warp_bwd(Wp["x"], Wp["flow"], Wp["dy"])
+        oracle.bslice_fwd(B["grid"], B["guide"], B["x"])
+        oracle.bslice_bwd(B["grid"], B["guide"], B["x"], B["dy"])
+        reps += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": round(reps * H * W / dt / 1e6, 4), "unit": UNIT, "cores": oracle.get_threads(),
+            "kind": "oracle",
+            "sample": f"{reps} x one sample (1 x 1024^2) of each layer of the step (STN C=16, warp C=3, "
+                      f"bslice 16x16x8), fp64 C oracle, OpenMP; host os.cpu_count()={os.cpu_count()}"}
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    import oracle
+    import synth
+
+    s = synth.stn_inputs(1, C_STN, H, W, cfg=5)
+    w = synth.warp_inputs(1, C_WARP, H, W, cfg=5)
+    b = synth.bslice_inputs(1, H, W, D, GH, GW, cfg=5)
+    S = {k: v.double().numpy() for k, v in s.items()}
+    Wp = {k: v.double().numpy() for k, v in w.items()}
+    B = {k: v.double().numpy() for k, v in b.items()}
+
+    def step():
+        oracle.stn_fwd(S["x"], S["theta"])
+        oracle.stn_bwd(S["x"], S["theta"], S["dy"])
+        oracle.warp_fwd(Wp["x"], Wp["flow"])
+        oracle.warp_bwd(Wp["x"], Wp["flow"], Wp["dy"])
+        oracle.bslice_fwd(B["grid"], B["guide"], B["x"])
+        oracle.bslice_bwd(B["grid"], B["guide"], B["x"], B["dy"])
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    v = round(H * W / dt / 1e6, 4)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (synth/, seeded)",
+        "config": {"workload": "configs[4] sample: 1 x 1024^2 per layer per step (bounded)",
+                   "layers": "stn C=16, warp C=3 smooth flow, bslice grid 16x16x8"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "kind": "oracle", "cores": oracle.get_threads(),
+                         "sample": "one 1024^2 sample of each layer per step"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# --------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-paper-shapes", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+
+    from paper_1904_12228_b200 import rsgrad as rs
+
+    dev = torch.device("cuda", local if world > 1 else 0)
+    n0, nb = shard(world, rank)
+    s, w, b = make_inputs(n0, nb, dev)
+    o = alloc_outputs(s, w, b)
+    calls = step_calls(rs, s, w, b, o)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        for _, fn in calls:
+            fn()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, events between the six calls on the launching stream
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(calls) + 1)] for _ in range(args.steps)]
+    clocks = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.3)
+    barrier(world)
+    torch.cuda.synchronize()
+    rs.launch_count(reset=True)
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for k in range(args.steps):
+        ev[k][0].record(stream)
+        for ci, (_, fn) in enumerate(calls):
+            fn()
+            ev[k][ci + 1].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    launches = rs.launch_count()
+    barrier(world)
+    clk = clocks.stop() if clocks else None
+    total_s = t_start.elapsed_time(t_end) * 1e-3
+    per_call = [sum(ev[k][ci].elapsed_time(ev[k][ci + 1]) for k in range(args.steps)) * 1e-3 / args.steps
+                for ci in range(len(calls))]
+    mx = max_over_ranks(world, [total_s] + per_call)
+    total_s, per_call = mx[0], mx[1:]
+    t_step = total_s / args.steps
+    P_global = BATCH * H * W
+    value = P_global / t_step / 1e6
+
+    # ---- e2e: the same step through the C ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(rs, s, w, b, args, world)
+
+    if rank != 0:
+        return
+    peak, peak_src = peak_hbm()
+    names = [n for n, _ in calls]
+    P_rank = nb * H * W
+    layers = {}
+    for L in ("stn", "warp", "bslice"):
+        tf, tb = per_call[names.index(f"{L}_fwd")], per_call[names.index(f"{L}_bwd")]
+        C = {"stn": C_STN, "warp": C_WARP, "bslice": 3}[L]
+        layers[L] = {
+            "fwd_bwd_mpix_s": round(P_global / (tf + tb) / 1e6, 1),
+            "fwd_ms": round(tf * 1e3, 4), "bwd_ms": round(tb * 1e3, 4),
+            "fwd_roofline_frac": round(BYTES[(L, "fwd")](C) * P_rank / tf / 1e9 / peak, 3),
+            "bwd_roofline_frac": round(BYTES[(L, "bwd")](C) * P_rank / tb / 1e9 / peak, 3),
+        }
+    dom = max(range(len(calls)), key=lambda i: per_call[i])
+    dname = names[dom]
+    achieved = CALL_BYTES[dname] * P_rank / per_call[dom] / 1e9
+    roof = {"bound": "hbm", "kernel": dname, "achieved": round(achieved, 1), "peak": peak,
+            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": ncu_traffic(dname, P_rank),
+            "algorithmic_bytes_per_launch": CALL_BYTES[dname] * P_rank, "peak_source": peak_src}
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (synth/: seeded per-sample recipe, generated on device)",
+        "config": {"workload": "configs[4]: batch 64 @ 1024x1024 per layer (STN C=16 | warp C=3 smooth "
+                               "flow | bslice grid 16x16x8x12), one step = fwd+bwd of all three",
+                   "global_batch": BATCH, "H": H, "W": W, "per_rank_batch": nb,
+                   "parallelism": f"batch-shard x{world}, no data-path collective",
+                   "l2": "inputs > L2 (4.3 GB STN tensors), no flush between steps"},
+        "layers": layers, "roofline": roof, "gpu_launches": launches,
+        "clocks": clk, "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(s, w, b)
+    if world == 1 and not args.no_paper_shapes:
+        line["paper_shapes"] = paper_shapes(rs, peak)
+    print(json.dumps(line), flush=True)
+
+
+def ncu_traffic(call, P_rank):
+    """dram bytes per launch from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        v = d.get(call)
+        if v is None:
+            return None
+        return {"dram_bytes": v["dram_bytes"], "per_pixel": v.get("per_pixel"),
+                "source": d.get("source", p)}
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def run_e2e(rs, s, w, b, args, world):
+    """Host-buffer step: the library copies every input H2D and output D2H on the stream."""
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:  # noqa: BLE001
+        avail = 0
+    nb_full = s["x"].shape[0]
+    per_sample = sum(v[0].numel() * 4 for d in (s, w, b) for v in d.values()) * 2
+    nb = nb_full
+    while nb > 1 and nb * per_sample * 1.5 > avail:
+        nb //= 2
+    pick = lambda d: {k: v[:nb].cpu().pin_memory() for k, v in d.items()}  # noqa: E731
+    hs, hw, hb = pick(s), pick(w), pick(b)
+    ho = alloc_outputs(hs, hw, hb, host=True)
+    calls = step_calls(rs, hs, hw, hb, ho)
+    h2d = (sum(hs[k].numel() for k in ("x", "theta")) + sum(hs[k].numel() for k in ("x", "theta", "dy"))
+           + sum(hw[k].numel() for k in ("x", "flow")) + sum(hw[k].numel() for k in ("x", "flow", "dy"))
+           + sum(hb[k].numel() for k in ("grid", "guide", "x"))
+           + sum(hb[k].numel() for k in ("grid", "guide", "x", "dy"))) * 4
+    d2h = sum(v.numel() for k, v in ho.items() if not k.startswith("_")) * 4
+    for _, fn in calls:  # warm-up
+        fn()
+    steps = max(1, min(args.steps, 3))
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        for _, fn in calls:
+            fn()
+    e1.record()
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) / steps
+    dt = max(e0.elapsed_time(e1) * 1e-3 / steps, 1e-9)
+    dt = max_over_ranks(world, [max(dt, wall)])[0]
+    v = world * nb * H * W / dt / 1e6
+    return {"value": round(v, 1), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "samples_per_rank": nb, "steps": steps,
+            "note": "pinned host buffers passed as host pointers to the C ABI (library-staged copies "
+                    "on the stream); wall clock incl. host staging, max over ranks"}
+
+
+if __name__ == "__main__":
+    main()

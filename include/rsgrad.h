@@ -1,0 +1,159 @@
+/*
+ * rsgrad.h — C ABI of the B200 (sm_100a) resampling-layer library.
+ *
+ * The forward pass and the reverse-mode adjoint (vector-Jacobian product) of
+ * the three custom layers of the gradient-Halide chapter, "Custom Neural
+ * Network Layers":
+ *   stn_*    spatial transformer: affine_grid + bilinear grid_sample
+ *   warp_*   FlowNet 2.0 per-pixel warp
+ *   bslice_* HDRNet bilateral slice-apply
+ * Each *_bwd takes "a buffer representing the adjoints" of the layer output
+ * and returns the adjoints of the inputs, i.e. df(x, dy) of
+ * PAPER.md:2239-2241.  The exact definitions (the paper prints none; its
+ * listings are missing) are DESIGN.md R1-R9.
+ *
+ * Conventions shared by every entry point
+ *   Tensors   fp32, C-contiguous (NCHW), no aliasing between inputs and outputs.
+ *   Pointers  device pointers (cudaMalloc / torch CUDA tensors) OR host pointers
+ *             (pinned or pageable).  Any host pointer is staged through a
+ *             stream-ordered temporary (cudaMallocAsync) and copied on `stream`;
+ *             host outputs are copied back on `stream` before the call returns
+ *             control of the stream (pinned: asynchronous; pageable: the call
+ *             synchronises on the copy).  All device work runs on `stream`.
+ *   Outputs   always OVERWRITTEN, never accumulated.  A NULL gradient pointer
+ *             skips that gradient's work.
+ *   Ownership the caller owns every buffer.  The library keeps no state except
+ *             the thread-local error string; it allocates only stream-ordered
+ *             temporaries that are released on `stream` before returning.
+ *   Workspace *_bwd take an optional device workspace (size from
+ *             rsgrad_bwd_workspace_bytes); NULL/too small => the library takes
+ *             a stream-ordered temporary of that size itself.
+ *   Errors    no exceptions cross the ABI: a negative rs_status is returned and
+ *             rsgrad_last_error() describes it.  Status reflects argument
+ *             validation and launch errors (cudaGetLastError) only; kernel
+ *             faults surface on the next synchronisation of `stream`.
+ *   Threads   re-entrant; concurrent calls on different streams are safe.
+ *   Determinism: with deterministic=1 every result is bitwise reproducible
+ *             (AUTO then never picks an atomic-scatter path); gather paths are
+ *             always deterministic.
+ */
+#ifndef RSGRAD_H
+#define RSGRAD_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Same object as cudaStream_t / CUstream; NULL = the legacy default stream. */
+typedef struct CUstream_st *rs_stream_t;
+
+typedef enum {
+    RS_OK = 0,
+    RS_ERR_NULL = -1,      /* a required pointer is NULL                      */
+    RS_ERR_SHAPE = -2,     /* a dimension is non-positive / degenerate         */
+    RS_ERR_ALIGN = -3,     /* reserved (misalignment takes a scalar path)      */
+    RS_ERR_FLAG = -4,      /* bad option, or algo not valid for these inputs   */
+    RS_ERR_CUDA = -5,      /* CUDA runtime error (message in last_error)       */
+    RS_ERR_WORKSPACE = -6  /* workspace could not be obtained                  */
+} rs_status;
+
+typedef enum { RS_PAD_ZEROS = 0, RS_PAD_BORDER = 1 } rs_padding;
+
+/* Backward algorithm for the input adjoint:
+ *   GATHER          scatter-to-gather conversion over the bounded footprint
+ *                   (deterministic, no memset, no atomics);
+ *   SCATTER_PRIV    shared-memory privatised scatter, one flush per tile;
+ *   SCATTER_ATOMIC  "general scatter using atomics";
+ *   AUTO            per layer / per sample choice, DESIGN.md "Algorithm choice". */
+typedef enum {
+    RS_ALGO_AUTO = 0,
+    RS_ALGO_GATHER = 1,
+    RS_ALGO_SCATTER_PRIV = 2,
+    RS_ALGO_SCATTER_ATOMIC = 3
+} rs_algo;
+
+typedef struct {
+    int align_corners; /* STN only: 1 (default, R2) or 0          */
+    int padding;       /* rs_padding: STN and warp; bslice always clamps     */
+    int algo;          /* rs_algo                                            */
+    int deterministic; /* 1 => bitwise reproducible results                  */
+} rs_opts;
+
+/* NULL opts pointer => {align_corners=1, padding=ZEROS, algo=AUTO, deterministic=0}. */
+
+/* ---------------------------------------------------------------------------
+ * Spatial transformer.
+ *   x      N x C x H x W        input feature map
+ *   theta  N x 2 x 3            per-sample affine, normalised coordinates
+ *   y      N x C x Ho x Wo      output
+ *   y[n,c,i,j] = bilinear(x[n,c], ix, iy) with (ix, iy) the un-normalised image
+ *   of theta_n [xt_j, yt_i, 1]^T (R1); taps outside the image read 0
+ *   (zeros) or the coordinate is clamped to the image (border).
+ * Shapes: N, C, H, W, Ho, Wo >= 1; align_corners=1 requires Ho, Wo >= 2.
+ * ------------------------------------------------------------------------- */
+rs_status stn_fwd(const float *x, const float *theta, int N, int C, int H, int W, int Ho,
+                  int Wo, const rs_opts *opts, float *y, rs_stream_t stream);
+
+/*   dy      N x C x Ho x Wo     adjoint of y
+ *   dx      N x C x H x W       adjoint of x (nullable)
+ *   dtheta  N x 2 x 3           adjoint of theta (nullable)
+ * GATHER is invalid with border padding (the clamp has no bounded inverse). */
+rs_status stn_bwd(const float *x, const float *theta, const float *dy, int N, int C, int H,
+                  int W, int Ho, int Wo, const rs_opts *opts, float *dx, float *dtheta,
+                  void *workspace, size_t ws_bytes, rs_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * FlowNet 2.0 warp: y[n,c,y,x] = bilinear(x[n,c], x+u, y+v),
+ * flow N x 2 x H x W in pixels, channel 0 = u (horizontal).  DESIGN.md R4.
+ * ------------------------------------------------------------------------- */
+rs_status warp_fwd(const float *x, const float *flow, int N, int C, int H, int W,
+                   const rs_opts *opts, float *y, rs_stream_t stream);
+
+/*   dx N x C x H x W (nullable), dflow N x 2 x H x W (nullable).
+ * GATHER is invalid (arbitrary flow has no bounded inverse). */
+rs_status warp_bwd(const float *x, const float *flow, const float *dy, int N, int C, int H,
+                   int W, const rs_opts *opts, float *dx, float *dflow, void *workspace,
+                   size_t ws_bytes, rs_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * HDRNet bilateral slice-apply.
+ *   grid   N x 12 x D x Gh x Gw   affine coefficients, q = 4*o + i (3x4 row-major)
+ *   guide  N x H x W              guidance map (any real value; clamped planes)
+ *   x      N x 3 x H x W          input image
+ *   y      N x 3 x H x W          y_o = sum_i A_{4o+i} x_i + A_{4o+3},
+ *   A = trilinear tent slice of grid at ((x+.5)Gw/W-.5, (y+.5)Gh/H-.5, guide*D-.5)
+ *   with indices clamped to the grid (R5-R7).  opts.padding ignored.
+ * ------------------------------------------------------------------------- */
+rs_status bslice_fwd(const float *grid, const float *guide, const float *x, int N, int H,
+                     int W, int D, int Gh, int Gw, const rs_opts *opts, float *y,
+                     rs_stream_t stream);
+
+/*   dgrid N x 12 x D x Gh x Gw, dguide N x H x W, dx N x 3 x H x W (each nullable). */
+rs_status bslice_bwd(const float *grid, const float *guide, const float *x, const float *dy,
+                     int N, int H, int W, int D, int Gh, int Gw, const rs_opts *opts,
+                     float *dgrid, float *dguide, float *dx, void *workspace, size_t ws_bytes,
+                     rs_stream_t stream);
+
+/* Workspace (bytes) *_bwd wants for these shapes.  layer: 0 = STN (uses
+ * N,C,H,W,Ho,Wo), 1 = warp (N,C,H,W), 2 = bslice (N,H,W,D,Gh,Gw); unused
+ * arguments are ignored.  Returns 0 for an unknown layer.  DESIGN.md "Workspace". */
+size_t rsgrad_bwd_workspace_bytes(int layer, int N, int C, int H, int W, int Ho, int Wo, int D,
+                                  int Gh, int Gw, const rs_opts *opts);
+
+/* Thread-local description of the last error on this thread ("" if none). */
+const char *rsgrad_last_error(void);
+
+/* Library version string, e.g. "rsgrad 0.1.0 sm_100a". */
+const char *rsgrad_version(void);
+
+/* Number of kernels the library enqueued on this thread since the last reset
+ * (launch accounting for bench.py's gpu_launches). */
+unsigned long long rsgrad_launch_count(int reset);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RSGRAD_H */

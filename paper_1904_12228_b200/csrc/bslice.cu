@@ -1,0 +1,626 @@
+// bslice.cu — HDRNet bilateral slice-apply, forward and adjoint, sm_100a.
+//
+// Geometry.  Pixel (y, x) sits at cell coordinates cx = (x+.5)Gw/W - .5,
+// cy = (y+.5)Gh/H - .5 (R5).  A "dual cell" (j, k), j in [-1, Gh-1],
+// k in [-1, Gw-1], is the set of pixels with floor(cy) = j and floor(cx) = k:
+// every pixel of a dual cell reads the SAME four spatial grid corners
+// (clamp(j+b), clamp(k+a)), b, a in {0,1}.  Blocks own a dual cell (or a
+// sub-tile of a large one), so the block's grid footprint is 4 x D x 12
+// coefficients staged once in shared memory (the "bounded footprint" of the
+// scatter-to-gather conversion) and the per-pixel
+// coefficients are applied on the fly, never materialised.
+//
+// Kernels
+//   bslice_fwd_tiled      per pixel: 2-plane slice from smem corner lerps, apply.
+//   bslice_bwd_tiled      per pixel: dX = A^T G, dguide = D G.(A_hi-A_lo)Xt, and
+//                         d_grid accumulated WITHOUT atomics: pixels are
+//                         counting-sorted by z-bin (floor(cz)) so a warp's 32
+//                         lanes share the two z-planes; each lane keeps the 96
+//                         (2 planes x 4 corners x 12 coeffs) sums in registers,
+//                         reduce-scattered across the warp (93 shuffles) when
+//                         the bin changes; per-warp smem slots are summed in
+//                         fixed order into one partial per (dual cell, corner).
+//   bslice_dgrid_gather   each grid cell sums its <=4 dual-cell partials in a
+//                         fixed order (deterministic; the rfactor "partial +
+//                         serial" split of PAPER.md:840).
+//   bslice_*_generic      any shape: thread per pixel, grid via L1, d_grid by
+//                         red.global.add (the atomic fallback).
+#include "common.cuh"
+
+namespace rs {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kTileX = 128;   // nominal max sub-tile width  (px)
+constexpr int kTileY = 64;    // nominal max sub-tile height (px)
+// a dual cell spans <= ceil(W/Gw) (+1 for fp rounding) pixels: smem holds +2 slack
+constexpr int kTileXS = kTileX + 2, kTileYS = kTileY + 2;
+constexpr int kPlaneStride = 13;  // float4 per z-plane in smem (12 + 1 pad: conflict-free)
+constexpr unsigned kInvalid = 0xffffffffu;
+
+// ----------------------------------------------------------------- exact coordinates (R5)
+RS_DEV double bs_cx(int x, int W, int Gw) {
+    return __dsub_rn(__ddiv_rn(__dmul_rn(__dadd_rn((double)x, 0.5), (double)Gw), (double)W), 0.5);
+}
+
+RS_DEV double bs_cz(float g, int D) { return __dsub_rn(__dmul_rn((double)g, (double)D), 0.5); }
+
+RS_DEV int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// z-bin of a guide value: bin = clamp(floor(cz)+1, 0, D); planes (bin-1, bin) clamped.
+RS_DEV void z_cell(float g, int D, int &bin, float &fz) {
+    const double cz = bs_cz(g, D);
+    const double fl = floor(cz);
+    fz = (float)__dsub_rn(cz, fl);
+    const double b = fl + 1.0;
+    bin = b < 0.0 ? 0 : (b > (double)D ? D : (int)b);
+    if (!(cz == cz)) { bin = 0; fz = 0.f; }  // NaN guide: defined, not meaningful
+}
+
+// first pixel index x with floor(cx(x)) >= k (exact, monotone search)
+RS_DEV int dual_begin(int k, int W, int G) {
+    if (k <= -1) return 0;
+    if (k >= G) return W;
+    int e = (int)ceil(((double)k + 0.5) * (double)W / (double)G - 0.5);
+    e = clampi(e, 0, W);
+    while (e > 0 && floor(bs_cx(e - 1, W, G)) >= (double)k) e--;
+    while (e < W && floor(bs_cx(e, W, G)) < (double)k) e++;
+    return e;
+}
+
+struct Tile {
+    int n, j, k;         // sample, dual cell
+    int ys, ye, xs, xe;  // pixel ranges [ys, ye) x [xs, xe)
+};
+
+RS_DEV Tile tile_of(int b, int Gh, int Gw, int SY, int SX, int H, int W) {
+    Tile t;
+    const int sx = b % SX;
+    b /= SX;
+    const int sy = b % SY;
+    b /= SY;
+    const int kk = b % (Gw + 1);
+    b /= (Gw + 1);
+    const int jj = b % (Gh + 1);
+    t.n = b / (Gh + 1);
+    t.j = jj - 1;
+    t.k = kk - 1;
+    const int yb = dual_begin(t.j, H, Gh), yend = dual_begin(t.j + 1, H, Gh);
+    const int xb = dual_begin(t.k, W, Gw), xend = dual_begin(t.k + 1, W, Gw);
+    const int hh = yend - yb, ww = xend - xb;
+    t.ys = yb + (int)(((long long)hh * sy) / SY);
+    t.ye = yb + (int)(((long long)hh * (sy + 1)) / SY);
+    t.xs = xb + (int)(((long long)ww * sx) / SX);
+    t.xe = xb + (int)(((long long)ww * (sx + 1)) / SX);
+    return t;
+}
+
+// Stage, for every z-bin b in [0, D] and coefficient q, the bilinear-lerp terms
+// S(fx, fy) = a + fx b + fy (c + fx d) of (i) the low plane clamp(b-1) and (ii)
+// the plane DIFFERENCE clamp(b) - clamp(b-1).  Slicing the difference directly
+// (instead of subtracting two slices) keeps dA/dcz accurate to fp32 relative
+// precision of the difference itself: it feeds d_guide (P3).
+RS_DEV float4 lerp_terms(float c00, float c01, float c10, float c11) {
+    return make_float4(c00, c01 - c00, c10 - c00, (c11 - c10) - (c01 - c00));
+}
+
+RS_DEV void stage_corners(float4 *glo, float4 *gdz, const float *grid, const Tile &t, int D,
+                          int Gh, int Gw) {
+    const int y0 = clampi(t.j, 0, Gh - 1), y1 = clampi(t.j + 1, 0, Gh - 1);
+    const int x0 = clampi(t.k, 0, Gw - 1), x1 = clampi(t.k + 1, 0, Gw - 1);
+    const long long plane = (long long)Gh * Gw;
+    const float *g = grid + (long long)t.n * 12 * D * plane;
+    for (int e = threadIdx.x; e < (D + 1) * 12; e += blockDim.x) {
+        const int b = e / 12, q = e - b * 12;
+        const int zl = clampi(b - 1, 0, D - 1), zh = clampi(b, 0, D - 1);
+        const float *pl = g + ((long long)q * D + zl) * plane;
+        const float *ph = g + ((long long)q * D + zh) * plane;
+        const float l00 = __ldg(pl + y0 * Gw + x0), l01 = __ldg(pl + y0 * Gw + x1);
+        const float l10 = __ldg(pl + y1 * Gw + x0), l11 = __ldg(pl + y1 * Gw + x1);
+        const float h00 = __ldg(ph + y0 * Gw + x0), h01 = __ldg(ph + y0 * Gw + x1);
+        const float h10 = __ldg(ph + y1 * Gw + x0), h11 = __ldg(ph + y1 * Gw + x1);
+        glo[b * kPlaneStride + q] = lerp_terms(l00, l01, l10, l11);
+        gdz[b * kPlaneStride + q] = lerp_terms(h00 - l00, h01 - l01, h10 - l10, h11 - l11);
+    }
+}
+
+RS_DEV float lerp2(const float4 c, float fx, float fy) {
+    return fmaf(fy, fmaf(fx, c.w, c.z), fmaf(fx, c.y, c.x));
+}
+
+// ----------------------------------------------------------------- forward, tiled
+__global__ void __launch_bounds__(kThreads)
+    bslice_fwd_tiled(BsliceArgs a, int SY, int SX) {
+    extern __shared__ float4 smem4[];
+    float4 *glo = smem4;                                       // (D+1) * 13
+    float4 *gdz = glo + (a.D + 1) * kPlaneStride;              // (D+1) * 13
+    float *fxt = (float *)(gdz + (a.D + 1) * kPlaneStride);    // kTileXS
+    float *fyt = fxt + kTileXS;                                // kTileYS
+    const Tile t = tile_of(blockIdx.x, a.Gh, a.Gw, SY, SX, a.H, a.W);
+    const int TW = t.xe - t.xs, TH = t.ye - t.ys;
+    if (TW <= 0 || TH <= 0) return;
+    stage_corners(glo, gdz, a.grid, t, a.D, a.Gh, a.Gw);
+    for (int c = threadIdx.x; c < TW; c += kThreads) {
+        const double cx = bs_cx(t.xs + c, a.W, a.Gw);
+        fxt[c] = (float)__dsub_rn(cx, floor(cx));
+    }
+    for (int r = threadIdx.x; r < TH; r += kThreads) {
+        const double cy = bs_cx(t.ys + r, a.H, a.Gh);
+        fyt[r] = (float)__dsub_rn(cy, floor(cy));
+    }
+    __syncthreads();
+    const long long HW = (long long)a.H * a.W;
+    const float *gd = a.guide + (long long)t.n * HW;
+    const float *xp = a.x + (long long)t.n * 3 * HW;
+    float *yp = a.y + (long long)t.n * 3 * HW;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int r = w; r < TH; r += kWarps) {
+        const float fy = fyt[r];
+        const long long rowoff = (long long)(t.ys + r) * a.W + t.xs;
+        for (int c = lane; c < TW; c += 32) {
+            const long long o = rowoff + c;
+            const float fx = fxt[c];
+            int bin;
+            float fz;
+            z_cell(ldg_stream(gd + o), a.D, bin, fz);
+            const float x0 = ldg_stream(xp + o), x1 = ldg_stream(xp + HW + o),
+                        x2 = ldg_stream(xp + 2 * HW + o);
+            const float4 *L = glo + bin * kPlaneStride, *Dz = gdz + bin * kPlaneStride;
+#pragma unroll
+            for (int oc = 0; oc < 3; oc++) {
+                float A[4];
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    const float lo = lerp2(L[4 * oc + i], fx, fy);
+                    const float dz = lerp2(Dz[4 * oc + i], fx, fy);
+                    A[i] = fmaf(fz, dz, lo);
+                }
+                yp[oc * HW + o] = fmaf(A[0], x0, fmaf(A[1], x1, fmaf(A[2], x2, A[3])));
+            }
+        }
+    }
+}
+
+// ----------------------------------------------------------------- backward, tiled
+// 96-vector reduce-scatter across the warp: after it lane holds 3 sums for
+// indices base .. base+2, base = 48 b4 + 24 b3 + 12 b2 + 6 b1 + 3 b0.
+template <int H>
+RS_DEV void rs_stage(float *v, int lane, int m) {
+    const bool hi = (lane & m) != 0;
+#pragma unroll
+    for (int k = 0; k < H; k++) {
+        const float send = hi ? v[k] : v[k + H];
+        const float keep = hi ? v[k + H] : v[k];
+        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+    }
+}
+
+// acc index: ((e*2 + b)*2 + a)*12 + q ; e = z-plane (0: zl, 1: zh), (b, a) = corner.
+// wacc (warp slot): [corner(4)][z(D)][q(12)]
+RS_DEV void flush_acc(float *acc, float *wacc, int bin, int D, int lane) {
+    rs_stage<48>(acc, lane, 16);
+    rs_stage<24>(acc, lane, 8);
+    rs_stage<12>(acc, lane, 4);
+    rs_stage<6>(acc, lane, 2);
+    rs_stage<3>(acc, lane, 1);
+    const int base = ((lane & 16) ? 48 : 0) + ((lane & 8) ? 24 : 0) + ((lane & 4) ? 12 : 0) +
+                     ((lane & 2) ? 6 : 0) + ((lane & 1) ? 3 : 0);
+    const int zl = clampi(bin - 1, 0, D - 1), zh = clampi(bin, 0, D - 1);
+    // e = 0 lanes (0..15) first, then e = 1: zl may equal zh (clamped planes)
+#pragma unroll
+    for (int ph = 0; ph < 2; ph++) {
+        if ((lane >> 4) == ph) {
+#pragma unroll
+            for (int t = 0; t < 3; t++) {
+                const int idx = base + t;
+                const int q = idx % 12, corner = (idx / 12) & 3, e = idx / 48;
+                wacc[(corner * D + (e ? zh : zl)) * 12 + q] += acc[t];
+            }
+        }
+        __syncwarp();
+    }
+#pragma unroll
+    for (int k = 0; k < 96; k++) acc[k] = 0.f;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    bslice_bwd_tiled(BsliceArgs a, int SY, int SX, float *__restrict__ partials) {
+    extern __shared__ float4 smem4[];
+    const int D = a.D, NB = D + 1;
+    float4 *glo = smem4;                                    // (D+1)*13 float4
+    float4 *gdz = glo + (D + 1) * kPlaneStride;             // (D+1)*13 float4
+    float *fxt = (float *)(gdz + (D + 1) * kPlaneStride);   // kTileXS
+    float *fyt = fxt + kTileXS;                             // kTileYS
+    float *wacc = fyt + kTileYS;                            // kWarps * 4 * D * 12
+    int *cnt = (int *)(wacc + kWarps * 4 * D * 12);         // kWarps * NB
+    int *bstart = cnt + kWarps * NB;                        // NB + 1
+    int *chunk_bin = bstart + NB + 1;                       // max chunks
+    const int max_chunks = (kTileXS * kTileYS) / 32 + 1 + NB;
+    unsigned *sorted = (unsigned *)(chunk_bin + max_chunks);  // max_chunks * 32
+    unsigned char *binv = (unsigned char *)(sorted + max_chunks * 32);  // kTileXS*kTileYS
+
+    const Tile t = tile_of(blockIdx.x, a.Gh, a.Gw, SY, SX, a.H, a.W);
+    const int TW = t.xe - t.xs, TH = t.ye - t.ys;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long long HW = (long long)a.H * a.W;
+    const float *gd = a.guide + (long long)t.n * HW;
+
+    stage_corners(glo, gdz, a.grid, t, D, a.Gh, a.Gw);
+    for (int c = threadIdx.x; c < TW; c += kThreads) {
+        const double cx = bs_cx(t.xs + c, a.W, a.Gw);
+        fxt[c] = (float)__dsub_rn(cx, floor(cx));
+    }
+    for (int r = threadIdx.x; r < TH; r += kThreads) {
+        const double cy = bs_cx(t.ys + r, a.H, a.Gh);
+        fyt[r] = (float)__dsub_rn(cy, floor(cy));
+    }
+    for (int e = threadIdx.x; e < kWarps * 4 * D * 12; e += kThreads) wacc[e] = 0.f;
+    for (int e = threadIdx.x; e < kWarps * NB; e += kThreads) cnt[e] = 0;
+    __syncthreads();
+
+    // ---- pass A: z-bin of every pixel, per-warp counts (warp w: rows w, w+8, ...)
+    for (int r = w; r < TH; r += kWarps) {
+        for (int c0 = 0; c0 < TW; c0 += 32) {
+            const int c = c0 + lane;
+            int bin = -1;
+            if (c < TW) {
+                float fz;
+                z_cell(__ldg(gd + (long long)(t.ys + r) * a.W + t.xs + c), D, bin, fz);
+                binv[r * TW + c] = (unsigned char)bin;
+            }
+            const unsigned m = __match_any_sync(0xffffffffu, bin);
+            if (bin >= 0 && lane == __ffs(m) - 1) cnt[w * NB + bin] += __popc(m);
+        }
+    }
+    __syncthreads();
+    // ---- scan: bin segments padded to 32, per-(warp, bin) offsets
+    if (threadIdx.x == 0) {
+        int run = 0;
+        for (int b = 0; b < NB; b++) {
+            bstart[b] = run;
+            for (int ww = 0; ww < kWarps; ww++) {
+                const int v = cnt[ww * NB + b];
+                cnt[ww * NB + b] = run;
+                run += v;
+            }
+            run = (run + 31) & ~31;
+        }
+        bstart[NB] = run;
+    }
+    __syncthreads();
+    const int L = bstart[NB], nchunks = L >> 5;
+    for (int e = threadIdx.x; e < L; e += kThreads) sorted[e] = kInvalid;
+    for (int c = threadIdx.x; c < nchunks; c += kThreads) {
+        int b = 0;
+        while (bstart[b + 1] <= c * 32) b++;
+        chunk_bin[c] = b;
+    }
+    __syncthreads();
+    // ---- pass B: stable placement (same walk order as pass A)
+    for (int r = w; r < TH; r += kWarps) {
+        for (int c0 = 0; c0 < TW; c0 += 32) {
+            const int c = c0 + lane;
+            const int bin = (c < TW) ? (int)binv[r * TW + c] : -1;
+            const unsigned m = __match_any_sync(0xffffffffu, bin);
+            if (bin >= 0) {
+                const int rank = __popc(m & ((1u << lane) - 1u));
+                sorted[cnt[w * NB + bin] + rank] = ((unsigned)r << 16) | (unsigned)c;
+            }
+            __syncwarp();
+            if (bin >= 0 && lane == __ffs(m) - 1) cnt[w * NB + bin] += __popc(m);
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+
+    // ---- pass C: per-chunk work, warp w takes a contiguous chunk range
+    const float *xp = a.x + (long long)t.n * 3 * HW;
+    const float *gp = a.dy + (long long)t.n * 3 * HW;
+    float *dxp = a.dx ? a.dx + (long long)t.n * 3 * HW : nullptr;
+    float *dgp = a.dguide ? a.dguide + (long long)t.n * HW : nullptr;
+    float *mywacc = wacc + w * 4 * D * 12;
+    const int cbeg = (int)(((long long)nchunks * w) / kWarps);
+    const int cend = (int)(((long long)nchunks * (w + 1)) / kWarps);
+    float acc[96];
+#pragma unroll
+    for (int k = 0; k < 96; k++) acc[k] = 0.f;
+    int cur_bin = cbeg < cend ? chunk_bin[cbeg] : 0;
+    for (int ch = cbeg; ch < cend; ch++) {
+        const int bin = chunk_bin[ch];
+        if (bin != cur_bin) {
+            flush_acc(acc, mywacc, cur_bin, D, lane);
+            cur_bin = bin;
+        }
+        const unsigned ent = sorted[ch * 32 + lane];
+        const bool valid = ent != kInvalid;
+        const int r = valid ? (int)(ent >> 16) : 0, c = valid ? (int)(ent & 0xffffu) : 0;
+        const long long o = (long long)(t.ys + r) * a.W + t.xs + c;
+        float fz = 0.f, X[3] = {0.f, 0.f, 0.f}, G[3] = {0.f, 0.f, 0.f};
+        const float fx = fxt[c], fy = fyt[r];
+        if (valid) {
+            int bb;
+            z_cell(__ldg(gd + o), D, bb, fz);
+#pragma unroll
+            for (int i = 0; i < 3; i++) {
+                X[i] = __ldg(xp + i * HW + o);
+                G[i] = __ldg(gp + i * HW + o);
+            }
+        }
+        const float4 *Lc = glo + bin * kPlaneStride, *Dc = gdz + bin * kPlaneStride;
+        const float wx1 = fx, wx0 = 1.f - fx, wy1 = fy, wy0 = 1.f - fy, wz1 = fz, wz0 = 1.f - fz;
+        float wt[8];
+        wt[0] = wz0 * wy0 * wx0; wt[1] = wz0 * wy0 * wx1;
+        wt[2] = wz0 * wy1 * wx0; wt[3] = wz0 * wy1 * wx1;
+        wt[4] = wz1 * wy0 * wx0; wt[5] = wz1 * wy0 * wx1;
+        wt[6] = wz1 * wy1 * wx0; wt[7] = wz1 * wy1 * wx1;
+        float dx[3] = {0.f, 0.f, 0.f}, dgd = 0.f;
+#pragma unroll
+        for (int oc = 0; oc < 3; oc++) {
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const int q = 4 * oc + i;
+                const float lo = lerp2(Lc[q], fx, fy);
+                const float d = lerp2(Dc[q], fx, fy);
+                const float P = (i < 3) ? G[oc] * X[i] : G[oc];
+                if (i < 3) dx[i] = fmaf(G[oc], fmaf(fz, d, lo), dx[i]);
+                dgd = fmaf(P, d, dgd);
+#pragma unroll
+                for (int tt = 0; tt < 8; tt++) acc[tt * 12 + q] = fmaf(wt[tt], P, acc[tt * 12 + q]);
+            }
+        }
+        if (valid) {
+            if (dxp) {
+#pragma unroll
+                for (int i = 0; i < 3; i++) dxp[i * HW + o] = dx[i];
+            }
+            if (dgp) dgp[o] = (float)D * dgd;
+        }
+    }
+    if (cbeg < cend) flush_acc(acc, mywacc, cur_bin, D, lane);
+    __syncthreads();
+    // ---- block partial: fixed-order sum over warps
+    float *part = partials + (long long)blockIdx.x * 4 * D * 12;
+    for (int e = threadIdx.x; e < 4 * D * 12; e += kThreads) {
+        float s = 0.f;
+#pragma unroll
+        for (int ww = 0; ww < kWarps; ww++) s += wacc[ww * 4 * D * 12 + e];
+        part[e] = s;
+    }
+}
+
+// dgrid[n,q,z,y,x] = fixed-order sum of the partials of the dual cells whose
+// clamped corners are (y, x).  partial layout: [block][corner][z][q].
+__global__ void __launch_bounds__(kThreads)
+    bslice_dgrid_gather(BsliceArgs a, int SY, int SX, const float *__restrict__ partials) {
+    const long long total = (long long)a.N * 12 * a.D * a.Gh * a.Gw;
+    const long long idx = (long long)blockIdx.x * kThreads + threadIdx.x;
+    if (idx >= total) return;
+    long long r = idx;
+    const int x = (int)(r % a.Gw); r /= a.Gw;
+    const int y = (int)(r % a.Gh); r /= a.Gh;
+    const int z = (int)(r % a.D); r /= a.D;
+    const int q = (int)(r % 12);
+    const int n = (int)(r / 12);
+    const int D = a.D;
+    float s = 0.f;
+    for (int jj = y; jj <= y + 1 && jj <= a.Gh; jj++) {
+        for (int b = 0; b < 2; b++) {
+            if (clampi(jj - 1 + b, 0, a.Gh - 1) != y) continue;
+            for (int kk = x; kk <= x + 1 && kk <= a.Gw; kk++) {
+                for (int aa = 0; aa < 2; aa++) {
+                    if (clampi(kk - 1 + aa, 0, a.Gw - 1) != x) continue;
+                    const long long blk0 =
+                        ((((long long)n * (a.Gh + 1) + jj) * (a.Gw + 1) + kk) * SY) * SX;
+                    for (int st = 0; st < SY * SX; st++) {
+                        const float *p = partials + (blk0 + st) * 4 * D * 12;
+                        s += p[((b * 2 + aa) * D + z) * 12 + q];
+                    }
+                }
+            }
+        }
+    }
+    a.dgrid[idx] = s;
+}
+
+// ----------------------------------------------------------------- generic (any shape)
+struct Slice8 {
+    int xi[2], yi[2], zi[2];
+    float wx[2], wy[2], wz[2];
+};
+
+RS_DEV Slice8 slice_geom(const BsliceArgs &a, int y, int x, float g) {
+    Slice8 s;
+    const double cx = bs_cx(x, a.W, a.Gw), cy = bs_cx(y, a.H, a.Gh), cz = bs_cz(g, a.D);
+    const Cell ccx = cell_of(cx), ccy = cell_of(cy), ccz = cell_of(cz);
+    s.wx[0] = 1.f - ccx.f; s.wx[1] = ccx.f;
+    s.wy[0] = 1.f - ccy.f; s.wy[1] = ccy.f;
+    s.wz[0] = 1.f - ccz.f; s.wz[1] = ccz.f;
+    for (int t = 0; t < 2; t++) {
+        s.xi[t] = clampi(ccx.i0 + t, 0, a.Gw - 1);
+        s.yi[t] = clampi(ccy.i0 + t, 0, a.Gh - 1);
+        s.zi[t] = clampi(ccz.i0 + t, 0, a.D - 1);
+    }
+    return s;
+}
+
+__global__ void __launch_bounds__(kThreads) bslice_fwd_generic(BsliceArgs a) {
+    const long long HW = (long long)a.H * a.W;
+    const long long idx = (long long)blockIdx.x * kThreads + threadIdx.x;
+    if (idx >= (long long)a.N * HW) return;
+    const int n = (int)(idx / HW);
+    const long long o = idx - (long long)n * HW;
+    const int y = (int)(o / a.W), x = (int)(o - (long long)y * a.W);
+    const Slice8 s = slice_geom(a, y, x, __ldg(a.guide + idx));
+    const long long plane = (long long)a.Gh * a.Gw;
+    const float *g = a.grid + (long long)n * 12 * a.D * plane;
+    const float *xp = a.x + (long long)n * 3 * HW + o;
+    const float X[3] = {__ldg(xp), __ldg(xp + HW), __ldg(xp + 2 * HW)};
+    float A[12];
+#pragma unroll
+    for (int q = 0; q < 12; q++) A[q] = 0.f;
+    for (int e = 0; e < 2; e++)
+        for (int b = 0; b < 2; b++)
+            for (int aa = 0; aa < 2; aa++) {
+                const float wt = s.wz[e] * s.wy[b] * s.wx[aa];
+                const long long off = ((long long)s.zi[e] * a.Gh + s.yi[b]) * a.Gw + s.xi[aa];
+#pragma unroll
+                for (int q = 0; q < 12; q++) A[q] = fmaf(wt, __ldg(g + q * a.D * plane + off), A[q]);
+            }
+    float *yp = a.y + (long long)n * 3 * HW + o;
+#pragma unroll
+    for (int oc = 0; oc < 3; oc++)
+        yp[oc * HW] = fmaf(A[4 * oc], X[0], fmaf(A[4 * oc + 1], X[1], fmaf(A[4 * oc + 2], X[2], A[4 * oc + 3])));
+}
+
+__global__ void __launch_bounds__(kThreads) bslice_bwd_generic(BsliceArgs a) {
+    const long long HW = (long long)a.H * a.W;
+    const long long idx = (long long)blockIdx.x * kThreads + threadIdx.x;
+    if (idx >= (long long)a.N * HW) return;
+    const int n = (int)(idx / HW);
+    const long long o = idx - (long long)n * HW;
+    const int y = (int)(o / a.W), x = (int)(o - (long long)y * a.W);
+    const Slice8 s = slice_geom(a, y, x, __ldg(a.guide + idx));
+    const long long plane = (long long)a.Gh * a.Gw;
+    const float *g = a.grid + (long long)n * 12 * a.D * plane;
+    const float *xp = a.x + (long long)n * 3 * HW + o;
+    const float *gp = a.dy + (long long)n * 3 * HW + o;
+    const float Xt[4] = {__ldg(xp), __ldg(xp + HW), __ldg(xp + 2 * HW), 1.f};
+    const float G[3] = {__ldg(gp), __ldg(gp + HW), __ldg(gp + 2 * HW)};
+    if (a.dx || a.dguide) {
+        // low-plane slice and the slice of the plane difference (P3)
+        float Alo[12], Adz[12];
+#pragma unroll
+        for (int q = 0; q < 12; q++) Alo[q] = Adz[q] = 0.f;
+        for (int b = 0; b < 2; b++)
+            for (int aa = 0; aa < 2; aa++) {
+                const float wt = s.wy[b] * s.wx[aa];
+                const long long sp = (long long)s.yi[b] * a.Gw + s.xi[aa];
+#pragma unroll
+                for (int q = 0; q < 12; q++) {
+                    const float gl = __ldg(g + (q * a.D + s.zi[0]) * plane + sp);
+                    const float gh = __ldg(g + (q * a.D + s.zi[1]) * plane + sp);
+                    Alo[q] = fmaf(wt, gl, Alo[q]);
+                    Adz[q] = fmaf(wt, gh - gl, Adz[q]);
+                }
+            }
+        float dgd = 0.f, dx[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+        for (int oc = 0; oc < 3; oc++)
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const int q = 4 * oc + i;
+                const float d = Adz[q];
+                if (i < 3) dx[i] = fmaf(G[oc], fmaf(s.wz[1], d, Alo[q]), dx[i]);
+                dgd = fmaf(G[oc] * Xt[i], d, dgd);
+            }
+        if (a.dx) {
+            float *dxp = a.dx + (long long)n * 3 * HW + o;
+            dxp[0] = dx[0];
+            dxp[HW] = dx[1];
+            dxp[2 * HW] = dx[2];
+        }
+        if (a.dguide) a.dguide[idx] = (float)a.D * dgd;
+    }
+    if (a.dgrid) {
+        float *dg = a.dgrid + (long long)n * 12 * a.D * plane;
+        for (int e = 0; e < 2; e++)
+            for (int b = 0; b < 2; b++)
+                for (int aa = 0; aa < 2; aa++) {
+                    const float wt = s.wz[e] * s.wy[b] * s.wx[aa];
+                    const long long off = ((long long)s.zi[e] * a.Gh + s.yi[b]) * a.Gw + s.xi[aa];
+#pragma unroll
+                    for (int oc = 0; oc < 3; oc++)
+#pragma unroll
+                        for (int i = 0; i < 4; i++)
+                            red_add(dg + (4 * oc + i) * a.D * plane + off, wt * G[oc] * Xt[i]);
+                }
+    }
+}
+
+// ----------------------------------------------------------------- host-side geometry
+struct TileGeom {
+    int SY, SX;
+    long long blocks;
+    bool ok;
+};
+
+TileGeom tile_geom(int N, int H, int W, int D, int Gh, int Gw) {
+    TileGeom g;
+    // dual cells must hold >= 8 px per axis for the tiled kernels to pay off
+    g.ok = (W >= 8 * Gw) && (H >= 8 * Gh) && D >= 1 && D <= 64;
+    const int maxw = (W + Gw - 1) / Gw, maxh = (H + Gh - 1) / Gh;
+    g.SX = (maxw + kTileX - 1) / kTileX;
+    g.SY = (maxh + kTileY - 1) / kTileY;
+    g.blocks = (long long)N * (Gh + 1) * (Gw + 1) * g.SY * g.SX;
+    return g;
+}
+
+size_t fwd_smem(int D) {
+    return sizeof(float4) * 2 * (D + 1) * kPlaneStride + sizeof(float) * (kTileXS + kTileYS);
+}
+
+size_t bwd_smem(int D) {
+    const int NB = D + 1;
+    const int max_chunks = (kTileXS * kTileYS) / 32 + 1 + NB;
+    return sizeof(float4) * 2 * (D + 1) * kPlaneStride + sizeof(float) * (kTileXS + kTileYS) +
+           sizeof(float) * kWarps * 4 * D * 12 + sizeof(int) * (kWarps * NB + NB + 1) +
+           sizeof(int) * max_chunks + sizeof(unsigned) * max_chunks * 32 + kTileXS * kTileYS;
+}
+
+}  // namespace
+
+size_t bslice_ws_bytes(int N, int H, int W, int D, int Gh, int Gw) {
+    const TileGeom g = tile_geom(N, H, W, D, Gh, Gw);
+    if (!g.ok) return 0;
+    return sizeof(float) * (size_t)g.blocks * 4 * D * 12;
+}
+
+cudaError_t bslice_fwd_launch(const BsliceArgs &a, cudaStream_t s) {
+    const TileGeom g = tile_geom(a.N, a.H, a.W, a.D, a.Gh, a.Gw);
+    if (g.ok) {
+        const size_t sm = fwd_smem(a.D);
+        bslice_fwd_tiled<<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX);
+    } else {
+        const long long total = (long long)a.N * a.H * a.W;
+        bslice_fwd_generic<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(a);
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t bslice_bwd_launch(const BsliceArgs &a, int algo, int deterministic, void *ws,
+                              size_t ws_bytes, cudaStream_t s) {
+    (void)deterministic;
+    const TileGeom g = tile_geom(a.N, a.H, a.W, a.D, a.Gh, a.Gw);
+    const bool tiled = g.ok && algo != 3 /*SCATTER_ATOMIC*/ && a.dgrid &&
+                       ws_bytes >= bslice_ws_bytes(a.N, a.H, a.W, a.D, a.Gh, a.Gw);
+    if (tiled) {
+        const size_t sm = bwd_smem(a.D);
+        static thread_local bool attr_set = false;
+        if (!attr_set) {
+            cudaFuncSetAttribute(bslice_bwd_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 200 * 1024);
+            attr_set = true;
+        }
+        float *partials = (float *)ws;
+        bslice_bwd_tiled<<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX, partials);
+        note_launch();
+        const long long total = (long long)a.N * 12 * a.D * a.Gh * a.Gw;
+        bslice_dgrid_gather<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(
+            a, g.SY, g.SX, partials);
+        note_launch();
+    } else {
+        if (a.dgrid) {
+            cudaError_t e = cudaMemsetAsync(
+                a.dgrid, 0, sizeof(float) * (size_t)a.N * 12 * a.D * a.Gh * a.Gw, s);
+            if (e != cudaSuccess) return e;
+        }
+        const long long total = (long long)a.N * a.H * a.W;
+        bslice_bwd_generic<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(a);
+        note_launch();
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace rs

@@ -1,0 +1,144 @@
+// common.cuh — device helpers shared by the rsgrad kernels (product path only).
+//
+// Precision contract (P1): every SAMPLE COORDINATE is evaluated in
+// fp64 with explicit round-to-nearest intrinsics (__dadd_rn/__dmul_rn/
+// __ddiv_rn) in the left-to-right order of the definition, so no FMA
+// contraction can move a coordinate across an integer: the cell a sample lands
+// in is the exact fp64 cell of the definition.  Fractions are then rounded to
+// fp32 and all data arithmetic (weights, taps, sums) is fp32.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define RS_DEV __device__ __forceinline__
+
+namespace rs {
+
+constexpr int kNumSMs = 148;  // B200
+
+// ----------------------------------------------------------------- launch accounting
+void note_launch();  // api.cu: thread-local counter behind rsgrad_launch_count()
+
+// ----------------------------------------------------------------- STN coordinates (R1)
+// normalised output coordinate of index j on an axis of length L
+RS_DEV double stn_norm(int j, int L, int ac) {
+    if (ac) return __dadd_rn(-1.0, __ddiv_rn(__dmul_rn(2.0, (double)j), (double)(L - 1)));
+    return __dsub_rn(__ddiv_rn(__dadd_rn(__dmul_rn(2.0, (double)j), 1.0), (double)L), 1.0);
+}
+
+// un-normalise a grid coordinate g to pixel units on an axis of length L
+RS_DEV double stn_unnorm(double g, int L, int ac) {
+    if (ac) return __dmul_rn(__dmul_rn(__dadd_rn(g, 1.0), (double)(L - 1)), 0.5);
+    return __dmul_rn(__dsub_rn(__dmul_rn(__dadd_rn(g, 1.0), (double)L), 1.0), 0.5);
+}
+
+// g = t0*a + t1*b + t2, evaluated as ((t0*a) + (t1*b)) + t2
+RS_DEV double affine3(double t0, double t1, double t2, double a, double b) {
+    return __dadd_rn(__dadd_rn(__dmul_rn(t0, a), __dmul_rn(t1, b)), t2);
+}
+
+// Border padding: clamp to [0, L-1]; derivative 1 strictly inside, else 0.
+RS_DEV double clamp_coord(double v, int L, float &dclamp) {
+    if (v <= 0.0) { dclamp = 0.f; return 0.0; }
+    if (v >= (double)(L - 1)) { dclamp = 0.f; return (double)(L - 1); }
+    dclamp = 1.f;
+    return v;
+}
+
+// Floor cell of a coordinate: integer corner and fp32 fraction.
+struct Cell {
+    int i0;
+    float f;
+};
+RS_DEV Cell cell_of(double v) {
+    double fl = floor(v);
+    Cell c;
+    // coordinates beyond +-2^30 px are far outside any image: clamp the
+    // integer so the bounds tests below stay well defined (weights unchanged)
+    c.i0 = fl < -1073741824.0 ? -1073741824 : (fl > 1073741824.0 ? 1073741824 : (int)fl);
+    c.f = (float)__dsub_rn(v, fl);
+    return c;
+}
+
+// ----------------------------------------------------------------- reductions
+RS_DEV float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+RS_DEV double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Vector reduction to global memory without return (sm_90+): 4 consecutive floats.
+RS_DEV void red_add_v4(float *addr, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b),
+                 "f"(c), "f"(d)
+                 : "memory");
+}
+
+RS_DEV void red_add(float *addr, float a) {
+    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(a) : "memory");
+}
+
+// streaming loads / stores (read-once data: no L1 allocation)
+RS_DEV float ldg_stream(const float *p) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+
+RS_DEV float4 ldg_stream4(const float4 *p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+RS_DEV void stg_stream(float *p, float v) {
+    asm volatile("st.global.L1::no_allocate.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
+}  // namespace rs
+
+// ----------------------------------------------------------------- launchers (internal ABI)
+namespace rs {
+struct StnArgs {
+    const float *x, *theta, *dy;
+    float *y, *dx, *dtheta;
+    int N, C, H, W, Ho, Wo;
+    int ac, border;
+};
+struct WarpArgs {
+    const float *x, *flow, *dy;
+    float *y, *dx, *dflow;
+    int N, C, H, W;
+    int border;
+};
+struct BsliceArgs {
+    const float *grid, *guide, *x, *dy;
+    float *y, *dgrid, *dguide, *dx;
+    int N, H, W, D, Gh, Gw;
+};
+
+// each returns a cudaError_t from the launches; algo is an rs_algo value
+cudaError_t stn_fwd_launch(const StnArgs &a, cudaStream_t s);
+cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *ws, size_t ws_bytes,
+                           cudaStream_t s);
+size_t stn_ws_bytes(int N, int C, int H, int W, int Ho, int Wo);
+
+cudaError_t warp_fwd_launch(const WarpArgs &a, cudaStream_t s);
+cudaError_t warp_bwd_launch(const WarpArgs &a, int algo, int deterministic, void *ws,
+                            size_t ws_bytes, cudaStream_t s);
+size_t warp_ws_bytes(int N, int C, int H, int W);
+
+cudaError_t bslice_fwd_launch(const BsliceArgs &a, cudaStream_t s);
+cudaError_t bslice_bwd_launch(const BsliceArgs &a, int algo, int deterministic, void *ws,
+                              size_t ws_bytes, cudaStream_t s);
+size_t bslice_ws_bytes(int N, int H, int W, int D, int Gh, int Gw);
+}  // namespace rs

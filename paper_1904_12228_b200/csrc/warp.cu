@@ -1,0 +1,151 @@
+// warp.cu — FlowNet 2.0 per-pixel warp, forward and adjoint, sm_100a.
+//
+// Kernels
+//   warp_fwd_kernel   one thread per pixel: coordinate x + u(x) in fp64, bilinear
+//                     gather over all channels.
+//   warp_bwd_kernel   one thread per pixel: d_flow is a pure gather (G and the X
+//                     taps); d_input is the reversed gather, which for an
+//                     arbitrary flow field has no bounded inverse, so it is
+//                     "a general scatter using atomics": fp32
+//                     red.global.add into a zero-filled dx.
+#include "common.cuh"
+
+namespace rs {
+namespace {
+
+constexpr int kThreads = 256;
+
+struct Tap {
+    long long o00;
+    float w00, w01, w10, w11;
+    float fx, fy;
+    bool k00, k01, k10, k11;
+};
+
+RS_DEV Tap warp_tap(const WarpArgs &a, int x, int y, float u, float v, float &cgx, float &cgy) {
+    double ix = __dadd_rn((double)x, (double)u);
+    double iy = __dadd_rn((double)y, (double)v);
+    cgx = 1.f;
+    cgy = 1.f;
+    if (a.border) {
+        ix = clamp_coord(ix, a.W, cgx);
+        iy = clamp_coord(iy, a.H, cgy);
+    }
+    const Cell cx = cell_of(ix), cy = cell_of(iy);
+    const bool x0ok = cx.i0 >= 0 && cx.i0 < a.W, x1ok = cx.i0 + 1 >= 0 && cx.i0 + 1 < a.W;
+    const bool y0ok = cy.i0 >= 0 && cy.i0 < a.H, y1ok = cy.i0 + 1 >= 0 && cy.i0 + 1 < a.H;
+    Tap t;
+    t.fx = cx.f;
+    t.fy = cy.f;
+    const float wx0 = 1.f - cx.f, wy0 = 1.f - cy.f;
+    t.w00 = wy0 * wx0;
+    t.w01 = wy0 * cx.f;
+    t.w10 = cy.f * wx0;
+    t.w11 = cy.f * cx.f;
+    t.k00 = y0ok && x0ok;
+    t.k01 = y0ok && x1ok;
+    t.k10 = y1ok && x0ok;
+    t.k11 = y1ok && x1ok;
+    t.o00 = (long long)cy.i0 * a.W + cx.i0;
+    return t;
+}
+
+__global__ void __launch_bounds__(kThreads) warp_fwd_kernel(WarpArgs a) {
+    const long long HW = (long long)a.H * a.W;
+    const long long idx = (long long)blockIdx.x * kThreads + threadIdx.x;
+    if (idx >= (long long)a.N * HW) return;
+    const int n = (int)(idx / HW);
+    const long long rem = idx - (long long)n * HW;
+    const int y = (int)(rem / a.W), x = (int)(rem - (long long)y * a.W);
+    const float *fp = a.flow + (long long)n * 2 * HW + rem;
+    const float u = ldg_stream(fp), v = ldg_stream(fp + HW);
+    float cgx, cgy;
+    const Tap t = warp_tap(a, x, y, u, v, cgx, cgy);
+    const float *xp = a.x + (long long)n * a.C * HW + t.o00;
+    float *yp = a.y + (long long)n * a.C * HW + rem;
+#pragma unroll 3
+    for (int c = 0; c < a.C; c++) {
+        const float *p = xp + (long long)c * HW;
+        float r = 0.f;
+        if (t.k00) r = fmaf(t.w00, __ldg(p), r);
+        if (t.k01) r = fmaf(t.w01, __ldg(p + 1), r);
+        if (t.k10) r = fmaf(t.w10, __ldg(p + a.W), r);
+        if (t.k11) r = fmaf(t.w11, __ldg(p + a.W + 1), r);
+        yp[(long long)c * HW] = r;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) warp_bwd_kernel(WarpArgs a) {
+    const long long HW = (long long)a.H * a.W;
+    const long long idx = (long long)blockIdx.x * kThreads + threadIdx.x;
+    if (idx >= (long long)a.N * HW) return;
+    const int n = (int)(idx / HW);
+    const long long rem = idx - (long long)n * HW;
+    const int y = (int)(rem / a.W), x = (int)(rem - (long long)y * a.W);
+    const float *fp = a.flow + (long long)n * 2 * HW + rem;
+    const float u = ldg_stream(fp), v = ldg_stream(fp + HW);
+    float cgx, cgy;
+    const Tap t = warp_tap(a, x, y, u, v, cgx, cgy);
+    const float *xp = a.x + (long long)n * a.C * HW + t.o00;
+    float *dxp = a.dx ? a.dx + (long long)n * a.C * HW + t.o00 : nullptr;
+    const float *gp = a.dy + (long long)n * a.C * HW + rem;
+    float dix = 0.f, diy = 0.f;
+    for (int c = 0; c < a.C; c++) {
+        const float g = ldg_stream(gp + (long long)c * HW);
+        if (a.dflow) {
+            const float *p = xp + (long long)c * HW;
+            const float v00 = t.k00 ? __ldg(p) : 0.f, v01 = t.k01 ? __ldg(p + 1) : 0.f;
+            const float v10 = t.k10 ? __ldg(p + a.W) : 0.f, v11 = t.k11 ? __ldg(p + a.W + 1) : 0.f;
+            dix = fmaf(g, fmaf(1.f - t.fy, v01 - v00, t.fy * (v11 - v10)), dix);
+            diy = fmaf(g, fmaf(1.f - t.fx, v10 - v00, t.fx * (v11 - v01)), diy);
+        }
+        if (dxp) {
+            float *q = dxp + (long long)c * HW;
+            if (t.k00) red_add(q, t.w00 * g);
+            if (t.k01) red_add(q + 1, t.w01 * g);
+            if (t.k10) red_add(q + a.W, t.w10 * g);
+            if (t.k11) red_add(q + a.W + 1, t.w11 * g);
+        }
+    }
+    if (a.dflow) {
+        float *dfp = a.dflow + (long long)n * 2 * HW + rem;
+        dfp[0] = dix * cgx;
+        dfp[HW] = diy * cgy;
+    }
+}
+
+}  // namespace
+
+size_t warp_ws_bytes(int N, int C, int H, int W) {
+    (void)N;
+    (void)C;
+    (void)H;
+    (void)W;
+    return 0;
+}
+
+cudaError_t warp_fwd_launch(const WarpArgs &a, cudaStream_t s) {
+    long long total = (long long)a.N * a.H * a.W;
+    warp_fwd_kernel<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(a);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t warp_bwd_launch(const WarpArgs &a, int algo, int deterministic, void *ws,
+                            size_t ws_bytes, cudaStream_t s) {
+    (void)algo;
+    (void)deterministic;
+    (void)ws;
+    (void)ws_bytes;
+    const long long HW = (long long)a.H * a.W;
+    if (a.dx) {
+        cudaError_t e = cudaMemsetAsync(a.dx, 0, sizeof(float) * (size_t)a.N * a.C * HW, s);
+        if (e != cudaSuccess) return e;
+    }
+    long long total = (long long)a.N * HW;
+    warp_bwd_kernel<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(a);
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace rs

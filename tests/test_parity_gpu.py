@@ -1,0 +1,304 @@
+"""CUDA path (through the C ABI) vs the fp64 oracle, element by element.
+
+Tolerance (tests/_tol.py): |g - r| <= rtol |r| + atol max(1, rms(r)); forward
+rtol 1e-5, gradients rtol 1e-4, atol 1e-6 (BASELINE.json north_star).
+Sizes: configs[0] (STN 1x3x16x16), ragged multi-tile shapes, and the paper
+shapes of configs[1..3] in full; configs[4] (batch 64 @ 1024^2) is run in the
+bench launch configuration and compared on sampled whole samples (every
+sample is independent).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_1904_12228_b200 import rsgrad
+from _tol import assert_close, compare  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def _cuda(d, dev):
+    return {k: v.to(dev).contiguous() for k, v in d.items()}
+
+
+def _np(t):
+    return t.detach().cpu().double().numpy()
+
+
+# ============================================================================ STN
+STN_SHAPES = [
+    (1, 3, 16, 16, 16, 16),     # configs[0]
+    (2, 5, 37, 53, 41, 29),     # ragged, several tiles, Ho != H
+    (3, 16, 64, 96, 64, 96),
+    (1, 1, 2, 2, 2, 2),         # minimum for align_corners=1
+]
+
+
+@pytest.mark.parametrize("shape", STN_SHAPES)
+@pytest.mark.parametrize("ac", [True, False])
+@pytest.mark.parametrize("padding", ["zeros", "border"])
+def test_stn_parity(cuda_device, shape, ac, padding):
+    N, C, H, W, Ho, Wo = shape
+    inp = synth.stn_inputs(N, C, H, W, Ho, Wo, cfg=1)
+    g = _cuda(inp, cuda_device)
+    y = rsgrad.stn_fwd(g["x"], g["theta"], Ho, Wo, align_corners=ac, padding=padding)
+    dx, dth = rsgrad.stn_bwd(g["x"], g["theta"], g["dy"], align_corners=ac, padding=padding)
+    x, th, dy = (inp[k].double().numpy() for k in ("x", "theta", "dy"))
+    border = padding == "border"
+    ry = oracle.stn_fwd(x, th, Ho, Wo, ac, border)
+    rdx, rdth = oracle.stn_bwd(x, th, dy, ac, border)
+    assert_close(_np(y), ry, "fwd", "y")
+    assert_close(_np(dx), rdx, "grad", "dx")
+    assert_close(_np(dth), rdth, "grad", "dtheta")
+
+
+@pytest.mark.parametrize("algo", ["gather", "scatter_atomic"])
+def test_stn_algos_agree_with_oracle(cuda_device, algo):
+    inp = synth.stn_inputs(2, 8, 48, 40, cfg=1)
+    g = _cuda(inp, cuda_device)
+    dx, _ = rsgrad.stn_bwd(g["x"], g["theta"], g["dy"], algo=algo, need_dtheta=False)
+    rdx, _ = oracle.stn_bwd(*(inp[k].double().numpy() for k in ("x", "theta", "dy")))
+    assert_close(_np(dx), rdx, "grad", f"dx[{algo}]")
+
+
+def test_stn_singular_theta_falls_back(cuda_device):
+    """A rank-deficient theta has no bounded preimage: AUTO must take the atomic scatter."""
+    inp = synth.stn_inputs(3, 4, 20, 24, cfg=1)
+    inp["theta"][1] = torch.tensor([[0.5, 0.5, 0.1], [0.5, 0.5, -0.2]])  # det = 0
+    inp["theta"][2] = torch.tensor([[0.01, 0.0, 0.0], [0.0, 0.01, 0.0]])  # huge preimage
+    g = _cuda(inp, cuda_device)
+    dx, dth = rsgrad.stn_bwd(g["x"], g["theta"], g["dy"])
+    rdx, rdth = oracle.stn_bwd(*(inp[k].double().numpy() for k in ("x", "theta", "dy")))
+    assert_close(_np(dx), rdx, "grad", "dx")
+    assert_close(_np(dth), rdth, "grad", "dtheta")
+
+
+def test_stn_identity_and_quarter_pixel(cuda_device):
+    N, C, H, W = 2, 3, 32, 48
+    inp = synth.stn_inputs(N, C, H, W, cfg=1, theta_kind="identity")
+    g = _cuda(inp, cuda_device)
+    y = rsgrad.stn_fwd(g["x"], g["theta"])
+    dx, dth = rsgrad.stn_bwd(g["x"], g["theta"], g["dy"])
+    x, th, dy = (inp[k].double().numpy() for k in ("x", "theta", "dy"))
+    assert_close(_np(y), x, "fwd", "identity y = x")
+    assert_close(_np(dx), dy, "grad", "identity dx = dy")
+    # the fp64 coordinates are bit-identical to the oracle's, so even the
+    # kink-sensitive d_theta at identity theta matches it (P1)
+    assert_close(_np(dth), oracle.stn_bwd(x, th, dy)[1], "grad", "identity dtheta")
+    q = torch.tensor([[1.0, 0.0, 0.5 / (W - 1)], [0.0, 1.0, 0.5 / (H - 1)]]).expand(N, 2, 3).contiguous()
+    dxq, dthq = rsgrad.stn_bwd(g["x"], q.to(cuda_device), g["dy"])
+    rq = oracle.stn_bwd(x, q.double().numpy(), dy)
+    assert_close(_np(dxq), rq[0], "grad", "quarter dx")
+    assert_close(_np(dthq), rq[1], "grad", "quarter dtheta")
+
+
+def test_stn_gather_is_deterministic(cuda_device):
+    inp = synth.stn_inputs(2, 16, 64, 64, cfg=1)
+    g = _cuda(inp, cuda_device)
+    a = rsgrad.stn_bwd(g["x"], g["theta"], g["dy"], deterministic=True)
+    b = rsgrad.stn_bwd(g["x"], g["theta"], g["dy"], deterministic=True)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+def test_stn_paper_shape_full(cuda_device):
+    """configs[1]: STN 4 x 16 x 512 x 512, every element vs the oracle."""
+    inp = synth.stn_inputs(4, 16, 512, 512, cfg=2)
+    g = _cuda(inp, cuda_device)
+    y = rsgrad.stn_fwd(g["x"], g["theta"])
+    dx, dth = rsgrad.stn_bwd(g["x"], g["theta"], g["dy"])
+    x, th, dy = (inp[k].double().numpy() for k in ("x", "theta", "dy"))
+    assert_close(_np(y), oracle.stn_fwd(x, th), "fwd", "y")
+    rdx, rdth = oracle.stn_bwd(x, th, dy)
+    assert_close(_np(dx), rdx, "grad", "dx")
+    assert_close(_np(dth), rdth, "grad", "dtheta")
+
+
+# ============================================================================ warp
+@pytest.mark.parametrize("shape", [(1, 3, 16, 16), (2, 3, 37, 61), (1, 7, 5, 130), (1, 1, 1, 1)])
+@pytest.mark.parametrize("flow", ["smooth", "stress", "zero"])
+@pytest.mark.parametrize("padding", ["zeros", "border"])
+def test_warp_parity(cuda_device, shape, flow, padding):
+    N, C, H, W = shape
+    inp = synth.warp_inputs(N, C, H, W, cfg=1, flow=flow)
+    g = _cuda(inp, cuda_device)
+    y = rsgrad.warp_fwd(g["x"], g["flow"], padding=padding)
+    dx, df = rsgrad.warp_bwd(g["x"], g["flow"], g["dy"], padding=padding)
+    x, fl, dy = (inp[k].double().numpy() for k in ("x", "flow", "dy"))
+    border = padding == "border"
+    assert_close(_np(y), oracle.warp_fwd(x, fl, border), "fwd", "y")
+    rdx, rdf = oracle.warp_bwd(x, fl, dy, border)
+    assert_close(_np(dx), rdx, "grad", "dx")
+    assert_close(_np(df), rdf, "grad", "dflow")
+
+
+@pytest.mark.parametrize("flow", ["smooth", "stress"])
+def test_warp_paper_shape_full(cuda_device, flow):
+    """configs[2]: warp 8 x 3 x 384 x 512, every element vs the oracle."""
+    inp = synth.warp_inputs(8, 3, 384, 512, cfg=3, flow=flow)
+    g = _cuda(inp, cuda_device)
+    y = rsgrad.warp_fwd(g["x"], g["flow"])
+    dx, df = rsgrad.warp_bwd(g["x"], g["flow"], g["dy"])
+    x, fl, dy = (inp[k].double().numpy() for k in ("x", "flow", "dy"))
+    assert_close(_np(y), oracle.warp_fwd(x, fl), "fwd", "y")
+    rdx, rdf = oracle.warp_bwd(x, fl, dy)
+    assert_close(_np(dx), rdx, "grad", "dx")
+    assert_close(_np(df), rdf, "grad", "dflow")
+
+
+# ============================================================================ bslice
+BS_SHAPES = [
+    (1, 64, 64, 8, 4, 4),        # tiled path, 16 px cells
+    (2, 100, 130, 8, 6, 7),      # ragged tiles, non-integer cell size
+    (1, 300, 260, 5, 3, 2),      # large dual cells -> sub-tiles
+    (1, 16, 16, 8, 16, 16),      # cells < 8 px -> generic atomic path
+    (1, 9, 11, 3, 1, 1),         # single cell
+    (1, 1, 1, 2, 1, 1),          # single pixel
+]
+
+
+@pytest.mark.parametrize("shape", BS_SHAPES)
+@pytest.mark.parametrize("guide", ["uniform", "wide", "smooth"])
+def test_bslice_parity(cuda_device, shape, guide):
+    N, H, W, D, Gh, Gw = shape
+    inp = synth.bslice_inputs(N, H, W, D, Gh, Gw, cfg=1, grid="iid", guide=guide)
+    g = _cuda(inp, cuda_device)
+    y = rsgrad.bslice_fwd(g["grid"], g["guide"], g["x"])
+    dgr, dgd, dx = rsgrad.bslice_bwd(g["grid"], g["guide"], g["x"], g["dy"])
+    gr, gd, x, dy = (inp[k].double().numpy() for k in ("grid", "guide", "x", "dy"))
+    assert_close(_np(y), oracle.bslice_fwd(gr, gd, x), "fwd", "y")
+    rgr, rgd, rdx = oracle.bslice_bwd(gr, gd, x, dy)
+    assert_close(_np(dx), rdx, "grad", "dx")
+    assert_close(_np(dgd), rgd, "grad", "dguide")
+    assert_close(_np(dgr), rgr, "grad", "dgrid")
+
+
+def test_bslice_atomic_algo_and_determinism(cuda_device):
+    inp = synth.bslice_inputs(2, 128, 96, 8, 8, 6, cfg=1)
+    g = _cuda(inp, cuda_device)
+    a = rsgrad.bslice_bwd(g["grid"], g["guide"], g["x"], g["dy"], deterministic=True)
+    b = rsgrad.bslice_bwd(g["grid"], g["guide"], g["x"], g["dy"], deterministic=True)
+    assert all(torch.equal(p, q) for p, q in zip(a, b))
+    c = rsgrad.bslice_bwd(g["grid"], g["guide"], g["x"], g["dy"], algo="scatter_atomic")
+    gr, gd, x, dy = (inp[k].double().numpy() for k in ("grid", "guide", "x", "dy"))
+    rgr = oracle.bslice_bwd(gr, gd, x, dy)[0]
+    assert_close(_np(c[0]), rgr, "grad", "dgrid atomic")
+
+
+def test_bslice_constant_grid_closed_form(cuda_device):
+    N, H, W, D, Gh, Gw = 2, 128, 128, 8, 8, 8
+    inp = synth.bslice_inputs(N, H, W, D, Gh, Gw, cfg=1)
+    A = torch.randn(N, 12, generator=torch.Generator().manual_seed(3))
+    inp["grid"] = A.view(N, 12, 1, 1, 1).expand(N, 12, D, Gh, Gw).contiguous()
+    g = _cuda(inp, cuda_device)
+    _, dgd, _ = rsgrad.bslice_bwd(g["grid"], g["guide"], g["x"], g["dy"])
+    assert float(dgd.abs().max()) < 1e-5
+
+
+def test_bslice_paper_shape_full(cuda_device):
+    """configs[3]: 4 x 1024^2, grid 16x16x8, every element vs the oracle."""
+    inp = synth.bslice_inputs(4, 1024, 1024, 8, 16, 16, cfg=4)
+    g = _cuda(inp, cuda_device)
+    y = rsgrad.bslice_fwd(g["grid"], g["guide"], g["x"])
+    dgr, dgd, dx = rsgrad.bslice_bwd(g["grid"], g["guide"], g["x"], g["dy"])
+    gr, gd, x, dy = (inp[k].double().numpy() for k in ("grid", "guide", "x", "dy"))
+    assert_close(_np(y), oracle.bslice_fwd(gr, gd, x), "fwd", "y")
+    rgr, rgd, rdx = oracle.bslice_bwd(gr, gd, x, dy)
+    assert_close(_np(dx), rdx, "grad", "dx")
+    assert_close(_np(dgd), rgd, "grad", "dguide")
+    assert_close(_np(dgr), rgr, "grad", "dgrid")
+
+
+def test_bslice_paper_grid_32(cuda_device):
+    """K4': the paper's own 1024^2 shape uses a 32x32x8 grid."""
+    inp = synth.bslice_inputs(1, 1024, 1024, 8, 32, 32, cfg=4)
+    g = _cuda(inp, cuda_device)
+    dgr, dgd, dx = rsgrad.bslice_bwd(g["grid"], g["guide"], g["x"], g["dy"])
+    gr, gd, x, dy = (inp[k].double().numpy() for k in ("grid", "guide", "x", "dy"))
+    rgr, rgd, rdx = oracle.bslice_bwd(gr, gd, x, dy)
+    assert_close(_np(dgr), rgr, "grad", "dgrid")
+    assert_close(_np(dgd), rgd, "grad", "dguide")
+
+
+# ============================================================================ configs[4] sampled
+def test_sweep_config_sampled(cuda_device):
+    """configs[4]: batch 64 @ 1024^2 per layer in the bench launch configuration;
+    samples {0, 41, 63} compared in full with the oracle."""
+    N, H, W = 64, 1024, 1024
+    pick = [0, 41, 63]
+    # STN, C = 16
+    inp = synth.stn_inputs(N, 16, H, W, cfg=5, device=cuda_device)
+    y = rsgrad.stn_fwd(inp["x"], inp["theta"])
+    dx, dth = rsgrad.stn_bwd(inp["x"], inp["theta"], inp["dy"])
+    sub = {k: _np(v[pick]) for k, v in inp.items()}
+    assert_close(_np(y[pick]), oracle.stn_fwd(sub["x"], sub["theta"]), "fwd", "stn y")
+    rdx, rdth = oracle.stn_bwd(sub["x"], sub["theta"], sub["dy"])
+    assert_close(_np(dx[pick]), rdx, "grad", "stn dx")
+    assert_close(_np(dth[pick]), rdth, "grad", "stn dtheta")
+    del inp, y, dx, dth
+    torch.cuda.empty_cache()
+    # warp, C = 3, smooth flow
+    inp = synth.warp_inputs(N, 3, H, W, cfg=5, device=cuda_device)
+    y = rsgrad.warp_fwd(inp["x"], inp["flow"])
+    dx, df = rsgrad.warp_bwd(inp["x"], inp["flow"], inp["dy"])
+    sub = {k: _np(v[pick]) for k, v in inp.items()}
+    assert_close(_np(y[pick]), oracle.warp_fwd(sub["x"], sub["flow"]), "fwd", "warp y")
+    rdx, rdf = oracle.warp_bwd(sub["x"], sub["flow"], sub["dy"])
+    assert_close(_np(dx[pick]), rdx, "grad", "warp dx")
+    assert_close(_np(df[pick]), rdf, "grad", "warp dflow")
+    del inp, y, dx, df
+    torch.cuda.empty_cache()
+    # bslice, grid 16x16x8
+    inp = synth.bslice_inputs(N, H, W, 8, 16, 16, cfg=5, device=cuda_device)
+    y = rsgrad.bslice_fwd(inp["grid"], inp["guide"], inp["x"])
+    dgr, dgd, dx = rsgrad.bslice_bwd(inp["grid"], inp["guide"], inp["x"], inp["dy"])
+    sub = {k: _np(v[pick]) for k, v in inp.items()}
+    assert_close(_np(y[pick]), oracle.bslice_fwd(sub["grid"], sub["guide"], sub["x"]), "fwd", "bs y")
+    rgr, rgd, rdx = oracle.bslice_bwd(sub["grid"], sub["guide"], sub["x"], sub["dy"])
+    assert_close(_np(dx[pick]), rdx, "grad", "bs dx")
+    assert_close(_np(dgd[pick]), rgd, "grad", "bs dguide")
+    assert_close(_np(dgr[pick]), rgr, "grad", "bs dgrid")
+
+
+# ============================================================================ boundary behaviour
+def test_host_pointer_path_matches_device(cuda_device):
+    """CPU (pinned and pageable) tensors go through the library's staging path."""
+    inp = synth.bslice_inputs(1, 64, 80, 8, 4, 5, cfg=1)
+    g = _cuda(inp, cuda_device)
+    ref = rsgrad.bslice_bwd(g["grid"], g["guide"], g["x"], g["dy"], deterministic=True)
+    pinned = {k: v.pin_memory() for k, v in inp.items()}
+    host = rsgrad.bslice_bwd(pinned["grid"], pinned["guide"], pinned["x"], pinned["dy"],
+                             deterministic=True)
+    for a, b in zip(ref, host):
+        assert not b.is_cuda and torch.equal(a.cpu(), b)
+    y_pageable = rsgrad.bslice_fwd(inp["grid"], inp["guide"], inp["x"])
+    assert torch.equal(y_pageable, rsgrad.bslice_fwd(g["grid"], g["guide"], g["x"]).cpu())
+
+
+def test_autograd_wrappers(cuda_device):
+    inp = synth.stn_inputs(2, 3, 24, 24, cfg=1)
+    x = inp["x"].to(cuda_device).requires_grad_()
+    th = inp["theta"].to(cuda_device).requires_grad_()
+    y = rsgrad.SpatialTransformer.apply(x, th)
+    y.backward(inp["dy"].to(cuda_device))
+    rdx, rdth = oracle.stn_bwd(*(inp[k].double().numpy() for k in ("x", "theta", "dy")))
+    assert_close(_np(x.grad), rdx, "grad", "dx")
+    assert_close(_np(th.grad), rdth, "grad", "dtheta")
+
+
+def test_launch_accounting(cuda_device):
+    inp = _cuda(synth.warp_inputs(1, 3, 32, 32, cfg=1), cuda_device)
+    rsgrad.launch_count(reset=True)
+    rsgrad.warp_fwd(inp["x"], inp["flow"])
+    rsgrad.warp_bwd(inp["x"], inp["flow"], inp["dy"])
+    assert rsgrad.launch_count() == 2
+
+
+def test_outputs_overwritten_not_accumulated(cuda_device):
+    inp = _cuda(synth.stn_inputs(1, 4, 32, 32, cfg=1), cuda_device)
+    dx = torch.full_like(inp["x"], 7.0)
+    dth = torch.full((1, 2, 3), 7.0, device=cuda_device)
+    rsgrad.stn_bwd(inp["x"], inp["theta"], inp["dy"], out=(dx, dth))
+    ref = rsgrad.stn_bwd(inp["x"], inp["theta"], inp["dy"])
+    assert torch.equal(dx, ref[0]) and torch.equal(dth, ref[1])
