@@ -141,7 +141,13 @@ def barrier(world):
 
 
 def max_over_ranks(world, vals):
-    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    """Element-wise MAX over ranks (timings are reported as the slowest rank)."""
+    dev = "cpu"
+    if world > 1:
+        import torch.distributed as dist
+
+        dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor(vals, dtype=torch.float64, device=dev)
     if world > 1:
         import torch.distributed as dist
 

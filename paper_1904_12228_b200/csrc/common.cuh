@@ -104,6 +104,73 @@ RS_DEV void stg_stream(float *p, float v) {
     asm volatile("st.global.L1::no_allocate.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 
+// ----------------------------------------------------------------- cp.async (LDGSTS) staging
+RS_DEV unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+RS_DEV void cp_async16(void *s, const void *g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+RS_DEV void cp_async4(void *s, const void *g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+RS_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+RS_DEV void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Compact row layout of a staged footprint: row r holds columns [xa[r], xa[r]+cnt[r])
+// of source row (ybase + r) at smem offset off[r] (16-B aligned when VEC).
+// Built by warp 0 from inclusive column ranges [lo[r], hi[r]] (lo > hi: empty row).
+template <bool VEC>
+RS_DEV void build_rows(int R, int Wlim, const int *lo, const int *hi, int *xa, int *off, int *cnt,
+                       int *Fout) {
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    int run = 0;
+    for (int base = 0; base < R; base += 32) {
+        const int r = base + lane;
+        int width = 0, a0 = 0, n = 0;
+        if (r < R && lo[r] <= hi[r]) {
+            a0 = VEC ? (lo[r] & ~3) : lo[r];
+            const int e = VEC ? min(Wlim, (hi[r] + 4) & ~3) : hi[r] + 1;
+            n = e - a0;
+            width = (n + 3) & ~3;
+        }
+        int v = width;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += t;
+        }
+        if (r < R) {
+            xa[r] = a0;
+            cnt[r] = n;
+            off[r] = run + v - width;
+        }
+        run += __shfl_sync(0xffffffffu, v, 31);
+    }
+    if (lane == 0) *Fout = run;
+}
+
+// Issue cp.async copies of nch channel planes' rows (channel stride cstride floats)
+// into dst + c*F + off[r].  Warp per (channel, row), lanes over 16-B (or 4-B) words.
+template <bool VEC>
+RS_DEV void stage_rows(float *dst, int F, const float *base, long long cstride, int nch, int R,
+                       int W, int ybase, const int *xa, const int *off, const int *cnt) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int p = warp; p < nch * R; p += nw) {
+        const int c = p / R, r = p - c * R;
+        const int w = cnt[r];
+        const float *src = base + c * cstride + (long long)(ybase + r) * W + xa[r];
+        float *d = dst + c * F + off[r];
+        if (VEC) {
+            for (int q = lane * 4; q < w; q += 128) cp_async16(d + q, src + q);
+        } else {
+            for (int q = lane; q < w; q += 32) cp_async4(d + q, src + q);
+        }
+    }
+}
+
 }  // namespace rs
 
 // ----------------------------------------------------------------- launchers (internal ABI)
