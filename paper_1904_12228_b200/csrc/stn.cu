@@ -2,27 +2,60 @@
 // adjoint, sm_100a.  PAPER.md:21-28 (layer), PAPER.md:700-733 (scatter-to-gather
 // conversion vs atomics), PAPER.md:838-840 (reductions: partial + serial).
 //
-// Kernels
-//   stn_fwd_kernel          one thread per output pixel, all channels; the
-//                           sampling grid is never materialised (K1).
-//   stn_tables_kernel       xt[Wo], yt[Ho] in fp64 (exact, shared by the bwd).
-//   stn_dtheta_kernel       per output pixel d_ix/d_iy over channels, then the
-//                           6 theta terms reduced warp -> block (fp32) -> fp64
-//                           per-block partials (rfactor-style).
-//   stn_dtheta_finalize     per-sample fixed-order fp64 sum of the partials.
-//   stn_dx_gather_kernel    scatter-to-gather by affine inversion: each input
-//                           pixel walks the bounding box of its preimage in
-//                           output space and re-derives which outputs sample
-//                           it; deterministic, no memset.
-//   stn_dx_scatter_kernel   atomic scatter fallback: border
-//                           padding, near-singular theta, or forced.
+// Forward / d_theta (output tiles, stn_out_tile):
+//   A block owns a 32x16 tile of OUTPUT pixels.  It computes every pixel's exact
+//   fp64 sample coordinate, derives the exact set of input taps the tile reads
+//   (per input row: [min x, max x] via shared-memory integer atomics), stages those
+//   row segments — the tile's footprint, a parallelogram, ~1.1x the useful bytes —
+//   into shared memory with cp.async, CH channels per stage, double-buffered, and
+//   gathers the bilinear taps from shared memory.  Global loads are coalesced row
+//   segments; the sampling grid is never materialised.
+//
+// Backward (input tiles, stn_bwd_cell):  "owner computes per floor cell".
+//   An output pixel q with floor cell (x0, y0) feeds exactly the four input pixels
+//   (x0..x0+1, y0..y0+1).  A block owns a 31x32 tile of input pixels; lane k of
+//   warp w owns floor-cell column x0 = xa0-1+k and walks the warp's 4 cell rows.
+//   The block stages dY over the exact preimage of its cells (compact rows, per
+//   output row i a j-interval from the inverse affine map) plus one 8-byte record
+//   per staged output pixel (its exact floor cell and fractions).  For its cell,
+//   a lane finds the (~1/det) output pixels whose floor cell it is, reads each dY
+//   ONCE per channel and distributes w*dY to its four input pixels in registers;
+//   the right neighbour's share arrives by one shuffle and the lower row's share
+//   is carried to the next cell row (or across warps through shared memory).
+//   This is the scatter-to-gather conversion of PAPER.md:700-731 applied at cell
+//   granularity: deterministic, no atomics, no memset.  d_theta is accumulated in
+//   the same pass for the cells the tile owns: d_ix = sum_c dY (1-fy)(V01-V00) +
+//   fy(V11-V10) from coalesced X loads, times [xt, yt, 1] — warp -> block in fp32,
+//   fp64 per-block partials, fixed-order finalize (rfactor).
+//
+// Fallbacks (decided on the device per sample, no host sync): a sample whose
+// affine map is singular or whose preimage exceeds the staging budget takes
+// d_theta from stn_out_tile (MODE_DTHETA) and d_input from the atomic scatter
+// (PAPER.md:733); border padding (no bounded inverse) always does.
 #include "common.cuh"
 
 namespace rs {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kMaxGatherCand = 256;  // preimage bbox budget per input pixel
+
+// forward tiles
+constexpr int kFJ = 32, kFI = 16;         // output tile (px)
+constexpr int kFRMax = 128;               // max staged input rows
+constexpr int kFStage = 6144;             // floats per pipeline stage
+
+// backward tiles
+constexpr int kBX = 31;                   // input px per warp row (32 cell columns)
+constexpr int kBRows = 4;                 // px rows per warp
+constexpr int kBWarps = 8;
+constexpr int kBTY = kBRows * kBWarps;    // 32 px rows per block
+constexpr int kBRQMax = 160;              // max staged output rows
+constexpr int kBFQMax = 2304;             // max staged output px (records)
+constexpr int kBStage = 4096;             // floats per pipeline stage
+constexpr int kBCH = 4;                   // max channels per stage (registers)
+constexpr int kBHits = 4;                 // cached hits per cell
+
+constexpr int MODE_FWD = 0, MODE_DTHETA = 1;
 
 struct Theta {
     double t[6];
@@ -35,172 +68,612 @@ RS_DEV Theta load_theta(const float *theta, int n) {
     return T;
 }
 
-// Sample coordinate of output (i, j) given its normalised coords.
+// Exact sample coordinate of output (i, j) from its normalised coords (R1, P1).
 RS_DEV void stn_coord(const Theta &T, double xt, double yt, int H, int W, int ac, double &ix,
                       double &iy) {
     ix = stn_unnorm(affine3(T.t[0], T.t[1], T.t[2], xt, yt), W, ac);
     iy = stn_unnorm(affine3(T.t[3], T.t[4], T.t[5], xt, yt), H, ac);
 }
 
-// Affine map q=(j,i) -> p=(ix,iy) in real arithmetic (for the preimage bbox
-// only; membership is always re-decided with the exact fp64 coordinate).
-struct AffineInv {
-    double m00, m01, m10, m11;  // inverse of d p / d q
+// Real-arithmetic affine map q = (j, i) -> p = (ix, iy) and its inverse; used only
+// to bound footprints (membership is always decided with the exact coordinate).
+struct Affine {
+    double m00, m01, m10, m11;  // d p / d q
+    double i00, i01, i10, i11;  // inverse
     double p0x, p0y;            // p at q = 0
-    double hj, hi;              // half extents of the preimage of a 2x2 px square
-    bool ok;
+    double det;
+    bool inv;
 };
 
-RS_DEV AffineInv stn_inverse(const Theta &T, int H, int W, int Ho, int Wo, int ac) {
-    double ax = ac ? 2.0 / (Wo - 1) : 2.0 / Wo, bx = ac ? -1.0 : 1.0 / Wo - 1.0;
-    double ay = ac ? 2.0 / (Ho - 1) : 2.0 / Ho, by = ac ? -1.0 : 1.0 / Ho - 1.0;
-    double sx = ac ? 0.5 * (W - 1) : 0.5 * W, ox = ac ? 0.0 : -0.5;
-    double sy = ac ? 0.5 * (H - 1) : 0.5 * H, oy = ac ? 0.0 : -0.5;
-    double a00 = sx * T.t[0] * ax, a01 = sx * T.t[1] * ay;
-    double a10 = sy * T.t[3] * ax, a11 = sy * T.t[4] * ay;
-    AffineInv r;
-    r.p0x = sx * (T.t[0] * bx + T.t[1] * by + T.t[2] + 1.0) + ox;
-    r.p0y = sy * (T.t[3] * bx + T.t[4] * by + T.t[5] + 1.0) + oy;
-    double det = a00 * a11 - a01 * a10;
-    double scale = fabs(a00 * a11) + fabs(a01 * a10);
-    r.ok = isfinite(det) && fabs(det) > 1e-9 * (scale > 0 ? scale : 1.0) && fabs(det) > 1e-12;
-    if (!r.ok) {
-        r.m00 = r.m01 = r.m10 = r.m11 = r.hj = r.hi = 0.0;
-        return r;
-    }
-    double id = 1.0 / det;
-    r.m00 = a11 * id;
-    r.m01 = -a01 * id;
-    r.m10 = -a10 * id;
-    r.m11 = a00 * id;
-    r.hj = fabs(r.m00) + fabs(r.m01);
-    r.hi = fabs(r.m10) + fabs(r.m11);
-    double cand = (2.0 * r.hj + 2.0) * (2.0 * r.hi + 2.0);
-    if (!(cand <= (double)kMaxGatherCand)) r.ok = false;
-    return r;
+RS_DEV Affine stn_affine(const Theta &T, int H, int W, int Ho, int Wo, int ac) {
+    const double ax = ac ? 2.0 / (Wo - 1) : 2.0 / Wo, bx = ac ? -1.0 : 1.0 / Wo - 1.0;
+    const double ay = ac ? 2.0 / (Ho - 1) : 2.0 / Ho, by = ac ? -1.0 : 1.0 / Ho - 1.0;
+    const double sx = ac ? 0.5 * (W - 1) : 0.5 * W, ox = ac ? 0.0 : -0.5;
+    const double sy = ac ? 0.5 * (H - 1) : 0.5 * H, oy = ac ? 0.0 : -0.5;
+    Affine A;
+    A.m00 = sx * T.t[0] * ax;
+    A.m01 = sx * T.t[1] * ay;
+    A.m10 = sy * T.t[3] * ax;
+    A.m11 = sy * T.t[4] * ay;
+    A.p0x = sx * (T.t[0] * bx + T.t[1] * by + T.t[2] + 1.0) + ox;
+    A.p0y = sy * (T.t[3] * bx + T.t[4] * by + T.t[5] + 1.0) + oy;
+    A.det = A.m00 * A.m11 - A.m01 * A.m10;
+    const double scale = fabs(A.m00 * A.m11) + fabs(A.m01 * A.m10);
+    A.inv = isfinite(A.det) && fabs(A.det) > 1e-9 * (scale > 0 ? scale : 1.0) && fabs(A.det) > 1e-12;
+    const double id = A.inv ? 1.0 / A.det : 0.0;
+    A.i00 = A.m11 * id;
+    A.i01 = -A.m01 * id;
+    A.i10 = -A.m10 * id;
+    A.i11 = A.m00 * id;
+    return A;
 }
 
-// ----------------------------------------------------------------- forward
-__global__ void __launch_bounds__(kThreads) stn_fwd_kernel(StnArgs a) {
-    const long long P = (long long)a.Ho * a.Wo;
-    const long long idx = (long long)blockIdx.x * kThreads + threadIdx.x;
-    if (idx >= (long long)a.N * P) return;
-    const int n = (int)(idx / P);
-    const long long rem = idx - (long long)n * P;
-    const int i = (int)(rem / a.Wo), j = (int)(rem - (long long)i * a.Wo);
-    const Theta T = load_theta(a.theta, n);
-    double ix, iy;
-    stn_coord(T, stn_norm(j, a.Wo, a.ac), stn_norm(i, a.Ho, a.ac), a.H, a.W, a.ac, ix, iy);
-    if (a.border) {
-        float d;
-        ix = clamp_coord(ix, a.W, d);
-        iy = clamp_coord(iy, a.H, d);
-    }
-    const Cell cx = cell_of(ix), cy = cell_of(iy);
-    const bool x0ok = cx.i0 >= 0 && cx.i0 < a.W, x1ok = cx.i0 + 1 >= 0 && cx.i0 + 1 < a.W;
-    const bool y0ok = cy.i0 >= 0 && cy.i0 < a.H, y1ok = cy.i0 + 1 >= 0 && cy.i0 + 1 < a.H;
-    const float wx0 = 1.f - cx.f, wx1 = cx.f, wy0 = 1.f - cy.f, wy1 = cy.f;
-    const float w00 = wy0 * wx0, w01 = wy0 * wx1, w10 = wy1 * wx0, w11 = wy1 * wx1;
-    const long long HW = (long long)a.H * a.W;
-    const long long o00 = (long long)cy.i0 * a.W + cx.i0;
-    const bool k00 = y0ok && x0ok, k01 = y0ok && x1ok, k10 = y1ok && x0ok, k11 = y1ok && x1ok;
-    const float *xp = a.x + (long long)n * a.C * HW;
-    float *yp = a.y + (long long)n * a.C * P + rem;
+// Can the sample take the cell-owner gather (zeros padding only)?  Bounds the
+// staged preimage of a block's 32 x 33 cells: rows and records must fit.
+RS_DEV bool stn_gatherable(const Affine &A, int Ho, int Wo) {
+    if (!A.inv || Ho > 65535 || Wo > 65535) return false;
+    const double hq = fabs(A.i10) * (kBX + 1) + fabs(A.i11) * (kBTY + 1);
+    const double rq = ceil(hq) + 3.0;
+    const double fq = (double)(kBX + 1) * (kBTY + 1) / fabs(A.det) + 8.0 * rq + 64.0;
+    // the per-cell candidate window stays small (hits are cached per cell)
+    const double wj = fabs(A.i00) + fabs(A.i01), wi = fabs(A.i10) + fabs(A.i11);
+    return rq <= kBRQMax && fq <= kBFQMax && (wj + 2.0) * (wi + 2.0) <= 16.0;
+}
+
+// ----------------------------------------------------------------- output-tile kernel
+// MODE_FWD: y.  MODE_DTHETA: per-tile fp64 partials of d_theta (6 per tile).
+// fb_list (optional): loop over the listed samples instead of blockIdx.y.
+template <int MODE, bool VEC>
+__global__ void __launch_bounds__(kThreads, 3)
+    stn_out_tile(StnArgs a, const double *__restrict__ xtab, const double *__restrict__ ytab,
+                 const int *__restrict__ fb_list, const int *__restrict__ fb_count,
+                 double *__restrict__ partials, int tiles_j, int tiles_i) {
+    extern __shared__ __align__(16) float4 sm4[];
+    int *rlo = (int *)sm4;
+    int *rhi = rlo + kFRMax;
+    int *rxa = rhi + kFRMax;
+    int *roff = rxa + kFRMax;
+    int *rcnt = roff + kFRMax;
+    int *ctl = rcnt + kFRMax;                // 16 ints
+    float *stage = (float *)(ctl + 16);      // 2 * kFStage (16-B aligned: 656 ints)
+    __shared__ float red[kThreads / 32][6];
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tj = blockIdx.x % tiles_j, ti = blockIdx.x / tiles_j;
+    const long long HW = (long long)a.H * a.W, P = (long long)a.Ho * a.Wo;
+    const int nloop = fb_list ? *fb_count : 1;
+    for (int f = 0; f < nloop; f++) {
+        const int n = fb_list ? fb_list[f] : blockIdx.y;
+        const Theta T = load_theta(a.theta, n);
+        int x0[2], y0[2];
+        float fx[2], fy[2], cgx[2], cgy[2], xtf[2], ytf[2];
+        bool in[2], xv0[2], xv1[2], yv0[2], yv1[2];
+        int ymin = INT_MAX, ymax = INT_MIN;
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+            const int i = ti * kFI + warp + 8 * k, j = tj * kFJ + lane;
+            in[k] = i < a.Ho && j < a.Wo;
+            x0[k] = y0[k] = 0;
+            fx[k] = fy[k] = 0.f;
+            cgx[k] = cgy[k] = 1.f;
+            xtf[k] = ytf[k] = 0.f;
+            xv0[k] = xv1[k] = yv0[k] = yv1[k] = false;
+            if (in[k]) {
+                const double xt = MODE == MODE_DTHETA ? xtab[j] : stn_norm(j, a.Wo, a.ac);
+                const double yt = MODE == MODE_DTHETA ? ytab[i] : stn_norm(i, a.Ho, a.ac);
+                xtf[k] = (float)xt;
+                ytf[k] = (float)yt;
+                double ix, iy;
+                stn_coord(T, xt, yt, a.H, a.W, a.ac, ix, iy);
+                if (a.border) {
+                    ix = clamp_coord(ix, a.W, cgx[k]);
+                    iy = clamp_coord(iy, a.H, cgy[k]);
+                }
+                const Cell cx = cell_of(ix), cy = cell_of(iy);
+                x0[k] = cx.i0;
+                y0[k] = cy.i0;
+                fx[k] = cx.f;
+                fy[k] = cy.f;
+                xv0[k] = cx.i0 >= 0 && cx.i0 < a.W;
+                xv1[k] = cx.i0 + 1 >= 0 && cx.i0 + 1 < a.W;
+                yv0[k] = cy.i0 >= 0 && cy.i0 < a.H;
+                yv1[k] = cy.i0 + 1 >= 0 && cy.i0 + 1 < a.H;
+                if (xv0[k] || xv1[k]) {
+                    if (yv0[k]) { ymin = min(ymin, y0[k]); ymax = max(ymax, y0[k]); }
+                    if (yv1[k]) { ymin = min(ymin, y0[k] + 1); ymax = max(ymax, y0[k] + 1); }
+                }
+            }
+        }
+        if (threadIdx.x == 0) {
+            ctl[0] = INT_MAX;
+            ctl[1] = INT_MIN;
+        }
+        for (int r = threadIdx.x; r < kFRMax; r += kThreads) {
+            rlo[r] = INT_MAX;
+            rhi[r] = INT_MIN;
+        }
+        __syncthreads();
+        ymin = __reduce_min_sync(0xffffffffu, ymin);
+        ymax = __reduce_max_sync(0xffffffffu, ymax);
+        if (lane == 0) {
+            atomicMin(&ctl[0], ymin);
+            atomicMax(&ctl[1], ymax);
+        }
+        __syncthreads();
+        const int ylo = ctl[0];
+        const int R = ctl[1] >= ylo ? ctl[1] - ylo + 1 : 0;
+        bool fallback = R > kFRMax;
+        if (!fallback) {
+#pragma unroll
+            for (int k = 0; k < 2; k++) {
+                if (!(in[k] && (xv0[k] || xv1[k]))) continue;
+                const int xl = xv0[k] ? x0[k] : x0[k] + 1, xh = xv1[k] ? x0[k] + 1 : x0[k];
+                if (yv0[k]) { atomicMin(&rlo[y0[k] - ylo], xl); atomicMax(&rhi[y0[k] - ylo], xh); }
+                if (yv1[k]) { atomicMin(&rlo[y0[k] + 1 - ylo], xl); atomicMax(&rhi[y0[k] + 1 - ylo], xh); }
+            }
+        }
+        __syncthreads();
+        if (!fallback) build_rows<VEC>(R, a.W, rlo, rhi, rxa, roff, rcnt, &ctl[2]);
+        __syncthreads();
+        const int F = fallback ? 0 : ctl[2];
+        fallback = fallback || F > kFStage;
+
+        float dix[2] = {0.f, 0.f}, diy[2] = {0.f, 0.f};
+        const float *xbase = a.x + (long long)n * a.C * HW;
+        if (fallback) {
+            // direct global gathers (rare: strongly zoomed-out tiles)
+#pragma unroll
+            for (int k = 0; k < 2; k++) {
+                if (!in[k]) continue;
+                const int i = ti * kFI + warp + 8 * k, j = tj * kFJ + lane;
+                const long long o00 = (long long)y0[k] * a.W + x0[k];
+                const float w00 = (1.f - fy[k]) * (1.f - fx[k]), w01 = (1.f - fy[k]) * fx[k];
+                const float w10 = fy[k] * (1.f - fx[k]), w11 = fy[k] * fx[k];
+                for (int c = 0; c < a.C; c++) {
+                    const float *p = xbase + (long long)c * HW + o00;
+                    const float v00 = (yv0[k] && xv0[k]) ? __ldg(p) : 0.f;
+                    const float v01 = (yv0[k] && xv1[k]) ? __ldg(p + 1) : 0.f;
+                    const float v10 = (yv1[k] && xv0[k]) ? __ldg(p + a.W) : 0.f;
+                    const float v11 = (yv1[k] && xv1[k]) ? __ldg(p + a.W + 1) : 0.f;
+                    const long long oo = ((long long)n * a.C + c) * P + (long long)i * a.Wo + j;
+                    if (MODE == MODE_FWD) {
+                        a.y[oo] = fmaf(w00, v00, fmaf(w01, v01, fmaf(w10, v10, w11 * v11)));
+                    } else {
+                        const float g = ldg_stream(a.dy + oo);
+                        dix[k] = fmaf(g, fmaf(1.f - fy[k], v01 - v00, fy[k] * (v11 - v10)), dix[k]);
+                        diy[k] = fmaf(g, fmaf(1.f - fx[k], v10 - v00, fx[k] * (v11 - v01)), diy[k]);
+                    }
+                }
+            }
+        } else {
+            int s0[2], s1[2];
+#pragma unroll
+            for (int k = 0; k < 2; k++) {
+                s0[k] = (in[k] && yv0[k]) ? roff[y0[k] - ylo] + (x0[k] - rxa[y0[k] - ylo]) : 0;
+                s1[k] = (in[k] && yv1[k]) ? roff[y0[k] + 1 - ylo] + (x0[k] - rxa[y0[k] + 1 - ylo]) : 0;
+            }
+            const int CH = min(a.C, F > 0 ? kFStage / F : a.C);
+            const int nch = (a.C + CH - 1) / CH;
+            if (F > 0) stage_rows<VEC>(stage, F, xbase, HW, min(CH, a.C), R, a.W, ylo, rxa, roff, rcnt);
+            cp_async_commit();
+            for (int kc = 0; kc < nch; kc++) {
+                const int c0 = kc * CH, cn = min(CH, a.C - c0);
+                if (kc + 1 < nch) {
+                    if (F > 0)
+                        stage_rows<VEC>(stage + ((kc + 1) & 1) * kFStage, F, xbase + (long long)(c0 + CH) * HW,
+                                        HW, min(CH, a.C - c0 - CH), R, a.W, ylo, rxa, roff, rcnt);
+                    cp_async_commit();
+                    cp_async_wait<1>();
+                } else {
+                    cp_async_wait<0>();
+                }
+                __syncthreads();
+                const float *S = stage + (kc & 1) * kFStage;
+#pragma unroll
+                for (int k = 0; k < 2; k++) {
+                    if (!in[k]) continue;
+                    const int i = ti * kFI + warp + 8 * k, j = tj * kFJ + lane;
+                    const bool k00 = yv0[k] && xv0[k], k01 = yv0[k] && xv1[k];
+                    const bool k10 = yv1[k] && xv0[k], k11 = yv1[k] && xv1[k];
+                    const float w00 = (1.f - fy[k]) * (1.f - fx[k]), w01 = (1.f - fy[k]) * fx[k];
+                    const float w10 = fy[k] * (1.f - fx[k]), w11 = fy[k] * fx[k];
+                    const long long ob = ((long long)n * a.C + c0) * P + (long long)i * a.Wo + j;
 #pragma unroll 4
-    for (int c = 0; c < a.C; c++) {
-        const float *p = xp + (long long)c * HW + o00;
-        float v = 0.f;
-        if (k00) v = fmaf(w00, __ldg(p), v);
-        if (k01) v = fmaf(w01, __ldg(p + 1), v);
-        if (k10) v = fmaf(w10, __ldg(p + a.W), v);
-        if (k11) v = fmaf(w11, __ldg(p + a.W + 1), v);
-        yp[(long long)c * P] = v;
+                    for (int c = 0; c < cn; c++) {
+                        const float *Sc = S + c * F;
+                        const float v00 = k00 ? Sc[s0[k]] : 0.f, v01 = k01 ? Sc[s0[k] + 1] : 0.f;
+                        const float v10 = k10 ? Sc[s1[k]] : 0.f, v11 = k11 ? Sc[s1[k] + 1] : 0.f;
+                        if (MODE == MODE_FWD) {
+                            a.y[ob + c * P] = fmaf(w00, v00, fmaf(w01, v01, fmaf(w10, v10, w11 * v11)));
+                        } else {
+                            const float g = ldg_stream(a.dy + ob + c * P);
+                            dix[k] = fmaf(g, fmaf(1.f - fy[k], v01 - v00, fy[k] * (v11 - v10)), dix[k]);
+                            diy[k] = fmaf(g, fmaf(1.f - fx[k], v10 - v00, fx[k] * (v11 - v01)), diy[k]);
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        if (MODE == MODE_DTHETA) {
+            const float sx = a.ac ? 0.5f * (a.W - 1) : 0.5f * a.W;
+            const float sy = a.ac ? 0.5f * (a.H - 1) : 0.5f * a.H;
+            float acc[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int k = 0; k < 2; k++) {
+                if (!in[k]) continue;
+                const float dgx = dix[k] * sx * cgx[k], dgy = diy[k] * sy * cgy[k];
+                acc[0] = fmaf(dgx, xtf[k], acc[0]);
+                acc[1] = fmaf(dgx, ytf[k], acc[1]);
+                acc[2] += dgx;
+                acc[3] = fmaf(dgy, xtf[k], acc[3]);
+                acc[4] = fmaf(dgy, ytf[k], acc[4]);
+                acc[5] += dgy;
+            }
+#pragma unroll
+            for (int k = 0; k < 6; k++) {
+                const float v = warp_sum(acc[k]);
+                if (lane == 0) red[warp][k] = v;
+            }
+            __syncthreads();
+            if (threadIdx.x < 6) {
+                double s = 0.0;
+                for (int w = 0; w < kThreads / 32; w++) s += (double)red[w][threadIdx.x];
+                partials[((long long)n * tiles_j * tiles_i + blockIdx.x) * 6 + threadIdx.x] = s;
+            }
+        }
+        __syncthreads();
     }
 }
 
-// ----------------------------------------------------------------- backward: tables
+// ----------------------------------------------------------------- backward: tables + classify
 __global__ void stn_tables_kernel(double *xt, double *yt, int Ho, int Wo, int ac) {
-    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t < Wo) xt[t] = stn_norm(t, Wo, ac);
     if (t < Ho) yt[t] = stn_norm(t, Ho, ac);
 }
 
-// ----------------------------------------------------------------- backward: d_theta
-__global__ void __launch_bounds__(kThreads)
-    stn_dtheta_kernel(StnArgs a, const double *__restrict__ xtab, const double *__restrict__ ytab,
-                      double *__restrict__ partials, int bps) {
-    const int n = blockIdx.y;
-    const long long P = (long long)a.Ho * a.Wo;
-    const long long HW = (long long)a.H * a.W;
-    const Theta T = load_theta(a.theta, n);
-    const float sx = a.ac ? 0.5f * (a.W - 1) : 0.5f * a.W;
-    const float sy = a.ac ? 0.5f * (a.H - 1) : 0.5f * a.H;
-    const float *xp = a.x + (long long)n * a.C * HW;
-    const float *gp = a.dy + (long long)n * a.C * P;
-    float acc[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (long long p = (long long)blockIdx.x * kThreads + threadIdx.x; p < P;
-         p += (long long)bps * kThreads) {
-        const int i = (int)(p / a.Wo), j = (int)(p - (long long)i * a.Wo);
-        const double xt = xtab[j], yt = ytab[i];
-        double ix, iy;
-        stn_coord(T, xt, yt, a.H, a.W, a.ac, ix, iy);
-        float cgx = 1.f, cgy = 1.f;
-        if (a.border) {
-            ix = clamp_coord(ix, a.W, cgx);
-            iy = clamp_coord(iy, a.H, cgy);
-        }
-        const Cell cx = cell_of(ix), cy = cell_of(iy);
-        const bool x0ok = cx.i0 >= 0 && cx.i0 < a.W, x1ok = cx.i0 + 1 >= 0 && cx.i0 + 1 < a.W;
-        const bool y0ok = cy.i0 >= 0 && cy.i0 < a.H, y1ok = cy.i0 + 1 >= 0 && cy.i0 + 1 < a.H;
-        const bool k00 = y0ok && x0ok, k01 = y0ok && x1ok, k10 = y1ok && x0ok, k11 = y1ok && x1ok;
-        const long long o00 = (long long)cy.i0 * a.W + cx.i0;
-        const float fx = cx.f, fy = cy.f;
-        float dix = 0.f, diy = 0.f;
-#pragma unroll 4
-        for (int c = 0; c < a.C; c++) {
-            const float *q = xp + (long long)c * HW + o00;
-            const float g = ldg_stream(gp + (long long)c * P + p);
-            const float v00 = k00 ? __ldg(q) : 0.f, v01 = k01 ? __ldg(q + 1) : 0.f;
-            const float v10 = k10 ? __ldg(q + a.W) : 0.f, v11 = k11 ? __ldg(q + a.W + 1) : 0.f;
-            dix = fmaf(g, fmaf(1.f - fy, v01 - v00, fy * (v11 - v10)), dix);
-            diy = fmaf(g, fmaf(1.f - fx, v10 - v00, fx * (v11 - v01)), diy);
-        }
-        const float dgx = dix * sx * cgx, dgy = diy * sy * cgy;
-        const float fxt = (float)xt, fyt = (float)yt;
-        acc[0] = fmaf(dgx, fxt, acc[0]);
-        acc[1] = fmaf(dgx, fyt, acc[1]);
-        acc[2] += dgx;
-        acc[3] = fmaf(dgy, fxt, acc[3]);
-        acc[4] = fmaf(dgy, fyt, acc[4]);
-        acc[5] += dgy;
+// flags[n] = 1 if sample n takes the cell-owner gather; fb_list = the others.
+__global__ void stn_classify_kernel(StnArgs a, int allow_gather, int *flags, int *fb_list,
+                                    int *fb_count) {
+    __shared__ int cnt;
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    for (int n = threadIdx.x; n < a.N; n += blockDim.x) {
+        const Theta T = load_theta(a.theta, n);
+        const bool g = allow_gather && !a.border &&
+                       stn_gatherable(stn_affine(T, a.H, a.W, a.Ho, a.Wo, a.ac), a.Ho, a.Wo);
+        flags[n] = g ? 1 : 0;
+        if (!g) fb_list[atomicAdd(&cnt, 1)] = n;
     }
-    __shared__ float red[kThreads / 32][6];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (threadIdx.x == 0) *fb_count = cnt;
+}
+
+// ----------------------------------------------------------------- backward: cell-owner gather
+RS_DEV uint2 pack_rec(int cx, int cy, float fx, float fy) {
+    unsigned ux = (unsigned)(fx * 16777216.0f + 0.5f), uy = (unsigned)(fy * 16777216.0f + 0.5f);
+    ux = ux > 0xffffffu ? 0xffffffu : ux;
+    uy = uy > 0xffffffu ? 0xffffffu : uy;
+    return make_uint2(((unsigned)cx << 24) | ux, ((unsigned)cy << 24) | uy);
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads, 2)
+    stn_bwd_cell(StnArgs a, const double *__restrict__ xtab, const double *__restrict__ ytab,
+                 const int *__restrict__ flags, double *__restrict__ partials, int tiles_x,
+                 int tiles_y) {
+    extern __shared__ __align__(16) float4 sm4[];
+    float *stage = (float *)sm4;                               // 2 * kBStage
+    uint2 *rec = (uint2 *)(stage + 2 * kBStage);               // kBFQMax
+    unsigned *ijs = (unsigned *)(rec + kBFQMax);               // kBFQMax
+    int4 *rowt = (int4 *)(ijs + kBFQMax);                      // kBRQMax {lo, hi, off - xa, -}
+    int *qlo = (int *)(rowt + kBRQMax);
+    int *qhi = qlo + kBRQMax;
+    int *qxa = qhi + kBRQMax;
+    int *qoff = qxa + kBRQMax;
+    int *qcnt = qoff + kBRQMax;
+    int *ctl = qcnt + kBRQMax;                                  // 8
+    float *carry = (float *)(ctl + 8);                          // kBWarps * 2 * kBCH * 32
+    __shared__ float red[kBWarps][6];
+
+    const int n = blockIdx.y;
+    const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
+    const int xa0 = tx * kBX, yb0 = ty * kBTY;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long HW = (long long)a.H * a.W, P = (long long)a.Ho * a.Wo;
+    const int px = xa0 - 1 + lane;  // this lane's cell column == the px column it finalises
+    float *dxn = a.dx ? a.dx + (long long)n * a.C * HW : nullptr;
+    double *part = partials + ((long long)n * tiles_x * tiles_y + blockIdx.x) * 6;
+
+    if (!flags[n]) {  // fallback sample: zero this tile's dx (atomic scatter adds later)
+        if (dxn && lane >= 1 && px < a.W)
+            for (int r = warp; r < kBTY; r += kBWarps) {
+                const int y = yb0 + r;
+                if (y < a.H)
+                    for (int c = 0; c < a.C; c++) dxn[(long long)c * HW + (long long)y * a.W + px] = 0.f;
+            }
+        if (threadIdx.x < 6) part[threadIdx.x] = 0.0;
+        return;
+    }
+    const Theta T = load_theta(a.theta, n);
+    const Affine A = stn_affine(T, a.H, a.W, a.Ho, a.Wo, a.ac);
+
+    // ---- preimage rows of the cells [xa0-1, xa0+kBX-1] x [yb0-1, yb0+kBTY-1]
+    const double eps = 1e-3;
+    const double Lx = xa0 - 1 - eps, Ux = xa0 + kBX + eps;
+    const double Ly = yb0 - 1 - eps, Uy = yb0 + kBTY + eps;
+    double imin = 1e300, imax = -1e300;
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+        const double px_ = (c & 1) ? Ux : Lx, py_ = (c & 2) ? Uy : Ly;
+        const double qi = A.i10 * (px_ - A.p0x) + A.i11 * (py_ - A.p0y);
+        imin = fmin(imin, qi);
+        imax = fmax(imax, qi);
+    }
+    const int ilo = max(0, (int)ceil(fmax(imin, -1e9)));
+    const int ihi = min(a.Ho - 1, (int)floor(fmin(imax, 1e9)));
+    const int RQ = min(kBRQMax, max(0, ihi - ilo + 1));
+    for (int r = threadIdx.x; r < RQ; r += kThreads) {
+        const int i = ilo + r;
+        double jl = -1e300, jh = 1e300;
+        // strip constraints  L <= m_0 j + m_1 i + p0 <= U  for x and y
+        const double ax_[2] = {A.m00, A.m10}, bx_[2] = {A.m01 * i + A.p0x, A.m11 * i + A.p0y};
+        const double L_[2] = {Lx, Ly}, U_[2] = {Ux, Uy};
+#pragma unroll
+        for (int d = 0; d < 2; d++) {
+            if (fabs(ax_[d]) < 1e-12) {
+                if (bx_[d] < L_[d] || bx_[d] > U_[d]) { jl = 1e300; jh = -1e300; }
+            } else {
+                double u = (L_[d] - bx_[d]) / ax_[d], v = (U_[d] - bx_[d]) / ax_[d];
+                if (u > v) { const double t = u; u = v; v = t; }
+                jl = fmax(jl, u);
+                jh = fmin(jh, v);
+            }
+        }
+        const int lo = max(0, (int)ceil(fmax(jl, -1e9))), hi = min(a.Wo - 1, (int)floor(fmin(jh, 1e9)));
+        qlo[r] = lo;
+        qhi[r] = hi;
+    }
+    __syncthreads();
+    build_rows<VEC>(RQ, a.Wo, qlo, qhi, qxa, qoff, qcnt, &ctl[0]);
+    __syncthreads();
+    const int FQ = min(ctl[0], kBFQMax);
+    for (int r = threadIdx.x; r < RQ; r += kThreads) rowt[r] = make_int4(qlo[r], qhi[r], qoff[r] - qxa[r], 0);
+    // ---- records: exact floor cell (relative to the block's cell origin) + fractions
+    for (int r = warp; r < RQ; r += kBWarps) {
+        const int i = ilo + r;
+        const double yt = ytab[i];
+        const int wr = (qcnt[r] + 3) & ~3;
+        for (int col = lane; col < wr; col += 32) {
+            const int j = qxa[r] + col, e = qoff[r] + col;
+            if (e >= kBFQMax) break;
+            uint2 R = make_uint2(0xff000000u, 0xff000000u);
+            if (col < qcnt[r] && j >= qlo[r] && j <= qhi[r]) {
+                double ix, iy;
+                stn_coord(T, xtab[j], yt, a.H, a.W, a.ac, ix, iy);
+                const Cell cx = cell_of(ix), cy = cell_of(iy);
+                const int rx = cx.i0 - (xa0 - 1), ry = cy.i0 - (yb0 - 1);
+                if (rx >= 0 && rx <= kBX && ry >= 0 && ry <= kBTY) R = pack_rec(rx, ry, cx.f, cy.f);
+            }
+            rec[e] = R;
+            ijs[e] = ((unsigned)i << 16) | (unsigned)j;
+        }
+    }
+    const int CH = min(min(a.C, kBCH), FQ > 0 ? max(1, kBStage / FQ) : kBCH);
+    const int nch = (a.C + CH - 1) / CH;
+    const float *gbase = a.dy + (long long)n * a.C * P;
+    const float *xbase = a.x + (long long)n * a.C * HW;
+    __syncthreads();
+    if (FQ > 0) stage_rows<VEC>(stage, FQ, gbase, P, min(CH, a.C), RQ, a.Wo, ilo, qxa, qoff, qcnt);
+    cp_async_commit();
+
+    // warp geometry: warp 0 also walks the halo cell row yb0-1
+    const int wy0 = (warp == 0) ? yb0 - 1 : yb0 + kBRows * warp;
+    const int nrows = (warp == 0) ? kBRows + 1 : kBRows;
+    const bool ownx = (px >= xa0) || (px == -1);
+    const float sxs = a.ac ? 0.5f * (a.W - 1) : 0.5f * a.W;
+    const float sys = a.ac ? 0.5f * (a.H - 1) : 0.5f * a.H;
+    const float axf = a.ac ? 2.f / (a.Wo - 1) : 2.f / a.Wo, bxf = a.ac ? -1.f : 1.f / a.Wo - 1.f;
+    const float ayf = a.ac ? 2.f / (a.Ho - 1) : 2.f / a.Ho, byf = a.ac ? -1.f : 1.f / a.Ho - 1.f;
+    // cell candidate window half extents (preimage of a unit square)
+    const double hj1 = 0.5 * (fabs(A.i00) + fabs(A.i01)) + eps, hi1 = 0.5 * (fabs(A.i10) + fabs(A.i11)) + eps;
+    const bool pxin = lane >= 1 && px < a.W;
+
+    float acc6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    unsigned hc[kBRows + 1][2];  // cached hits: 4 x u16 record index per cell row
+    int hn[kBRows + 1];          // hit count per cell row (kBHits + 1 = overflow)
+#pragma unroll
+    for (int rr = 0; rr <= kBRows; rr++) { hc[rr][0] = hc[rr][1] = 0u; hn[rr] = 0; }
+
+    for (int kc = 0; kc < nch; kc++) {
+        const int c0 = kc * CH, cn = min(CH, a.C - c0);
+        if (kc + 1 < nch) {
+            if (FQ > 0)
+                stage_rows<VEC>(stage + ((kc + 1) & 1) * kBStage, FQ, gbase + (long long)(c0 + CH) * P, P,
+                                min(CH, a.C - c0 - CH), RQ, a.Wo, ilo, qxa, qoff, qcnt);
+            cp_async_commit();
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const float *S = stage + (kc & 1) * kBStage;
+        float L[kBCH], Rr[kBCH], NL[kBCH], NR[kBCH], FL[kBCH], FR[kBCH];
+        float xc0[kBCH], xc1[kBCH];  // X row y0 at columns px, px+1
+#pragma unroll
+        for (int c = 0; c < kBCH; c++) { NL[c] = NR[c] = FL[c] = FR[c] = 0.f; L[c] = Rr[c] = 0.f; }
+        {
+            const int y = wy0;
+            const bool yv = y >= 0 && y < a.H;
+#pragma unroll
+            for (int c = 0; c < kBCH; c++) {
+                const float *p = xbase + (long long)(c0 + c) * HW + (long long)y * a.W + px;
+                xc0[c] = (c < cn && yv && px >= 0 && px < a.W) ? __ldg(p) : 0.f;
+                xc1[c] = (c < cn && yv && px + 1 >= 0 && px + 1 < a.W) ? __ldg(p + 1) : 0.f;
+            }
+        }
+#pragma unroll
+        for (int rr = 0; rr <= kBRows; rr++) {
+            if (rr < nrows) {
+                const int y0 = wy0 + rr;
+                const bool owny = (y0 >= yb0) || (y0 == -1);
+                const bool owned = ownx && owny;
+                // X row y0+1
+                float xn0[kBCH], xn1[kBCH];
+                {
+                    const int y = y0 + 1;
+                    const bool yv = y >= 0 && y < a.H;
+#pragma unroll
+                    for (int c = 0; c < kBCH; c++) {
+                        const float *p = xbase + (long long)(c0 + c) * HW + (long long)y * a.W + px;
+                        xn0[c] = (c < cn && yv && px >= 0 && px < a.W) ? __ldg(p) : 0.f;
+                        xn1[c] = (c < cn && yv && px + 1 >= 0 && px + 1 < a.W) ? __ldg(p + 1) : 0.f;
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < kBCH; c++) { L[c] = NL[c]; Rr[c] = NR[c]; NL[c] = 0.f; NR[c] = 0.f; }
+                // ---- the output pixels whose floor cell is (px, y0)
+                auto process = [&](int e, unsigned ij) {
+                    const uint2 R = rec[e];
+                    const float fx = (float)(R.x & 0xffffffu) * (1.f / 16777216.f);
+                    const float fy = (float)(R.y & 0xffffffu) * (1.f / 16777216.f);
+                    const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx;
+                    const float w10 = fy * (1.f - fx), w11 = fy * fx;
+                    float dq = 0.f, dr = 0.f;
+#pragma unroll
+                    for (int c = 0; c < kBCH; c++) {
+                        if (c < cn) {
+                            const float g = S[c * FQ + e];
+                            L[c] = fmaf(w00, g, L[c]);
+                            Rr[c] = fmaf(w01, g, Rr[c]);
+                            NL[c] = fmaf(w10, g, NL[c]);
+                            NR[c] = fmaf(w11, g, NR[c]);
+                            const float dxa = xc1[c] - xc0[c], dxb = xn1[c] - xn0[c];
+                            const float dya = xn0[c] - xc0[c], dyb = xn1[c] - xc1[c];
+                            dq = fmaf(g, fmaf(fy, dxb - dxa, dxa), dq);
+                            dr = fmaf(g, fmaf(fx, dyb - dya, dya), dr);
+                        }
+                    }
+                    if (owned) {
+                        const float xt = fmaf(axf, (float)(ij & 0xffffu), bxf);
+                        const float yt = fmaf(ayf, (float)(ij >> 16), byf);
+                        const float dgx = dq * sxs, dgy = dr * sys;
+                        acc6[0] = fmaf(dgx, xt, acc6[0]);
+                        acc6[1] = fmaf(dgx, yt, acc6[1]);
+                        acc6[2] += dgx;
+                        acc6[3] = fmaf(dgy, xt, acc6[3]);
+                        acc6[4] = fmaf(dgy, yt, acc6[4]);
+                        acc6[5] += dgy;
+                    }
+                };
+                const unsigned cxw = (unsigned)(px - (xa0 - 1)), cyw = (unsigned)(y0 - (yb0 - 1));
+                if (kc == 0 || hn[rr] > kBHits) {
+                    // search the preimage window of the unit cell
+                    const double ux = (double)px + 0.5 - A.p0x, uy = (double)y0 + 0.5 - A.p0y;
+                    const double qj = A.i00 * ux + A.i01 * uy, qi = A.i10 * ux + A.i11 * uy;
+                    const int jl = (int)ceil(qj - hj1), jh = (int)floor(qj + hj1);
+                    const int il = max(ilo, (int)ceil(qi - hi1)), ih = min(ilo + RQ - 1, (int)floor(qi + hi1));
+                    int cnt = 0;
+                    unsigned h0 = 0u, h1 = 0u;
+                    for (int i = il; i <= ih; i++) {
+                        const int4 rt = rowt[i - ilo];
+                        const int ja = max(jl, rt.x), jb = min(jh, rt.y);
+                        for (int j = ja; j <= jb; j++) {
+                            const int e = rt.z + j;
+                            const uint2 R = rec[e];
+                            if ((R.x >> 24) == cxw && (R.y >> 24) == cyw) {
+                                process(e, ((unsigned)i << 16) | (unsigned)j);
+                                if (cnt < 2) h0 |= (unsigned)e << (16 * cnt);
+                                else if (cnt < 4) h1 |= (unsigned)e << (16 * (cnt - 2));
+                                cnt++;
+                            }
+                        }
+                    }
+                    if (kc == 0) {
+                        hc[rr][0] = h0;
+                        hc[rr][1] = h1;
+                        hn[rr] = cnt > kBHits ? kBHits + 1 : cnt;
+                    }
+                } else {
+#pragma unroll
+                    for (int h = 0; h < kBHits; h++) {
+                        if (h < hn[rr]) {
+                            const int e = (int)((hc[rr][h >> 1] >> (16 * (h & 1))) & 0xffffu);
+                            process(e, ijs[e]);
+                        }
+                    }
+                }
+                // ---- finalise px row y0: own left share + left neighbour's right share
+                if (y0 >= yb0) {
+                    if (warp > 0 && rr == 0) {
+#pragma unroll
+                        for (int c = 0; c < kBCH; c++) { FL[c] = L[c]; FR[c] = Rr[c]; }
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < kBCH; c++) {
+                            const float v = L[c] + __shfl_up_sync(0xffffffffu, Rr[c], 1);
+                            if (c < cn && dxn && pxin && y0 < a.H)
+                                dxn[(long long)(c0 + c) * HW + (long long)y0 * a.W + px] = v;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < kBCH; c++) { xc0[c] = xn0[c]; xc1[c] = xn1[c]; }
+            }
+        }
+        // ---- carry the last cell row's lower share to the warp below
+        float *cw = carry + warp * 2 * kBCH * 32;
+        if (warp < kBWarps - 1) {
+#pragma unroll
+            for (int c = 0; c < kBCH; c++) { cw[c * 32 + lane] = NL[c]; cw[(kBCH + c) * 32 + lane] = NR[c]; }
+        }
+        __syncthreads();
+        if (warp > 0) {
+            const float *cu = carry + (warp - 1) * 2 * kBCH * 32;
+            const int y = yb0 + kBRows * warp;
+#pragma unroll
+            for (int c = 0; c < kBCH; c++) {
+                const float l = FL[c] + cu[c * 32 + lane], r = FR[c] + cu[(kBCH + c) * 32 + lane];
+                const float v = l + __shfl_up_sync(0xffffffffu, r, 1);
+                if (c < cn && dxn && pxin && y < a.H)
+                    dxn[(long long)(c0 + c) * HW + (long long)y * a.W + px] = v;
+            }
+        }
+        __syncthreads();
+    }
+    // ---- d_theta partial of the cells this tile owns
 #pragma unroll
     for (int k = 0; k < 6; k++) {
-        float v = warp_sum(acc[k]);
-        if (lane == 0) red[wid][k] = v;
+        const float v = warp_sum(acc6[k]);
+        if (lane == 0) red[warp][k] = v;
     }
     __syncthreads();
     if (threadIdx.x < 6) {
         double s = 0.0;
-        for (int w = 0; w < kThreads / 32; w++) s += (double)red[w][threadIdx.x];
-        partials[((long long)n * bps + blockIdx.x) * 6 + threadIdx.x] = s;
+        for (int w = 0; w < kBWarps; w++) s += (double)red[w][threadIdx.x];
+        part[threadIdx.x] = s;
     }
 }
 
+// ----------------------------------------------------------------- d_theta finalize
+// dtheta[n] = fixed-order fp64 sum of the partials of the path sample n took.
 __global__ void __launch_bounds__(kThreads)
-    stn_dtheta_finalize(const double *__restrict__ partials, int bps, float *dtheta) {
+    stn_dtheta_finalize(const double *__restrict__ pb, int nb, const double *__restrict__ pf, int nf,
+                        const int *__restrict__ flags, float *dtheta) {
     const int n = blockIdx.x;
+    const bool g = flags[n] != 0;
+    const double *p = g ? pb + (long long)n * nb * 6 : pf + (long long)n * nf * 6;
+    const int nt = g ? nb : nf;
     __shared__ double red[kThreads / 32][6];
     double s[6] = {0, 0, 0, 0, 0, 0};
-    for (int b = threadIdx.x; b < bps; b += kThreads)
+    for (int b = threadIdx.x; b < nt; b += kThreads)
 #pragma unroll
-        for (int k = 0; k < 6; k++) s[k] += partials[((long long)n * bps + b) * 6 + k];
+        for (int k = 0; k < 6; k++) s[k] += p[(long long)b * 6 + k];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
     for (int k = 0; k < 6; k++) {
-        double v = warp_sum_d(s[k]);
+        const double v = warp_sum_d(s[k]);
         if (lane == 0) red[wid][k] = v;
     }
     __syncthreads();
@@ -211,180 +684,186 @@ __global__ void __launch_bounds__(kThreads)
     }
 }
 
-// ----------------------------------------------------------------- backward: dx, gather form
-// CT channels per pass over the preimage bbox.
-template <int CT>
+// ----------------------------------------------------------------- atomic scatter (fallback samples)
 __global__ void __launch_bounds__(kThreads)
-    stn_dx_gather_kernel(StnArgs a, const double *__restrict__ xtab,
-                         const double *__restrict__ ytab) {
-    const long long HW = (long long)a.H * a.W;
-    const long long idx = (long long)blockIdx.x * kThreads + threadIdx.x;
-    if (idx >= (long long)a.N * HW) return;
-    const int n = (int)(idx / HW);
-    const long long rem = idx - (long long)n * HW;
-    const int y = (int)(rem / a.W), x = (int)(rem - (long long)y * a.W);
-    const Theta T = load_theta(a.theta, n);
-    const AffineInv inv = stn_inverse(T, a.H, a.W, a.Ho, a.Wo, a.ac);
-    float *dxp = a.dx + (long long)n * a.C * HW + rem;
-    if (!inv.ok) {  // this sample takes the atomic scatter: zero-fill for it
-        for (int c = 0; c < a.C; c++) dxp[(long long)c * HW] = 0.f;
-        return;
-    }
-    // preimage of p in [x-1, x+1] x [y-1, y+1]
-    const double ux = (double)x - inv.p0x, uy = (double)y - inv.p0y;
-    const double qj = inv.m00 * ux + inv.m01 * uy, qi = inv.m10 * ux + inv.m11 * uy;
-    const double mj = inv.hj + 1e-3, mi = inv.hi + 1e-3;
-    const int jlo = max(0, (int)ceil(qj - mj)), jhi = min(a.Wo - 1, (int)floor(qj + mj));
-    const int ilo = max(0, (int)ceil(qi - mi)), ihi = min(a.Ho - 1, (int)floor(qi + mi));
-    const long long P = (long long)a.Ho * a.Wo;
-    const float *gp = a.dy + (long long)n * a.C * P;
-    for (int cb = 0; cb < a.C; cb += CT) {
-        float acc[CT];
-#pragma unroll
-        for (int c = 0; c < CT; c++) acc[c] = 0.f;
-        for (int i = ilo; i <= ihi; i++) {
-            const double yt = ytab[i];
-            const double t1y = __dmul_rn(T.t[1], yt), t4y = __dmul_rn(T.t[4], yt);
-            for (int j = jlo; j <= jhi; j++) {
-                const double xt = xtab[j];
-                const double ix = stn_unnorm(
-                    __dadd_rn(__dadd_rn(__dmul_rn(T.t[0], xt), t1y), T.t[2]), a.W, a.ac);
-                const double iy = stn_unnorm(
-                    __dadd_rn(__dadd_rn(__dmul_rn(T.t[3], xt), t4y), T.t[5]), a.H, a.ac);
-                const Cell cx = cell_of(ix), cy = cell_of(iy);
-                const bool hx = (cx.i0 == x) || (cx.i0 == x - 1);
-                const bool hy = (cy.i0 == y) || (cy.i0 == y - 1);
-                if (!(hx && hy)) continue;
-                const float wx = (cx.i0 == x) ? 1.f - cx.f : cx.f;
-                const float wy = (cy.i0 == y) ? 1.f - cy.f : cy.f;
-                const float w = wy * wx;
-                const float *g = gp + (long long)i * a.Wo + j + (long long)cb * P;
-#pragma unroll
-                for (int c = 0; c < CT; c++)
-                    if (cb + c < a.C) acc[c] = fmaf(w, __ldg(g + (long long)c * P), acc[c]);
+    stn_dx_scatter(StnArgs a, const int *__restrict__ fb_list, const int *__restrict__ fb_count) {
+    const long long P = (long long)a.Ho * a.Wo, HW = (long long)a.H * a.W;
+    const int nf = *fb_count;
+    for (int f = 0; f < nf; f++) {
+        const int n = fb_list[f];
+        const Theta T = load_theta(a.theta, n);
+        for (long long rem = (long long)blockIdx.x * kThreads + threadIdx.x; rem < P;
+             rem += (long long)gridDim.x * kThreads) {
+            const int i = (int)(rem / a.Wo), j = (int)(rem - (long long)i * a.Wo);
+            double ix, iy;
+            stn_coord(T, stn_norm(j, a.Wo, a.ac), stn_norm(i, a.Ho, a.ac), a.H, a.W, a.ac, ix, iy);
+            if (a.border) {
+                float d;
+                ix = clamp_coord(ix, a.W, d);
+                iy = clamp_coord(iy, a.H, d);
+            }
+            const Cell cx = cell_of(ix), cy = cell_of(iy);
+            const bool x0ok = cx.i0 >= 0 && cx.i0 < a.W, x1ok = cx.i0 + 1 >= 0 && cx.i0 + 1 < a.W;
+            const bool y0ok = cy.i0 >= 0 && cy.i0 < a.H, y1ok = cy.i0 + 1 >= 0 && cy.i0 + 1 < a.H;
+            if (!((x0ok || x1ok) && (y0ok || y1ok))) continue;
+            const float w00 = (1.f - cy.f) * (1.f - cx.f), w01 = (1.f - cy.f) * cx.f;
+            const float w10 = cy.f * (1.f - cx.f), w11 = cy.f * cx.f;
+            const long long o00 = (long long)cy.i0 * a.W + cx.i0;
+            float *dxp = a.dx + (long long)n * a.C * HW + o00;
+            const float *gp = a.dy + (long long)n * a.C * P + rem;
+            for (int c = 0; c < a.C; c++) {
+                const float g = ldg_stream(gp + (long long)c * P);
+                float *q = dxp + (long long)c * HW;
+                if (y0ok && x0ok) red_add(q, w00 * g);
+                if (y0ok && x1ok) red_add(q + 1, w01 * g);
+                if (y1ok && x0ok) red_add(q + a.W, w10 * g);
+                if (y1ok && x1ok) red_add(q + a.W + 1, w11 * g);
             }
         }
-#pragma unroll
-        for (int c = 0; c < CT; c++)
-            if (cb + c < a.C) dxp[(long long)(cb + c) * HW] = acc[c];
     }
 }
 
-// ----------------------------------------------------------------- backward: dx, atomic scatter
-// only_nongather: skip samples the gather kernel handled (AUTO).  Grid is
-// (blocks per sample, N) so a skipped sample costs one early-exit per block.
-__global__ void __launch_bounds__(kThreads) stn_dx_scatter_kernel(StnArgs a, int only_nongather) {
-    const int n = blockIdx.y;
-    const Theta T = load_theta(a.theta, n);
-    if (only_nongather && stn_inverse(T, a.H, a.W, a.Ho, a.Wo, a.ac).ok) return;
-    const long long P = (long long)a.Ho * a.Wo;
-    const long long HW = (long long)a.H * a.W;
-    for (long long rem = (long long)blockIdx.x * kThreads + threadIdx.x; rem < P;
-         rem += (long long)gridDim.x * kThreads) {
-        const int i = (int)(rem / a.Wo), j = (int)(rem - (long long)i * a.Wo);
-        double ix, iy;
-        stn_coord(T, stn_norm(j, a.Wo, a.ac), stn_norm(i, a.Ho, a.ac), a.H, a.W, a.ac, ix, iy);
-        if (a.border) {
-            float d;
-            ix = clamp_coord(ix, a.W, d);
-            iy = clamp_coord(iy, a.H, d);
-        }
-        const Cell cx = cell_of(ix), cy = cell_of(iy);
-        const bool x0ok = cx.i0 >= 0 && cx.i0 < a.W, x1ok = cx.i0 + 1 >= 0 && cx.i0 + 1 < a.W;
-        const bool y0ok = cy.i0 >= 0 && cy.i0 < a.H, y1ok = cy.i0 + 1 >= 0 && cy.i0 + 1 < a.H;
-        const float wx0 = 1.f - cx.f, wx1 = cx.f, wy0 = 1.f - cy.f, wy1 = cy.f;
-        const float w00 = wy0 * wx0, w01 = wy0 * wx1, w10 = wy1 * wx0, w11 = wy1 * wx1;
-        const long long o00 = (long long)cy.i0 * a.W + cx.i0;
-        float *dxp = a.dx + (long long)n * a.C * HW + o00;
-        const float *gp = a.dy + (long long)n * a.C * P + rem;
-        for (int c = 0; c < a.C; c++) {
-            const float g = ldg_stream(gp + (long long)c * P);
-            float *q = dxp + (long long)c * HW;
-            if (y0ok && x0ok) red_add(q, w00 * g);
-            if (y0ok && x1ok) red_add(q + 1, w01 * g);
-            if (y1ok && x0ok) red_add(q + a.W, w10 * g);
-            if (y1ok && x1ok) red_add(q + a.W + 1, w11 * g);
-        }
-    }
-}
-
-int scatter_blocks_per_sample(long long P) {
-    long long b = (P + kThreads - 1) / kThreads;
-    return (int)(b > 4096 ? 4096 : b);
-}
-
-int dtheta_blocks_per_sample(int N, long long P) {
-    long long by_pixels = (P + kThreads - 1) / kThreads;
-    long long want = (8LL * kNumSMs + N - 1) / N;
-    long long b = by_pixels < want ? by_pixels : want;
-    return (int)(b < 1 ? 1 : b);
-}
-
+// ----------------------------------------------------------------- host helpers
 size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+struct StnGeom {
+    int fj, fi;  // output tiles
+    int bx, by;  // input tiles
+};
+
+StnGeom stn_geom(int H, int W, int Ho, int Wo) {
+    StnGeom g;
+    g.fj = (Wo + kFJ - 1) / kFJ;
+    g.fi = (Ho + kFI - 1) / kFI;
+    g.bx = (W + kBX - 1) / kBX;
+    g.by = (H + kBTY - 1) / kBTY;
+    return g;
+}
+
+struct StnWs {
+    double *xtab, *ytab, *pb, *pf;
+    int *flags, *fb_list, *fb_count;
+    size_t bytes;
+};
+
+StnWs stn_ws_layout(void *base, int N, int H, int W, int Ho, int Wo) {
+    const StnGeom g = stn_geom(H, W, Ho, Wo);
+    StnWs w;
+    size_t off = 0;
+    char *b = (char *)base;
+    auto take = [&](size_t bytes) {
+        void *p = b ? b + off : nullptr;
+        off += align256(bytes);
+        return p;
+    };
+    w.xtab = (double *)take(sizeof(double) * Wo);
+    w.ytab = (double *)take(sizeof(double) * Ho);
+    w.flags = (int *)take(sizeof(int) * N);
+    w.fb_list = (int *)take(sizeof(int) * N);
+    w.fb_count = (int *)take(sizeof(int));
+    w.pb = (double *)take(sizeof(double) * 6 * (size_t)N * g.bx * g.by);
+    w.pf = (double *)take(sizeof(double) * 6 * (size_t)N * g.fj * g.fi);
+    w.bytes = off;
+    return w;
+}
+
+size_t out_tile_smem() { return sizeof(int) * (5 * kFRMax + 16) + sizeof(float) * 2 * kFStage; }
+size_t bwd_cell_smem() {
+    return sizeof(float) * 2 * kBStage + (sizeof(uint2) + sizeof(unsigned)) * kBFQMax +
+           sizeof(int4) * kBRQMax + sizeof(int) * (5 * kBRQMax + 8) + sizeof(float) * kBWarps * 2 * kBCH * 32;
+}
+
+template <typename K>
+void set_smem(K kernel, size_t bytes) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
 
 }  // namespace
 
 size_t stn_ws_bytes(int N, int C, int H, int W, int Ho, int Wo) {
     (void)C;
-    (void)H;
-    (void)W;
-    long long P = (long long)Ho * Wo;
-    int bps = dtheta_blocks_per_sample(N, P);
-    return align256(sizeof(double) * (size_t)N * bps * 6) + align256(sizeof(double) * Wo) +
-           align256(sizeof(double) * Ho);
+    return stn_ws_layout(nullptr, N, H, W, Ho, Wo).bytes;
 }
 
 cudaError_t stn_fwd_launch(const StnArgs &a, cudaStream_t s) {
-    long long total = (long long)a.N * a.Ho * a.Wo;
-    unsigned blocks = (unsigned)((total + kThreads - 1) / kThreads);
-    stn_fwd_kernel<<<blocks, kThreads, 0, s>>>(a);
+    const StnGeom g = stn_geom(a.H, a.W, a.Ho, a.Wo);
+    const bool vec = (a.W % 4 == 0) && aligned16(a.x);
+    const size_t sm = out_tile_smem();
+    dim3 grid(g.fj * g.fi, a.N);
+    if (vec) {
+        set_smem(stn_out_tile<MODE_FWD, true>, sm);
+        stn_out_tile<MODE_FWD, true><<<grid, kThreads, sm, s>>>(a, nullptr, nullptr, nullptr, nullptr,
+                                                                nullptr, g.fj, g.fi);
+    } else {
+        set_smem(stn_out_tile<MODE_FWD, false>, sm);
+        stn_out_tile<MODE_FWD, false><<<grid, kThreads, sm, s>>>(a, nullptr, nullptr, nullptr, nullptr,
+                                                                 nullptr, g.fj, g.fi);
+    }
     note_launch();
     return cudaGetLastError();
 }
 
-cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *ws,
-                           size_t ws_bytes, cudaStream_t s) {
+cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *ws, size_t ws_bytes,
+                           cudaStream_t s) {
     (void)ws_bytes;
     (void)deterministic;
-    const long long P = (long long)a.Ho * a.Wo;
-    const int bps = dtheta_blocks_per_sample(a.N, P);
-    char *w = (char *)ws;
-    double *partials = (double *)w;
-    w += align256(sizeof(double) * (size_t)a.N * bps * 6);
-    double *xtab = (double *)w;
-    w += align256(sizeof(double) * a.Wo);
-    double *ytab = (double *)w;
+    const StnGeom g = stn_geom(a.H, a.W, a.Ho, a.Wo);
+    const StnWs w = stn_ws_layout(ws, a.N, a.H, a.W, a.Ho, a.Wo);
+    const long long HW = (long long)a.H * a.W;
     const int tmax = a.Wo > a.Ho ? a.Wo : a.Ho;
-    stn_tables_kernel<<<(tmax + 255) / 256, 256, 0, s>>>(xtab, ytab, a.Ho, a.Wo, a.ac);
+    stn_tables_kernel<<<(tmax + 255) / 256, 256, 0, s>>>(w.xtab, w.ytab, a.Ho, a.Wo, a.ac);
     note_launch();
-    if (a.dtheta) {
-        stn_dtheta_kernel<<<dim3(bps, a.N), kThreads, 0, s>>>(a, xtab, ytab, partials, bps);
-        note_launch();
-        stn_dtheta_finalize<<<a.N, kThreads, 0, s>>>(partials, bps, a.dtheta);
+    // AUTO / GATHER: cell-owner gather where the preimage is bounded (zeros padding);
+    // SCATTER_ATOMIC or border padding: every sample takes the fallback pair.
+    const int allow_gather = (algo == 0 || algo == 1) && !a.border;
+    stn_classify_kernel<<<1, 256, 0, s>>>(a, allow_gather, w.flags, w.fb_list, w.fb_count);
+    note_launch();
+    if (!allow_gather && a.dx) {
+        cudaError_t e = cudaMemsetAsync(a.dx, 0, sizeof(float) * (size_t)a.N * a.C * HW, s);
+        if (e != cudaSuccess) return e;
+    }
+    const bool vin = (a.W % 4 == 0) && aligned16(a.x);
+    const bool vout = (a.Wo % 4 == 0) && aligned16(a.dy);
+    if (allow_gather) {
+        const size_t sm = bwd_cell_smem();
+        dim3 grid(g.bx * g.by, a.N);
+        if (vout) {
+            set_smem(stn_bwd_cell<true>, sm);
+            stn_bwd_cell<true><<<grid, kThreads, sm, s>>>(a, w.xtab, w.ytab, w.flags, w.pb, g.bx, g.by);
+        } else {
+            set_smem(stn_bwd_cell<false>, sm);
+            stn_bwd_cell<false><<<grid, kThreads, sm, s>>>(a, w.xtab, w.ytab, w.flags, w.pb, g.bx, g.by);
+        }
         note_launch();
     }
-    if (a.dx) {
-        // AUTO: gather (bounded affine preimage) unless border padding, where the clamp
-        // has no bounded inverse (the API refuses deterministic=1 with border).
-        const bool gather = (algo == 0 || algo == 1) && !a.border;
-        const long long HW = (long long)a.H * a.W;
-        if (gather) {
-            unsigned blocks = (unsigned)(((long long)a.N * HW + kThreads - 1) / kThreads);
-            if (a.C >= 16)
-                stn_dx_gather_kernel<16><<<blocks, kThreads, 0, s>>>(a, xtab, ytab);
-            else if (a.C >= 8)
-                stn_dx_gather_kernel<8><<<blocks, kThreads, 0, s>>>(a, xtab, ytab);
-            else
-                stn_dx_gather_kernel<4><<<blocks, kThreads, 0, s>>>(a, xtab, ytab);
-            note_launch();
-            // samples whose theta is near-singular fall back to atomics
-            stn_dx_scatter_kernel<<<dim3(scatter_blocks_per_sample(P), a.N), kThreads, 0, s>>>(a, 1);
-            note_launch();
+    // fallback samples (all samples when !allow_gather): d_theta from output tiles ...
+    if (a.dtheta) {
+        const size_t sm = out_tile_smem();
+        dim3 grid(g.fj * g.fi, 1);
+        if (vin) {
+            set_smem(stn_out_tile<MODE_DTHETA, true>, sm);
+            stn_out_tile<MODE_DTHETA, true><<<grid, kThreads, sm, s>>>(a, w.xtab, w.ytab, w.fb_list, w.fb_count,
+                                                                       w.pf, g.fj, g.fi);
         } else {
-            cudaMemsetAsync(a.dx, 0, sizeof(float) * (size_t)a.N * a.C * HW, s);
-            stn_dx_scatter_kernel<<<dim3(scatter_blocks_per_sample(P), a.N), kThreads, 0, s>>>(a, 0);
-            note_launch();
+            set_smem(stn_out_tile<MODE_DTHETA, false>, sm);
+            stn_out_tile<MODE_DTHETA, false><<<grid, kThreads, sm, s>>>(a, w.xtab, w.ytab, w.fb_list,
+                                                                        w.fb_count, w.pf, g.fj, g.fi);
         }
+        note_launch();
+    }
+    // ... and d_input from the atomic scatter
+    if (a.dx) {
+        const long long P = (long long)a.Ho * a.Wo;
+        long long blocks = (P + kThreads - 1) / kThreads;
+        if (blocks > 4 * kNumSMs * 8) blocks = 4 * kNumSMs * 8;
+        stn_dx_scatter<<<(unsigned)blocks, kThreads, 0, s>>>(a, w.fb_list, w.fb_count);
+        note_launch();
+    }
+    if (a.dtheta) {
+        stn_dtheta_finalize<<<a.N, kThreads, 0, s>>>(w.pb, g.bx * g.by, w.pf, g.fj * g.fi, w.flags, a.dtheta);
+        note_launch();
     }
     return cudaGetLastError();
 }
