@@ -153,24 +153,28 @@ RS_DEV void build_rows(int R, int Wlim, const int *lo, const int *hi, int *xa, i
 }
 
 // Issue cp.async copies of nch channel planes' rows (channel stride cstride floats)
-// into dst + c*F + off[r].  Warp per (channel, row), lanes over 16-B (or 4-B) words.
+// into dst + c*F + off[r].  Eight lanes per row (4 rows per warp instruction), the
+// channel loop innermost; no integer division.
 template <bool VEC>
 RS_DEV void stage_rows(float *dst, int F, const float *base, long long cstride, int nch, int R,
                        int W, int ybase, const int *xa, const int *off, const int *cnt) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int p = warp; p < nch * R; p += nw) {
-        const int c = p / R, r = p - c * R;
+    const int sub = lane >> 3, l8 = lane & 7;
+    for (int r = warp * 4 + sub; r < R; r += nw * 4) {
         const int w = cnt[r];
-        const float *src = base + c * cstride + (long long)(ybase + r) * W + xa[r];
-        float *d = dst + c * F + off[r];
-        if (VEC) {
-            for (int q = lane * 4; q < w; q += 128) cp_async16(d + q, src + q);
-        } else {
-            for (int q = lane; q < w; q += 32) cp_async4(d + q, src + q);
+        const float *src = base + (long long)(ybase + r) * W + xa[r];
+        float *d = dst + off[r];
+        for (int c = 0; c < nch; c++) {
+            if (VEC) {
+                for (int q = l8 * 4; q < w; q += 32) cp_async16(d + q, src + q);
+            } else {
+                for (int q = l8; q < w; q += 8) cp_async4(d + q, src + q);
+            }
+            src += cstride;
+            d += F;
         }
     }
 }
-
 }  // namespace rs
 
 // ----------------------------------------------------------------- launchers (internal ABI)

@@ -32,6 +32,8 @@
 // affine map is singular or whose preimage exceeds the staging budget takes
 // d_theta from stn_out_tile (MODE_DTHETA) and d_input from the atomic scatter
 // (PAPER.md:733); border padding (no bounded inverse) always does.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace rs {
@@ -51,9 +53,9 @@ constexpr int kBWarps = 8;
 constexpr int kBTY = kBRows * kBWarps;    // 32 px rows per block
 constexpr int kBRQMax = 160;              // max staged output rows
 constexpr int kBFQMax = 2304;             // max staged output px (records)
-constexpr int kBStage = 4096;             // floats per pipeline stage
+constexpr int kBStage = 6144;             // floats per pipeline stage
 constexpr int kBCH = 4;                   // max channels per stage (registers)
-constexpr int kBHits = 4;                 // cached hits per cell
+constexpr int kBHits = 6;                 // cached hits per cell (more: re-searched)
 
 constexpr int MODE_FWD = 0, MODE_DTHETA = 1;
 
@@ -138,9 +140,17 @@ __global__ void __launch_bounds__(kThreads, 3)
     float *stage = (float *)(ctl + 16);      // 2 * kFStage (16-B aligned: 656 ints)
     __shared__ float red[kThreads / 32][6];
 
+    __shared__ double ntab[kFJ + kFI];  // normalised coordinates of the tile's columns / rows
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tj = blockIdx.x % tiles_j, ti = blockIdx.x / tiles_j;
     const long long HW = (long long)a.H * a.W, P = (long long)a.Ho * a.Wo;
+    if (threadIdx.x < kFJ + kFI) {
+        const bool col = threadIdx.x < kFJ;
+        const int idx = col ? tj * kFJ + threadIdx.x : ti * kFI + threadIdx.x - kFJ;
+        const int L = col ? a.Wo : a.Ho;
+        ntab[threadIdx.x] = idx < L ? (MODE == MODE_DTHETA ? (col ? xtab[idx] : ytab[idx]) : stn_norm(idx, L, a.ac)) : 0.0;
+    }
+    __syncthreads();
     const int nloop = fb_list ? *fb_count : 1;
     for (int f = 0; f < nloop; f++) {
         const int n = fb_list ? fb_list[f] : blockIdx.y;
@@ -159,8 +169,7 @@ __global__ void __launch_bounds__(kThreads, 3)
             xtf[k] = ytf[k] = 0.f;
             xv0[k] = xv1[k] = yv0[k] = yv1[k] = false;
             if (in[k]) {
-                const double xt = MODE == MODE_DTHETA ? xtab[j] : stn_norm(j, a.Wo, a.ac);
-                const double yt = MODE == MODE_DTHETA ? ytab[i] : stn_norm(i, a.Ho, a.ac);
+                const double xt = ntab[lane], yt = ntab[kFJ + warp + 8 * k];
                 xtf[k] = (float)xt;
                 ytf[k] = (float)yt;
                 double ix, iy;
@@ -375,6 +384,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     int *qcnt = qoff + kBRQMax;
     int *ctl = qcnt + kBRQMax;                                  // 8
     float *carry = (float *)(ctl + 8);                          // kBWarps * 2 * kBCH * 32
+    unsigned short *hlist = (unsigned short *)(carry + kBWarps * 2 * kBCH * 32);  // [warp][row][hit][lane]
+    unsigned char *hcnt = (unsigned char *)(hlist + kBWarps * (kBRows + 1) * kBHits * 32);  // [warp][row][lane]
     __shared__ float red[kBWarps][6];
 
     const int n = blockIdx.y;
@@ -472,19 +483,156 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int wy0 = (warp == 0) ? yb0 - 1 : yb0 + kBRows * warp;
     const int nrows = (warp == 0) ? kBRows + 1 : kBRows;
     const bool ownx = (px >= xa0) || (px == -1);
+    const bool pxin = lane >= 1 && px < a.W;
+    const bool vx0 = px >= 0 && px < a.W, vx1 = px + 1 < a.W;
+    const unsigned cxw = (unsigned)(px - (xa0 - 1));
+    const double hj1 = 0.5 * (fabs(A.i00) + fabs(A.i01)) + eps, hi1 = 0.5 * (fabs(A.i10) + fabs(A.i11)) + eps;
+    unsigned short *myhl = hlist + warp * (kBRows + 1) * kBHits * 32 + lane;
+    unsigned char *myhc = hcnt + warp * (kBRows + 1) * 32 + lane;
+
+    // ---- search (overlaps the first stage's copy): output pixels whose floor cell is (px, y0)
+    auto search = [&](int y0, int rr, bool store, auto &&fn) {
+        const unsigned cyw = (unsigned)(y0 - (yb0 - 1));
+        const double ux = (double)px + 0.5 - A.p0x, uy = (double)y0 + 0.5 - A.p0y;
+        const double qj = A.i00 * ux + A.i01 * uy, qi = A.i10 * ux + A.i11 * uy;
+        const int jl = (int)ceil(qj - hj1), jh = (int)floor(qj + hj1);
+        const int il = max(ilo, (int)ceil(qi - hi1)), ih = min(ilo + RQ - 1, (int)floor(qi + hi1));
+        int cnt = 0;
+        for (int i = il; i <= ih; i++) {
+            const int4 rt = rowt[i - ilo];
+            const int ja = max(jl, rt.x), jb = min(jh, rt.y);
+            for (int j = ja; j <= jb; j++) {
+                const int e = rt.z + j;
+                const uint2 R = rec[e];
+                if ((R.x >> 24) == cxw && (R.y >> 24) == cyw) {
+                    if (store && cnt < kBHits) myhl[(rr * kBHits + cnt) * 32] = (unsigned short)e;
+                    fn(e);
+                    cnt++;
+                }
+            }
+        }
+        if (store) myhc[rr * 32] = (unsigned char)(cnt > kBHits ? 255 : cnt);
+    };
+    for (int rr = 0; rr < nrows; rr++) search(wy0 + rr, rr, true, [](int) {});
+
+    float acc6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     const float sxs = a.ac ? 0.5f * (a.W - 1) : 0.5f * a.W;
     const float sys = a.ac ? 0.5f * (a.H - 1) : 0.5f * a.H;
     const float axf = a.ac ? 2.f / (a.Wo - 1) : 2.f / a.Wo, bxf = a.ac ? -1.f : 1.f / a.Wo - 1.f;
     const float ayf = a.ac ? 2.f / (a.Ho - 1) : 2.f / a.Ho, byf = a.ac ? -1.f : 1.f / a.Ho - 1.f;
-    // cell candidate window half extents (preimage of a unit square)
-    const double hj1 = 0.5 * (fabs(A.i00) + fabs(A.i01)) + eps, hi1 = 0.5 * (fabs(A.i10) + fabs(A.i11)) + eps;
-    const bool pxin = lane >= 1 && px < a.W;
 
-    float acc6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    unsigned hc[kBRows + 1][2];  // cached hits: 4 x u16 record index per cell row
-    int hn[kBRows + 1];          // hit count per cell row (kBHits + 1 = overflow)
+
+    // One chunk of NC channels (compile-time, so no predicated-off channel work).
+    auto run_chunk = [&](const float *S, int c0, auto ncc) {
+        constexpr int NC = decltype(ncc)::value;
+        const float *xch = xbase + (long long)c0 * HW + px;
+        float *dxc = dxn ? dxn + (long long)c0 * HW + px : nullptr;
+        float L[NC], Rr[NC], NL[NC], NR[NC], FL[NC], FR[NC], xc0[NC], xc1[NC];
+        const bool yv0 = wy0 >= 0 && wy0 < a.H;
 #pragma unroll
-    for (int rr = 0; rr <= kBRows; rr++) { hc[rr][0] = hc[rr][1] = 0u; hn[rr] = 0; }
+        for (int c = 0; c < NC; c++) {
+            NL[c] = NR[c] = FL[c] = FR[c] = 0.f;
+            const float *p = xch + (long long)c * HW + (long long)wy0 * a.W;
+            xc0[c] = (yv0 && vx0) ? __ldg(p) : 0.f;
+            xc1[c] = (yv0 && vx1) ? __ldg(p + 1) : 0.f;
+        }
+        const float *xrow = xch + (long long)(wy0 + 1) * a.W;
+        float *drow = dxc ? dxc + (long long)wy0 * a.W : nullptr;
+#pragma unroll 1
+        for (int rr = 0; rr < nrows; rr++, xrow += a.W, drow += a.W) {
+            const int y0 = wy0 + rr;
+            const bool owned = ownx && ((y0 >= yb0) || (y0 == -1));
+            const bool yv = y0 + 1 >= 0 && y0 + 1 < a.H;
+            float dxa[NC], ddx[NC], dya[NC], ddy[NC];
+#pragma unroll
+            for (int c = 0; c < NC; c++) {
+                const float *p = xrow + (long long)c * HW;
+                const float n0 = (yv && vx0) ? __ldg(p) : 0.f;
+                const float n1 = (yv && vx1) ? __ldg(p + 1) : 0.f;
+                dxa[c] = xc1[c] - xc0[c];
+                ddx[c] = (n1 - n0) - dxa[c];
+                dya[c] = n0 - xc0[c];
+                ddy[c] = (n1 - xc1[c]) - dya[c];
+                xc0[c] = n0;
+                xc1[c] = n1;
+                L[c] = NL[c];
+                Rr[c] = NR[c];
+                NL[c] = 0.f;
+                NR[c] = 0.f;
+            }
+            auto process = [&](int e) {
+                const uint2 R = rec[e];
+                const float fx = (float)(R.x & 0xffffffu) * (1.f / 16777216.f);
+                const float fy = (float)(R.y & 0xffffffu) * (1.f / 16777216.f);
+                const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx;
+                const float w10 = fy * (1.f - fx), w11 = fy * fx;
+                float dq = 0.f, dr = 0.f;
+                const float *Se = S + e;
+#pragma unroll
+                for (int c = 0; c < NC; c++) {
+                    const float g = Se[c * FQ];
+                    L[c] = fmaf(w00, g, L[c]);
+                    Rr[c] = fmaf(w01, g, Rr[c]);
+                    NL[c] = fmaf(w10, g, NL[c]);
+                    NR[c] = fmaf(w11, g, NR[c]);
+                    dq = fmaf(g, fmaf(fy, ddx[c], dxa[c]), dq);
+                    dr = fmaf(g, fmaf(fx, ddy[c], dya[c]), dr);
+                }
+                if (owned) {
+                    const unsigned ij = ijs[e];
+                    const float xt = fmaf(axf, (float)(ij & 0xffffu), bxf);
+                    const float yt = fmaf(ayf, (float)(ij >> 16), byf);
+                    const float dgx = dq * sxs, dgy = dr * sys;
+                    acc6[0] = fmaf(dgx, xt, acc6[0]);
+                    acc6[1] = fmaf(dgx, yt, acc6[1]);
+                    acc6[2] += dgx;
+                    acc6[3] = fmaf(dgy, xt, acc6[3]);
+                    acc6[4] = fmaf(dgy, yt, acc6[4]);
+                    acc6[5] += dgy;
+                }
+            };
+            const int hn = myhc[rr * 32];
+            const int hmax = __reduce_max_sync(0xffffffffu, hn == 255 ? 0 : hn);
+            if (hn == 255) {
+                search(y0, rr, false, process);  // > kBHits output pixels in this cell (rare)
+            } else {
+                for (int h = 0; h < hmax; h++)
+                    if (h < hn) process(myhl[(rr * kBHits + h) * 32]);
+            }
+            // ---- finalise px row y0: own left share + left neighbour's right share
+            if (y0 >= yb0) {
+                if (warp > 0 && rr == 0) {  // needs the warp above's carry: after the barrier
+#pragma unroll
+                    for (int c = 0; c < NC; c++) { FL[c] = L[c]; FR[c] = Rr[c]; }
+                } else {
+                    const bool wr = drow && pxin && y0 < a.H;
+#pragma unroll
+                    for (int c = 0; c < NC; c++) {
+                        const float v = L[c] + __shfl_up_sync(0xffffffffu, Rr[c], 1);
+                        if (wr) drow[(long long)c * HW] = v;
+                    }
+                }
+            }
+        }
+        // ---- carry the last cell row's lower share to the warp below
+        if (warp < kBWarps - 1) {
+            float *cw = carry + warp * 2 * kBCH * 32;
+#pragma unroll
+            for (int c = 0; c < NC; c++) { cw[c * 32 + lane] = NL[c]; cw[(kBCH + c) * 32 + lane] = NR[c]; }
+        }
+        __syncthreads();
+        if (warp > 0) {
+            const float *cu = carry + (warp - 1) * 2 * kBCH * 32;
+            const int y = yb0 + kBRows * warp;
+            const bool wr = dxc && pxin && y < a.H;
+#pragma unroll
+            for (int c = 0; c < NC; c++) {
+                const float l = FL[c] + cu[c * 32 + lane], r = FR[c] + cu[(kBCH + c) * 32 + lane];
+                const float v = l + __shfl_up_sync(0xffffffffu, r, 1);
+                if (wr) dxc[(long long)c * HW + (long long)y * a.W] = v;
+            }
+        }
+    };
 
     for (int kc = 0; kc < nch; kc++) {
         const int c0 = kc * CH, cn = min(CH, a.C - c0);
@@ -499,146 +647,11 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         __syncthreads();
         const float *S = stage + (kc & 1) * kBStage;
-        float L[kBCH], Rr[kBCH], NL[kBCH], NR[kBCH], FL[kBCH], FR[kBCH];
-        float xc0[kBCH], xc1[kBCH];  // X row y0 at columns px, px+1
-#pragma unroll
-        for (int c = 0; c < kBCH; c++) { NL[c] = NR[c] = FL[c] = FR[c] = 0.f; L[c] = Rr[c] = 0.f; }
-        {
-            const int y = wy0;
-            const bool yv = y >= 0 && y < a.H;
-#pragma unroll
-            for (int c = 0; c < kBCH; c++) {
-                const float *p = xbase + (long long)(c0 + c) * HW + (long long)y * a.W + px;
-                xc0[c] = (c < cn && yv && px >= 0 && px < a.W) ? __ldg(p) : 0.f;
-                xc1[c] = (c < cn && yv && px + 1 >= 0 && px + 1 < a.W) ? __ldg(p + 1) : 0.f;
-            }
-        }
-#pragma unroll
-        for (int rr = 0; rr <= kBRows; rr++) {
-            if (rr < nrows) {
-                const int y0 = wy0 + rr;
-                const bool owny = (y0 >= yb0) || (y0 == -1);
-                const bool owned = ownx && owny;
-                // X row y0+1
-                float xn0[kBCH], xn1[kBCH];
-                {
-                    const int y = y0 + 1;
-                    const bool yv = y >= 0 && y < a.H;
-#pragma unroll
-                    for (int c = 0; c < kBCH; c++) {
-                        const float *p = xbase + (long long)(c0 + c) * HW + (long long)y * a.W + px;
-                        xn0[c] = (c < cn && yv && px >= 0 && px < a.W) ? __ldg(p) : 0.f;
-                        xn1[c] = (c < cn && yv && px + 1 >= 0 && px + 1 < a.W) ? __ldg(p + 1) : 0.f;
-                    }
-                }
-#pragma unroll
-                for (int c = 0; c < kBCH; c++) { L[c] = NL[c]; Rr[c] = NR[c]; NL[c] = 0.f; NR[c] = 0.f; }
-                // ---- the output pixels whose floor cell is (px, y0)
-                auto process = [&](int e, unsigned ij) {
-                    const uint2 R = rec[e];
-                    const float fx = (float)(R.x & 0xffffffu) * (1.f / 16777216.f);
-                    const float fy = (float)(R.y & 0xffffffu) * (1.f / 16777216.f);
-                    const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx;
-                    const float w10 = fy * (1.f - fx), w11 = fy * fx;
-                    float dq = 0.f, dr = 0.f;
-#pragma unroll
-                    for (int c = 0; c < kBCH; c++) {
-                        if (c < cn) {
-                            const float g = S[c * FQ + e];
-                            L[c] = fmaf(w00, g, L[c]);
-                            Rr[c] = fmaf(w01, g, Rr[c]);
-                            NL[c] = fmaf(w10, g, NL[c]);
-                            NR[c] = fmaf(w11, g, NR[c]);
-                            const float dxa = xc1[c] - xc0[c], dxb = xn1[c] - xn0[c];
-                            const float dya = xn0[c] - xc0[c], dyb = xn1[c] - xc1[c];
-                            dq = fmaf(g, fmaf(fy, dxb - dxa, dxa), dq);
-                            dr = fmaf(g, fmaf(fx, dyb - dya, dya), dr);
-                        }
-                    }
-                    if (owned) {
-                        const float xt = fmaf(axf, (float)(ij & 0xffffu), bxf);
-                        const float yt = fmaf(ayf, (float)(ij >> 16), byf);
-                        const float dgx = dq * sxs, dgy = dr * sys;
-                        acc6[0] = fmaf(dgx, xt, acc6[0]);
-                        acc6[1] = fmaf(dgx, yt, acc6[1]);
-                        acc6[2] += dgx;
-                        acc6[3] = fmaf(dgy, xt, acc6[3]);
-                        acc6[4] = fmaf(dgy, yt, acc6[4]);
-                        acc6[5] += dgy;
-                    }
-                };
-                const unsigned cxw = (unsigned)(px - (xa0 - 1)), cyw = (unsigned)(y0 - (yb0 - 1));
-                if (kc == 0 || hn[rr] > kBHits) {
-                    // search the preimage window of the unit cell
-                    const double ux = (double)px + 0.5 - A.p0x, uy = (double)y0 + 0.5 - A.p0y;
-                    const double qj = A.i00 * ux + A.i01 * uy, qi = A.i10 * ux + A.i11 * uy;
-                    const int jl = (int)ceil(qj - hj1), jh = (int)floor(qj + hj1);
-                    const int il = max(ilo, (int)ceil(qi - hi1)), ih = min(ilo + RQ - 1, (int)floor(qi + hi1));
-                    int cnt = 0;
-                    unsigned h0 = 0u, h1 = 0u;
-                    for (int i = il; i <= ih; i++) {
-                        const int4 rt = rowt[i - ilo];
-                        const int ja = max(jl, rt.x), jb = min(jh, rt.y);
-                        for (int j = ja; j <= jb; j++) {
-                            const int e = rt.z + j;
-                            const uint2 R = rec[e];
-                            if ((R.x >> 24) == cxw && (R.y >> 24) == cyw) {
-                                process(e, ((unsigned)i << 16) | (unsigned)j);
-                                if (cnt < 2) h0 |= (unsigned)e << (16 * cnt);
-                                else if (cnt < 4) h1 |= (unsigned)e << (16 * (cnt - 2));
-                                cnt++;
-                            }
-                        }
-                    }
-                    if (kc == 0) {
-                        hc[rr][0] = h0;
-                        hc[rr][1] = h1;
-                        hn[rr] = cnt > kBHits ? kBHits + 1 : cnt;
-                    }
-                } else {
-#pragma unroll
-                    for (int h = 0; h < kBHits; h++) {
-                        if (h < hn[rr]) {
-                            const int e = (int)((hc[rr][h >> 1] >> (16 * (h & 1))) & 0xffffu);
-                            process(e, ijs[e]);
-                        }
-                    }
-                }
-                // ---- finalise px row y0: own left share + left neighbour's right share
-                if (y0 >= yb0) {
-                    if (warp > 0 && rr == 0) {
-#pragma unroll
-                        for (int c = 0; c < kBCH; c++) { FL[c] = L[c]; FR[c] = Rr[c]; }
-                    } else {
-#pragma unroll
-                        for (int c = 0; c < kBCH; c++) {
-                            const float v = L[c] + __shfl_up_sync(0xffffffffu, Rr[c], 1);
-                            if (c < cn && dxn && pxin && y0 < a.H)
-                                dxn[(long long)(c0 + c) * HW + (long long)y0 * a.W + px] = v;
-                        }
-                    }
-                }
-#pragma unroll
-                for (int c = 0; c < kBCH; c++) { xc0[c] = xn0[c]; xc1[c] = xn1[c]; }
-            }
-        }
-        // ---- carry the last cell row's lower share to the warp below
-        float *cw = carry + warp * 2 * kBCH * 32;
-        if (warp < kBWarps - 1) {
-#pragma unroll
-            for (int c = 0; c < kBCH; c++) { cw[c * 32 + lane] = NL[c]; cw[(kBCH + c) * 32 + lane] = NR[c]; }
-        }
-        __syncthreads();
-        if (warp > 0) {
-            const float *cu = carry + (warp - 1) * 2 * kBCH * 32;
-            const int y = yb0 + kBRows * warp;
-#pragma unroll
-            for (int c = 0; c < kBCH; c++) {
-                const float l = FL[c] + cu[c * 32 + lane], r = FR[c] + cu[(kBCH + c) * 32 + lane];
-                const float v = l + __shfl_up_sync(0xffffffffu, r, 1);
-                if (c < cn && dxn && pxin && y < a.H)
-                    dxn[(long long)(c0 + c) * HW + (long long)y * a.W + px] = v;
-            }
+        switch (cn) {
+            case 4: run_chunk(S, c0, std::integral_constant<int, 4>{}); break;
+            case 3: run_chunk(S, c0, std::integral_constant<int, 3>{}); break;
+            case 2: run_chunk(S, c0, std::integral_constant<int, 2>{}); break;
+            default: run_chunk(S, c0, std::integral_constant<int, 1>{}); break;
         }
         __syncthreads();
     }
@@ -770,7 +783,8 @@ StnWs stn_ws_layout(void *base, int N, int H, int W, int Ho, int Wo) {
 size_t out_tile_smem() { return sizeof(int) * (5 * kFRMax + 16) + sizeof(float) * 2 * kFStage; }
 size_t bwd_cell_smem() {
     return sizeof(float) * 2 * kBStage + (sizeof(uint2) + sizeof(unsigned)) * kBFQMax +
-           sizeof(int4) * kBRQMax + sizeof(int) * (5 * kBRQMax + 8) + sizeof(float) * kBWarps * 2 * kBCH * 32;
+           sizeof(int4) * kBRQMax + sizeof(int) * (5 * kBRQMax + 8) + sizeof(float) * kBWarps * 2 * kBCH * 32 +
+           sizeof(unsigned short) * kBWarps * (kBRows + 1) * kBHits * 32 + kBWarps * (kBRows + 1) * 32;
 }
 
 template <typename K>
@@ -817,7 +831,7 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
     note_launch();
     // AUTO / GATHER: cell-owner gather where the preimage is bounded (zeros padding);
     // SCATTER_ATOMIC or border padding: every sample takes the fallback pair.
-    const int allow_gather = (algo == 0 || algo == 1) && !a.border;
+    const int allow_gather = (algo == 0 || algo == 1) && !a.border && HW * kBCH < (1LL << 31);
     stn_classify_kernel<<<1, 256, 0, s>>>(a, allow_gather, w.flags, w.fb_list, w.fb_count);
     note_launch();
     if (!allow_gather && a.dx) {
