@@ -38,6 +38,7 @@ constexpr int kTileY = 64;    // nominal max sub-tile height (px)
 constexpr int kTileXS = kTileX + 2, kTileYS = kTileY + 2;
 constexpr int kPlaneStride = 13;  // float4 per z-plane in smem (12 + 1 pad: conflict-free)
 constexpr unsigned kInvalid = 0xffffffffu;
+constexpr int kChunk = 16;  // pixels per warp step in the backward (lane pairs)
 
 // ----------------------------------------------------------------- exact coordinates (R5)
 RS_DEV double bs_cx(int x, int W, int Gw) {
@@ -196,35 +197,37 @@ RS_DEV void rs_stage(float *v, int lane, int m) {
     }
 }
 
-// acc index: ((e*2 + b)*2 + a)*12 + q ; e = z-plane (0: zl, 1: zh), (b, a) = corner.
+// Lane pairs: lane 2s+e owns pixel slot s of the chunk and z-plane e (0: clamp(bin-1),
+// 1: clamp(bin)).  acc index: (b*2 + a)*12 + q, (b, a) = spatial corner.
+// Reduce-scatter across the 16 lanes of the same plane (xor 16, 8, 4, 2: 45
+// shuffles); lane then owns 3 sums, base = 24 b4 + 12 b3 + 6 b2 + 3 b1.
 // wacc (warp slot): [corner(4)][z(D)][q(12)]
 RS_DEV void flush_acc(float *acc, float *wacc, int bin, int D, int lane) {
-    rs_stage<48>(acc, lane, 16);
-    rs_stage<24>(acc, lane, 8);
-    rs_stage<12>(acc, lane, 4);
-    rs_stage<6>(acc, lane, 2);
-    rs_stage<3>(acc, lane, 1);
-    const int base = ((lane & 16) ? 48 : 0) + ((lane & 8) ? 24 : 0) + ((lane & 4) ? 12 : 0) +
-                     ((lane & 2) ? 6 : 0) + ((lane & 1) ? 3 : 0);
-    const int zl = clampi(bin - 1, 0, D - 1), zh = clampi(bin, 0, D - 1);
-    // e = 0 lanes (0..15) first, then e = 1: zl may equal zh (clamped planes)
+    rs_stage<24>(acc, lane, 16);
+    rs_stage<12>(acc, lane, 8);
+    rs_stage<6>(acc, lane, 4);
+    rs_stage<3>(acc, lane, 2);
+    const int base = ((lane & 16) ? 24 : 0) + ((lane & 8) ? 12 : 0) + ((lane & 4) ? 6 : 0) + ((lane & 2) ? 3 : 0);
+    const int e = lane & 1;
+    const int z = e ? clampi(bin, 0, D - 1) : clampi(bin - 1, 0, D - 1);
+    // plane-0 lanes first, then plane-1: the two planes coincide when clamped
 #pragma unroll
     for (int ph = 0; ph < 2; ph++) {
-        if ((lane >> 4) == ph) {
+        if (e == ph) {
 #pragma unroll
             for (int t = 0; t < 3; t++) {
                 const int idx = base + t;
-                const int q = idx % 12, corner = (idx / 12) & 3, e = idx / 48;
-                wacc[(corner * D + (e ? zh : zl)) * 12 + q] += acc[t];
+                const int q = idx % 12, corner = idx / 12;
+                wacc[(corner * D + z) * 12 + q] += acc[t];
             }
         }
         __syncwarp();
     }
 #pragma unroll
-    for (int k = 0; k < 96; k++) acc[k] = 0.f;
+    for (int k = 0; k < 48; k++) acc[k] = 0.f;
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
     bslice_bwd_tiled(BsliceArgs a, int SY, int SX, float *__restrict__ partials) {
     extern __shared__ float4 smem4[];
     const int D = a.D, NB = D + 1;
@@ -236,15 +239,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     int *cnt = (int *)(wacc + kWarps * 4 * D * 12);         // kWarps * NB
     int *bstart = cnt + kWarps * NB;                        // NB + 1
     int *chunk_bin = bstart + NB + 1;                       // max chunks
-    const int max_chunks = (kTileXS * kTileYS) / 32 + 1 + NB;
-    unsigned *sorted = (unsigned *)(chunk_bin + max_chunks);  // max_chunks * 32
-    unsigned char *binv = (unsigned char *)(sorted + max_chunks * 32);  // kTileXS*kTileYS
+    const int max_chunks = (kTileXS * kTileYS) / kChunk + 1 + NB;
+    unsigned *sorted = (unsigned *)(chunk_bin + max_chunks);  // max_chunks * kChunk
+    float *fzv = (float *)(((uintptr_t)(sorted + max_chunks * kChunk) + 15) & ~(uintptr_t)15);  // kTileXS*kTileYS
+    unsigned char *binv = (unsigned char *)(fzv + kTileXS * kTileYS);    // kTileXS*kTileYS
 
     const Tile t = tile_of(blockIdx.x, a.Gh, a.Gw, SY, SX, a.H, a.W);
     const int TW = t.xe - t.xs, TH = t.ye - t.ys;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const long long HW = (long long)a.H * a.W;
     const float *gd = a.guide + (long long)t.n * HW;
+
+    // guide tile -> smem (cp.async; overlaps the corner staging below)
+    {
+        const bool vec = (TW % 4 == 0) && (a.W % 4 == 0) && (t.xs % 4 == 0) &&
+                         (((uintptr_t)a.guide & 15u) == 0);
+        const int wq = vec ? TW / 4 : TW;
+        for (int e = threadIdx.x; e < TH * wq; e += kThreads) {
+            const int r = e / wq, q = e - r * wq;
+            const float *src = gd + (long long)(t.ys + r) * a.W + t.xs;
+            if (vec) cp_async16(fzv + r * TW + 4 * q, src + 4 * q);
+            else cp_async4(fzv + r * TW + q, src + q);
+        }
+        cp_async_commit();
+    }
 
     stage_corners(glo, gdz, a.grid, t, D, a.Gh, a.Gw);
     for (int c = threadIdx.x; c < TW; c += kThreads) {
@@ -257,6 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int e = threadIdx.x; e < kWarps * 4 * D * 12; e += kThreads) wacc[e] = 0.f;
     for (int e = threadIdx.x; e < kWarps * NB; e += kThreads) cnt[e] = 0;
+    cp_async_wait<0>();
     __syncthreads();
 
     // ---- pass A: z-bin of every pixel, per-warp counts (warp w: rows w, w+8, ...)
@@ -266,8 +285,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             int bin = -1;
             if (c < TW) {
                 float fz;
-                z_cell(__ldg(gd + (long long)(t.ys + r) * a.W + t.xs + c), D, bin, fz);
+                z_cell(fzv[r * TW + c], D, bin, fz);  // guide value staged above, fz in place
                 binv[r * TW + c] = (unsigned char)bin;
+                fzv[r * TW + c] = fz;
             }
             const unsigned m = __match_any_sync(0xffffffffu, bin);
             if (bin >= 0 && lane == __ffs(m) - 1) cnt[w * NB + bin] += __popc(m);
@@ -284,16 +304,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 cnt[ww * NB + b] = run;
                 run += v;
             }
-            run = (run + 31) & ~31;
+            run = (run + kChunk - 1) & ~(kChunk - 1);
         }
         bstart[NB] = run;
     }
     __syncthreads();
-    const int L = bstart[NB], nchunks = L >> 5;
+    const int L = bstart[NB], nchunks = L / kChunk;
     for (int e = threadIdx.x; e < L; e += kThreads) sorted[e] = kInvalid;
     for (int c = threadIdx.x; c < nchunks; c += kThreads) {
         int b = 0;
-        while (bstart[b + 1] <= c * 32) b++;
+        while (bstart[b + 1] <= c * kChunk) b++;
         chunk_bin[c] = b;
     }
     __syncthreads();
@@ -322,38 +342,54 @@ __global__ void __launch_bounds__(kThreads, 1)
     float *mywacc = wacc + w * 4 * D * 12;
     const int cbeg = (int)(((long long)nchunks * w) / kWarps);
     const int cend = (int)(((long long)nchunks * (w + 1)) / kWarps);
-    float acc[96];
+    float acc[48];
 #pragma unroll
-    for (int k = 0; k < 96; k++) acc[k] = 0.f;
+    for (int k = 0; k < 48; k++) acc[k] = 0.f;
+    const int slot = lane >> 1, e_pl = lane & 1;
     int cur_bin = cbeg < cend ? chunk_bin[cbeg] : 0;
+    // software pipeline: the next chunk's X / dY loads are in flight while this one computes
+    unsigned ent_n = cbeg < cend ? sorted[cbeg * kChunk + slot] : kInvalid;
+    float Xn[3] = {0.f, 0.f, 0.f}, Gn[3] = {0.f, 0.f, 0.f};
+    auto fetch = [&](unsigned ent) {
+        if (ent != kInvalid) {
+            const long long o = (long long)(t.ys + (int)(ent >> 16)) * a.W + t.xs + (int)(ent & 0xffffu);
+#pragma unroll
+            for (int i = 0; i < 3; i++) {
+                Xn[i] = __ldg(xp + i * HW + o);
+                Gn[i] = __ldg(gp + i * HW + o);
+            }
+        }
+    };
+    fetch(ent_n);
     for (int ch = cbeg; ch < cend; ch++) {
         const int bin = chunk_bin[ch];
         if (bin != cur_bin) {
             flush_acc(acc, mywacc, cur_bin, D, lane);
             cur_bin = bin;
         }
-        const unsigned ent = sorted[ch * 32 + lane];
+        const unsigned ent = ent_n;
+        float X[3], G[3];
+#pragma unroll
+        for (int i = 0; i < 3; i++) { X[i] = Xn[i]; G[i] = Gn[i]; }
+        if (ch + 1 < cend) {
+            ent_n = sorted[(ch + 1) * kChunk + slot];
+            fetch(ent_n);
+        }
         const bool valid = ent != kInvalid;
         const int r = valid ? (int)(ent >> 16) : 0, c = valid ? (int)(ent & 0xffffu) : 0;
         const long long o = (long long)(t.ys + r) * a.W + t.xs + c;
-        float fz = 0.f, X[3] = {0.f, 0.f, 0.f}, G[3] = {0.f, 0.f, 0.f};
         const float fx = fxt[c], fy = fyt[r];
-        if (valid) {
-            int bb;
-            z_cell(__ldg(gd + o), D, bb, fz);
+        const float fz = valid ? fzv[r * TW + c] : 0.f;
+        if (!valid) {
 #pragma unroll
-            for (int i = 0; i < 3; i++) {
-                X[i] = __ldg(xp + i * HW + o);
-                G[i] = __ldg(gp + i * HW + o);
-            }
+            for (int i = 0; i < 3; i++) { X[i] = 0.f; G[i] = 0.f; }
         }
         const float4 *Lc = glo + bin * kPlaneStride, *Dc = gdz + bin * kPlaneStride;
-        const float wx1 = fx, wx0 = 1.f - fx, wy1 = fy, wy0 = 1.f - fy, wz1 = fz, wz0 = 1.f - fz;
-        float wt[8];
-        wt[0] = wz0 * wy0 * wx0; wt[1] = wz0 * wy0 * wx1;
-        wt[2] = wz0 * wy1 * wx0; wt[3] = wz0 * wy1 * wx1;
-        wt[4] = wz1 * wy0 * wx0; wt[5] = wz1 * wy0 * wx1;
-        wt[6] = wz1 * wy1 * wx0; wt[7] = wz1 * wy1 * wx1;
+        const float wz = e_pl ? fz : 1.f - fz;
+        const float wzy0 = wz * (1.f - fy), wzy1 = wz * fy;
+        float wt[4];
+        wt[0] = wzy0 * (1.f - fx); wt[1] = wzy0 * fx;
+        wt[2] = wzy1 * (1.f - fx); wt[3] = wzy1 * fx;
         float dx[3] = {0.f, 0.f, 0.f}, dgd = 0.f;
 #pragma unroll
         for (int oc = 0; oc < 3; oc++) {
@@ -366,10 +402,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (i < 3) dx[i] = fmaf(G[oc], fmaf(fz, d, lo), dx[i]);
                 dgd = fmaf(P, d, dgd);
 #pragma unroll
-                for (int tt = 0; tt < 8; tt++) acc[tt * 12 + q] = fmaf(wt[tt], P, acc[tt * 12 + q]);
+                for (int tt = 0; tt < 4; tt++) acc[tt * 12 + q] = fmaf(wt[tt], P, acc[tt * 12 + q]);
             }
         }
-        if (valid) {
+        if (valid && e_pl == 0) {
             if (dxp) {
 #pragma unroll
                 for (int i = 0; i < 3; i++) dxp[i * HW + o] = dx[i];
@@ -562,10 +598,11 @@ size_t fwd_smem(int D) {
 
 size_t bwd_smem(int D) {
     const int NB = D + 1;
-    const int max_chunks = (kTileXS * kTileYS) / 32 + 1 + NB;
+    const int max_chunks = (kTileXS * kTileYS) / kChunk + 1 + NB;
     return sizeof(float4) * 2 * (D + 1) * kPlaneStride + sizeof(float) * (kTileXS + kTileYS) +
            sizeof(float) * kWarps * 4 * D * 12 + sizeof(int) * (kWarps * NB + NB + 1) +
-           sizeof(int) * max_chunks + sizeof(unsigned) * max_chunks * 32 + kTileXS * kTileYS;
+           sizeof(int) * max_chunks + sizeof(unsigned) * max_chunks * kChunk + kTileXS * kTileYS +
+           sizeof(float) * kTileXS * kTileYS + 16;
 }
 
 }  // namespace
