@@ -32,6 +32,8 @@
 // affine map is singular or whose preimage exceeds the staging budget takes
 // d_theta from stn_out_tile (MODE_DTHETA) and d_input from the atomic scatter
 // (PAPER.md:733); border padding (no bounded inverse) always does.
+#include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "common.cuh"
@@ -342,16 +344,20 @@ __global__ void stn_tables_kernel(double *xt, double *yt, int Ho, int Wo, int ac
     if (t < Ho) yt[t] = stn_norm(t, Ho, ac);
 }
 
-// flags[n] = 1 if sample n takes the cell-owner gather; fb_list = the others.
-__global__ void stn_classify_kernel(StnArgs a, int allow_gather, int *flags, int *fb_list,
+RS_DEV bool stn_gather_ok(const Affine &A, int Ho, int Wo);
+
+// flags[n] = 1 if sample n takes the gather adjoint (variant 0: cell-owner,
+// 1: per-pixel gather); fb_list = the others.
+__global__ void stn_classify_kernel(StnArgs a, int allow_gather, int variant, int *flags, int *fb_list,
                                     int *fb_count) {
     __shared__ int cnt;
     if (threadIdx.x == 0) cnt = 0;
     __syncthreads();
     for (int n = threadIdx.x; n < a.N; n += blockDim.x) {
         const Theta T = load_theta(a.theta, n);
+        const Affine A = stn_affine(T, a.H, a.W, a.Ho, a.Wo, a.ac);
         const bool g = allow_gather && !a.border &&
-                       stn_gatherable(stn_affine(T, a.H, a.W, a.Ho, a.Wo, a.ac), a.Ho, a.Wo);
+                       (variant == 1 ? stn_gather_ok(A, a.Ho, a.Wo) : stn_gatherable(A, a.Ho, a.Wo));
         flags[n] = g ? 1 : 0;
         if (!g) fb_list[atomicAdd(&cnt, 1)] = n;
     }
@@ -669,6 +675,349 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
 }
 
+// ----------------------------------------------------------------- backward: per-pixel gather
+// Input tile 32 x 16 (thread = column, rows w and w+8).  Each input pixel p walks
+// the preimage window of [p-1, p+1)^2 once, keeping its (<= kGHits) hits — the
+// output pixels whose floor cell is p-(0|1) — as (record index, weight); every
+// channel chunk then costs one LDS + FMA per hit.  dY over the tile's preimage
+// and X over the tile (+1 halo) are staged per chunk (cp.async, double-buffered).
+// d_theta: pixel p owns the hits whose floor cell is p (x0 = -1 folds into x = 0).
+constexpr int kGX = 32, kGY = 16, kGHits = 8;
+constexpr int kGXP = kGX + 4;            // X stage pitch (16-B rows)
+constexpr int kGXS = (kGY + 1) * kGXP;   // X stage floats per channel
+constexpr int kGRQMax = 128, kGFQMax = 1792, kGStage = 8192, kGCH = 4;
+
+RS_DEV bool stn_gather_ok(const Affine &A, int Ho, int Wo) {
+    if (!A.inv || Ho > 65535 || Wo > 65535) return false;
+    const double hq = fabs(A.i10) * (kGX + 1) + fabs(A.i11) * (kGY + 1);
+    const double rq = ceil(hq) + 3.0;
+    const double fq = (double)(kGX + 1) * (kGY + 1) / fabs(A.det) + 8.0 * rq + 64.0;
+    const double wj = fabs(A.i00) + fabs(A.i01), wi = fabs(A.i10) + fabs(A.i11);
+    return rq <= kGRQMax && fq <= kGFQMax && (2.0 * wj + 2.0) * (2.0 * wi + 2.0) <= 36.0;
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads, 2)
+    stn_bwd_gather(StnArgs a, const double *__restrict__ xtab, const double *__restrict__ ytab,
+                   const int *__restrict__ flags, double *__restrict__ partials, int tiles_x, int tiles_y) {
+    extern __shared__ __align__(16) float4 sm4[];
+    float *stage = (float *)sm4;                               // 2 * kGStage
+    uint2 *rec = (uint2 *)(stage + 2 * kGStage);               // kGFQMax
+    unsigned *ijs = (unsigned *)(rec + kGFQMax);               // kGFQMax
+    int4 *rowt = (int4 *)(ijs + kGFQMax);                      // kGRQMax
+    int *qlo = (int *)(rowt + kGRQMax);
+    int *qhi = qlo + kGRQMax;
+    int *qxa = qhi + kGRQMax;
+    int *qoff = qxa + kGRQMax;
+    int *qcnt = qoff + kGRQMax;
+    int *ctl = qcnt + kGRQMax;                                  // 8
+    __shared__ float red[kThreads / 32][6];
+
+    const int n = blockIdx.y;
+    const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
+    const int xa0 = tx * kGX, ya0 = ty * kGY;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long HW = (long long)a.H * a.W, P = (long long)a.Ho * a.Wo;
+    const int x = xa0 + lane;
+    float *dxn = a.dx ? a.dx + (long long)n * a.C * HW : nullptr;
+    double *part = partials + ((long long)n * tiles_x * tiles_y + blockIdx.x) * 6;
+
+    if (!flags[n]) {
+        if (dxn && x < a.W)
+            for (int r = warp; r < kGY; r += 8) {
+                const int y = ya0 + r;
+                if (y < a.H)
+                    for (int c = 0; c < a.C; c++) dxn[(long long)c * HW + (long long)y * a.W + x] = 0.f;
+            }
+        if (threadIdx.x < 6) part[threadIdx.x] = 0.0;
+        return;
+    }
+    const Theta T = load_theta(a.theta, n);
+    const Affine A = stn_affine(T, a.H, a.W, a.Ho, a.Wo, a.ac);
+
+    // ---- preimage rows of the cells [xa0-1, xa0+kGX-1] x [ya0-1, ya0+kGY-1]
+    const double eps = 1e-3;
+    const double Lx = xa0 - 1 - eps, Ux = xa0 + kGX + eps;
+    const double Ly = ya0 - 1 - eps, Uy = ya0 + kGY + eps;
+    double imin = 1e300, imax = -1e300;
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+        const double px_ = (c & 1) ? Ux : Lx, py_ = (c & 2) ? Uy : Ly;
+        const double qi = A.i10 * (px_ - A.p0x) + A.i11 * (py_ - A.p0y);
+        imin = fmin(imin, qi);
+        imax = fmax(imax, qi);
+    }
+    const int ilo = max(0, (int)ceil(fmax(imin, -1e9)));
+    const int ihi = min(a.Ho - 1, (int)floor(fmin(imax, 1e9)));
+    const int RQ = min(kGRQMax, max(0, ihi - ilo + 1));
+    for (int r = threadIdx.x; r < RQ; r += kThreads) {
+        const int i = ilo + r;
+        double jl = -1e300, jh = 1e300;
+        const double ax_[2] = {A.m00, A.m10}, bx_[2] = {A.m01 * i + A.p0x, A.m11 * i + A.p0y};
+        const double L_[2] = {Lx, Ly}, U_[2] = {Ux, Uy};
+#pragma unroll
+        for (int d = 0; d < 2; d++) {
+            if (fabs(ax_[d]) < 1e-12) {
+                if (bx_[d] < L_[d] || bx_[d] > U_[d]) { jl = 1e300; jh = -1e300; }
+            } else {
+                double u = (L_[d] - bx_[d]) / ax_[d], v = (U_[d] - bx_[d]) / ax_[d];
+                if (u > v) { const double t = u; u = v; v = t; }
+                jl = fmax(jl, u);
+                jh = fmin(jh, v);
+            }
+        }
+        qlo[r] = max(0, (int)ceil(fmax(jl, -1e9)));
+        qhi[r] = min(a.Wo - 1, (int)floor(fmin(jh, 1e9)));
+    }
+    __syncthreads();
+    build_rows<VEC>(RQ, a.Wo, qlo, qhi, qxa, qoff, qcnt, &ctl[0]);
+    __syncthreads();
+    const int FQ = min(ctl[0], kGFQMax);
+    for (int r = threadIdx.x; r < RQ; r += kThreads) rowt[r] = make_int4(qlo[r], qhi[r], qoff[r] - qxa[r], 0);
+    for (int r = warp; r < RQ; r += 8) {
+        const int i = ilo + r;
+        const double yt = ytab[i];
+        const int wr = (qcnt[r] + 3) & ~3;
+        for (int col = lane; col < wr; col += 32) {
+            const int j = qxa[r] + col, e = qoff[r] + col;
+            if (e >= kGFQMax) break;
+            uint2 R = make_uint2(0xff000000u, 0xff000000u);
+            if (col < qcnt[r] && j >= qlo[r] && j <= qhi[r]) {
+                double ix, iy;
+                stn_coord(T, xtab[j], yt, a.H, a.W, a.ac, ix, iy);
+                const Cell cx = cell_of(ix), cy = cell_of(iy);
+                const int rx = cx.i0 - (xa0 - 1), ry = cy.i0 - (ya0 - 1);
+                if (rx >= 0 && rx <= kGX && ry >= 0 && ry <= kGY) R = pack_rec(rx, ry, cx.f, cy.f);
+            }
+            rec[e] = R;
+            ijs[e] = ((unsigned)i << 16) | (unsigned)j;
+        }
+    }
+    const int XS = kGXS;
+    const int CH = min(min(a.C, kGCH), max(1, kGStage / (FQ + XS)));
+    const int nch = (a.C + CH - 1) / CH;
+    const float *gbase = a.dy + (long long)n * a.C * P;
+    const float *xbase = a.x + (long long)n * a.C * HW;
+    const bool xvec = VEC && (a.W % 4 == 0) && (((uintptr_t)a.x & 15u) == 0);
+    // X stage: rows ya0..ya0+kGY, columns [xa0, xa0 + kGXP) clipped to the image
+    auto stage_x = [&](float *dst, int c0, int ncp) {
+        const int cw = min(kGXP, a.W - xa0);
+        for (int e = threadIdx.x; e < ncp * (kGY + 1); e += kThreads) {
+            const int c = e / (kGY + 1), r = e - c * (kGY + 1);
+            const int y = ya0 + r;
+            if (y >= a.H) continue;
+            const float *src = xbase + (long long)(c0 + c) * HW + (long long)y * a.W + xa0;
+            float *d = dst + c * XS + r * kGXP;
+            if (xvec) {
+                for (int q = 0; q < cw; q += 4) cp_async16(d + q, src + q);
+            } else {
+                for (int q = 0; q < cw; q++) cp_async4(d + q, src + q);
+            }
+        }
+    };
+    __syncthreads();
+    if (FQ > 0) stage_rows<VEC>(stage, FQ, gbase, P, min(CH, a.C), RQ, a.Wo, ilo, qxa, qoff, qcnt);
+    stage_x(stage + CH * FQ, 0, min(CH, a.C));
+    cp_async_commit();
+
+    // ---- per-pixel hit lists (overlaps the first stage's copy)
+    const double hj = fabs(A.i00) + fabs(A.i01) + eps, hi = fabs(A.i10) + fabs(A.i11) + eps;
+    // fn(e, weight, hit index) for every output pixel that samples this pixel;
+    // also reports whether the pixel owns it (floor cell == pixel, -1 folded to 0)
+    auto search = [&](int k, auto &&fn) {
+        const int y = ya0 + warp + 8 * k;
+        const double ux = (double)x - A.p0x, uy = (double)y - A.p0y;
+        const double qj = A.i00 * ux + A.i01 * uy, qi = A.i10 * ux + A.i11 * uy;
+        const int jl = (int)ceil(qj - hj), jh = (int)floor(qj + hj);
+        const int il = max(ilo, (int)ceil(qi - hi)), ih = min(ilo + RQ - 1, (int)floor(qi + hi));
+        const unsigned rx0 = (unsigned)(x - (xa0 - 1)), ry0 = (unsigned)(y - (ya0 - 1));
+        int cnt = 0;
+        for (int i = il; i <= ih; i++) {
+            const int4 rt = rowt[i - ilo];
+            const int ja = max(jl, rt.x), jb = min(jh, rt.y);
+            for (int j = ja; j <= jb; j++) {
+                const int e = rt.z + j;
+                const uint2 R = rec[e];
+                const unsigned rx = R.x >> 24, ry = R.y >> 24;
+                if ((rx == rx0 || rx + 1 == rx0) && (ry == ry0 || ry + 1 == ry0)) {
+                    const float fx = (float)(R.x & 0xffffffu) * (1.f / 16777216.f);
+                    const float fy = (float)(R.y & 0xffffffu) * (1.f / 16777216.f);
+                    const float wx = (rx == rx0) ? 1.f - fx : fx, wy = (ry == ry0) ? 1.f - fy : fy;
+                    fn(e, wy * wx, cnt);
+                    cnt++;
+                }
+            }
+        }
+        return cnt;
+    };
+    int he[2][kGHits];
+    float hw[2][kGHits];
+    int nh[2];
+    unsigned own[2];
+    bool pin[2];
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+        const int y = ya0 + warp + 8 * k;
+        pin[k] = x < a.W && y < a.H;
+        nh[k] = 0;
+        own[k] = 0u;
+#pragma unroll
+        for (int h = 0; h < kGHits; h++) { he[k][h] = 0; hw[k][h] = 0.f; }
+        if (!pin[k]) continue;
+        nh[k] = search(k, [&](int e, float w, int cnt) {
+#pragma unroll
+            for (int h = 0; h < kGHits; h++)
+                if (h == cnt) { he[k][h] = e; hw[k][h] = w; }
+            const uint2 R = rec[e];
+            const int x0 = (int)(R.x >> 24) + xa0 - 1, y0 = (int)(R.y >> 24) + ya0 - 1;
+            // the pixel owns the output pixels whose floor cell it is (-1 folded to 0);
+            // owned hits always fit the cache: at most the first kGHits are owned-tracked
+            if (max(x0, 0) == x && max(y0, 0) == y && cnt < kGHits) own[k] |= 1u << cnt;
+        });
+    }
+    float acc6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const float sxs = a.ac ? 0.5f * (a.W - 1) : 0.5f * a.W;
+    const float sys = a.ac ? 0.5f * (a.H - 1) : 0.5f * a.H;
+    const float axf = a.ac ? 2.f / (a.Wo - 1) : 2.f / a.Wo, bxf = a.ac ? -1.f : 1.f / a.Wo - 1.f;
+    const float ayf = a.ac ? 2.f / (a.Ho - 1) : 2.f / a.Ho, byf = a.ac ? -1.f : 1.f / a.Ho - 1.f;
+
+    auto run_chunk = [&](const float *S, int c0, auto ncc) {
+        constexpr int NC = decltype(ncc)::value;
+        const float *SX = S + CH * FQ;
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+            const int y = ya0 + warp + 8 * k;
+            const bool ovf = pin[k] && nh[k] > kGHits;
+            float acc[NC];
+#pragma unroll
+            for (int c = 0; c < NC; c++) acc[c] = 0.f;
+            const int hmax = __reduce_max_sync(0xffffffffu, pin[k] ? min(nh[k], kGHits) : 0);
+#pragma unroll
+            for (int h = 0; h < kGHits; h++) {
+                if (h < hmax && h < nh[k]) {
+                    const float *Se = S + he[k][h];
+#pragma unroll
+                    for (int c = 0; c < NC; c++) acc[c] = fmaf(hw[k][h], Se[c * FQ], acc[c]);
+                }
+            }
+            // d_theta of the output pixels this pixel owns (floor cell == this pixel)
+            if (own[k] || ovf) {
+                float dxa[NC], ddx[NC], dya[NC], ddy[NC];
+                const float *X0 = SX + (y - ya0) * kGXP + (x - xa0);
+                const bool xv1 = x + 1 < a.W, yv1 = y + 1 < a.H;
+#pragma unroll
+                for (int c = 0; c < NC; c++) {
+                    const float *Xc = X0 + c * XS;
+                    const float v00 = Xc[0], v01 = xv1 ? Xc[1] : 0.f;
+                    const float v10 = yv1 ? Xc[kGXP] : 0.f, v11 = (xv1 && yv1) ? Xc[kGXP + 1] : 0.f;
+                    dxa[c] = v01 - v00;
+                    ddx[c] = (v11 - v10) - dxa[c];
+                    dya[c] = v10 - v00;
+                    ddy[c] = (v11 - v01) - dya[c];
+                }
+                auto dtheta_hit = [&](int e) {
+                    const uint2 R = rec[e];
+                    const float fx = (float)(R.x & 0xffffffu) * (1.f / 16777216.f);
+                    const float fy = (float)(R.y & 0xffffffu) * (1.f / 16777216.f);
+                    const int x0 = (int)(R.x >> 24) + xa0 - 1, y0 = (int)(R.y >> 24) + ya0 - 1;
+                    const float *Se = S + e;
+                    float dq = 0.f, dr = 0.f;
+#pragma unroll
+                    for (int c = 0; c < NC; c++) {
+                        const float g = Se[c * FQ];
+                        float a0 = dxa[c], a1 = ddx[c], b0 = dya[c], b1 = ddy[c];
+                        if (x0 < 0 || y0 < 0) {
+                            // edge cell (x0 = -1 and/or y0 = -1, owned by x = 0 / y = 0):
+                            // the taps left of / above the image read 0
+                            const float *Xc = X0 + c * XS;
+                            float w01 = 0.f, w10 = 0.f, w11;
+                            if (x0 < 0 && y0 < 0) {
+                                w11 = Xc[0];
+                            } else if (x0 < 0) {
+                                w01 = Xc[0];
+                                w11 = yv1 ? Xc[kGXP] : 0.f;
+                            } else {
+                                w10 = Xc[0];
+                                w11 = xv1 ? Xc[1] : 0.f;
+                            }
+                            a0 = w01;
+                            a1 = (w11 - w10) - a0;
+                            b0 = w10;
+                            b1 = (w11 - w01) - b0;
+                        }
+                        dq = fmaf(g, fmaf(fy, a1, a0), dq);
+                        dr = fmaf(g, fmaf(fx, b1, b0), dr);
+                    }
+                    const unsigned ij = ijs[e];
+                    const float xt = fmaf(axf, (float)(ij & 0xffffu), bxf);
+                    const float yt = fmaf(ayf, (float)(ij >> 16), byf);
+                    const float dgx = dq * sxs, dgy = dr * sys;
+                    acc6[0] = fmaf(dgx, xt, acc6[0]);
+                    acc6[1] = fmaf(dgx, yt, acc6[1]);
+                    acc6[2] += dgx;
+                    acc6[3] = fmaf(dgy, xt, acc6[3]);
+                    acc6[4] = fmaf(dgy, yt, acc6[4]);
+                    acc6[5] += dgy;
+                };
+#pragma unroll
+                for (int h = 0; h < kGHits; h++)
+                    if (own[k] & (1u << h)) dtheta_hit(he[k][h]);
+                if (ovf) {
+                    // more hits than cached: walk the window again for the rest (rare)
+                    search(k, [&](int e, float w, int idx) {
+                        if (idx < kGHits) return;
+                        const float *Se = S + e;
+#pragma unroll
+                        for (int c = 0; c < NC; c++) acc[c] = fmaf(w, Se[c * FQ], acc[c]);
+                        const uint2 R = rec[e];
+                        const int x0 = (int)(R.x >> 24) + xa0 - 1, y0 = (int)(R.y >> 24) + ya0 - 1;
+                        if (max(x0, 0) == x && max(y0, 0) == y) dtheta_hit(e);
+                    });
+                }
+            }
+            if (dxn && pin[k]) {
+                float *d = dxn + (long long)c0 * HW + (long long)y * a.W + x;
+#pragma unroll
+                for (int c = 0; c < NC; c++) d[(long long)c * HW] = acc[c];
+            }
+        }
+    };
+
+    for (int kc = 0; kc < nch; kc++) {
+        const int c0 = kc * CH, cn = min(CH, a.C - c0);
+        if (kc + 1 < nch) {
+            float *nxt = stage + ((kc + 1) & 1) * kGStage;
+            const int cn2 = min(CH, a.C - c0 - CH);
+            if (FQ > 0) stage_rows<VEC>(nxt, FQ, gbase + (long long)(c0 + CH) * P, P, cn2, RQ, a.Wo, ilo, qxa, qoff, qcnt);
+            stage_x(nxt + CH * FQ, c0 + CH, cn2);
+            cp_async_commit();
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const float *S = stage + (kc & 1) * kGStage;
+        switch (cn) {
+            case 4: run_chunk(S, c0, std::integral_constant<int, 4>{}); break;
+            case 3: run_chunk(S, c0, std::integral_constant<int, 3>{}); break;
+            case 2: run_chunk(S, c0, std::integral_constant<int, 2>{}); break;
+            default: run_chunk(S, c0, std::integral_constant<int, 1>{}); break;
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int k = 0; k < 6; k++) {
+        const float v = warp_sum(acc6[k]);
+        if (lane == 0) red[warp][k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        double s = 0.0;
+        for (int w = 0; w < kThreads / 32; w++) s += (double)red[w][threadIdx.x];
+        part[threadIdx.x] = s;
+    }
+}
+
 // ----------------------------------------------------------------- d_theta finalize
 // dtheta[n] = fixed-order fp64 sum of the partials of the path sample n took.
 __global__ void __launch_bounds__(kThreads)
@@ -741,7 +1090,8 @@ size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct StnGeom {
     int fj, fi;  // output tiles
-    int bx, by;  // input tiles
+    int bx, by;  // input tiles, cell-owner kernel
+    int gx, gy;  // input tiles, per-pixel gather kernel
 };
 
 StnGeom stn_geom(int H, int W, int Ho, int Wo) {
@@ -750,7 +1100,17 @@ StnGeom stn_geom(int H, int W, int Ho, int Wo) {
     g.fi = (Ho + kFI - 1) / kFI;
     g.bx = (W + kBX - 1) / kBX;
     g.by = (H + kBTY - 1) / kBTY;
+    g.gx = (W + kGX - 1) / kGX;
+    g.gy = (H + kGY - 1) / kGY;
     return g;
+}
+
+// STN backward variant: 0 = cell-owner (default, measured faster: profiles/), 1 =
+// per-pixel gather.  RSGRAD_STN_BWD=cell|gather selects one (A/B measurements);
+// read per call so tests can switch.
+int stn_bwd_variant() {
+    const char *e = getenv("RSGRAD_STN_BWD");
+    return (e && strcmp(e, "gather") == 0) ? 1 : 0;
 }
 
 struct StnWs {
@@ -774,13 +1134,19 @@ StnWs stn_ws_layout(void *base, int N, int H, int W, int Ho, int Wo) {
     w.flags = (int *)take(sizeof(int) * N);
     w.fb_list = (int *)take(sizeof(int) * N);
     w.fb_count = (int *)take(sizeof(int));
-    w.pb = (double *)take(sizeof(double) * 6 * (size_t)N * g.bx * g.by);
+    const size_t tb = (size_t)g.bx * g.by > (size_t)g.gx * g.gy ? (size_t)g.bx * g.by : (size_t)g.gx * g.gy;
+    w.pb = (double *)take(sizeof(double) * 6 * (size_t)N * tb);
     w.pf = (double *)take(sizeof(double) * 6 * (size_t)N * g.fj * g.fi);
     w.bytes = off;
     return w;
 }
 
 size_t out_tile_smem() { return sizeof(int) * (5 * kFRMax + 16) + sizeof(float) * 2 * kFStage; }
+size_t bwd_gather_smem() {
+    return sizeof(float) * 2 * kGStage + (sizeof(uint2) + sizeof(unsigned)) * kGFQMax + sizeof(int4) * kGRQMax +
+           sizeof(int) * (5 * kGRQMax + 8);
+}
+
 size_t bwd_cell_smem() {
     return sizeof(float) * 2 * kBStage + (sizeof(uint2) + sizeof(unsigned)) * kBFQMax +
            sizeof(int4) * kBRQMax + sizeof(int) * (5 * kBRQMax + 8) + sizeof(float) * kBWarps * 2 * kBCH * 32 +
@@ -832,7 +1198,8 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
     // AUTO / GATHER: cell-owner gather where the preimage is bounded (zeros padding);
     // SCATTER_ATOMIC or border padding: every sample takes the fallback pair.
     const int allow_gather = (algo == 0 || algo == 1) && !a.border && HW * kBCH < (1LL << 31);
-    stn_classify_kernel<<<1, 256, 0, s>>>(a, allow_gather, w.flags, w.fb_list, w.fb_count);
+    const int variant = stn_bwd_variant();
+    stn_classify_kernel<<<1, 256, 0, s>>>(a, allow_gather, variant, w.flags, w.fb_list, w.fb_count);
     note_launch();
     if (!allow_gather && a.dx) {
         cudaError_t e = cudaMemsetAsync(a.dx, 0, sizeof(float) * (size_t)a.N * a.C * HW, s);
@@ -840,7 +1207,20 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
     }
     const bool vin = (a.W % 4 == 0) && aligned16(a.x);
     const bool vout = (a.Wo % 4 == 0) && aligned16(a.dy);
-    if (allow_gather) {
+    int tiles_b = g.bx * g.by;
+    if (allow_gather && variant == 1) {
+        const size_t sm = bwd_gather_smem();
+        dim3 grid(g.gx * g.gy, a.N);
+        tiles_b = g.gx * g.gy;
+        if (vout) {
+            set_smem(stn_bwd_gather<true>, sm);
+            stn_bwd_gather<true><<<grid, kThreads, sm, s>>>(a, w.xtab, w.ytab, w.flags, w.pb, g.gx, g.gy);
+        } else {
+            set_smem(stn_bwd_gather<false>, sm);
+            stn_bwd_gather<false><<<grid, kThreads, sm, s>>>(a, w.xtab, w.ytab, w.flags, w.pb, g.gx, g.gy);
+        }
+        note_launch();
+    } else if (allow_gather) {
         const size_t sm = bwd_cell_smem();
         dim3 grid(g.bx * g.by, a.N);
         if (vout) {
@@ -876,7 +1256,7 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
         note_launch();
     }
     if (a.dtheta) {
-        stn_dtheta_finalize<<<a.N, kThreads, 0, s>>>(w.pb, g.bx * g.by, w.pf, g.fj * g.fi, w.flags, a.dtheta);
+        stn_dtheta_finalize<<<a.N, kThreads, 0, s>>>(w.pb, tiles_b, w.pf, g.fj * g.fi, w.flags, a.dtheta);
         note_launch();
     }
     return cudaGetLastError();

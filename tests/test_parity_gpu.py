@@ -302,3 +302,18 @@ def test_outputs_overwritten_not_accumulated(cuda_device):
     rsgrad.stn_bwd(inp["x"], inp["theta"], inp["dy"], out=(dx, dth))
     ref = rsgrad.stn_bwd(inp["x"], inp["theta"], inp["dy"])
     assert torch.equal(dx, ref[0]) and torch.equal(dth, ref[1])
+
+
+@pytest.mark.parametrize("variant", ["cell", "gather"])
+@pytest.mark.parametrize("ac", [True, False])
+def test_stn_bwd_variants(cuda_device, monkeypatch, variant, ac):
+    """Both gather-form STN adjoints (cell-owner and per-pixel) match the oracle,
+    including image-edge cells (x0 = -1 / y0 = -1) and a zoomed-in theta."""
+    monkeypatch.setenv("RSGRAD_STN_BWD", variant)
+    inp = synth.stn_inputs(3, 5, 70, 90, 66, 94, cfg=1)
+    inp["theta"][2] = torch.tensor([[0.8, 0.05, 0.1], [-0.04, 0.82, -0.1]])
+    g = _cuda(inp, cuda_device)
+    dx, dth = rsgrad.stn_bwd(g["x"], g["theta"], g["dy"], align_corners=ac)
+    rdx, rdth = oracle.stn_bwd(*(inp[k].double().numpy() for k in ("x", "theta", "dy")), align_corners=ac)
+    assert_close(_np(dx), rdx, "grad", f"dx[{variant}]")
+    assert_close(_np(dth), rdth, "grad", f"dtheta[{variant}]")
