@@ -425,6 +425,7 @@ def main():
     achieved = CALL_BYTES[dname] * P_rank / per_call[dom] / 1e9
     roof = {"bound": "hbm", "kernel": dname, "achieved": round(achieved, 1), "peak": peak,
             "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": ncu_traffic(dname, P_rank),
+            "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram__bytes_read+write per pixel x pixels per launch)",
             "algorithmic_bytes_per_launch": CALL_BYTES[dname] * P_rank, "peak_source": peak_src}
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
@@ -447,7 +448,9 @@ def main():
 
 
 def ncu_traffic(call, P_rank):
-    """dram bytes per launch from the committed ncu --set full summary, if any."""
+    """dram_bytes_read + dram_bytes_write per launch of `call`, from the committed
+    `ncu --set full` capture (profiles/ncu_traffic.json, measured per pixel at a
+    smaller batch and scaled to this launch's pixels), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
@@ -455,8 +458,7 @@ def ncu_traffic(call, P_rank):
         v = d.get(call)
         if v is None:
             return None
-        return {"dram_bytes": v["dram_bytes"], "per_pixel": v.get("per_pixel"),
-                "source": d.get("source", p)}
+        return round(v["per_pixel"] * P_rank)
     except Exception:  # noqa: BLE001
         return None
 

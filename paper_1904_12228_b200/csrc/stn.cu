@@ -373,8 +373,11 @@ RS_DEV uint2 pack_rec(int cx, int cy, float fx, float fy) {
     return make_uint2(((unsigned)cx << 24) | ux, ((unsigned)cy << 24) | uy);
 }
 
+#ifndef RS_CELL_MINB
+#define RS_CELL_MINB 2
+#endif
 template <bool VEC>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, RS_CELL_MINB)
     stn_bwd_cell(StnArgs a, const double *__restrict__ xtab, const double *__restrict__ ytab,
                  const int *__restrict__ flags, double *__restrict__ partials, int tiles_x,
                  int tiles_y) {
