@@ -118,6 +118,53 @@ RS_DEV void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// ----------------------------------------------------------------- TMA bulk copies (UBLKCP) + mbarrier
+RS_DEV void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+RS_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+// order this thread's earlier generic shared accesses before later async-proxy writes
+RS_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+RS_DEV void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+RS_DEV void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+RS_DEV bool mbar_try_wait(unsigned long long *bar, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+RS_DEV void mbar_wait(unsigned long long *bar, unsigned parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+
+// One bulk copy per (channel, row) segment (16-B aligned rows, widths multiple of
+// 16 B).  The caller's thread 0 arms `bar` with mbar_expect_tx(nch * sum(cnt) * 4).
+RS_DEV void stage_rows_bulk(float *dst, int F, const float *base, long long cstride, int nch, int R, int W,
+                            int ybase, const int *xa, const int *off, const int *cnt,
+                            unsigned long long *bar) {
+    fence_proxy_async();
+    for (int p = threadIdx.x; p < nch * R; p += blockDim.x) {
+        const int c = p / R, r = p - c * R;
+        const int w = cnt[r];
+        if (w > 0)
+            bulk_g2s(dst + c * F + off[r], base + c * cstride + (long long)(ybase + r) * W + xa[r],
+                     (unsigned)w * 4u, bar);
+    }
+}
+
 // Compact row layout of a staged footprint: row r holds columns [xa[r], xa[r]+cnt[r])
 // of source row (ybase + r) at smem offset off[r] (16-B aligned when VEC).
 // Built by warp 0 from inclusive column ranges [lo[r], hi[r]] (lo > hi: empty row).
@@ -150,6 +197,15 @@ RS_DEV void build_rows(int R, int Wlim, const int *lo, const int *hi, int *xa, i
         run += __shfl_sync(0xffffffffu, v, 31);
     }
     if (lane == 0) *Fout = run;
+}
+
+// sum of cnt[0..R) (floats actually copied per channel), by warp 0
+RS_DEV void sum_rows(int R, const int *cnt, int *out) {
+    if (threadIdx.x >= 32) return;
+    int s = 0;
+    for (int r = threadIdx.x; r < R; r += 32) s += cnt[r];
+    s = __reduce_add_sync(0xffffffffu, s);
+    if (threadIdx.x == 0) *out = s;
 }
 
 // Issue cp.async copies of nch channel planes' rows (channel stride cstride floats)

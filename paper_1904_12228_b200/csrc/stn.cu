@@ -263,16 +263,45 @@ __global__ void __launch_bounds__(kThreads, 3)
                 s0[k] = (in[k] && yv0[k]) ? roff[y0[k] - ylo] + (x0[k] - rxa[y0[k] - ylo]) : 0;
                 s1[k] = (in[k] && yv1[k]) ? roff[y0[k] + 1 - ylo] + (x0[k] - rxa[y0[k] + 1 - ylo]) : 0;
             }
-            const int CH = min(a.C, F > 0 ? kFStage / F : a.C);
+            // d_theta also stages the tile's dY rows (kFI x kFJ per channel) after the X footprint
+            constexpr int GT = (MODE == MODE_DTHETA) ? kFI * kFJ : 0;
+            const int CH = min(a.C, kFStage / (F + GT > 0 ? F + GT : 1));
             const int nch = (a.C + CH - 1) / CH;
+            const bool gvec = (a.Wo % 4 == 0) && (((uintptr_t)a.dy & 15u) == 0);
+            auto stage_g = [&](float *dst, int c0s, int ncp) {
+                if (MODE != MODE_DTHETA) return;
+                const int jb = tj * kFJ;
+                if (gvec) {
+                    for (int e = threadIdx.x; e < ncp * kFI * (kFJ / 4); e += kThreads) {
+                        const int c = e / (kFI * (kFJ / 4)), rem = e - c * (kFI * (kFJ / 4));
+                        const int r = rem / (kFJ / 4), q4 = (rem - r * (kFJ / 4)) * 4;
+                        const int i = ti * kFI + r;
+                        if (i < a.Ho && jb + q4 < a.Wo)
+                            cp_async16(dst + c * GT + r * kFJ + q4,
+                                       a.dy + ((long long)n * a.C + c0s + c) * P + (long long)i * a.Wo + jb + q4);
+                    }
+                } else {
+                    for (int e = threadIdx.x; e < ncp * kFI * kFJ; e += kThreads) {
+                        const int c = e / (kFI * kFJ), rem = e - c * (kFI * kFJ);
+                        const int r = rem / kFJ, q = rem - r * kFJ;
+                        const int i = ti * kFI + r;
+                        if (i < a.Ho && jb + q < a.Wo)
+                            cp_async4(dst + c * GT + r * kFJ + q,
+                                      a.dy + ((long long)n * a.C + c0s + c) * P + (long long)i * a.Wo + jb + q);
+                    }
+                }
+            };
             if (F > 0) stage_rows<VEC>(stage, F, xbase, HW, min(CH, a.C), R, a.W, ylo, rxa, roff, rcnt);
+            stage_g(stage + CH * F, 0, min(CH, a.C));
             cp_async_commit();
             for (int kc = 0; kc < nch; kc++) {
                 const int c0 = kc * CH, cn = min(CH, a.C - c0);
                 if (kc + 1 < nch) {
+                    float *nxt = stage + ((kc + 1) & 1) * kFStage;
                     if (F > 0)
-                        stage_rows<VEC>(stage + ((kc + 1) & 1) * kFStage, F, xbase + (long long)(c0 + CH) * HW,
+                        stage_rows<VEC>(nxt, F, xbase + (long long)(c0 + CH) * HW,
                                         HW, min(CH, a.C - c0 - CH), R, a.W, ylo, rxa, roff, rcnt);
+                    stage_g(nxt + CH * F, c0 + CH, min(CH, a.C - c0 - CH));
                     cp_async_commit();
                     cp_async_wait<1>();
                 } else {
@@ -297,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                         if (MODE == MODE_FWD) {
                             a.y[ob + c * P] = fmaf(w00, v00, fmaf(w01, v01, fmaf(w10, v10, w11 * v11)));
                         } else {
-                            const float g = ldg_stream(a.dy + ob + c * P);
+                            const float g = S[CH * F + c * GT + (warp + 8 * k) * kFJ + lane];
                             dix[k] = fmaf(g, fmaf(1.f - fy[k], v01 - v00, fy[k] * (v11 - v10)), dix[k]);
                             diy[k] = fmaf(g, fmaf(1.f - fx[k], v10 - v00, fx[k] * (v11 - v01)), diy[k]);
                         }
@@ -345,6 +374,7 @@ __global__ void stn_tables_kernel(double *xt, double *yt, int Ho, int Wo, int ac
 }
 
 RS_DEV bool stn_gather_ok(const Affine &A, int Ho, int Wo);
+RS_DEV bool stn_lean_ok(const Affine &A, int Ho, int Wo);
 
 // flags[n] = 1 if sample n takes the gather adjoint (variant 0: cell-owner,
 // 1: per-pixel gather); fb_list = the others.
@@ -357,7 +387,8 @@ __global__ void stn_classify_kernel(StnArgs a, int allow_gather, int variant, in
         const Theta T = load_theta(a.theta, n);
         const Affine A = stn_affine(T, a.H, a.W, a.Ho, a.Wo, a.ac);
         const bool g = allow_gather && !a.border &&
-                       (variant == 1 ? stn_gather_ok(A, a.Ho, a.Wo) : stn_gatherable(A, a.Ho, a.Wo));
+                       (variant == 1 ? stn_gather_ok(A, a.Ho, a.Wo)
+                                     : variant == 2 ? stn_lean_ok(A, a.Ho, a.Wo) : stn_gatherable(A, a.Ho, a.Wo));
         flags[n] = g ? 1 : 0;
         if (!g) fb_list[atomicAdd(&cnt, 1)] = n;
     }
@@ -675,6 +706,242 @@ __global__ void __launch_bounds__(kThreads, RS_CELL_MINB)
         double s = 0.0;
         for (int w = 0; w < kBWarps; w++) s += (double)red[w][threadIdx.x];
         part[threadIdx.x] = s;
+    }
+}
+
+// ----------------------------------------------------------------- backward: lean cell-owner dX
+// d_input only (d_theta comes from stn_out_tile<DTHETA> for every sample).  Same
+// ownership as stn_bwd_cell, but every warp walks its own halo cell row (no
+// cross-warp carry, no barrier inside the chunk loop) and up to kLCH channels
+// share one walk, so the per-(cell row, chunk) overhead is paid C/kLCH times.
+constexpr int kLRows = 4;                 // px rows per warp
+constexpr int kLTY = kLRows * 8;          // 32 px rows per block
+constexpr int kLRQMax = 160, kLFQMax = 2304, kLStage = 8192, kLCH = 8, kLHits = 6;
+
+RS_DEV bool stn_lean_ok(const Affine &A, int Ho, int Wo) {
+    if (!A.inv || Ho > 65535 || Wo > 65535) return false;
+    const double hq = fabs(A.i10) * (kBX + 1) + fabs(A.i11) * (kLTY + 1);
+    const double rq = ceil(hq) + 3.0;
+    const double fq = (double)(kBX + 1) * (kLTY + 1) / fabs(A.det) + 8.0 * rq + 64.0;
+    const double wj = fabs(A.i00) + fabs(A.i01), wi = fabs(A.i10) + fabs(A.i11);
+    return rq <= kLRQMax && fq <= kLFQMax && (wj + 2.0) * (wi + 2.0) <= 16.0;
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads, 2)
+    stn_bwd_lean(StnArgs a, const double *__restrict__ xtab, const double *__restrict__ ytab,
+                 const int *__restrict__ flags, int tiles_x, int tiles_y) {
+    extern __shared__ __align__(16) float4 sm4[];
+    float *stage = (float *)sm4;                               // 2 * kLStage
+    uint2 *rec = (uint2 *)(stage + 2 * kLStage);               // kLFQMax
+    int4 *rowt = (int4 *)(rec + kLFQMax);                      // kLRQMax
+    int *qlo = (int *)(rowt + kLRQMax);
+    int *qhi = qlo + kLRQMax;
+    int *qxa = qhi + kLRQMax;
+    int *qoff = qxa + kLRQMax;
+    int *qcnt = qoff + kLRQMax;
+    int *ctl = qcnt + kLRQMax;                                  // 8
+    unsigned short *hlist = (unsigned short *)(ctl + 8);        // [warp][row][hit][lane]
+    unsigned char *hcnt = (unsigned char *)(hlist + 8 * (kLRows + 1) * kLHits * 32);
+    __shared__ unsigned long long bars[2];  // TMA bulk-copy completion, one per stage
+
+    const int n = blockIdx.y;
+    const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
+    const int xa0 = tx * kBX, yb0 = ty * kLTY;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long HW = (long long)a.H * a.W, P = (long long)a.Ho * a.Wo;
+    const int px = xa0 - 1 + lane;
+    float *dxn = a.dx + (long long)n * a.C * HW;
+    if (!flags[n]) {  // fallback sample: zero this tile (the atomic scatter adds later)
+        if (lane >= 1 && px < a.W)
+            for (int r = warp; r < kLTY; r += 8) {
+                const int y = yb0 + r;
+                if (y < a.H)
+                    for (int c = 0; c < a.C; c++) dxn[(long long)c * HW + (long long)y * a.W + px] = 0.f;
+            }
+        return;
+    }
+    const Theta T = load_theta(a.theta, n);
+    const Affine A = stn_affine(T, a.H, a.W, a.Ho, a.Wo, a.ac);
+    const double eps = 1e-3;
+    const double Lx = xa0 - 1 - eps, Ux = xa0 + kBX + eps;
+    const double Ly = yb0 - 1 - eps, Uy = yb0 + kLTY + eps;
+    double imin = 1e300, imax = -1e300;
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+        const double px_ = (c & 1) ? Ux : Lx, py_ = (c & 2) ? Uy : Ly;
+        const double qi = A.i10 * (px_ - A.p0x) + A.i11 * (py_ - A.p0y);
+        imin = fmin(imin, qi);
+        imax = fmax(imax, qi);
+    }
+    const int ilo = max(0, (int)ceil(fmax(imin, -1e9)));
+    const int ihi = min(a.Ho - 1, (int)floor(fmin(imax, 1e9)));
+    const int RQ = min(kLRQMax, max(0, ihi - ilo + 1));
+    for (int r = threadIdx.x; r < RQ; r += kThreads) {
+        const int i = ilo + r;
+        double jl = -1e300, jh = 1e300;
+        const double ax_[2] = {A.m00, A.m10}, bx_[2] = {A.m01 * i + A.p0x, A.m11 * i + A.p0y};
+        const double L_[2] = {Lx, Ly}, U_[2] = {Ux, Uy};
+#pragma unroll
+        for (int d = 0; d < 2; d++) {
+            if (fabs(ax_[d]) < 1e-12) {
+                if (bx_[d] < L_[d] || bx_[d] > U_[d]) { jl = 1e300; jh = -1e300; }
+            } else {
+                double u = (L_[d] - bx_[d]) / ax_[d], v = (U_[d] - bx_[d]) / ax_[d];
+                if (u > v) { const double t = u; u = v; v = t; }
+                jl = fmax(jl, u);
+                jh = fmin(jh, v);
+            }
+        }
+        qlo[r] = max(0, (int)ceil(fmax(jl, -1e9)));
+        qhi[r] = min(a.Wo - 1, (int)floor(fmin(jh, 1e9)));
+    }
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    build_rows<VEC>(RQ, a.Wo, qlo, qhi, qxa, qoff, qcnt, &ctl[0]);
+    __syncthreads();
+    sum_rows(RQ, qcnt, &ctl[1]);
+    const int FQ = min(ctl[0], kLFQMax);
+    for (int r = threadIdx.x; r < RQ; r += kThreads) rowt[r] = make_int4(qlo[r], qhi[r], qoff[r] - qxa[r], 0);
+    for (int r = warp; r < RQ; r += 8) {
+        const int i = ilo + r;
+        const double yt = ytab[i];
+        const int wr = (qcnt[r] + 3) & ~3;
+        for (int col = lane; col < wr; col += 32) {
+            const int j = qxa[r] + col, e = qoff[r] + col;
+            if (e >= kLFQMax) break;
+            uint2 R = make_uint2(0xff000000u, 0xff000000u);
+            if (col < qcnt[r] && j >= qlo[r] && j <= qhi[r]) {
+                double ix, iy;
+                stn_coord(T, xtab[j], yt, a.H, a.W, a.ac, ix, iy);
+                const Cell cx = cell_of(ix), cy = cell_of(iy);
+                const int rx = cx.i0 - (xa0 - 1), ry = cy.i0 - (yb0 - 1);
+                if (rx >= 0 && rx <= kBX && ry >= 0 && ry <= kLTY) R = pack_rec(rx, ry, cx.f, cy.f);
+            }
+            rec[e] = R;
+        }
+    }
+    const int CH = min(min(a.C, kLCH), FQ > 0 ? max(1, kLStage / FQ) : kLCH);
+    const int nch = (a.C + CH - 1) / CH;
+    const float *gbase = a.dy + (long long)n * a.C * P;
+    __syncthreads();
+    const int Fc = ctl[1];  // floats copied per channel
+    // VEC: one TMA bulk copy per (channel, row) segment; else 4-B LDGSTS
+    auto issue = [&](float *dst, int c0s, int ncp, int slot) {
+        if (VEC) {
+            if (threadIdx.x == 0) mbar_expect_tx(&bars[slot], (unsigned)(ncp * Fc) * 4u);
+            if (FQ > 0) stage_rows_bulk(dst, FQ, gbase + (long long)c0s * P, P, ncp, RQ, a.Wo, ilo, qxa, qoff, qcnt,
+                                        &bars[slot]);
+        } else {
+            if (FQ > 0) stage_rows<VEC>(dst, FQ, gbase + (long long)c0s * P, P, ncp, RQ, a.Wo, ilo, qxa, qoff, qcnt);
+            cp_async_commit();
+        }
+    };
+    issue(stage, 0, min(CH, a.C), 0);
+
+    // every warp walks its own halo cell row: rows wy0-1 .. wy0+kLRows-1
+    const int wy0 = yb0 + kLRows * warp;
+    const bool pxin = lane >= 1 && px < a.W;
+    const unsigned cxw = (unsigned)(px - (xa0 - 1));
+    const double hj1 = 0.5 * (fabs(A.i00) + fabs(A.i01)) + eps, hi1 = 0.5 * (fabs(A.i10) + fabs(A.i11)) + eps;
+    unsigned short *myhl = hlist + warp * (kLRows + 1) * kLHits * 32 + lane;
+    unsigned char *myhc = hcnt + warp * (kLRows + 1) * 32 + lane;
+    auto search = [&](int y0, int rr, bool store, auto &&fn) {
+        const unsigned cyw = (unsigned)(y0 - (yb0 - 1));
+        const double ux = (double)px + 0.5 - A.p0x, uy = (double)y0 + 0.5 - A.p0y;
+        const double qj = A.i00 * ux + A.i01 * uy, qi = A.i10 * ux + A.i11 * uy;
+        const int jl = (int)ceil(qj - hj1), jh = (int)floor(qj + hj1);
+        const int il = max(ilo, (int)ceil(qi - hi1)), ih = min(ilo + RQ - 1, (int)floor(qi + hi1));
+        int cnt = 0;
+        for (int i = il; i <= ih; i++) {
+            const int4 rt = rowt[i - ilo];
+            const int ja = max(jl, rt.x), jb = min(jh, rt.y);
+            for (int j = ja; j <= jb; j++) {
+                const int e = rt.z + j;
+                const uint2 R = rec[e];
+                if ((R.x >> 24) == cxw && (R.y >> 24) == cyw) {
+                    if (store && cnt < kLHits) myhl[(rr * kLHits + cnt) * 32] = (unsigned short)e;
+                    fn(e);
+                    cnt++;
+                }
+            }
+        }
+        if (store) myhc[rr * 32] = (unsigned char)(cnt > kLHits ? 255 : cnt);
+    };
+    for (int rr = 0; rr <= kLRows; rr++) search(wy0 - 1 + rr, rr, true, [](int) {});
+
+    auto run_chunk = [&](const float *S, int c0, auto ncc) {
+        constexpr int NC = decltype(ncc)::value;
+        float L[NC], Rr[NC], NL[NC], NR[NC];
+#pragma unroll
+        for (int c = 0; c < NC; c++) NL[c] = NR[c] = 0.f;
+        float *drow = dxn + (long long)c0 * HW + (long long)(wy0 - 1) * a.W + px;
+#pragma unroll 1
+        for (int rr = 0; rr <= kLRows; rr++, drow += a.W) {
+            const int y0 = wy0 - 1 + rr;
+#pragma unroll
+            for (int c = 0; c < NC; c++) { L[c] = NL[c]; Rr[c] = NR[c]; NL[c] = 0.f; NR[c] = 0.f; }
+            auto process = [&](int e) {
+                const uint2 R = rec[e];
+                const float fx = (float)(R.x & 0xffffffu) * (1.f / 16777216.f);
+                const float fy = (float)(R.y & 0xffffffu) * (1.f / 16777216.f);
+                const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx;
+                const float w10 = fy * (1.f - fx), w11 = fy * fx;
+                const float *Se = S + e;
+#pragma unroll
+                for (int c = 0; c < NC; c++) {
+                    const float g = Se[c * FQ];
+                    L[c] = fmaf(w00, g, L[c]);
+                    Rr[c] = fmaf(w01, g, Rr[c]);
+                    NL[c] = fmaf(w10, g, NL[c]);
+                    NR[c] = fmaf(w11, g, NR[c]);
+                }
+            };
+            const int hn = myhc[rr * 32];
+            const int hmax = __reduce_max_sync(0xffffffffu, hn == 255 ? 0 : hn);
+            if (hn == 255) {
+                search(y0, rr, false, process);
+            } else {
+                for (int h = 0; h < hmax; h++)
+                    if (h < hn) process(myhl[(rr * kLHits + h) * 32]);
+            }
+            if (rr > 0) {  // row 0 is the halo: it only seeds the carry
+                const bool wr = pxin && y0 < a.H;
+#pragma unroll
+                for (int c = 0; c < NC; c++) {
+                    const float v = L[c] + __shfl_up_sync(0xffffffffu, Rr[c], 1);
+                    if (wr) drow[(long long)c * HW] = v;
+                }
+            }
+        }
+    };
+
+    for (int kc = 0; kc < nch; kc++) {
+        const int c0 = kc * CH, cn = min(CH, a.C - c0);
+        if (kc + 1 < nch) issue(stage + ((kc + 1) & 1) * kLStage, c0 + CH, min(CH, a.C - c0 - CH), (kc + 1) & 1);
+        if (VEC) {
+            mbar_wait(&bars[kc & 1], (unsigned)((kc >> 1) & 1));
+        } else {
+            if (kc + 1 < nch) cp_async_wait<1>();
+            else cp_async_wait<0>();
+        }
+        __syncthreads();
+        const float *S = stage + (kc & 1) * kLStage;
+        switch (cn) {
+            case 8: run_chunk(S, c0, std::integral_constant<int, 8>{}); break;
+            case 7: run_chunk(S, c0, std::integral_constant<int, 7>{}); break;
+            case 6: run_chunk(S, c0, std::integral_constant<int, 6>{}); break;
+            case 5: run_chunk(S, c0, std::integral_constant<int, 5>{}); break;
+            case 4: run_chunk(S, c0, std::integral_constant<int, 4>{}); break;
+            case 3: run_chunk(S, c0, std::integral_constant<int, 3>{}); break;
+            case 2: run_chunk(S, c0, std::integral_constant<int, 2>{}); break;
+            default: run_chunk(S, c0, std::integral_constant<int, 1>{}); break;
+        }
+        __syncthreads();
     }
 }
 
@@ -1027,7 +1294,7 @@ __global__ void __launch_bounds__(kThreads)
     stn_dtheta_finalize(const double *__restrict__ pb, int nb, const double *__restrict__ pf, int nf,
                         const int *__restrict__ flags, float *dtheta) {
     const int n = blockIdx.x;
-    const bool g = flags[n] != 0;
+    const bool g = flags ? flags[n] != 0 : false;  // flags == nullptr: every sample used the output tiles
     const double *p = g ? pb + (long long)n * nb * 6 : pf + (long long)n * nf * 6;
     const int nt = g ? nb : nf;
     __shared__ double red[kThreads / 32][6];
@@ -1113,7 +1380,9 @@ StnGeom stn_geom(int H, int W, int Ho, int Wo) {
 // read per call so tests can switch.
 int stn_bwd_variant() {
     const char *e = getenv("RSGRAD_STN_BWD");
-    return (e && strcmp(e, "gather") == 0) ? 1 : 0;
+    if (e && strcmp(e, "gather") == 0) return 1;
+    if (e && strcmp(e, "cell") == 0) return 0;
+    return 2;  // lean dX + staged output-tile d_theta (measured fastest)
 }
 
 struct StnWs {
@@ -1145,6 +1414,12 @@ StnWs stn_ws_layout(void *base, int N, int H, int W, int Ho, int Wo) {
 }
 
 size_t out_tile_smem() { return sizeof(int) * (5 * kFRMax + 16) + sizeof(float) * 2 * kFStage; }
+size_t bwd_lean_smem() {
+    return sizeof(float) * 2 * kLStage + sizeof(uint2) * kLFQMax + sizeof(int4) * kLRQMax +
+           sizeof(int) * (5 * kLRQMax + 8) + sizeof(unsigned short) * 8 * (kLRows + 1) * kLHits * 32 +
+           8 * (kLRows + 1) * 32;
+}
+
 size_t bwd_gather_smem() {
     return sizeof(float) * 2 * kGStage + (sizeof(uint2) + sizeof(unsigned)) * kGFQMax + sizeof(int4) * kGRQMax +
            sizeof(int) * (5 * kGRQMax + 8);
@@ -1211,7 +1486,22 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
     const bool vin = (a.W % 4 == 0) && aligned16(a.x);
     const bool vout = (a.Wo % 4 == 0) && aligned16(a.dy);
     int tiles_b = g.bx * g.by;
-    if (allow_gather && variant == 1) {
+    if (allow_gather && variant == 2) {
+        // lean dX kernel; every sample's d_theta comes from the output-tile kernel
+        const size_t sm = bwd_lean_smem();
+        const int ly = (a.H + kLTY - 1) / kLTY;
+        dim3 grid(g.bx * ly, a.N);
+        if (a.dx) {
+            if (vout) {
+                set_smem(stn_bwd_lean<true>, sm);
+                stn_bwd_lean<true><<<grid, kThreads, sm, s>>>(a, w.xtab, w.ytab, w.flags, g.bx, ly);
+            } else {
+                set_smem(stn_bwd_lean<false>, sm);
+                stn_bwd_lean<false><<<grid, kThreads, sm, s>>>(a, w.xtab, w.ytab, w.flags, g.bx, ly);
+            }
+            note_launch();
+        }
+    } else if (allow_gather && variant == 1) {
         const size_t sm = bwd_gather_smem();
         dim3 grid(g.gx * g.gy, a.N);
         tiles_b = g.gx * g.gy;
@@ -1235,18 +1525,21 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
         }
         note_launch();
     }
-    // fallback samples (all samples when !allow_gather): d_theta from output tiles ...
+    // fallback samples (all samples when !allow_gather or the lean dX kernel):
+    // d_theta from output tiles ...
+    const bool dth_all = allow_gather && variant == 2;
     if (a.dtheta) {
         const size_t sm = out_tile_smem();
-        dim3 grid(g.fj * g.fi, 1);
+        dim3 grid(g.fj * g.fi, dth_all ? a.N : 1);
+        const int *fbl = dth_all ? nullptr : w.fb_list;
         if (vin) {
             set_smem(stn_out_tile<MODE_DTHETA, true>, sm);
-            stn_out_tile<MODE_DTHETA, true><<<grid, kThreads, sm, s>>>(a, w.xtab, w.ytab, w.fb_list, w.fb_count,
+            stn_out_tile<MODE_DTHETA, true><<<grid, kThreads, sm, s>>>(a, w.xtab, w.ytab, fbl, w.fb_count,
                                                                        w.pf, g.fj, g.fi);
         } else {
             set_smem(stn_out_tile<MODE_DTHETA, false>, sm);
-            stn_out_tile<MODE_DTHETA, false><<<grid, kThreads, sm, s>>>(a, w.xtab, w.ytab, w.fb_list,
-                                                                        w.fb_count, w.pf, g.fj, g.fi);
+            stn_out_tile<MODE_DTHETA, false><<<grid, kThreads, sm, s>>>(a, w.xtab, w.ytab, fbl, w.fb_count,
+                                                                        w.pf, g.fj, g.fi);
         }
         note_launch();
     }
@@ -1259,7 +1552,8 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
         note_launch();
     }
     if (a.dtheta) {
-        stn_dtheta_finalize<<<a.N, kThreads, 0, s>>>(w.pb, tiles_b, w.pf, g.fj * g.fi, w.flags, a.dtheta);
+        stn_dtheta_finalize<<<a.N, kThreads, 0, s>>>(w.pb, tiles_b, w.pf, g.fj * g.fi,
+                                                      dth_all ? nullptr : w.flags, a.dtheta);
         note_launch();
     }
     return cudaGetLastError();
