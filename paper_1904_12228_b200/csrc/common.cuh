@@ -240,6 +240,8 @@ struct StnArgs {
     float *y, *dx, *dtheta;
     int N, C, H, W, Ho, Wo;
     int ac, border;
+    const float *flow;  // warp layer through the output-tile kernel (theta unused)
+    float *dflow;
 };
 struct WarpArgs {
     const float *x, *flow, *dy;
@@ -259,6 +261,8 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
                            cudaStream_t s);
 size_t stn_ws_bytes(int N, int C, int H, int W, int Ho, int Wo);
 
+// output-tile kernel driven by a flow field (warp.cu): mode 0 = y, 2 = d_flow (+ dx reds)
+cudaError_t flow_tile_launch(const StnArgs &a, int mode, cudaStream_t s);
 cudaError_t warp_fwd_launch(const WarpArgs &a, cudaStream_t s);
 cudaError_t warp_bwd_launch(const WarpArgs &a, int algo, int deterministic, void *ws,
                             size_t ws_bytes, cudaStream_t s);

@@ -59,7 +59,7 @@ constexpr int kBStage = 6144;             // floats per pipeline stage
 constexpr int kBCH = 4;                   // max channels per stage (registers)
 constexpr int kBHits = 6;                 // cached hits per cell (more: re-searched)
 
-constexpr int MODE_FWD = 0, MODE_DTHETA = 1;
+constexpr int MODE_FWD = 0, MODE_DTHETA = 1, MODE_DFLOW = 2;
 
 struct Theta {
     double t[6];
@@ -127,7 +127,7 @@ RS_DEV bool stn_gatherable(const Affine &A, int Ho, int Wo) {
 // ----------------------------------------------------------------- output-tile kernel
 // MODE_FWD: y.  MODE_DTHETA: per-tile fp64 partials of d_theta (6 per tile).
 // fb_list (optional): loop over the listed samples instead of blockIdx.y.
-template <int MODE, bool VEC>
+template <int MODE, bool VEC, bool FLOW = false>
 __global__ void __launch_bounds__(kThreads, 3)
     stn_out_tile(StnArgs a, const double *__restrict__ xtab, const double *__restrict__ ytab,
                  const int *__restrict__ fb_list, const int *__restrict__ fb_count,
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kThreads, 3)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tj = blockIdx.x % tiles_j, ti = blockIdx.x / tiles_j;
     const long long HW = (long long)a.H * a.W, P = (long long)a.Ho * a.Wo;
-    if (threadIdx.x < kFJ + kFI) {
+    if (!FLOW && threadIdx.x < kFJ + kFI) {
         const bool col = threadIdx.x < kFJ;
         const int idx = col ? tj * kFJ + threadIdx.x : ti * kFI + threadIdx.x - kFJ;
         const int L = col ? a.Wo : a.Ho;
@@ -156,7 +156,8 @@ __global__ void __launch_bounds__(kThreads, 3)
     const int nloop = fb_list ? *fb_count : 1;
     for (int f = 0; f < nloop; f++) {
         const int n = fb_list ? fb_list[f] : blockIdx.y;
-        const Theta T = load_theta(a.theta, n);
+        Theta T;
+        if (!FLOW) T = load_theta(a.theta, n);
         int x0[2], y0[2];
         float fx[2], fy[2], cgx[2], cgy[2], xtf[2], ytf[2];
         bool in[2], xv0[2], xv1[2], yv0[2], yv1[2];
@@ -171,11 +172,17 @@ __global__ void __launch_bounds__(kThreads, 3)
             xtf[k] = ytf[k] = 0.f;
             xv0[k] = xv1[k] = yv0[k] = yv1[k] = false;
             if (in[k]) {
-                const double xt = ntab[lane], yt = ntab[kFJ + warp + 8 * k];
-                xtf[k] = (float)xt;
-                ytf[k] = (float)yt;
                 double ix, iy;
-                stn_coord(T, xt, yt, a.H, a.W, a.ac, ix, iy);
+                if (FLOW) {  // FlowNet warp (R4): x + u, y + v in pixels, exact in fp64
+                    const float *fp = a.flow + (long long)n * 2 * P + (long long)i * a.Wo + j;
+                    ix = __dadd_rn((double)j, (double)ldg_stream(fp));
+                    iy = __dadd_rn((double)i, (double)ldg_stream(fp + P));
+                } else {
+                    const double xt = ntab[lane], yt = ntab[kFJ + warp + 8 * k];
+                    xtf[k] = (float)xt;
+                    ytf[k] = (float)yt;
+                    stn_coord(T, xt, yt, a.H, a.W, a.ac, ix, iy);
+                }
                 if (a.border) {
                     ix = clamp_coord(ix, a.W, cgx[k]);
                     iy = clamp_coord(iy, a.H, cgy[k]);
@@ -227,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 3)
         if (!fallback) build_rows<VEC>(R, a.W, rlo, rhi, rxa, roff, rcnt, &ctl[2]);
         __syncthreads();
         const int F = fallback ? 0 : ctl[2];
-        fallback = fallback || F > kFStage;
+        fallback = fallback || F + ((MODE != MODE_FWD) ? kFI * kFJ : 0) > kFStage;
 
         float dix[2] = {0.f, 0.f}, diy[2] = {0.f, 0.f};
         const float *xbase = a.x + (long long)n * a.C * HW;
@@ -253,6 +260,13 @@ __global__ void __launch_bounds__(kThreads, 3)
                         const float g = ldg_stream(a.dy + oo);
                         dix[k] = fmaf(g, fmaf(1.f - fy[k], v01 - v00, fy[k] * (v11 - v10)), dix[k]);
                         diy[k] = fmaf(g, fmaf(1.f - fx[k], v10 - v00, fx[k] * (v11 - v01)), diy[k]);
+                        if (MODE == MODE_DFLOW && a.dx) {
+                            float *q = a.dx + ((long long)n * a.C + c) * HW + o00;
+                            if (yv0[k] && xv0[k]) red_add(q, w00 * g);
+                            if (yv0[k] && xv1[k]) red_add(q + 1, w01 * g);
+                            if (yv1[k] && xv0[k]) red_add(q + a.W, w10 * g);
+                            if (yv1[k] && xv1[k]) red_add(q + a.W + 1, w11 * g);
+                        }
                     }
                 }
             }
@@ -264,12 +278,12 @@ __global__ void __launch_bounds__(kThreads, 3)
                 s1[k] = (in[k] && yv1[k]) ? roff[y0[k] + 1 - ylo] + (x0[k] - rxa[y0[k] + 1 - ylo]) : 0;
             }
             // d_theta also stages the tile's dY rows (kFI x kFJ per channel) after the X footprint
-            constexpr int GT = (MODE == MODE_DTHETA) ? kFI * kFJ : 0;
+            constexpr int GT = (MODE != MODE_FWD) ? kFI * kFJ : 0;
             const int CH = min(a.C, kFStage / (F + GT > 0 ? F + GT : 1));
             const int nch = (a.C + CH - 1) / CH;
             const bool gvec = (a.Wo % 4 == 0) && (((uintptr_t)a.dy & 15u) == 0);
             auto stage_g = [&](float *dst, int c0s, int ncp) {
-                if (MODE != MODE_DTHETA) return;
+                if (MODE == MODE_FWD) return;
                 const int jb = tj * kFJ;
                 if (gvec) {
                     for (int e = threadIdx.x; e < ncp * kFI * (kFJ / 4); e += kThreads) {
@@ -329,10 +343,28 @@ __global__ void __launch_bounds__(kThreads, 3)
                             const float g = S[CH * F + c * GT + (warp + 8 * k) * kFJ + lane];
                             dix[k] = fmaf(g, fmaf(1.f - fy[k], v01 - v00, fy[k] * (v11 - v10)), dix[k]);
                             diy[k] = fmaf(g, fmaf(1.f - fx[k], v10 - v00, fx[k] * (v11 - v01)), diy[k]);
+                            if (MODE == MODE_DFLOW && a.dx) {  // no bounded inverse: atomic scatter
+                                float *q = a.dx + ((long long)n * a.C + c0 + c) * HW +
+                                           (long long)y0[k] * a.W + x0[k];
+                                if (k00) red_add(q, w00 * g);
+                                if (k01) red_add(q + 1, w01 * g);
+                                if (k10) red_add(q + a.W, w10 * g);
+                                if (k11) red_add(q + a.W + 1, w11 * g);
+                            }
                         }
                     }
                 }
                 __syncthreads();
+            }
+        }
+        if (MODE == MODE_DFLOW && a.dflow) {
+#pragma unroll
+            for (int k = 0; k < 2; k++) {
+                if (!in[k]) continue;
+                const int i = ti * kFI + warp + 8 * k, j = tj * kFJ + lane;
+                float *dfp = a.dflow + (long long)n * 2 * P + (long long)i * a.Wo + j;
+                dfp[0] = dix[k] * cgx[k];
+                dfp[P] = diy[k] * cgy[k];
             }
         }
         if (MODE == MODE_DTHETA) {
@@ -1458,6 +1490,36 @@ cudaError_t stn_fwd_launch(const StnArgs &a, cudaStream_t s) {
         set_smem(stn_out_tile<MODE_FWD, false>, sm);
         stn_out_tile<MODE_FWD, false><<<grid, kThreads, sm, s>>>(a, nullptr, nullptr, nullptr, nullptr,
                                                                  nullptr, g.fj, g.fi);
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t flow_tile_launch(const StnArgs &a, int mode, cudaStream_t s) {
+    const StnGeom g = stn_geom(a.H, a.W, a.Ho, a.Wo);
+    const bool vec = (a.W % 4 == 0) && aligned16(a.x);
+    const size_t sm = out_tile_smem();
+    dim3 grid(g.fj * g.fi, a.N);
+    if (mode == MODE_FWD) {
+        if (vec) {
+            set_smem(stn_out_tile<MODE_FWD, true, true>, sm);
+            stn_out_tile<MODE_FWD, true, true><<<grid, kThreads, sm, s>>>(a, nullptr, nullptr, nullptr, nullptr,
+                                                                          nullptr, g.fj, g.fi);
+        } else {
+            set_smem(stn_out_tile<MODE_FWD, false, true>, sm);
+            stn_out_tile<MODE_FWD, false, true><<<grid, kThreads, sm, s>>>(a, nullptr, nullptr, nullptr, nullptr,
+                                                                           nullptr, g.fj, g.fi);
+        }
+    } else {
+        if (vec) {
+            set_smem(stn_out_tile<MODE_DFLOW, true, true>, sm);
+            stn_out_tile<MODE_DFLOW, true, true><<<grid, kThreads, sm, s>>>(a, nullptr, nullptr, nullptr, nullptr,
+                                                                            nullptr, g.fj, g.fi);
+        } else {
+            set_smem(stn_out_tile<MODE_DFLOW, false, true>, sm);
+            stn_out_tile<MODE_DFLOW, false, true><<<grid, kThreads, sm, s>>>(a, nullptr, nullptr, nullptr, nullptr,
+                                                                             nullptr, g.fj, g.fi);
+        }
     }
     note_launch();
     return cudaGetLastError();

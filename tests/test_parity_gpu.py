@@ -317,3 +317,21 @@ def test_stn_bwd_variants(cuda_device, monkeypatch, variant, ac):
     rdx, rdth = oracle.stn_bwd(*(inp[k].double().numpy() for k in ("x", "theta", "dy")), align_corners=ac)
     assert_close(_np(dx), rdx, "grad", f"dx[{variant}]")
     assert_close(_np(dth), rdth, "grad", f"dtheta[{variant}]")
+
+
+@pytest.mark.parametrize("flow", ["smooth", "stress"])
+@pytest.mark.parametrize("padding", ["zeros", "border"])
+def test_warp_tiled_variant(cuda_device, monkeypatch, flow, padding):
+    """The staged-footprint warp path (RSGRAD_WARP=tiled) matches the oracle too,
+    including the in-kernel direct-gather fallback for large (stress) footprints."""
+    monkeypatch.setenv("RSGRAD_WARP", "tiled")
+    inp = synth.warp_inputs(2, 3, 70, 100, cfg=1, flow=flow)
+    g = _cuda(inp, cuda_device)
+    y = rsgrad.warp_fwd(g["x"], g["flow"], padding=padding)
+    dx, df = rsgrad.warp_bwd(g["x"], g["flow"], g["dy"], padding=padding)
+    x, fl, dy = (inp[k].double().numpy() for k in ("x", "flow", "dy"))
+    border = padding == "border"
+    assert_close(_np(y), oracle.warp_fwd(x, fl, border), "fwd", "y")
+    rdx, rdf = oracle.warp_bwd(x, fl, dy, border)
+    assert_close(_np(dx), rdx, "grad", "dx")
+    assert_close(_np(df), rdf, "grad", "dflow")
