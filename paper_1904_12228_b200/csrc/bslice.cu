@@ -156,8 +156,20 @@ __global__ void __launch_bounds__(kThreads)
     const float *xp = a.x + (long long)t.n * 3 * HW;
     float *yp = a.y + (long long)t.n * 3 * HW;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int NB = a.D + 1;
+    // per-warp row table: for the current row's fy, (a + fy c, b + fy d) of the low
+    // plane and of the plane difference, for every (q, bin): one LDS.128 per q and pixel
+    float4 *rt = (float4 *)(fyt + kTileYS) + w * 12 * NB;
     for (int r = w; r < TH; r += kWarps) {
         const float fy = fyt[r];
+        __syncwarp();
+        for (int e = lane; e < 12 * NB; e += 32) {
+            const int q = e / NB, b = e - q * NB;
+            const float4 L = glo[b * kPlaneStride + q], Dz = gdz[b * kPlaneStride + q];
+            rt[q * NB + b] = make_float4(fmaf(fy, L.z, L.x), fmaf(fy, L.w, L.y), fmaf(fy, Dz.z, Dz.x),
+                                         fmaf(fy, Dz.w, Dz.y));
+        }
+        __syncwarp();
         const long long rowoff = (long long)(t.ys + r) * a.W + t.xs;
         for (int c = lane; c < TW; c += 32) {
             const long long o = rowoff + c;
@@ -167,15 +179,14 @@ __global__ void __launch_bounds__(kThreads)
             z_cell(ldg_stream(gd + o), a.D, bin, fz);
             const float x0 = ldg_stream(xp + o), x1 = ldg_stream(xp + HW + o),
                         x2 = ldg_stream(xp + 2 * HW + o);
-            const float4 *L = glo + bin * kPlaneStride, *Dz = gdz + bin * kPlaneStride;
+            const float4 *T = rt + bin;
 #pragma unroll
             for (int oc = 0; oc < 3; oc++) {
                 float A[4];
 #pragma unroll
                 for (int i = 0; i < 4; i++) {
-                    const float lo = lerp2(L[4 * oc + i], fx, fy);
-                    const float dz = lerp2(Dz[4 * oc + i], fx, fy);
-                    A[i] = fmaf(fz, dz, lo);
+                    const float4 v = T[(4 * oc + i) * NB];
+                    A[i] = fmaf(fz, fmaf(fx, v.w, v.z), fmaf(fx, v.y, v.x));
                 }
                 yp[oc * HW + o] = fmaf(A[0], x0, fmaf(A[1], x1, fmaf(A[2], x2, A[3])));
             }
@@ -593,7 +604,8 @@ TileGeom tile_geom(int N, int H, int W, int D, int Gh, int Gw) {
 }
 
 size_t fwd_smem(int D) {
-    return sizeof(float4) * 2 * (D + 1) * kPlaneStride + sizeof(float) * (kTileXS + kTileYS);
+    return sizeof(float4) * 2 * (D + 1) * kPlaneStride + sizeof(float) * (kTileXS + kTileYS) +
+           sizeof(float4) * kWarps * 12 * (D + 1) + 16;
 }
 
 size_t bwd_smem(int D) {
@@ -617,6 +629,8 @@ cudaError_t bslice_fwd_launch(const BsliceArgs &a, cudaStream_t s) {
     const TileGeom g = tile_geom(a.N, a.H, a.W, a.D, a.Gh, a.Gw);
     if (g.ok) {
         const size_t sm = fwd_smem(a.D);
+        if (sm > 48 * 1024)
+            cudaFuncSetAttribute(bslice_fwd_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         bslice_fwd_tiled<<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX);
     } else {
         const long long total = (long long)a.N * a.H * a.W;
