@@ -158,37 +158,53 @@ __global__ void __launch_bounds__(kThreads)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int NB = a.D + 1;
     // per-warp row table: for the current row's fy, (a + fy c, b + fy d) of the low
-    // plane and of the plane difference, for every (q, bin): one LDS.128 per q and pixel
-    float4 *rt = (float4 *)(fyt + kTileYS) + w * 12 * NB;
+    // plane and of the plane difference, for every (bin, q), bins kPlaneStride float4
+    // apart (conflict-free across bins): one LDS.128 per coefficient and pixel
+    float4 *rt = (float4 *)(fyt + kTileYS) + w * kPlaneStride * NB;
     for (int r = w; r < TH; r += kWarps) {
         const float fy = fyt[r];
         __syncwarp();
         for (int e = lane; e < 12 * NB; e += 32) {
-            const int q = e / NB, b = e - q * NB;
+            const int b = e / 12, q = e - b * 12;
             const float4 L = glo[b * kPlaneStride + q], Dz = gdz[b * kPlaneStride + q];
-            rt[q * NB + b] = make_float4(fmaf(fy, L.z, L.x), fmaf(fy, L.w, L.y), fmaf(fy, Dz.z, Dz.x),
-                                         fmaf(fy, Dz.w, Dz.y));
+            rt[b * kPlaneStride + q] = make_float4(fmaf(fy, L.z, L.x), fmaf(fy, L.w, L.y), fmaf(fy, Dz.z, Dz.x),
+                                                   fmaf(fy, Dz.w, Dz.y));
         }
         __syncwarp();
         const long long rowoff = (long long)(t.ys + r) * a.W + t.xs;
-        for (int c = lane; c < TW; c += 32) {
-            const long long o = rowoff + c;
-            const float fx = fxt[c];
-            int bin;
-            float fz;
-            z_cell(ldg_stream(gd + o), a.D, bin, fz);
-            const float x0 = ldg_stream(xp + o), x1 = ldg_stream(xp + HW + o),
-                        x2 = ldg_stream(xp + 2 * HW + o);
-            const float4 *T = rt + bin;
+        // two pixels per lane per step, their loads issued together
+        for (int c0 = lane; c0 < TW; c0 += 64) {
+            float gv[2], xv[2][3];
+            bool ok[2];
 #pragma unroll
-            for (int oc = 0; oc < 3; oc++) {
-                float A[4];
+            for (int k = 0; k < 2; k++) {
+                const int c = c0 + 32 * k;
+                ok[k] = c < TW;
+                const long long o = rowoff + (ok[k] ? c : 0);
+                gv[k] = ok[k] ? ldg_stream(gd + o) : 0.f;
 #pragma unroll
-                for (int i = 0; i < 4; i++) {
-                    const float4 v = T[(4 * oc + i) * NB];
-                    A[i] = fmaf(fz, fmaf(fx, v.w, v.z), fmaf(fx, v.y, v.x));
+                for (int i = 0; i < 3; i++) xv[k][i] = ok[k] ? ldg_stream(xp + i * HW + o) : 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < 2; k++) {
+                if (!ok[k]) continue;
+                const int c = c0 + 32 * k;
+                const long long o = rowoff + c;
+                const float fx = fxt[c];
+                int bin;
+                float fz;
+                z_cell(gv[k], a.D, bin, fz);
+                const float4 *T = rt + bin * kPlaneStride;
+#pragma unroll
+                for (int oc = 0; oc < 3; oc++) {
+                    float A[4];
+#pragma unroll
+                    for (int i = 0; i < 4; i++) {
+                        const float4 v = T[4 * oc + i];
+                        A[i] = fmaf(fz, fmaf(fx, v.w, v.z), fmaf(fx, v.y, v.x));
+                    }
+                    yp[oc * HW + o] = fmaf(A[0], xv[k][0], fmaf(A[1], xv[k][1], fmaf(A[2], xv[k][2], A[3])));
                 }
-                yp[oc * HW + o] = fmaf(A[0], x0, fmaf(A[1], x1, fmaf(A[2], x2, A[3])));
             }
         }
     }
@@ -605,7 +621,7 @@ TileGeom tile_geom(int N, int H, int W, int D, int Gh, int Gw) {
 
 size_t fwd_smem(int D) {
     return sizeof(float4) * 2 * (D + 1) * kPlaneStride + sizeof(float) * (kTileXS + kTileYS) +
-           sizeof(float4) * kWarps * 12 * (D + 1) + 16;
+           sizeof(float4) * kWarps * kPlaneStride * (D + 1) + 16;
 }
 
 size_t bwd_smem(int D) {
