@@ -374,33 +374,36 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int k = 0; k < 48; k++) acc[k] = 0.f;
     const int slot = lane >> 1, e_pl = lane & 1;
     int cur_bin = cbeg < cend ? chunk_bin[cbeg] : 0;
-    // software pipeline: the next chunk's X / dY loads are in flight while this one computes
-    unsigned ent_n = cbeg < cend ? sorted[cbeg * kChunk + slot] : kInvalid;
-    float Xn[3] = {0.f, 0.f, 0.f}, Gn[3] = {0.f, 0.f, 0.f};
-    auto fetch = [&](unsigned ent) {
+    // software pipeline, distance 2: chunk ch+2's X / dY loads are issued while ch computes
+    unsigned ent_a = cbeg < cend ? sorted[cbeg * kChunk + slot] : kInvalid;
+    unsigned ent_b = cbeg + 1 < cend ? sorted[(cbeg + 1) * kChunk + slot] : kInvalid;
+    float Xa[3] = {0.f, 0.f, 0.f}, Ga[3] = {0.f, 0.f, 0.f}, Xb[3] = {0.f, 0.f, 0.f}, Gb[3] = {0.f, 0.f, 0.f};
+    auto fetch = [&](unsigned ent, float *Xd, float *Gd) {
         if (ent != kInvalid) {
             const long long o = (long long)(t.ys + (int)(ent >> 16)) * a.W + t.xs + (int)(ent & 0xffffu);
 #pragma unroll
             for (int i = 0; i < 3; i++) {
-                Xn[i] = __ldg(xp + i * HW + o);
-                Gn[i] = __ldg(gp + i * HW + o);
+                Xd[i] = __ldg(xp + i * HW + o);
+                Gd[i] = __ldg(gp + i * HW + o);
             }
         }
     };
-    fetch(ent_n);
+    fetch(ent_a, Xa, Ga);
+    fetch(ent_b, Xb, Gb);
     for (int ch = cbeg; ch < cend; ch++) {
         const int bin = chunk_bin[ch];
         if (bin != cur_bin) {
             flush_acc(acc, mywacc, cur_bin, D, lane);
             cur_bin = bin;
         }
-        const unsigned ent = ent_n;
+        const unsigned ent = ent_a;
         float X[3], G[3];
 #pragma unroll
-        for (int i = 0; i < 3; i++) { X[i] = Xn[i]; G[i] = Gn[i]; }
-        if (ch + 1 < cend) {
-            ent_n = sorted[(ch + 1) * kChunk + slot];
-            fetch(ent_n);
+        for (int i = 0; i < 3; i++) { X[i] = Xa[i]; G[i] = Ga[i]; Xa[i] = Xb[i]; Ga[i] = Gb[i]; }
+        ent_a = ent_b;
+        if (ch + 2 < cend) {
+            ent_b = sorted[(ch + 2) * kChunk + slot];
+            fetch(ent_b, Xb, Gb);
         }
         const bool valid = ent != kInvalid;
         const int r = valid ? (int)(ent >> 16) : 0, c = valid ? (int)(ent & 0xffffu) : 0;
