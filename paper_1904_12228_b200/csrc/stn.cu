@@ -44,7 +44,8 @@ namespace {
 constexpr int kThreads = 256;
 
 // forward tiles
-constexpr int kFJ = 32, kFI = 16;         // output tile (px)
+constexpr int kFJ = 32;                   // output tile width (px)
+constexpr int kFIfwd = 32, kFIdth = 16;   // output tile rows: forward / d_theta (measured)
 constexpr int kFRMax = 128;               // max staged input rows
 constexpr int kFStage = 6144;             // floats per pipeline stage
 
@@ -127,11 +128,12 @@ RS_DEV bool stn_gatherable(const Affine &A, int Ho, int Wo) {
 // ----------------------------------------------------------------- output-tile kernel
 // MODE_FWD: y.  MODE_DTHETA: per-tile fp64 partials of d_theta (6 per tile).
 // fb_list (optional): loop over the listed samples instead of blockIdx.y.
-template <int MODE, bool VEC, bool FLOW = false>
+template <int MODE, bool VEC, bool FLOW = false, int kFI = (MODE == 0 ? kFIfwd : kFIdth)>
 __global__ void __launch_bounds__(kThreads, 3)
     stn_out_tile(StnArgs a, const double *__restrict__ xtab, const double *__restrict__ ytab,
                  const int *__restrict__ fb_list, const int *__restrict__ fb_count,
                  double *__restrict__ partials, int tiles_j, int tiles_i) {
+    constexpr int kFP = kFI / 8;  // output pixels per thread
     extern __shared__ __align__(16) float4 sm4[];
     int *rlo = (int *)sm4;
     int *rhi = rlo + kFRMax;
@@ -158,12 +160,12 @@ __global__ void __launch_bounds__(kThreads, 3)
         const int n = fb_list ? fb_list[f] : blockIdx.y;
         Theta T;
         if (!FLOW) T = load_theta(a.theta, n);
-        int x0[2], y0[2];
-        float fx[2], fy[2], cgx[2], cgy[2], xtf[2], ytf[2];
-        bool in[2], xv0[2], xv1[2], yv0[2], yv1[2];
+        int x0[kFP], y0[kFP];
+        float fx[kFP], fy[kFP], cgx[kFP], cgy[kFP], xtf[kFP], ytf[kFP];
+        bool in[kFP], xv0[kFP], xv1[kFP], yv0[kFP], yv1[kFP];
         int ymin = INT_MAX, ymax = INT_MIN;
 #pragma unroll
-        for (int k = 0; k < 2; k++) {
+        for (int k = 0; k < kFP; k++) {
             const int i = ti * kFI + warp + 8 * k, j = tj * kFJ + lane;
             in[k] = i < a.Ho && j < a.Wo;
             x0[k] = y0[k] = 0;
@@ -223,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, 3)
         bool fallback = R > kFRMax;
         if (!fallback) {
 #pragma unroll
-            for (int k = 0; k < 2; k++) {
+            for (int k = 0; k < kFP; k++) {
                 if (!(in[k] && (xv0[k] || xv1[k]))) continue;
                 const int xl = xv0[k] ? x0[k] : x0[k] + 1, xh = xv1[k] ? x0[k] + 1 : x0[k];
                 if (yv0[k]) { atomicMin(&rlo[y0[k] - ylo], xl); atomicMax(&rhi[y0[k] - ylo], xh); }
@@ -236,12 +238,14 @@ __global__ void __launch_bounds__(kThreads, 3)
         const int F = fallback ? 0 : ctl[2];
         fallback = fallback || F + ((MODE != MODE_FWD) ? kFI * kFJ : 0) > kFStage;
 
-        float dix[2] = {0.f, 0.f}, diy[2] = {0.f, 0.f};
+        float dix[kFP], diy[kFP];
+#pragma unroll
+        for (int k = 0; k < kFP; k++) dix[k] = diy[k] = 0.f;
         const float *xbase = a.x + (long long)n * a.C * HW;
         if (fallback) {
             // direct global gathers (rare: strongly zoomed-out tiles)
 #pragma unroll
-            for (int k = 0; k < 2; k++) {
+            for (int k = 0; k < kFP; k++) {
                 if (!in[k]) continue;
                 const int i = ti * kFI + warp + 8 * k, j = tj * kFJ + lane;
                 const long long o00 = (long long)y0[k] * a.W + x0[k];
@@ -271,9 +275,9 @@ __global__ void __launch_bounds__(kThreads, 3)
                 }
             }
         } else {
-            int s0[2], s1[2];
+            int s0[kFP], s1[kFP];
 #pragma unroll
-            for (int k = 0; k < 2; k++) {
+            for (int k = 0; k < kFP; k++) {
                 s0[k] = (in[k] && yv0[k]) ? roff[y0[k] - ylo] + (x0[k] - rxa[y0[k] - ylo]) : 0;
                 s1[k] = (in[k] && yv1[k]) ? roff[y0[k] + 1 - ylo] + (x0[k] - rxa[y0[k] + 1 - ylo]) : 0;
             }
@@ -324,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                 __syncthreads();
                 const float *S = stage + (kc & 1) * kFStage;
 #pragma unroll
-                for (int k = 0; k < 2; k++) {
+                for (int k = 0; k < kFP; k++) {
                     if (!in[k]) continue;
                     const int i = ti * kFI + warp + 8 * k, j = tj * kFJ + lane;
                     const bool k00 = yv0[k] && xv0[k], k01 = yv0[k] && xv1[k];
@@ -359,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, 3)
         }
         if (MODE == MODE_DFLOW && a.dflow) {
 #pragma unroll
-            for (int k = 0; k < 2; k++) {
+            for (int k = 0; k < kFP; k++) {
                 if (!in[k]) continue;
                 const int i = ti * kFI + warp + 8 * k, j = tj * kFJ + lane;
                 float *dfp = a.dflow + (long long)n * 2 * P + (long long)i * a.Wo + j;
@@ -372,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, 3)
             const float sy = a.ac ? 0.5f * (a.H - 1) : 0.5f * a.H;
             float acc[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int k = 0; k < 2; k++) {
+            for (int k = 0; k < kFP; k++) {
                 if (!in[k]) continue;
                 const float dgx = dix[k] * sx * cgx[k], dgy = diy[k] * sy * cgy[k];
                 acc[0] = fmaf(dgx, xtf[k], acc[0]);
@@ -1391,7 +1395,8 @@ __global__ void __launch_bounds__(kThreads)
 size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct StnGeom {
-    int fj, fi;  // output tiles
+    int fj, fi;  // output tiles (d_theta tile rows)
+    int fi_fwd;  // output tile rows of the forward
     int bx, by;  // input tiles, cell-owner kernel
     int gx, gy;  // input tiles, per-pixel gather kernel
 };
@@ -1399,7 +1404,8 @@ struct StnGeom {
 StnGeom stn_geom(int H, int W, int Ho, int Wo) {
     StnGeom g;
     g.fj = (Wo + kFJ - 1) / kFJ;
-    g.fi = (Ho + kFI - 1) / kFI;
+    g.fi = (Ho + kFIdth - 1) / kFIdth;
+    g.fi_fwd = (Ho + kFIfwd - 1) / kFIfwd;
     g.bx = (W + kBX - 1) / kBX;
     g.by = (H + kBTY - 1) / kBTY;
     g.gx = (W + kGX - 1) / kGX;
@@ -1481,15 +1487,15 @@ cudaError_t stn_fwd_launch(const StnArgs &a, cudaStream_t s) {
     const StnGeom g = stn_geom(a.H, a.W, a.Ho, a.Wo);
     const bool vec = (a.W % 4 == 0) && aligned16(a.x);
     const size_t sm = out_tile_smem();
-    dim3 grid(g.fj * g.fi, a.N);
+    dim3 grid(g.fj * g.fi_fwd, a.N);
     if (vec) {
         set_smem(stn_out_tile<MODE_FWD, true>, sm);
         stn_out_tile<MODE_FWD, true><<<grid, kThreads, sm, s>>>(a, nullptr, nullptr, nullptr, nullptr,
-                                                                nullptr, g.fj, g.fi);
+                                                                nullptr, g.fj, g.fi_fwd);
     } else {
         set_smem(stn_out_tile<MODE_FWD, false>, sm);
         stn_out_tile<MODE_FWD, false><<<grid, kThreads, sm, s>>>(a, nullptr, nullptr, nullptr, nullptr,
-                                                                 nullptr, g.fj, g.fi);
+                                                                 nullptr, g.fj, g.fi_fwd);
     }
     note_launch();
     return cudaGetLastError();
@@ -1501,14 +1507,15 @@ cudaError_t flow_tile_launch(const StnArgs &a, int mode, cudaStream_t s) {
     const size_t sm = out_tile_smem();
     dim3 grid(g.fj * g.fi, a.N);
     if (mode == MODE_FWD) {
+        grid.x = g.fj * g.fi_fwd;
         if (vec) {
             set_smem(stn_out_tile<MODE_FWD, true, true>, sm);
             stn_out_tile<MODE_FWD, true, true><<<grid, kThreads, sm, s>>>(a, nullptr, nullptr, nullptr, nullptr,
-                                                                          nullptr, g.fj, g.fi);
+                                                                          nullptr, g.fj, g.fi_fwd);
         } else {
             set_smem(stn_out_tile<MODE_FWD, false, true>, sm);
             stn_out_tile<MODE_FWD, false, true><<<grid, kThreads, sm, s>>>(a, nullptr, nullptr, nullptr, nullptr,
-                                                                           nullptr, g.fj, g.fi);
+                                                                           nullptr, g.fj, g.fi_fwd);
         }
     } else {
         if (vec) {
