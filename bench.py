@@ -186,6 +186,14 @@ def alloc_outputs(s, w, b, host=False):
     }
 
 
+def config_dict(world):
+    return {"workload": "configs[4]: batch 64 @ 1024x1024 per layer (STN C=16 | warp C=3 smooth "
+                        "flow | bslice grid 16x16x8x12), one step = fwd+bwd of all three",
+            "global_batch": BATCH, "H": H, "W": W, "per_rank_batch": BATCH // world,
+            "parallelism": f"batch-shard x{world}, no data-path collective",
+            "l2": "inputs > L2 (4.3 GB STN tensors), no flush between steps"}
+
+
 def step_calls(rs, s, w, b, o):
     """The six C-ABI calls of one step, as (name, thunk)."""
     return [
@@ -331,10 +339,10 @@ def run_reference(args, world, rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (synth/, seeded)",
-        "config": {"workload": "configs[4] sample: 1 x 1024^2 per layer per step (bounded)",
-                   "layers": "stn C=16, warp C=3 smooth flow, bslice grid 16x16x8"},
+        "config": config_dict(1),
         "cpu_baseline": {"value": v, "unit": UNIT, "kind": "oracle", "cores": oracle.get_threads(),
-                         "sample": "one 1024^2 sample of each layer per step"},
+                         "sample": "each step = one 1024^2 sample (of the 64) of each layer, fp64 C "
+                                   "oracle, OpenMP; value = that sample's pixels / step time"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -432,11 +440,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (synth/: seeded per-sample recipe, generated on device)",
-        "config": {"workload": "configs[4]: batch 64 @ 1024x1024 per layer (STN C=16 | warp C=3 smooth "
-                               "flow | bslice grid 16x16x8x12), one step = fwd+bwd of all three",
-                   "global_batch": BATCH, "H": H, "W": W, "per_rank_batch": nb,
-                   "parallelism": f"batch-shard x{world}, no data-path collective",
-                   "l2": "inputs > L2 (4.3 GB STN tensors), no flush between steps"},
+        "config": config_dict(world),
         "layers": layers, "roofline": roof, "gpu_launches": launches,
         "clocks": clk, "e2e": e2e,
     }
