@@ -185,6 +185,8 @@ static rs_status stn_validate(const float *x, const float *theta, int N, int C, 
                     C, H, W, Ho, Wo);
     if (o.align_corners && (Ho < 2 || Wo < 2))
         return fail(RS_ERR_SHAPE, "stn: align_corners=1 needs Ho, Wo >= 2 (got %d, %d)", Ho, Wo);
+    if (N > 65535 || (long long)H * W >= (1LL << 31) || (long long)Ho * Wo >= (1LL << 31))
+        return fail(RS_ERR_SHAPE, "stn: N <= 65535 and H*W, Ho*Wo < 2^31 per launch (split the batch)");
     return check_opts(o);
 }
 
@@ -255,6 +257,8 @@ static rs_status warp_validate(const float *x, const float *flow, int N, int C, 
     if (!x || !flow) return fail(RS_ERR_NULL, "warp: x and flow are required");
     if (!pos(N) || !pos(C) || !pos(H) || !pos(W))
         return fail(RS_ERR_SHAPE, "warp: dims must be positive (N=%d C=%d H=%d W=%d)", N, C, H, W);
+    if (N > 65535 || (long long)H * W >= (1LL << 31))
+        return fail(RS_ERR_SHAPE, "warp: N <= 65535 and H*W < 2^31 per launch (split the batch)");
     return check_opts(o);
 }
 
@@ -317,6 +321,8 @@ static rs_status bslice_validate(const float *grid, const float *guide, const fl
         return fail(RS_ERR_SHAPE, "bslice: dims must be positive (N=%d H=%d W=%d D=%d Gh=%d Gw=%d)",
                     N, H, W, D, Gh, Gw);
     if (H > 65535 || W > 65535) return fail(RS_ERR_SHAPE, "bslice: H, W must be <= 65535");
+    if ((long long)N * (Gh + 1) * (Gw + 1) * 4 >= (1LL << 31))
+        return fail(RS_ERR_SHAPE, "bslice: too many dual-cell tiles per launch (split the batch)");
     return check_opts(o);
 }
 

@@ -61,6 +61,16 @@ RS_DEV Cell cell_of(double v) {
     return c;
 }
 
+// ----------------------------------------------------------------- cheap integer division
+// a / d for 0 <= a < 2^31, d >= 1, via a double reciprocal and a one-step fix-up
+// (avoids the 64-bit software division routine in per-pixel index math).
+RS_DEV int fast_div(int a, int d, double inv_d) {
+    int q = (int)((double)a * inv_d);
+    if (q * d > a) q--;
+    if ((q + 1) * d <= a) q++;
+    return q;
+}
+
 // ----------------------------------------------------------------- reductions
 RS_DEV float warp_sum(float v) {
 #pragma unroll
@@ -89,6 +99,14 @@ RS_DEV void red_add(float *addr, float a) {
 RS_DEV float ldg_stream(const float *p) {
     float v;
     asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+
+// read-only gather load with a 128-B L2 fetch hint (the neighbours of a bilinear tap
+// are read by adjacent lanes / rows soon after)
+RS_DEV float ldg_tap(const float *p) {
+    float v;
+    asm volatile("ld.global.nc.L2::128B.f32 %0, [%1];" : "=f"(v) : "l"(p));
     return v;
 }
 

@@ -18,6 +18,15 @@ namespace {
 
 constexpr int kThreads = 256;
 
+#ifndef RS_TAP_HINT
+#define RS_TAP_HINT 1
+#endif
+#if RS_TAP_HINT
+#define TAPLD(p) ldg_tap(p)
+#else
+#define TAPLD(p) __ldg(p)
+#endif
+
 struct Tap {
     long long o00;
     float w00, w01, w10, w11;
@@ -53,64 +62,84 @@ RS_DEV Tap warp_tap(const WarpArgs &a, int x, int y, float u, float v, float &cg
     return t;
 }
 
-__global__ void __launch_bounds__(kThreads) warp_fwd_kernel(WarpArgs a) {
-    const long long HW = (long long)a.H * a.W;
-    const long long idx = (long long)blockIdx.x * kThreads + threadIdx.x;
-    if (idx >= (long long)a.N * HW) return;
-    const int n = (int)(idx / HW);
-    const long long rem = idx - (long long)n * HW;
-    const int y = (int)(rem / a.W), x = (int)(rem - (long long)y * a.W);
+// grid = (ceil(H*W / 256), N): sample from blockIdx.y, 32-bit offsets inside a sample
+// (H*W < 2^31 is validated by the API), row from a reciprocal-multiply division.
+__global__ void __launch_bounds__(kThreads) warp_fwd_kernel(WarpArgs a, double invW) {
+    const int HW = a.H * a.W;
+    const int rem = blockIdx.x * kThreads + threadIdx.x;
+    if (rem >= HW) return;
+    const int n = blockIdx.y;
+    const int y = fast_div(rem, a.W, invW), x = rem - y * a.W;
     const float *fp = a.flow + (long long)n * 2 * HW + rem;
     const float u = ldg_stream(fp), v = ldg_stream(fp + HW);
     float cgx, cgy;
     const Tap t = warp_tap(a, x, y, u, v, cgx, cgy);
-    const float *xp = a.x + (long long)n * a.C * HW + t.o00;
+    const float *xp = a.x + (long long)n * a.C * HW;
     float *yp = a.y + (long long)n * a.C * HW + rem;
+    const int o00 = (int)t.o00;
 #pragma unroll 3
     for (int c = 0; c < a.C; c++) {
-        const float *p = xp + (long long)c * HW;
+        const float *p = xp + o00;
         float r = 0.f;
-        if (t.k00) r = fmaf(t.w00, __ldg(p), r);
-        if (t.k01) r = fmaf(t.w01, __ldg(p + 1), r);
-        if (t.k10) r = fmaf(t.w10, __ldg(p + a.W), r);
-        if (t.k11) r = fmaf(t.w11, __ldg(p + a.W + 1), r);
-        yp[(long long)c * HW] = r;
+        if (t.k00) r = fmaf(t.w00, TAPLD(p), r);
+        if (t.k01) r = fmaf(t.w01, TAPLD(p + 1), r);
+        if (t.k10) r = fmaf(t.w10, TAPLD(p + a.W), r);
+        if (t.k11) r = fmaf(t.w11, TAPLD(p + a.W + 1), r);
+        *yp = r;
+        xp += HW;
+        yp += HW;
     }
 }
 
-__global__ void __launch_bounds__(kThreads) warp_bwd_kernel(WarpArgs a) {
-    const long long HW = (long long)a.H * a.W;
-    const long long idx = (long long)blockIdx.x * kThreads + threadIdx.x;
-    if (idx >= (long long)a.N * HW) return;
-    const int n = (int)(idx / HW);
-    const long long rem = idx - (long long)n * HW;
-    const int y = (int)(rem / a.W), x = (int)(rem - (long long)y * a.W);
+__global__ void __launch_bounds__(kThreads) warp_bwd_kernel(WarpArgs a, double invW) {
+    const int HW = a.H * a.W;
+    const int rem0 = blockIdx.x * kThreads + threadIdx.x;
+    const bool live = rem0 < HW;
+    const int rem = live ? rem0 : HW - 1;  // tail lanes shadow the last pixel (all work masked)
+    const int n = blockIdx.y;
+    const int y = fast_div(rem, a.W, invW), x = rem - y * a.W;
     const float *fp = a.flow + (long long)n * 2 * HW + rem;
     const float u = ldg_stream(fp), v = ldg_stream(fp + HW);
     float cgx, cgy;
-    const Tap t = warp_tap(a, x, y, u, v, cgx, cgy);
-    const float *xp = a.x + (long long)n * a.C * HW + t.o00;
-    float *dxp = a.dx ? a.dx + (long long)n * a.C * HW + t.o00 : nullptr;
+    Tap t = warp_tap(a, x, y, u, v, cgx, cgy);
+    if (!live) t.k00 = t.k01 = t.k10 = t.k11 = false;
+    const int o00 = (int)t.o00;
+    const float *xp = a.x + (long long)n * a.C * HW + o00;
+    float *dxp = a.dx ? a.dx + (long long)n * a.C * HW + o00 : nullptr;
+    // lane l absorbs lane l-1's right taps if they are the same addresses (o00 one apart,
+    // same sample: blocks never straddle samples, and a row step changes o00 by W)
+    const int lane = threadIdx.x & 31;
+    const int o_prev = __shfl_up_sync(0xffffffffu, o00, 1);
+    const bool k01_prev = __shfl_up_sync(0xffffffffu, (int)t.k01, 1) != 0;
+    const bool k11_prev = __shfl_up_sync(0xffffffffu, (int)t.k11, 1) != 0;
+    const bool absorb = lane > 0 && o_prev + 1 == o00 && k01_prev == t.k00 && k11_prev == t.k10;
+    const bool given = __shfl_down_sync(0xffffffffu, (int)absorb, 1) != 0 && lane < 31;
     const float *gp = a.dy + (long long)n * a.C * HW + rem;
     float dix = 0.f, diy = 0.f;
     for (int c = 0; c < a.C; c++) {
-        const float g = ldg_stream(gp + (long long)c * HW);
+        const float g = ldg_stream(gp);
         if (a.dflow) {
-            const float *p = xp + (long long)c * HW;
-            const float v00 = t.k00 ? __ldg(p) : 0.f, v01 = t.k01 ? __ldg(p + 1) : 0.f;
-            const float v10 = t.k10 ? __ldg(p + a.W) : 0.f, v11 = t.k11 ? __ldg(p + a.W + 1) : 0.f;
+            const float v00 = t.k00 ? TAPLD(xp) : 0.f, v01 = t.k01 ? TAPLD(xp + 1) : 0.f;
+            const float v10 = t.k10 ? TAPLD(xp + a.W) : 0.f, v11 = t.k11 ? TAPLD(xp + a.W + 1) : 0.f;
             dix = fmaf(g, fmaf(1.f - t.fy, v01 - v00, t.fy * (v11 - v10)), dix);
             diy = fmaf(g, fmaf(1.f - t.fx, v10 - v00, t.fx * (v11 - v01)), diy);
         }
         if (dxp) {
-            float *q = dxp + (long long)c * HW;
-            if (t.k00) red_add(q, t.w00 * g);
-            if (t.k01) red_add(q + 1, t.w01 * g);
-            if (t.k10) red_add(q + a.W, t.w10 * g);
-            if (t.k11) red_add(q + a.W + 1, t.w11 * g);
+            // merge with the left neighbour lane when its right taps are our left taps
+            // (same row, floor cell one to the left): about half the reds for smooth flow
+            const float r01 = __shfl_up_sync(0xffffffffu, t.w01 * g, 1);
+            const float r11 = __shfl_up_sync(0xffffffffu, t.w11 * g, 1);
+            const float l00 = t.w00 * g + (absorb ? r01 : 0.f), l10 = t.w10 * g + (absorb ? r11 : 0.f);
+            if (t.k00) red_add(dxp, l00);
+            if (t.k01 && !given) red_add(dxp + 1, t.w01 * g);
+            if (t.k10) red_add(dxp + a.W, l10);
+            if (t.k11 && !given) red_add(dxp + a.W + 1, t.w11 * g);
+            dxp += HW;
         }
+        gp += HW;
+        xp += HW;
     }
-    if (a.dflow) {
+    if (a.dflow && live) {
         float *dfp = a.dflow + (long long)n * 2 * HW + rem;
         dfp[0] = dix * cgx;
         dfp[HW] = diy * cgy;
@@ -147,8 +176,8 @@ static bool warp_direct() {
 
 cudaError_t warp_fwd_launch(const WarpArgs &a, cudaStream_t s) {
     if (!warp_direct()) return flow_tile_launch(as_tile_args(a), 0, s);
-    long long total = (long long)a.N * a.H * a.W;
-    warp_fwd_kernel<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(a);
+    const int HW = a.H * a.W;
+    warp_fwd_kernel<<<dim3((HW + kThreads - 1) / kThreads, a.N), kThreads, 0, s>>>(a, 1.0 / a.W);
     note_launch();
     return cudaGetLastError();
 }
@@ -165,8 +194,7 @@ cudaError_t warp_bwd_launch(const WarpArgs &a, int algo, int deterministic, void
         if (e != cudaSuccess) return e;
     }
     if (!warp_direct()) return flow_tile_launch(as_tile_args(a), 2, s);
-    long long total = (long long)a.N * HW;
-    warp_bwd_kernel<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(a);
+    warp_bwd_kernel<<<dim3((unsigned)((HW + kThreads - 1) / kThreads), a.N), kThreads, 0, s>>>(a, 1.0 / a.W);
     note_launch();
     return cudaGetLastError();
 }
