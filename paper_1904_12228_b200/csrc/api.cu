@@ -58,85 +58,108 @@ rs_status check_opts(const rs_opts &o) {
     return RS_OK;
 }
 
-// Host-or-device pointer staging.  Every buffer the call touches is registered;
-// host ones get a stream-ordered device temporary.
-class Stager {
-   public:
-    explicit Stager(cudaStream_t s) : s_(s) {}
-    ~Stager() {
-        for (auto &e : ents_)
-            if (e.dev && e.owned) cudaFreeAsync(e.dev, s_);
-    }
-    // returns the device-visible pointer (nullptr stays nullptr)
-    template <typename T>
-    T *in(const T *p, size_t count, rs_status &st) {
-        return (T *)stage((void *)p, count * sizeof(T), true, false, st);
-    }
-    template <typename T>
-    T *out(T *p, size_t count, rs_status &st) {
-        return (T *)stage((void *)p, count * sizeof(T), false, true, st);
-    }
-    void *scratch(size_t bytes, rs_status &st) {
-        void *d = nullptr;
-        cudaError_t e = cudaMallocAsync(&d, bytes ? bytes : 1, s_);
-        if (e != cudaSuccess) {
-            st = fail(RS_ERR_WORKSPACE, "workspace cudaMallocAsync(%zu): %s", bytes, cudaGetErrorString(e));
-            return nullptr;
-        }
-        ents_.push_back({nullptr, d, 0, false, true});
-        return d;
-    }
-    // copy staged outputs back to the caller's host buffers
-    rs_status finish() {
-        for (auto &e : ents_) {
-            if (e.host && e.is_out) {
-                cudaError_t c = cudaMemcpyAsync(e.host, e.dev, e.bytes, cudaMemcpyDeviceToHost, s_);
-                if (c != cudaSuccess)
-                    return fail(RS_ERR_CUDA, "D2H copy: %s", cudaGetErrorString(c));
-            }
-        }
-        return RS_OK;
-    }
-    size_t h2d_bytes() const { return h2d_; }
-
-   private:
-    struct Ent {
-        void *host;
-        void *dev;
-        size_t bytes;
-        bool is_out;
-        bool owned;
-    };
-    void *stage(void *p, size_t bytes, bool is_in, bool is_out, rs_status &st) {
-        if (!p) return nullptr;
-        cudaPointerAttributes at;
-        cudaError_t e = cudaPointerGetAttributes(&at, p);
-        if (e != cudaSuccess) {
-            cudaGetLastError();  // clear
-            at.type = cudaMemoryTypeUnregistered;
-        }
-        if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) return p;
-        void *d = nullptr;
-        e = cudaMallocAsync(&d, bytes ? bytes : 1, s_);
-        if (e != cudaSuccess) {
-            st = fail(RS_ERR_CUDA, "staging cudaMallocAsync(%zu): %s", bytes, cudaGetErrorString(e));
-            return nullptr;
-        }
-        ents_.push_back({p, d, bytes, is_out, true});
-        if (is_in) {
-            e = cudaMemcpyAsync(d, p, bytes, cudaMemcpyHostToDevice, s_);
-            if (e != cudaSuccess) {
-                st = fail(RS_ERR_CUDA, "H2D copy: %s", cudaGetErrorString(e));
-                return nullptr;
-            }
-            h2d_ += bytes;
-        }
-        return d;
-    }
-    cudaStream_t s_;
-    std::vector<Ent> ents_;
-    size_t h2d_ = 0;
+// One tensor argument of an entry point: pointer (device, host or NULL), bytes per
+// sample, direction.
+struct TArg {
+    const void *p;
+    size_t per_sample;
+    bool in;
+    bool out;
 };
+
+bool is_device_ptr(const void *p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();  // clear: unregistered host memory on old drivers
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// Run launch(n0, nc, ptrs, stream, workspace) over samples [0, N).
+//  * all pointers device memory: one launch on `s` with the caller's pointers and
+//    workspace (allocated stream-ordered on `s` if absent / too small);
+//  * any host pointer: the batch is split into sample chunks processed on two
+//    internal streams ordered after `s` (and `s` after them): per chunk, host inputs
+//    are copied H2D into stream-ordered temporaries, the kernels run, host outputs
+//    are copied D2H — copies of one chunk overlap the kernels of the other (every
+//    sample is independent).  Pinned host memory keeps all of it asynchronous.
+template <class F, class WS>
+rs_status run_batched(int N, std::vector<TArg> &args, cudaStream_t s, void *workspace, size_t ws_bytes,
+                      WS &&ws_need, F &&launch) {
+    const int na = (int)args.size();
+    std::vector<bool> host(na, false);
+    bool any_host = false;
+    for (int i = 0; i < na; i++)
+        if (args[i].p && !is_device_ptr(args[i].p)) host[i] = any_host = true;
+    std::vector<void *> ptr(na);
+    if (!any_host) {
+        for (int i = 0; i < na; i++) ptr[i] = const_cast<void *>(args[i].p);
+        const size_t need = ws_need(N);
+        void *ws = workspace;
+        bool own = false;
+        if (need && (!ws || ws_bytes < need)) {
+            cudaError_t e = cudaMallocAsync(&ws, need, s);
+            if (e != cudaSuccess) return fail(RS_ERR_WORKSPACE, "workspace cudaMallocAsync(%zu): %s", need, cudaGetErrorString(e));
+            own = true;
+        }
+        cudaError_t e = launch(0, N, ptr.data(), s, ws);
+        if (own) cudaFreeAsync(ws, s);
+        if (e != cudaSuccess) return fail(RS_ERR_CUDA, "launch: %s", cudaGetErrorString(e));
+        return ok();
+    }
+    const int nchunk = N < 8 ? N : 8;
+    const int cs = (N + nchunk - 1) / nchunk;
+    cudaStream_t st[2];
+    cudaEvent_t ev0, evs[2];
+    for (int k = 0; k < 2; k++) cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
+    cudaEventRecord(ev0, s);
+    std::vector<void *> buf[2];
+    void *wsk[2] = {nullptr, nullptr};
+    cudaError_t err = cudaSuccess;
+    for (int k = 0; k < 2; k++) {
+        cudaStreamWaitEvent(st[k], ev0, 0);
+        buf[k].assign(na, nullptr);
+        for (int i = 0; i < na; i++)
+            if (host[i] && err == cudaSuccess) err = cudaMallocAsync(&buf[k][i], args[i].per_sample * cs, st[k]);
+        const size_t need = ws_need(cs);
+        if (need && err == cudaSuccess) err = cudaMallocAsync(&wsk[k], need, st[k]);
+    }
+    for (int c = 0, n0 = 0; n0 < N && err == cudaSuccess; c++, n0 += cs) {
+        const int nc = N - n0 < cs ? N - n0 : cs, k = c & 1;
+        for (int i = 0; i < na && err == cudaSuccess; i++) {
+            const size_t off = args[i].per_sample * (size_t)n0, bytes = args[i].per_sample * (size_t)nc;
+            if (!args[i].p) {
+                ptr[i] = nullptr;
+            } else if (host[i]) {
+                ptr[i] = buf[k][i];
+                if (args[i].in)
+                    err = cudaMemcpyAsync(ptr[i], (const char *)args[i].p + off, bytes, cudaMemcpyHostToDevice, st[k]);
+            } else {
+                ptr[i] = (char *)const_cast<void *>(args[i].p) + off;
+            }
+        }
+        if (err == cudaSuccess) err = launch(n0, nc, ptr.data(), st[k], wsk[k]);
+        for (int i = 0; i < na && err == cudaSuccess; i++)
+            if (host[i] && args[i].out)
+                err = cudaMemcpyAsync((char *)const_cast<void *>(args[i].p) + args[i].per_sample * (size_t)n0, ptr[i],
+                                      args[i].per_sample * (size_t)nc, cudaMemcpyDeviceToHost, st[k]);
+    }
+    for (int k = 0; k < 2; k++) {
+        for (int i = 0; i < na; i++)
+            if (buf[k][i]) cudaFreeAsync(buf[k][i], st[k]);
+        if (wsk[k]) cudaFreeAsync(wsk[k], st[k]);
+        cudaEventCreateWithFlags(&evs[k], cudaEventDisableTiming);
+        cudaEventRecord(evs[k], st[k]);
+        cudaStreamWaitEvent(s, evs[k], 0);
+        cudaEventDestroy(evs[k]);
+        cudaStreamDestroy(st[k]);  // released once its queued work completes
+    }
+    cudaEventDestroy(ev0);
+    if (err != cudaSuccess) return fail(RS_ERR_CUDA, "host-staged path: %s", cudaGetErrorString(err));
+    return ok();
+}
 
 rs_status launched(cudaError_t e, const char *what) {
     if (e != cudaSuccess) return fail(RS_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
@@ -197,18 +220,20 @@ rs_status stn_fwd(const float *x, const float *theta, int N, int C, int H, int W
     if (st != RS_OK) return st;
     if (!y) return fail(RS_ERR_NULL, "stn_fwd: y is required");
     cudaStream_t s = (cudaStream_t)stream;
-    Stager sg(s);
-    rs::StnArgs a{};
-    a.x = sg.in(x, (size_t)N * C * H * W, st);
-    a.theta = sg.in(theta, (size_t)N * 6, st);
-    a.y = sg.out(y, (size_t)N * C * Ho * Wo, st);
-    if (st != RS_OK) return st;
-    a.N = N; a.C = C; a.H = H; a.W = W; a.Ho = Ho; a.Wo = Wo;
-    a.ac = o.align_corners;
-    a.border = o.padding == RS_PAD_BORDER;
-    st = launched(rs::stn_fwd_launch(a, s), "stn_fwd launch");
-    if (st != RS_OK) return st;
-    return sg.finish() == RS_OK ? ok() : RS_ERR_CUDA;
+    std::vector<TArg> args = {{x, sizeof(float) * (size_t)C * H * W, true, false},
+                              {theta, sizeof(float) * 6, true, false},
+                              {y, sizeof(float) * (size_t)C * Ho * Wo, false, true}};
+    return run_batched(N, args, s, nullptr, 0, [](int) { return (size_t)0; },
+                       [&](int, int nc, void **p, cudaStream_t t, void *) {
+                           rs::StnArgs a{};
+                           a.x = (const float *)p[0];
+                           a.theta = (const float *)p[1];
+                           a.y = (float *)p[2];
+                           a.N = nc; a.C = C; a.H = H; a.W = W; a.Ho = Ho; a.Wo = Wo;
+                           a.ac = o.align_corners;
+                           a.border = o.padding == RS_PAD_BORDER;
+                           return rs::stn_fwd_launch(a, t);
+                       });
 }
 
 rs_status stn_bwd(const float *x, const float *theta, const float *dy, int N, int C, int H, int W,
@@ -229,26 +254,26 @@ rs_status stn_bwd(const float *x, const float *theta, const float *dy, int N, in
         return fail(RS_ERR_FLAG, "stn_bwd: SCATTER_ATOMIC is not deterministic");
     if (!dx && !dtheta) return ok();
     cudaStream_t s = (cudaStream_t)stream;
-    Stager sg(s);
-    rs::StnArgs a{};
-    a.x = sg.in(x, (size_t)N * C * H * W, st);
-    a.theta = sg.in(theta, (size_t)N * 6, st);
-    a.dy = sg.in(dy, (size_t)N * C * Ho * Wo, st);
-    a.dx = sg.out(dx, (size_t)N * C * H * W, st);
-    a.dtheta = sg.out(dtheta, (size_t)N * 6, st);
-    if (st != RS_OK) return st;
-    const size_t need = rs::stn_ws_bytes(N, C, H, W, Ho, Wo);
-    void *ws = workspace;
-    if (!ws || ws_bytes < need) {
-        ws = sg.scratch(need, st);
-        if (st != RS_OK) return st;
-    }
-    a.N = N; a.C = C; a.H = H; a.W = W; a.Ho = Ho; a.Wo = Wo;
-    a.ac = o.align_corners;
-    a.border = border;
-    st = launched(rs::stn_bwd_launch(a, o.algo, o.deterministic, ws, need, s), "stn_bwd launch");
-    if (st != RS_OK) return st;
-    return sg.finish() == RS_OK ? ok() : RS_ERR_CUDA;
+    std::vector<TArg> args = {{x, sizeof(float) * (size_t)C * H * W, true, false},
+                              {theta, sizeof(float) * 6, true, false},
+                              {dy, sizeof(float) * (size_t)C * Ho * Wo, true, false},
+                              {dx, sizeof(float) * (size_t)C * H * W, false, true},
+                              {dtheta, sizeof(float) * 6, false, true}};
+    return run_batched(N, args, s, workspace, ws_bytes,
+                       [&](int n) { return rs::stn_ws_bytes(n, C, H, W, Ho, Wo); },
+                       [&](int, int nc, void **p, cudaStream_t t, void *ws) {
+                           rs::StnArgs a{};
+                           a.x = (const float *)p[0];
+                           a.theta = (const float *)p[1];
+                           a.dy = (const float *)p[2];
+                           a.dx = (float *)p[3];
+                           a.dtheta = (float *)p[4];
+                           a.N = nc; a.C = C; a.H = H; a.W = W; a.Ho = Ho; a.Wo = Wo;
+                           a.ac = o.align_corners;
+                           a.border = border;
+                           return rs::stn_bwd_launch(a, o.algo, o.deterministic, ws,
+                                                     rs::stn_ws_bytes(nc, C, H, W, Ho, Wo), t);
+                       });
 }
 
 // ------------------------------------------------------------------------------ warp
@@ -269,17 +294,19 @@ rs_status warp_fwd(const float *x, const float *flow, int N, int C, int H, int W
     if (st != RS_OK) return st;
     if (!y) return fail(RS_ERR_NULL, "warp_fwd: y is required");
     cudaStream_t s = (cudaStream_t)stream;
-    Stager sg(s);
-    rs::WarpArgs a{};
-    a.x = sg.in(x, (size_t)N * C * H * W, st);
-    a.flow = sg.in(flow, (size_t)N * 2 * H * W, st);
-    a.y = sg.out(y, (size_t)N * C * H * W, st);
-    if (st != RS_OK) return st;
-    a.N = N; a.C = C; a.H = H; a.W = W;
-    a.border = o.padding == RS_PAD_BORDER;
-    st = launched(rs::warp_fwd_launch(a, s), "warp_fwd launch");
-    if (st != RS_OK) return st;
-    return sg.finish() == RS_OK ? ok() : RS_ERR_CUDA;
+    std::vector<TArg> args = {{x, sizeof(float) * (size_t)C * H * W, true, false},
+                              {flow, sizeof(float) * 2 * (size_t)H * W, true, false},
+                              {y, sizeof(float) * (size_t)C * H * W, false, true}};
+    return run_batched(N, args, s, nullptr, 0, [](int) { return (size_t)0; },
+                       [&](int, int nc, void **p, cudaStream_t t, void *) {
+                           rs::WarpArgs a{};
+                           a.x = (const float *)p[0];
+                           a.flow = (const float *)p[1];
+                           a.y = (float *)p[2];
+                           a.N = nc; a.C = C; a.H = H; a.W = W;
+                           a.border = o.padding == RS_PAD_BORDER;
+                           return rs::warp_fwd_launch(a, t);
+                       });
 }
 
 rs_status warp_bwd(const float *x, const float *flow, const float *dy, int N, int C, int H, int W,
@@ -297,20 +324,23 @@ rs_status warp_bwd(const float *x, const float *flow, const float *dy, int N, in
         return fail(RS_ERR_FLAG, "warp_bwd: no deterministic d_input path (atomic scatter)");
     if (!dx && !dflow) return ok();
     cudaStream_t s = (cudaStream_t)stream;
-    Stager sg(s);
-    rs::WarpArgs a{};
-    a.x = sg.in(x, (size_t)N * C * H * W, st);
-    a.flow = sg.in(flow, (size_t)N * 2 * H * W, st);
-    a.dy = sg.in(dy, (size_t)N * C * H * W, st);
-    a.dx = sg.out(dx, (size_t)N * C * H * W, st);
-    a.dflow = sg.out(dflow, (size_t)N * 2 * H * W, st);
-    if (st != RS_OK) return st;
-    a.N = N; a.C = C; a.H = H; a.W = W;
-    a.border = o.padding == RS_PAD_BORDER;
-    st = launched(rs::warp_bwd_launch(a, o.algo, o.deterministic, workspace, ws_bytes, s),
-                  "warp_bwd launch");
-    if (st != RS_OK) return st;
-    return sg.finish() == RS_OK ? ok() : RS_ERR_CUDA;
+    std::vector<TArg> args = {{x, sizeof(float) * (size_t)C * H * W, true, false},
+                              {flow, sizeof(float) * 2 * (size_t)H * W, true, false},
+                              {dy, sizeof(float) * (size_t)C * H * W, true, false},
+                              {dx, sizeof(float) * (size_t)C * H * W, false, true},
+                              {dflow, sizeof(float) * 2 * (size_t)H * W, false, true}};
+    return run_batched(N, args, s, workspace, ws_bytes, [&](int n) { return rs::warp_ws_bytes(n, C, H, W); },
+                       [&](int, int nc, void **p, cudaStream_t t, void *ws) {
+                           rs::WarpArgs a{};
+                           a.x = (const float *)p[0];
+                           a.flow = (const float *)p[1];
+                           a.dy = (const float *)p[2];
+                           a.dx = (float *)p[3];
+                           a.dflow = (float *)p[4];
+                           a.N = nc; a.C = C; a.H = H; a.W = W;
+                           a.border = o.padding == RS_PAD_BORDER;
+                           return rs::warp_bwd_launch(a, o.algo, o.deterministic, ws, 0, t);
+                       });
 }
 
 // ------------------------------------------------------------------------------ bslice
@@ -333,17 +363,20 @@ rs_status bslice_fwd(const float *grid, const float *guide, const float *x, int 
     if (st != RS_OK) return st;
     if (!y) return fail(RS_ERR_NULL, "bslice_fwd: y is required");
     cudaStream_t s = (cudaStream_t)stream;
-    Stager sg(s);
-    rs::BsliceArgs a{};
-    a.grid = sg.in(grid, (size_t)N * 12 * D * Gh * Gw, st);
-    a.guide = sg.in(guide, (size_t)N * H * W, st);
-    a.x = sg.in(x, (size_t)N * 3 * H * W, st);
-    a.y = sg.out(y, (size_t)N * 3 * H * W, st);
-    if (st != RS_OK) return st;
-    a.N = N; a.H = H; a.W = W; a.D = D; a.Gh = Gh; a.Gw = Gw;
-    st = launched(rs::bslice_fwd_launch(a, s), "bslice_fwd launch");
-    if (st != RS_OK) return st;
-    return sg.finish() == RS_OK ? ok() : RS_ERR_CUDA;
+    std::vector<TArg> args = {{grid, sizeof(float) * 12 * (size_t)D * Gh * Gw, true, false},
+                              {guide, sizeof(float) * (size_t)H * W, true, false},
+                              {x, sizeof(float) * 3 * (size_t)H * W, true, false},
+                              {y, sizeof(float) * 3 * (size_t)H * W, false, true}};
+    return run_batched(N, args, s, nullptr, 0, [](int) { return (size_t)0; },
+                       [&](int, int nc, void **p, cudaStream_t t, void *) {
+                           rs::BsliceArgs a{};
+                           a.grid = (const float *)p[0];
+                           a.guide = (const float *)p[1];
+                           a.x = (const float *)p[2];
+                           a.y = (float *)p[3];
+                           a.N = nc; a.H = H; a.W = W; a.D = D; a.Gh = Gh; a.Gw = Gw;
+                           return rs::bslice_fwd_launch(a, t);
+                       });
 }
 
 rs_status bslice_bwd(const float *grid, const float *guide, const float *x, const float *dy, int N,
@@ -360,26 +393,28 @@ rs_status bslice_bwd(const float *grid, const float *guide, const float *x, cons
         return fail(RS_ERR_FLAG, "bslice_bwd: shape needs the atomic d_grid path (cells < 8 px); not deterministic");
     if (!dgrid && !dguide && !dx) return ok();
     cudaStream_t s = (cudaStream_t)stream;
-    Stager sg(s);
-    rs::BsliceArgs a{};
-    a.grid = sg.in(grid, (size_t)N * 12 * D * Gh * Gw, st);
-    a.guide = sg.in(guide, (size_t)N * H * W, st);
-    a.x = sg.in(x, (size_t)N * 3 * H * W, st);
-    a.dy = sg.in(dy, (size_t)N * 3 * H * W, st);
-    a.dgrid = sg.out(dgrid, (size_t)N * 12 * D * Gh * Gw, st);
-    a.dguide = sg.out(dguide, (size_t)N * H * W, st);
-    a.dx = sg.out(dx, (size_t)N * 3 * H * W, st);
-    if (st != RS_OK) return st;
-    a.N = N; a.H = H; a.W = W; a.D = D; a.Gh = Gh; a.Gw = Gw;
-    size_t need = rs::bslice_ws_bytes(N, H, W, D, Gh, Gw);
-    void *ws = workspace;
-    if (need && (!ws || ws_bytes < need)) {
-        ws = sg.scratch(need, st);
-        if (st != RS_OK) return st;
-    }
-    st = launched(rs::bslice_bwd_launch(a, o.algo, o.deterministic, ws, need, s), "bslice_bwd launch");
-    if (st != RS_OK) return st;
-    return sg.finish() == RS_OK ? ok() : RS_ERR_CUDA;
+    std::vector<TArg> args = {{grid, sizeof(float) * 12 * (size_t)D * Gh * Gw, true, false},
+                              {guide, sizeof(float) * (size_t)H * W, true, false},
+                              {x, sizeof(float) * 3 * (size_t)H * W, true, false},
+                              {dy, sizeof(float) * 3 * (size_t)H * W, true, false},
+                              {dgrid, sizeof(float) * 12 * (size_t)D * Gh * Gw, false, true},
+                              {dguide, sizeof(float) * (size_t)H * W, false, true},
+                              {dx, sizeof(float) * 3 * (size_t)H * W, false, true}};
+    return run_batched(N, args, s, workspace, ws_bytes,
+                       [&](int n) { return rs::bslice_ws_bytes(n, H, W, D, Gh, Gw); },
+                       [&](int, int nc, void **p, cudaStream_t t, void *ws) {
+                           rs::BsliceArgs a{};
+                           a.grid = (const float *)p[0];
+                           a.guide = (const float *)p[1];
+                           a.x = (const float *)p[2];
+                           a.dy = (const float *)p[3];
+                           a.dgrid = (float *)p[4];
+                           a.dguide = (float *)p[5];
+                           a.dx = (float *)p[6];
+                           a.N = nc; a.H = H; a.W = W; a.D = D; a.Gh = Gh; a.Gw = Gw;
+                           return rs::bslice_bwd_launch(a, o.algo, o.deterministic, ws,
+                                                        rs::bslice_ws_bytes(nc, H, W, D, Gh, Gw), t);
+                       });
 }
 
 }  // extern "C"

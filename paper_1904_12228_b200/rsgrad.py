@@ -114,8 +114,10 @@ def _like(ref, shape):
     return torch.empty(shape, dtype=torch.float32, pin_memory=torch.cuda.is_available())
 
 
-def _sync_if_host(dev, *outs):
-    if any(o is not None and not o.is_cuda for o in outs):
+def _sync_if_host(dev, sync, *outs):
+    """Host outputs are written by async D2H copies on the stream: unless the caller
+    passed sync=False (and synchronises the stream itself), wait for them."""
+    if sync and any(o is not None and not o.is_cuda for o in outs):
         (torch.cuda.current_stream(dev) if dev is not None else torch.cuda.current_stream()).synchronize()
 
 
@@ -132,7 +134,7 @@ def workspace_bytes(layer, N, C=0, H=0, W=0, Ho=0, Wo=0, D=0, Gh=0, Gw=0, opts=N
 
 
 # ----------------------------------------------------------------------------- STN
-def stn_fwd(x, theta, Ho=None, Wo=None, *, align_corners=True, padding="zeros", out=None):
+def stn_fwd(x, theta, Ho=None, Wo=None, *, align_corners=True, padding="zeros", out=None, sync=True):
     N, C, H, W = x.shape
     Ho = H if Ho is None else int(Ho)
     Wo = W if Wo is None else int(Wo)
@@ -141,12 +143,12 @@ def stn_fwd(x, theta, Ho=None, Wo=None, *, align_corners=True, padding="zeros", 
     o = _opts(align_corners, padding)
     _check(lib().stn_fwd(_ptr(x), _ptr(theta), N, C, H, W, Ho, Wo, ctypes.byref(o), _ptr(y),
                          _stream(dev)), "stn_fwd")
-    _sync_if_host(dev, y)
+    _sync_if_host(dev, sync, y)
     return y
 
 
 def stn_bwd(x, theta, dy, *, align_corners=True, padding="zeros", algo="auto", deterministic=False,
-            need_dx=True, need_dtheta=True, out=None):
+            need_dx=True, need_dtheta=True, out=None, sync=True):
     N, C, H, W = x.shape
     Ho, Wo = dy.shape[2:]
     dx, dth = out if out is not None else (
@@ -157,24 +159,24 @@ def stn_bwd(x, theta, dy, *, align_corners=True, padding="zeros", algo="auto", d
     _check(lib().stn_bwd(_ptr(x), _ptr(theta), _ptr(dy), N, C, H, W, Ho, Wo, ctypes.byref(o),
                          _ptr(dx), _ptr(dth), None if ws is None else ctypes.c_void_p(ws.data_ptr()),
                          nws, _stream(dev)), "stn_bwd")
-    _sync_if_host(dev, dx, dth)
+    _sync_if_host(dev, sync, dx, dth)
     return dx, dth
 
 
 # ----------------------------------------------------------------------------- warp
-def warp_fwd(x, flow, *, padding="zeros", out=None):
+def warp_fwd(x, flow, *, padding="zeros", out=None, sync=True):
     N, C, H, W = x.shape
     y = out if out is not None else _like(x, (N, C, H, W))
     dev = _device_of(x, flow, y)
     o = _opts(True, padding)
     _check(lib().warp_fwd(_ptr(x), _ptr(flow), N, C, H, W, ctypes.byref(o), _ptr(y), _stream(dev)),
            "warp_fwd")
-    _sync_if_host(dev, y)
+    _sync_if_host(dev, sync, y)
     return y
 
 
 def warp_bwd(x, flow, dy, *, padding="zeros", algo="auto", deterministic=False, need_dx=True,
-             need_dflow=True, out=None):
+             need_dflow=True, out=None, sync=True):
     N, C, H, W = x.shape
     dx, df = out if out is not None else (
         _like(x, (N, C, H, W)) if need_dx else None, _like(x, (N, 2, H, W)) if need_dflow else None)
@@ -184,12 +186,12 @@ def warp_bwd(x, flow, dy, *, padding="zeros", algo="auto", deterministic=False, 
     _check(lib().warp_bwd(_ptr(x), _ptr(flow), _ptr(dy), N, C, H, W, ctypes.byref(o), _ptr(dx),
                           _ptr(df), None if ws is None else ctypes.c_void_p(ws.data_ptr()), nws,
                           _stream(dev)), "warp_bwd")
-    _sync_if_host(dev, dx, df)
+    _sync_if_host(dev, sync, dx, df)
     return dx, df
 
 
 # ----------------------------------------------------------------------------- bslice
-def bslice_fwd(grid, guide, x, *, out=None):
+def bslice_fwd(grid, guide, x, *, out=None, sync=True):
     N, Q, D, Gh, Gw = grid.shape
     if Q != 12 or x.shape[1] != 3:
         raise ValueError("bslice: grid must be N x 12 x D x Gh x Gw and x N x 3 x H x W")
@@ -199,12 +201,12 @@ def bslice_fwd(grid, guide, x, *, out=None):
     o = _opts()
     _check(lib().bslice_fwd(_ptr(grid), _ptr(guide), _ptr(x), N, H, W, D, Gh, Gw, ctypes.byref(o),
                             _ptr(y), _stream(dev)), "bslice_fwd")
-    _sync_if_host(dev, y)
+    _sync_if_host(dev, sync, y)
     return y
 
 
 def bslice_bwd(grid, guide, x, dy, *, algo="auto", deterministic=False, need_dgrid=True,
-               need_dguide=True, need_dx=True, out=None):
+               need_dguide=True, need_dx=True, out=None, sync=True):
     N, Q, D, Gh, Gw = grid.shape
     H, W = guide.shape[1:]
     if out is not None:
@@ -220,7 +222,7 @@ def bslice_bwd(grid, guide, x, dy, *, algo="auto", deterministic=False, need_dgr
                             ctypes.byref(o), _ptr(dgr), _ptr(dgd), _ptr(dx),
                             None if ws is None else ctypes.c_void_p(ws.data_ptr()), nws,
                             _stream(dev)), "bslice_bwd")
-    _sync_if_host(dev, dgr, dgd, dx)
+    _sync_if_host(dev, sync, dgr, dgd, dx)
     return dgr, dgd, dx
 
 

@@ -335,3 +335,30 @@ def test_warp_tiled_variant(cuda_device, monkeypatch, flow, padding):
     rdx, rdf = oracle.warp_bwd(x, fl, dy, border)
     assert_close(_np(dx), rdx, "grad", "dx")
     assert_close(_np(df), rdf, "grad", "dflow")
+
+
+def test_host_pointer_chunked_all_layers(cuda_device):
+    """Host buffers (pinned) take the library's chunked two-stream staging path
+    (batch split into sample chunks, last one ragged); results equal the device path."""
+    N = 5
+    s = synth.stn_inputs(N, 4, 40, 48, cfg=1)
+    hs = {k: v.pin_memory() for k, v in s.items()}
+    gs = _cuda(s, cuda_device)
+    assert torch.equal(rsgrad.stn_fwd(hs["x"], hs["theta"]), rsgrad.stn_fwd(gs["x"], gs["theta"]).cpu())
+    a = rsgrad.stn_bwd(hs["x"], hs["theta"], hs["dy"], deterministic=True)
+    b = rsgrad.stn_bwd(gs["x"], gs["theta"], gs["dy"], deterministic=True)
+    assert all(torch.equal(p, q.cpu()) for p, q in zip(a, b))
+    w = synth.warp_inputs(N, 3, 33, 41, cfg=1)
+    hw = {k: v.pin_memory() for k, v in w.items()}
+    gw = _cuda(w, cuda_device)
+    assert torch.equal(rsgrad.warp_fwd(hw["x"], hw["flow"]), rsgrad.warp_fwd(gw["x"], gw["flow"]).cpu())
+    a = rsgrad.warp_bwd(hw["x"], hw["flow"], hw["dy"])
+    rdx, rdf = oracle.warp_bwd(*(w[k].double().numpy() for k in ("x", "flow", "dy")))
+    assert_close(_np(a[0]), rdx, "grad", "host dx")
+    assert_close(_np(a[1]), rdf, "grad", "host dflow")
+    bs = synth.bslice_inputs(N, 64, 48, 8, 4, 3, cfg=1)
+    hb = {k: v.pin_memory() for k, v in bs.items()}
+    gb = _cuda(bs, cuda_device)
+    a = rsgrad.bslice_bwd(hb["grid"], hb["guide"], hb["x"], hb["dy"], deterministic=True)
+    b = rsgrad.bslice_bwd(gb["grid"], gb["guide"], gb["x"], gb["dy"], deterministic=True)
+    assert all(torch.equal(p, q.cpu()) for p, q in zip(a, b))
