@@ -15,11 +15,15 @@
  * Conventions shared by every entry point
  *   Tensors   fp32, C-contiguous (NCHW), no aliasing between inputs and outputs.
  *   Pointers  device pointers (cudaMalloc / torch CUDA tensors) OR host pointers
- *             (pinned or pageable).  Any host pointer is staged through a
- *             stream-ordered temporary (cudaMallocAsync) and copied on `stream`;
- *             host outputs are copied back on `stream` before the call returns
- *             control of the stream (pinned: asynchronous; pageable: the call
- *             synchronises on the copy).  All device work runs on `stream`.
+ *             (pinned or pageable).  All-device calls run entirely on `stream`.
+ *             If any pointer is host memory the batch is processed in sample
+ *             chunks on two library-internal streams that are ordered after
+ *             `stream` (event wait) and before its later work (event wait back):
+ *             per chunk, host inputs are copied H2D into stream-ordered
+ *             temporaries (cudaMallocAsync), the kernels run, host outputs are
+ *             copied D2H, so copies and kernels of different chunks overlap.
+ *             Host outputs are valid once `stream` has been synchronised (pinned
+ *             memory: fully asynchronous; pageable: copies may block the caller).
  *   Outputs   always OVERWRITTEN, never accumulated.  A NULL gradient pointer
  *             skips that gradient's work.
  *   Ownership the caller owns every buffer.  The library keeps no state except
