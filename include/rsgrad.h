@@ -28,7 +28,7 @@
  *             skips that gradient's work.
  *   Ownership the caller owns every buffer.  The library keeps no state except
  *             the thread-local error string; it allocates only stream-ordered
- *             temporaries that are released on `stream` before returning.
+ *             temporaries (workspace, host staging) released in stream order.
  *   Workspace *_bwd take an optional device workspace (size from
  *             rsgrad_bwd_workspace_bytes); NULL/too small => the library takes
  *             a stream-ordered temporary of that size itself.
@@ -65,12 +65,19 @@ typedef enum {
 
 typedef enum { RS_PAD_ZEROS = 0, RS_PAD_BORDER = 1 } rs_padding;
 
-/* Backward algorithm for the input adjoint:
- *   GATHER          scatter-to-gather conversion over the bounded footprint
- *                   (deterministic, no memset, no atomics);
- *   SCATTER_PRIV    shared-memory privatised scatter, one flush per tile;
- *   SCATTER_ATOMIC  "general scatter using atomics";
- *   AUTO            per layer / per sample choice, DESIGN.md "Algorithm choice". */
+/* Backward algorithm for the scattered adjoint (convert scatters
+ * to gathers where a bounded inverse exists, else "a general scattering operation"
+ * with atomics).  What each layer accepts:
+ *   stn_bwd  d_input  AUTO, GATHER: cell-owner gather over the affine preimage
+ *                     (zeros padding; per-sample fallback to atomics for singular
+ *                     theta); SCATTER_ATOMIC; SCATTER_PRIV -> RS_ERR_FLAG.
+ *                     Border padding always scatters (no bounded inverse).
+ *   warp_bwd d_input  AUTO, SCATTER_ATOMIC (no bounded inverse); GATHER and
+ *                     SCATTER_PRIV -> RS_ERR_FLAG.
+ *   bslice_bwd d_grid AUTO, GATHER, SCATTER_PRIV: dual-cell register-privatised
+ *                     accumulation + fixed-order partial gather (deterministic;
+ *                     cells >= 8 px); SCATTER_ATOMIC: global atomics.
+ * d_theta, d_flow, d_guide and bslice d_input are always gathers. */
 typedef enum {
     RS_ALGO_AUTO = 0,
     RS_ALGO_GATHER = 1,
