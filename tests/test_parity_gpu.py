@@ -362,3 +362,55 @@ def test_host_pointer_chunked_all_layers(cuda_device):
     a = rsgrad.bslice_bwd(hb["grid"], hb["guide"], hb["x"], hb["dy"], deterministic=True)
     b = rsgrad.bslice_bwd(gb["grid"], gb["guide"], gb["x"], gb["dy"], deterministic=True)
     assert all(torch.equal(p, q.cpu()) for p, q in zip(a, b))
+
+
+@pytest.mark.parametrize("C", [1, 7, 33])
+def test_stn_channel_chunking(cuda_device, C):
+    """C not a multiple of any channel-chunk size (ragged last chunk), C = 1."""
+    inp = synth.stn_inputs(2, C, 45, 70, 52, 61, cfg=1)
+    g = _cuda(inp, cuda_device)
+    y = rsgrad.stn_fwd(g["x"], g["theta"], 52, 61)
+    dx, dth = rsgrad.stn_bwd(g["x"], g["theta"], g["dy"])
+    x, th, dy = (inp[k].double().numpy() for k in ("x", "theta", "dy"))
+    assert_close(_np(y), oracle.stn_fwd(x, th, 52, 61), "fwd", "y")
+    rdx, rdth = oracle.stn_bwd(x, th, dy)
+    assert_close(_np(dx), rdx, "grad", "dx")
+    assert_close(_np(dth), rdth, "grad", "dtheta")
+
+
+def test_null_gradient_outputs(cuda_device):
+    """A NULL gradient pointer skips that gradient; the others are unchanged."""
+    s = _cuda(synth.stn_inputs(2, 4, 32, 40, cfg=1), cuda_device)
+    full = rsgrad.stn_bwd(s["x"], s["theta"], s["dy"])
+    only_dx = rsgrad.stn_bwd(s["x"], s["theta"], s["dy"], need_dtheta=False)
+    only_dth = rsgrad.stn_bwd(s["x"], s["theta"], s["dy"], need_dx=False)
+    assert only_dx[1] is None and only_dth[0] is None
+    assert torch.equal(only_dx[0], full[0]) and torch.equal(only_dth[1], full[1])
+    w = _cuda(synth.warp_inputs(1, 3, 30, 34, cfg=1), cuda_device)
+    fw = rsgrad.warp_bwd(w["x"], w["flow"], w["dy"])
+    df = rsgrad.warp_bwd(w["x"], w["flow"], w["dy"], need_dx=False)[1]
+    assert torch.equal(df, fw[1])
+    b = _cuda(synth.bslice_inputs(1, 64, 64, 8, 4, 4, cfg=1), cuda_device)
+    fb = rsgrad.bslice_bwd(b["grid"], b["guide"], b["x"], b["dy"])
+    for mask in [(True, False, False), (False, True, False), (False, False, True)]:
+        part = rsgrad.bslice_bwd(b["grid"], b["guide"], b["x"], b["dy"], need_dgrid=mask[0],
+                                 need_dguide=mask[1], need_dx=mask[2])
+        for want, got, ref in zip(mask, part, fb):
+            if want:
+                assert_close(_np(got), _np(ref), "grad", "partial bslice output")
+            else:
+                assert got is None
+
+
+def test_bslice_many_planes_and_coarse_grid(cuda_device):
+    """D = 16 planes, a 2x3 grid on 200x300 pixels (dual cells split into sub-tiles)."""
+    inp = synth.bslice_inputs(1, 200, 300, 16, 2, 3, cfg=1, grid="iid", guide="wide")
+    g = _cuda(inp, cuda_device)
+    y = rsgrad.bslice_fwd(g["grid"], g["guide"], g["x"])
+    dgr, dgd, dx = rsgrad.bslice_bwd(g["grid"], g["guide"], g["x"], g["dy"])
+    gr, gd, x, dy = (inp[k].double().numpy() for k in ("grid", "guide", "x", "dy"))
+    assert_close(_np(y), oracle.bslice_fwd(gr, gd, x), "fwd", "y")
+    rgr, rgd, rdx = oracle.bslice_bwd(gr, gd, x, dy)
+    assert_close(_np(dgr), rgr, "grad", "dgrid")
+    assert_close(_np(dgd), rgd, "grad", "dguide")
+    assert_close(_np(dx), rdx, "grad", "dx")
