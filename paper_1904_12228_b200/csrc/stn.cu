@@ -128,7 +128,52 @@ RS_DEV bool stn_gatherable(const Affine &A, int Ho, int Wo) {
 // ----------------------------------------------------------------- output-tile kernel
 // MODE_FWD: y.  MODE_DTHETA: per-tile fp64 partials of d_theta (6 per tile).
 // fb_list (optional): loop over the listed samples instead of blockIdx.y.
-template <int MODE, bool VEC, bool FLOW = false, int kFI = (MODE == 0 ? kFIfwd : kFIdth)>
+// FAST (x rows 16-B aligned, affine, no fb_list): TMA bulk row copies completing on
+// mbarriers, a compile-time channel-slice stride (immediate smem offsets) with a zero
+// slot per slice so every tap is an unpredicated shared load, and for d_theta four
+// per-tap accumulators sum_c dY*V (4 FMAs per channel) combined once at the end.
+#ifndef RS_NS
+#define RS_NS 3
+#endif
+#ifndef RS_FST
+#define RS_FST 5120
+#endif
+#ifndef RS_FIDF
+#define RS_FIDF 32
+#endif
+constexpr int kNS = RS_NS;     // FAST: stages in the ring
+constexpr int kFSt = RS_FST;   // FAST: floats per stage
+constexpr int kFIdf = RS_FIDF; // FAST: d_theta tile rows
+static_assert(kFIdf >= 16, "d_theta partials are sized for >= 16-row tiles");
+template <int MODE>
+struct FastSlices;
+template <>
+struct FastSlices<0> {  // forward: no dY in the stage
+    static constexpr int n = 6;  // channels per stage: 8, 5, 4, 3, 2, 1
+    __host__ __device__ static constexpr int cls(int nc) { return (kFSt / nc) & ~3; }
+    __host__ __device__ static constexpr int at(int i) {
+        return cls(i == 0 ? 8 : 6 - i);
+    }
+};
+template <>
+struct FastSlices<1> {  // d_theta: + kFIdf x kFJ dY floats per channel; 5..1 channels per stage
+    static constexpr int n = 5;
+    __host__ __device__ static constexpr int cls(int nc) { return (kFSt / nc - kFIdf * kFJ) & ~3; }
+    __host__ __device__ static constexpr int at(int i) { return cls(5 - i); }
+};
+
+// smallest slice stride >= need (the caller guarantees need <= the largest)
+template <int I, class FS, class Fn>
+RS_DEV void dispatch_slice(int need, Fn &&fn) {
+    if constexpr (I == FS::n - 1) {
+        fn(std::integral_constant<int, FS::at(I)>{});
+    } else {
+        if (need <= FS::at(I)) fn(std::integral_constant<int, FS::at(I)>{});
+        else dispatch_slice<I + 1, FS>(need, fn);
+    }
+}
+
+template <int MODE, bool VEC, bool FLOW = false, int kFI = (MODE == 0 ? kFIfwd : kFIdth), bool FAST = false>
 __global__ void __launch_bounds__(kThreads, 3)
     stn_out_tile(StnArgs a, const double *__restrict__ xtab, const double *__restrict__ ytab,
                  const int *__restrict__ fb_list, const int *__restrict__ fb_count,
@@ -145,7 +190,17 @@ __global__ void __launch_bounds__(kThreads, 3)
     __shared__ float red[kThreads / 32][6];
 
     __shared__ double ntab[kFJ + kFI];  // normalised coordinates of the tile's columns / rows
+    // FAST (single tile per block, fb_list == nullptr): full[s] = TMA bytes landed,
+    // empty[s] = all 8 warps done reading stage s
+    __shared__ unsigned long long full[kNS], empty[kNS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (FAST && threadIdx.x == 0) {
+        for (int b = 0; b < kNS; b++) {
+            mbar_init(&full[b], kThreads);
+            mbar_init(&empty[b], kThreads / 32);
+        }
+        fence_mbar_init();
+    }
     const int tj = blockIdx.x % tiles_j, ti = blockIdx.x / tiles_j;
     const long long HW = (long long)a.H * a.W, P = (long long)a.Ho * a.Wo;
     if (!FLOW && threadIdx.x < kFJ + kFI) {
@@ -235,8 +290,13 @@ __global__ void __launch_bounds__(kThreads, 3)
         __syncthreads();
         if (!fallback) build_rows<VEC>(R, a.W, rlo, rhi, rxa, roff, rcnt, &ctl[2]);
         __syncthreads();
+        if (FAST && !fallback) sum_rows(R, rcnt, &ctl[3]);
         const int F = fallback ? 0 : ctl[2];
-        fallback = fallback || F + ((MODE != MODE_FWD) ? kFI * kFJ : 0) > kFStage;
+        if (FAST) {
+            fallback = fallback || F + 4 > FastSlices<MODE == MODE_FWD ? 0 : 1>::at(FastSlices<MODE == MODE_FWD ? 0 : 1>::n - 1);
+        } else {
+            fallback = fallback || F + ((MODE != MODE_FWD) ? kFI * kFJ : 0) > kFStage;
+        }
 
         float dix[kFP], diy[kFP];
 #pragma unroll
@@ -272,6 +332,117 @@ __global__ void __launch_bounds__(kThreads, 3)
                             if (yv1[k] && xv1[k]) red_add(q + a.W + 1, w11 * g);
                         }
                     }
+                }
+            }
+        } else if constexpr (FAST) {
+            __syncthreads();  // ctl[3] (sum_rows) visible
+            const int Fc = ctl[3];  // floats copied per channel
+            // tap offsets into a channel slice; a tap outside the image reads the zero slot F
+            int t00[kFP], t01[kFP], t10[kFP], t11[kFP];
+#pragma unroll
+            for (int k = 0; k < kFP; k++) {
+                const int s0 = (in[k] && yv0[k]) ? roff[y0[k] - ylo] + (x0[k] - rxa[y0[k] - ylo]) : 0;
+                const int s1 = (in[k] && yv1[k]) ? roff[y0[k] + 1 - ylo] + (x0[k] - rxa[y0[k] + 1 - ylo]) : 0;
+                t00[k] = (in[k] && yv0[k] && xv0[k]) ? s0 : F;
+                t01[k] = (in[k] && yv0[k] && xv1[k]) ? s0 + 1 : F;
+                t10[k] = (in[k] && yv1[k] && xv0[k]) ? s1 : F;
+                t11[k] = (in[k] && yv1[k] && xv1[k]) ? s1 + 1 : F;
+            }
+            constexpr int GT = (MODE != MODE_FWD) ? kFI * kFJ : 0;
+            const int jb = tj * kFJ;
+            const int vrows = min(kFI, a.Ho - ti * kFI), vcols = min(kFJ, a.Wo - jb);
+            const int Gc = (MODE != MODE_FWD) ? vrows * vcols : 0;  // dY floats copied per channel
+            float acc[kFP][4];
+#pragma unroll
+            for (int k = 0; k < kFP; k++) acc[k][0] = acc[k][1] = acc[k][2] = acc[k][3] = 0.f;
+            auto run = [&](auto ksc) {
+                constexpr int kS = decltype(ksc)::value;  // channel slice stride (floats) >= F + 4
+                constexpr int NC0 = kFSt / (kS + GT);
+                constexpr int NC = NC0 < 8 ? NC0 : 8;
+                const int nch = (a.C + NC - 1) / NC;
+                for (int e = threadIdx.x; e < kNS * NC * 4; e += kThreads)
+                    stage[(e / (4 * NC)) * kFSt + ((e >> 2) % NC) * kS + F + (e & 3)] = 0.f;
+                __syncthreads();
+                // every thread issues its share of chunk kc's 16-B cp.async copies and arrives
+                // on full[slot] when they have landed (TMA bulk copies are request-rate bound
+                // at these 60-130 B row segments: measured 2.7 TB/s at 64 B, scripts/micro)
+                auto issue = [&](int kc) {
+                    const int slot = kc % kNS, c0s = kc * NC, ncp = min(NC, a.C - c0s);
+                    float *dst = stage + slot * kFSt;
+                    const float *xs = xbase + (long long)c0s * HW;
+                    // X: four lanes per footprint row, channels innermost
+                    for (int r = threadIdx.x >> 2; r < R; r += kThreads / 4) {
+                        const int w = rcnt[r];
+                        const float *src = xs + (long long)(ylo + r) * a.W + rxa[r];
+                        float *d = dst + roff[r];
+                        for (int c = 0; c < ncp; c++) {
+                            for (int q = (threadIdx.x & 3) * 4; q < w; q += 16) cp_async16(d + q, src + q);
+                            src += HW;
+                            d += kS;
+                        }
+                    }
+                    if (MODE != MODE_FWD) {  // dY tile: eight lanes per row
+                        const int per = vrows * 8;
+                        for (int e = threadIdx.x; e < ncp * per; e += kThreads) {
+                            const int c = e / per, rem = e - c * per, r = rem >> 3, q = (rem & 7) * 4;
+                            if (q < vcols)
+                                cp_async16(dst + NC * kS + c * GT + r * kFJ + q,
+                                           a.dy + ((long long)n * a.C + c0s + c) * P +
+                                               (long long)(ti * kFI + r) * a.Wo + jb + q);
+                        }
+                    }
+                    cp_async_arrive(&full[slot]);
+                };
+                for (int kc = 0; kc < kNS - 1 && kc < nch; kc++) issue(kc);
+                for (int kc = 0; kc < nch; kc++) {
+                    const int c0 = kc * NC, kn = kc + kNS - 1;
+                    if (kn < nch) {
+                        // slot kn % kNS last held chunk kn - kNS: wait until every warp released it
+                        if (kn >= kNS) mbar_wait(&empty[kn % kNS], (unsigned)((kn / kNS - 1) & 1));
+                        issue(kn);
+                    }
+                    mbar_wait(&full[kc % kNS], (unsigned)((kc / kNS) & 1));
+                    const float *S = stage + (kc % kNS) * kFSt;
+                    const bool fullc = c0 + NC <= a.C;
+#pragma unroll
+                    for (int k = 0; k < kFP; k++) {
+                        const float *p00 = S + t00[k], *p01 = S + t01[k], *p10 = S + t10[k], *p11 = S + t11[k];
+                        if (MODE == MODE_FWD) {
+                            if (!in[k]) continue;
+                            const float w00 = (1.f - fy[k]) * (1.f - fx[k]), w01 = (1.f - fy[k]) * fx[k];
+                            const float w10 = fy[k] * (1.f - fx[k]), w11 = fy[k] * fx[k];
+                            const int i = ti * kFI + warp + 8 * k, j = jb + lane;
+                            float *yp = a.y + ((long long)n * a.C + c0) * P + (long long)i * a.Wo + j;
+#pragma unroll
+                            for (int c = 0; c < NC; c++) {
+                                if (!fullc && c0 + c >= a.C) break;
+                                const float v = fmaf(w00, p00[c * kS], fmaf(w01, p01[c * kS],
+                                                     fmaf(w10, p10[c * kS], w11 * p11[c * kS])));
+                                yp[(long long)c * P] = v;
+                            }
+                        } else {
+                            const float *gp = S + NC * kS + (warp + 8 * k) * kFJ + lane;
+#pragma unroll
+                            for (int c = 0; c < NC; c++) {
+                                if (!fullc && c0 + c >= a.C) break;
+                                const float g = gp[c * GT];
+                                acc[k][0] = fmaf(g, p00[c * kS], acc[k][0]);
+                                acc[k][1] = fmaf(g, p01[c * kS], acc[k][1]);
+                                acc[k][2] = fmaf(g, p10[c * kS], acc[k][2]);
+                                acc[k][3] = fmaf(g, p11[c * kS], acc[k][3]);
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[kc % kNS]);
+                }
+            };
+            dispatch_slice<0, FastSlices<MODE == MODE_FWD ? 0 : 1>>(F + 4, run);
+            if (MODE != MODE_FWD) {
+#pragma unroll
+                for (int k = 0; k < kFP; k++) {  // d_ix = sum_c dY dV/dx, d_iy likewise (R1)
+                    dix[k] = fmaf(1.f - fy[k], acc[k][1] - acc[k][0], fy[k] * (acc[k][3] - acc[k][2]));
+                    diy[k] = fmaf(1.f - fx[k], acc[k][2] - acc[k][0], fx[k] * (acc[k][3] - acc[k][1]));
                 }
             }
         } else {
@@ -1451,7 +1622,16 @@ StnWs stn_ws_layout(void *base, int N, int H, int W, int Ho, int Wo) {
     return w;
 }
 
-size_t out_tile_smem() { return sizeof(int) * (5 * kFRMax + 16) + sizeof(float) * 2 * kFStage; }
+// RSGRAD_STN_TILES=slow selects the cp.async output-tile path (A/B comparisons)
+bool stn_slow_tiles() {
+    const char *e = getenv("RSGRAD_STN_TILES");
+    return e && strcmp(e, "slow") == 0;
+}
+
+size_t out_tile_smem() {
+    const int st = 2 * kFStage > kNS * kFSt ? 2 * kFStage : kNS * kFSt;
+    return sizeof(int) * (5 * kFRMax + 16) + sizeof(float) * st;
+}
 size_t bwd_lean_smem() {
     return sizeof(float) * 2 * kLStage + sizeof(uint2) * kLFQMax + sizeof(int4) * kLRQMax +
            sizeof(int) * (5 * kLRQMax + 8) + sizeof(unsigned short) * 8 * (kLRows + 1) * kLHits * 32 +
@@ -1488,7 +1668,11 @@ cudaError_t stn_fwd_launch(const StnArgs &a, cudaStream_t s) {
     const bool vec = (a.W % 4 == 0) && aligned16(a.x);
     const size_t sm = out_tile_smem();
     dim3 grid(g.fj * g.fi_fwd, a.N);
-    if (vec) {
+    if (vec && !stn_slow_tiles()) {
+        auto k = stn_out_tile<MODE_FWD, true, false, kFIfwd, true>;
+        set_smem(k, sm);
+        k<<<grid, kThreads, sm, s>>>(a, nullptr, nullptr, nullptr, nullptr, nullptr, g.fj, g.fi_fwd);
+    } else if (vec) {
         set_smem(stn_out_tile<MODE_FWD, true>, sm);
         stn_out_tile<MODE_FWD, true><<<grid, kThreads, sm, s>>>(a, nullptr, nullptr, nullptr, nullptr,
                                                                 nullptr, g.fj, g.fi_fwd);
@@ -1597,11 +1781,18 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
     // fallback samples (all samples when !allow_gather or the lean dX kernel):
     // d_theta from output tiles ...
     const bool dth_all = allow_gather && variant == 2;
+    const bool dth_fast = vin && vout && dth_all && !stn_slow_tiles();
+    const int fi_df = (a.Ho + kFIdf - 1) / kFIdf;  // d_theta tiles per column, fast path
     if (a.dtheta) {
         const size_t sm = out_tile_smem();
         dim3 grid(g.fj * g.fi, dth_all ? a.N : 1);
         const int *fbl = dth_all ? nullptr : w.fb_list;
-        if (vin) {
+        if (dth_fast) {
+            auto k = stn_out_tile<MODE_DTHETA, true, false, kFIdf, true>;
+            set_smem(k, sm);
+            grid.x = g.fj * fi_df;
+            k<<<grid, kThreads, sm, s>>>(a, w.xtab, w.ytab, nullptr, w.fb_count, w.pf, g.fj, fi_df);
+        } else if (vin) {
             set_smem(stn_out_tile<MODE_DTHETA, true>, sm);
             stn_out_tile<MODE_DTHETA, true><<<grid, kThreads, sm, s>>>(a, w.xtab, w.ytab, fbl, w.fb_count,
                                                                        w.pf, g.fj, g.fi);
@@ -1621,7 +1812,7 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
         note_launch();
     }
     if (a.dtheta) {
-        stn_dtheta_finalize<<<a.N, kThreads, 0, s>>>(w.pb, tiles_b, w.pf, g.fj * g.fi,
+        stn_dtheta_finalize<<<a.N, kThreads, 0, s>>>(w.pb, tiles_b, w.pf, g.fj * (dth_fast ? fi_df : g.fi),
                                                       dth_all ? nullptr : w.flags, a.dtheta);
         note_launch();
     }
