@@ -224,9 +224,10 @@ RS_DEV void rs_stage(float *v, int lane, int m) {
     }
 }
 
-// Lane pairs: lane 2s+e owns pixel slot s of the chunk and z-plane e (0: clamp(bin-1),
-// 1: clamp(bin)).  acc index: (b*2 + a)*12 + q, (b, a) = spatial corner.
-// Reduce-scatter across the 16 lanes of the same plane (xor 16, 8, 4, 2: 45
+// Lane pairs: lane 2s+e owns pixel slot s of the chunk and coefficient half e
+// (q = 6e .. 6e+5) of BOTH z-planes.  acc index: (p*4 + corner)*6 + qq, p = plane
+// (0: clamp(bin-1), 1: clamp(bin)), corner = b*2 + a (spatial), q = 6e + qq.
+// Reduce-scatter across the 16 lanes of the same half (xor 16, 8, 4, 2: 45
 // shuffles); lane then owns 3 sums, base = 24 b4 + 12 b3 + 6 b2 + 3 b1.
 // wacc (warp slot): [corner(4)][z(D)][q(12)]
 RS_DEV void flush_acc(float *acc, float *wacc, int bin, int D, int lane) {
@@ -235,16 +236,16 @@ RS_DEV void flush_acc(float *acc, float *wacc, int bin, int D, int lane) {
     rs_stage<6>(acc, lane, 4);
     rs_stage<3>(acc, lane, 2);
     const int base = ((lane & 16) ? 24 : 0) + ((lane & 8) ? 12 : 0) + ((lane & 4) ? 6 : 0) + ((lane & 2) ? 3 : 0);
-    const int e = lane & 1;
-    const int z = e ? clampi(bin, 0, D - 1) : clampi(bin - 1, 0, D - 1);
+    const int e = lane & 1, p = (lane >> 4) & 1;
+    const int z = p ? clampi(bin, 0, D - 1) : clampi(bin - 1, 0, D - 1);
     // plane-0 lanes first, then plane-1: the two planes coincide when clamped
 #pragma unroll
     for (int ph = 0; ph < 2; ph++) {
-        if (e == ph) {
+        if (p == ph) {
 #pragma unroll
             for (int t = 0; t < 3; t++) {
-                const int idx = base + t;
-                const int q = idx % 12, corner = idx / 12;
+                const int idx = (base + t) % 24;  // (corner, qq) within the plane
+                const int corner = idx / 6, q = 6 * e + idx % 6;
                 wacc[(corner * D + z) * 12 + q] += acc[t];
             }
         }
@@ -414,33 +415,52 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
             for (int i = 0; i < 3; i++) { X[i] = 0.f; G[i] = 0.f; }
         }
-        const float4 *Lc = glo + bin * kPlaneStride, *Dc = gdz + bin * kPlaneStride;
-        const float wz = e_pl ? fz : 1.f - fz;
-        const float wzy0 = wz * (1.f - fy), wzy1 = wz * fy;
-        float wt[4];
-        wt[0] = wzy0 * (1.f - fx); wt[1] = wzy0 * fx;
-        wt[2] = wzy1 * (1.f - fx); wt[3] = wzy1 * fx;
-        float dx[3] = {0.f, 0.f, 0.f}, dgd = 0.f;
+        // this lane's coefficient half: q = 6 e + qq, (oc, i) = (q / 4, q % 4)
+        const float4 *Lc = glo + bin * kPlaneStride + 6 * e_pl, *Dc = gdz + bin * kPlaneStride + 6 * e_pl;
+        const bool e1 = e_pl != 0;
+        const float Gq[6] = {e1 ? G[1] : G[0], e1 ? G[1] : G[0], e1 ? G[2] : G[0],
+                             e1 ? G[2] : G[0], e1 ? G[2] : G[1], e1 ? G[2] : G[1]};
+        const float Xq[6] = {e1 ? X[2] : X[0], e1 ? 1.f : X[1], e1 ? X[0] : X[2],
+                             e1 ? X[1] : 1.f, e1 ? X[2] : X[0], e1 ? 1.f : X[1]};
+        float wt[8];  // (plane, corner) trilinear weights
+        {
+            const float wy[2] = {1.f - fy, fy}, wx[2] = {1.f - fx, fx}, wz[2] = {1.f - fz, fz};
 #pragma unroll
-        for (int oc = 0; oc < 3; oc++) {
+            for (int pl = 0; pl < 2; pl++)
 #pragma unroll
-            for (int i = 0; i < 4; i++) {
-                const int q = 4 * oc + i;
-                const float lo = lerp2(Lc[q], fx, fy);
-                const float d = lerp2(Dc[q], fx, fy);
-                const float P = (i < 3) ? G[oc] * X[i] : G[oc];
-                if (i < 3) dx[i] = fmaf(G[oc], fmaf(fz, d, lo), dx[i]);
-                dgd = fmaf(P, d, dgd);
-#pragma unroll
-                for (int tt = 0; tt < 4; tt++) acc[tt * 12 + q] = fmaf(wt[tt], P, acc[tt * 12 + q]);
-            }
+                for (int bb = 0; bb < 2; bb++) {
+                    const float wzy = wz[pl] * wy[bb];
+                    wt[pl * 4 + bb * 2] = wzy * wx[0];
+                    wt[pl * 4 + bb * 2 + 1] = wzy * wx[1];
+                }
         }
-        if (valid && e_pl == 0) {
-            if (dxp) {
+        float u[4] = {0.f, 0.f, 0.f, 0.f}, dgd = 0.f;
 #pragma unroll
-                for (int i = 0; i < 3; i++) dxp[i * HW + o] = dx[i];
+        for (int qq = 0; qq < 6; qq++) {
+            const float lo = lerp2(Lc[qq], fx, fy);
+            const float d = lerp2(Dc[qq], fx, fy);
+            const float P = Gq[qq] * Xq[qq];
+            u[qq & 3] = fmaf(Gq[qq], fmaf(fz, d, lo), u[qq & 3]);  // A_q G_oc (i = 3 slots unused)
+            dgd = fmaf(P, d, dgd);
+#pragma unroll
+            for (int tt = 0; tt < 8; tt++) acc[tt * 6 + qq] = fmaf(wt[tt], P, acc[tt * 6 + qq]);
+        }
+        // dX_i = sum_oc A_{4oc+i} G_oc: this half's slots, then the partner's half
+        float dx0 = e1 ? u[2] : u[0], dx1 = e1 ? u[3] : u[1], dx2 = e1 ? u[0] : u[2];
+        dx0 += __shfl_xor_sync(0xffffffffu, dx0, 1);
+        dx1 += __shfl_xor_sync(0xffffffffu, dx1, 1);
+        dx2 += __shfl_xor_sync(0xffffffffu, dx2, 1);
+        dgd += __shfl_xor_sync(0xffffffffu, dgd, 1);
+        if (valid) {
+            if (e_pl == 0) {
+                if (dxp) {
+                    dxp[o] = dx0;
+                    dxp[HW + o] = dx1;
+                }
+            } else {
+                if (dxp) dxp[2 * HW + o] = dx2;
+                if (dgp) dgp[o] = (float)D * dgd;
             }
-            if (dgp) dgp[o] = (float)D * dgd;
         }
     }
     if (cbeg < cend) flush_acc(acc, mywacc, cur_bin, D, lane);

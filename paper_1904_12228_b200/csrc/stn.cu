@@ -934,6 +934,11 @@ RS_DEV bool stn_lean_ok(const Affine &A, int Ho, int Wo) {
     return rq <= kLRQMax && fq <= kLFQMax && (wj + 2.0) * (wi + 2.0) <= 16.0;
 }
 
+#ifndef RS_LEAN_CPA
+#define RS_LEAN_CPA 1
+#endif
+constexpr bool kLeanCpa = RS_LEAN_CPA;  // dY rows by cp.async (else TMA bulk copies)
+
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads, 2)
     stn_bwd_lean(StnArgs a, const double *__restrict__ xtab, const double *__restrict__ ytab,
@@ -1004,8 +1009,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         qhi[r] = min(a.Wo - 1, (int)floor(fmin(jh, 1e9)));
     }
     if (threadIdx.x == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+        mbar_init(&bars[0], kLeanCpa ? kThreads : 1);
+        mbar_init(&bars[1], kLeanCpa ? kThreads : 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -1039,7 +1044,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int Fc = ctl[1];  // floats copied per channel
     // VEC: one TMA bulk copy per (channel, row) segment; else 4-B LDGSTS
     auto issue = [&](float *dst, int c0s, int ncp, int slot) {
-        if (VEC) {
+        if (VEC && kLeanCpa) {  // 16-B cp.async, completion tracked on the stage's mbarrier
+            if (FQ > 0) stage_rows<true>(dst, FQ, gbase + (long long)c0s * P, P, ncp, RQ, a.Wo, ilo, qxa, qoff, qcnt);
+            cp_async_arrive(&bars[slot]);
+        } else if (VEC) {
             if (threadIdx.x == 0) mbar_expect_tx(&bars[slot], (unsigned)(ncp * Fc) * 4u);
             if (FQ > 0) stage_rows_bulk(dst, FQ, gbase + (long long)c0s * P, P, ncp, RQ, a.Wo, ilo, qxa, qoff, qcnt,
                                         &bars[slot]);
