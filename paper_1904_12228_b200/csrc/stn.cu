@@ -923,7 +923,17 @@ __global__ void __launch_bounds__(kThreads, RS_CELL_MINB)
 // share one walk, so the per-(cell row, chunk) overhead is paid C/kLCH times.
 constexpr int kLRows = 4;                 // px rows per warp
 constexpr int kLTY = kLRows * 8;          // 32 px rows per block
-constexpr int kLRQMax = 160, kLFQMax = 2304, kLStage = 8192, kLCH = 8, kLHits = 6;
+#ifndef RS_LSTAGE
+#define RS_LSTAGE 16384
+#endif
+#ifndef RS_LCH
+#define RS_LCH 8
+#endif
+#ifndef RS_LBUFS
+#define RS_LBUFS 1
+#endif
+constexpr int kLBufs = RS_LBUFS;  // dY stage buffers (1: the other block on the SM overlaps)
+constexpr int kLRQMax = 160, kLFQMax = 2304, kLStage = RS_LSTAGE, kLCH = RS_LCH, kLHits = 6;
 
 RS_DEV bool stn_lean_ok(const Affine &A, int Ho, int Wo) {
     if (!A.inv || Ho > 65535 || Wo > 65535) return false;
@@ -944,8 +954,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     stn_bwd_lean(StnArgs a, const double *__restrict__ xtab, const double *__restrict__ ytab,
                  const int *__restrict__ flags, int tiles_x, int tiles_y) {
     extern __shared__ __align__(16) float4 sm4[];
-    float *stage = (float *)sm4;                               // 2 * kLStage
-    uint2 *rec = (uint2 *)(stage + 2 * kLStage);               // kLFQMax
+    float *stage = (float *)sm4;                               // kLBufs * kLStage
+    uint2 *rec = (uint2 *)(stage + kLBufs * kLStage);          // kLFQMax
     int4 *rowt = (int4 *)(rec + kLFQMax);                      // kLRQMax
     int *qlo = (int *)(rowt + kLRQMax);
     int *qhi = qlo + kLRQMax;
@@ -1137,15 +1147,16 @@ __global__ void __launch_bounds__(kThreads, 2)
 
     for (int kc = 0; kc < nch; kc++) {
         const int c0 = kc * CH, cn = min(CH, a.C - c0);
-        if (kc + 1 < nch) issue(stage + ((kc + 1) & 1) * kLStage, c0 + CH, min(CH, a.C - c0 - CH), (kc + 1) & 1);
+        if (kLBufs == 2 && kc + 1 < nch)
+            issue(stage + ((kc + 1) % kLBufs) * kLStage, c0 + CH, min(CH, a.C - c0 - CH), (kc + 1) & 1);
         if (VEC) {
             mbar_wait(&bars[kc & 1], (unsigned)((kc >> 1) & 1));
         } else {
-            if (kc + 1 < nch) cp_async_wait<1>();
+            if (kLBufs == 2 && kc + 1 < nch) cp_async_wait<1>();
             else cp_async_wait<0>();
         }
-        __syncthreads();
-        const float *S = stage + (kc & 1) * kLStage;
+        if (!VEC || !kLeanCpa) __syncthreads();
+        const float *S = stage + (kc % kLBufs) * kLStage;
         switch (cn) {
             case 8: run_chunk(S, c0, std::integral_constant<int, 8>{}); break;
             case 7: run_chunk(S, c0, std::integral_constant<int, 7>{}); break;
@@ -1157,6 +1168,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             default: run_chunk(S, c0, std::integral_constant<int, 1>{}); break;
         }
         __syncthreads();
+        if (kLBufs == 1 && kc + 1 < nch) issue(stage, c0 + CH, min(CH, a.C - c0 - CH), (kc + 1) & 1);
     }
 }
 
@@ -1641,7 +1653,7 @@ size_t out_tile_smem() {
     return sizeof(int) * (5 * kFRMax + 16) + sizeof(float) * st;
 }
 size_t bwd_lean_smem() {
-    return sizeof(float) * 2 * kLStage + sizeof(uint2) * kLFQMax + sizeof(int4) * kLRQMax +
+    return sizeof(float) * kLBufs * kLStage + sizeof(uint2) * kLFQMax + sizeof(int4) * kLRQMax +
            sizeof(int) * (5 * kLRQMax + 8) + sizeof(unsigned short) * 8 * (kLRows + 1) * kLHits * 32 +
            8 * (kLRows + 1) * 32;
 }
