@@ -70,10 +70,15 @@ typedef enum { RS_PAD_ZEROS = 0, RS_PAD_BORDER = 1 } rs_padding;
  * with atomics).  What each layer accepts:
  *   stn_bwd  d_input  AUTO, GATHER: cell-owner gather over the affine preimage
  *                     (zeros padding; per-sample fallback to atomics for singular
- *                     theta); SCATTER_ATOMIC; SCATTER_PRIV -> RS_ERR_FLAG.
- *                     Border padding always scatters (no bounded inverse).
- *   warp_bwd d_input  AUTO, SCATTER_ATOMIC (no bounded inverse); GATHER and
- *                     SCATTER_PRIV -> RS_ERR_FLAG.
+ *                     theta); SCATTER_ATOMIC: per-tap global atomics;
+ *                     SCATTER_PRIV: per output tile, taps accumulate in a shared-
+ *                     memory copy of the tile's input footprint, flushed with one
+ *                     global atomic per touched element.  Border padding never
+ *                     gathers (no bounded inverse).
+ *   warp_bwd d_input  AUTO and SCATTER_ATOMIC: per-tap global atomics (adjacent
+ *                     lanes' shared taps merged first); SCATTER_PRIV as for STN;
+ *                     GATHER -> RS_ERR_FLAG (no bounded inverse).
+ *                     AUTO picks the measured-faster path.
  *   bslice_bwd d_grid AUTO, GATHER, SCATTER_PRIV: dual-cell register-privatised
  *                     accumulation + fixed-order partial gather (deterministic;
  *                     cells >= 8 px); SCATTER_ATOMIC: global atomics.

@@ -248,10 +248,8 @@ rs_status stn_bwd(const float *x, const float *theta, const float *dy, int N, in
         return fail(RS_ERR_FLAG, "stn_bwd: GATHER needs zeros padding (border clamp has no bounded inverse)");
     if (dx && border && o.deterministic)
         return fail(RS_ERR_FLAG, "stn_bwd: no deterministic d_input path with border padding");
-    if (dx && o.algo == RS_ALGO_SCATTER_PRIV)
-        return fail(RS_ERR_FLAG, "stn_bwd: SCATTER_PRIV not implemented for STN (use AUTO/GATHER/SCATTER_ATOMIC)");
-    if (dx && o.algo == RS_ALGO_SCATTER_ATOMIC && o.deterministic)
-        return fail(RS_ERR_FLAG, "stn_bwd: SCATTER_ATOMIC is not deterministic");
+    if (dx && (o.algo == RS_ALGO_SCATTER_ATOMIC || o.algo == RS_ALGO_SCATTER_PRIV) && o.deterministic)
+        return fail(RS_ERR_FLAG, "stn_bwd: scatter paths (atomics) are not deterministic");
     if (!dx && !dtheta) return ok();
     cudaStream_t s = (cudaStream_t)stream;
     std::vector<TArg> args = {{x, sizeof(float) * (size_t)C * H * W, true, false},
@@ -318,8 +316,6 @@ rs_status warp_bwd(const float *x, const float *flow, const float *dy, int N, in
     if (!dy) return fail(RS_ERR_NULL, "warp_bwd: dy is required");
     if (dx && o.algo == RS_ALGO_GATHER)
         return fail(RS_ERR_FLAG, "warp_bwd: GATHER invalid (arbitrary flow has no bounded inverse)");
-    if (dx && o.algo == RS_ALGO_SCATTER_PRIV)
-        return fail(RS_ERR_FLAG, "warp_bwd: SCATTER_PRIV not implemented yet (use AUTO/SCATTER_ATOMIC)");
     if (dx && o.deterministic)
         return fail(RS_ERR_FLAG, "warp_bwd: no deterministic d_input path (atomic scatter)");
     if (!dx && !dflow) return ok();

@@ -288,7 +288,7 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
 size_t stn_ws_bytes(int N, int C, int H, int W, int Ho, int Wo);
 
 // output-tile kernel driven by a flow field (warp.cu): mode 0 = y, 2 = d_flow (+ dx reds)
-cudaError_t flow_tile_launch(const StnArgs &a, int mode, cudaStream_t s);
+cudaError_t flow_tile_launch(const StnArgs &a, int mode, bool priv, cudaStream_t s);
 cudaError_t warp_fwd_launch(const WarpArgs &a, cudaStream_t s);
 cudaError_t warp_bwd_launch(const WarpArgs &a, int algo, int deterministic, void *ws,
                             size_t ws_bytes, cudaStream_t s);

@@ -173,7 +173,12 @@ RS_DEV void dispatch_slice(int need, Fn &&fn) {
     }
 }
 
-template <int MODE, bool VEC, bool FLOW = false, int kFI = (MODE == 0 ? kFIfwd : kFIdth), bool FAST = false>
+// PRIV (MODE_DTHETA / MODE_DFLOW): d_input by shared-memory privatised scatter: the
+// taps add into a footprint-shaped accumulator laid out like the staged X footprint
+// (same row table), flushed once per channel chunk with one red.global.add per
+// touched footprint element (PAPER.md:733's atomics, made block-local first).
+template <int MODE, bool VEC, bool FLOW = false, int kFI = (MODE == 0 ? kFIfwd : kFIdth), bool FAST = false,
+          bool PRIV = false>
 __global__ void __launch_bounds__(kThreads, 3)
     stn_out_tile(StnArgs a, const double *__restrict__ xtab, const double *__restrict__ ytab,
                  const int *__restrict__ fb_list, const int *__restrict__ fb_count,
@@ -324,7 +329,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                         const float g = ldg_stream(a.dy + oo);
                         dix[k] = fmaf(g, fmaf(1.f - fy[k], v01 - v00, fy[k] * (v11 - v10)), dix[k]);
                         diy[k] = fmaf(g, fmaf(1.f - fx[k], v10 - v00, fx[k] * (v11 - v01)), diy[k]);
-                        if (MODE == MODE_DFLOW && a.dx) {
+                        if ((MODE == MODE_DFLOW || PRIV) && a.dx) {
                             float *q = a.dx + ((long long)n * a.C + c) * HW + o00;
                             if (yv0[k] && xv0[k]) red_add(q, w00 * g);
                             if (yv0[k] && xv1[k]) red_add(q + 1, w01 * g);
@@ -480,6 +485,9 @@ __global__ void __launch_bounds__(kThreads, 3)
                     }
                 }
             };
+            float *pacc = stage + 2 * kFStage;  // PRIV: CH x F accumulator (CH * F <= kFStage)
+            if (PRIV && a.dx)
+                for (int e = threadIdx.x; e < CH * F; e += kThreads) pacc[e] = 0.f;
             if (F > 0) stage_rows<VEC>(stage, F, xbase, HW, min(CH, a.C), R, a.W, ylo, rxa, roff, rcnt);
             stage_g(stage + CH * F, 0, min(CH, a.C));
             cp_async_commit();
@@ -518,7 +526,13 @@ __global__ void __launch_bounds__(kThreads, 3)
                             const float g = S[CH * F + c * GT + (warp + 8 * k) * kFJ + lane];
                             dix[k] = fmaf(g, fmaf(1.f - fy[k], v01 - v00, fy[k] * (v11 - v10)), dix[k]);
                             diy[k] = fmaf(g, fmaf(1.f - fx[k], v10 - v00, fx[k] * (v11 - v01)), diy[k]);
-                            if (MODE == MODE_DFLOW && a.dx) {  // no bounded inverse: atomic scatter
+                            if (PRIV && a.dx) {  // block-private accumulator (shared atomics)
+                                float *pc = pacc + c * F;
+                                if (k00) atomicAdd(pc + s0[k], w00 * g);
+                                if (k01) atomicAdd(pc + s0[k] + 1, w01 * g);
+                                if (k10) atomicAdd(pc + s1[k], w10 * g);
+                                if (k11) atomicAdd(pc + s1[k] + 1, w11 * g);
+                            } else if (MODE == MODE_DFLOW && a.dx) {  // no bounded inverse: atomic scatter
                                 float *q = a.dx + ((long long)n * a.C + c0 + c) * HW +
                                            (long long)y0[k] * a.W + x0[k];
                                 if (k00) red_add(q, w00 * g);
@@ -530,6 +544,25 @@ __global__ void __launch_bounds__(kThreads, 3)
                     }
                 }
                 __syncthreads();
+                if (PRIV && a.dx) {
+                    // flush: one red per touched footprint element, then re-zero (8 lanes per row)
+                    float *dxc = a.dx + ((long long)n * a.C + c0) * HW;
+                    for (int r = (threadIdx.x >> 3); r < R; r += kThreads / 8) {
+                        const int wdt = rcnt[r];
+                        float *gr = dxc + (long long)(ylo + r) * a.W + rxa[r];
+                        for (int c = 0; c < cn; c++) {
+                            float *pr = pacc + c * F + roff[r];
+                            for (int q = threadIdx.x & 7; q < wdt; q += 8) {
+                                const float v = pr[q];
+                                if (v != 0.f) {
+                                    red_add(gr + (long long)c * HW + q, v);
+                                    pr[q] = 0.f;
+                                }
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
             }
         }
         if (MODE == MODE_DFLOW && a.dflow) {
@@ -1705,7 +1738,7 @@ cudaError_t stn_fwd_launch(const StnArgs &a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t flow_tile_launch(const StnArgs &a, int mode, cudaStream_t s) {
+cudaError_t flow_tile_launch(const StnArgs &a, int mode, bool priv, cudaStream_t s) {
     const StnGeom g = stn_geom(a.H, a.W, a.Ho, a.Wo);
     const bool vec = (a.W % 4 == 0) && aligned16(a.x);
     const size_t sm = out_tile_smem();
@@ -1720,6 +1753,17 @@ cudaError_t flow_tile_launch(const StnArgs &a, int mode, cudaStream_t s) {
             set_smem(stn_out_tile<MODE_FWD, false, true>, sm);
             stn_out_tile<MODE_FWD, false, true><<<grid, kThreads, sm, s>>>(a, nullptr, nullptr, nullptr, nullptr,
                                                                            nullptr, g.fj, g.fi_fwd);
+        }
+    } else if (priv) {
+        const size_t smp = sm + sizeof(float) * kFStage;
+        if (vec) {
+            auto k = stn_out_tile<MODE_DFLOW, true, true, kFIdth, false, true>;
+            set_smem(k, smp);
+            k<<<grid, kThreads, smp, s>>>(a, nullptr, nullptr, nullptr, nullptr, nullptr, g.fj, g.fi);
+        } else {
+            auto k = stn_out_tile<MODE_DFLOW, false, true, kFIdth, false, true>;
+            set_smem(k, smp);
+            k<<<grid, kThreads, smp, s>>>(a, nullptr, nullptr, nullptr, nullptr, nullptr, g.fj, g.fi);
         }
     } else {
         if (vec) {
@@ -1803,8 +1847,12 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
     const bool dth_all = allow_gather && variant == 2;
     const bool dth_fast = vin && vout && dth_all && !stn_slow_tiles();
     const int fi_df = (a.Ho + kFIdf - 1) / kFIdf;  // d_theta tiles per column, fast path
+    // fallback d_input: per-tap global atomics (AUTO, SCATTER_ATOMIC), or block-private
+    // footprint accumulation (SCATTER_PRIV; measured slower on sm_100, where shared-memory
+    // float atomics are CAS loops: 3.45 vs 3.10 ms at 16x16x1024^2)
+    const bool priv = a.dx && algo == 2;
+    const size_t sm = out_tile_smem(), smp = sm + sizeof(float) * kFStage;
     if (a.dtheta) {
-        const size_t sm = out_tile_smem();
         dim3 grid(g.fj * g.fi, dth_all ? a.N : 1);
         const int *fbl = dth_all ? nullptr : w.fb_list;
         if (dth_fast) {
@@ -1812,6 +1860,11 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
             set_smem(k, sm);
             grid.x = g.fj * fi_df;
             k<<<grid, kThreads, sm, s>>>(a, w.xtab, w.ytab, nullptr, w.fb_count, w.pf, g.fj, fi_df);
+        } else if (priv && !dth_all) {  // fallback samples: d_theta and privatised d_input
+            auto k = vin ? stn_out_tile<MODE_DTHETA, true, false, kFIdth, false, true>
+                         : stn_out_tile<MODE_DTHETA, false, false, kFIdth, false, true>;
+            set_smem(k, smp);
+            k<<<grid, kThreads, smp, s>>>(a, w.xtab, w.ytab, fbl, w.fb_count, w.pf, g.fj, g.fi);
         } else if (vin) {
             set_smem(stn_out_tile<MODE_DTHETA, true>, sm);
             stn_out_tile<MODE_DTHETA, true><<<grid, kThreads, sm, s>>>(a, w.xtab, w.ytab, fbl, w.fb_count,
@@ -1823,8 +1876,16 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
         }
         note_launch();
     }
-    // ... and d_input from the atomic scatter
-    if (a.dx) {
+    if (a.dx && priv && (dth_all || !a.dtheta)) {
+        // fallback samples' d_input alone: MODE_DFLOW with affine coordinates, no d_flow
+        StnArgs b = a;
+        b.dflow = nullptr;
+        auto k = vin ? stn_out_tile<MODE_DFLOW, true, false, kFIdth, false, true>
+                     : stn_out_tile<MODE_DFLOW, false, false, kFIdth, false, true>;
+        set_smem(k, smp);
+        k<<<dim3(g.fj * g.fi, 1), kThreads, smp, s>>>(b, w.xtab, w.ytab, w.fb_list, w.fb_count, nullptr, g.fj, g.fi);
+        note_launch();
+    } else if (a.dx && !priv) {
         const long long P = (long long)a.Ho * a.Wo;
         long long blocks = (P + kThreads - 1) / kThreads;
         if (blocks > 4 * kNumSMs * 8) blocks = 4 * kNumSMs * 8;

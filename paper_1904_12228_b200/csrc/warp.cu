@@ -175,7 +175,7 @@ static bool warp_direct() {
 }
 
 cudaError_t warp_fwd_launch(const WarpArgs &a, cudaStream_t s) {
-    if (!warp_direct()) return flow_tile_launch(as_tile_args(a), 0, s);
+    if (!warp_direct()) return flow_tile_launch(as_tile_args(a), 0, false, s);
     const int HW = a.H * a.W;
     warp_fwd_kernel<<<dim3((HW + kThreads - 1) / kThreads, a.N), kThreads, 0, s>>>(a, 1.0 / a.W);
     note_launch();
@@ -184,7 +184,6 @@ cudaError_t warp_fwd_launch(const WarpArgs &a, cudaStream_t s) {
 
 cudaError_t warp_bwd_launch(const WarpArgs &a, int algo, int deterministic, void *ws,
                             size_t ws_bytes, cudaStream_t s) {
-    (void)algo;
     (void)deterministic;
     (void)ws;
     (void)ws_bytes;
@@ -193,7 +192,9 @@ cudaError_t warp_bwd_launch(const WarpArgs &a, int algo, int deterministic, void
         cudaError_t e = cudaMemsetAsync(a.dx, 0, sizeof(float) * (size_t)a.N * a.C * HW, s);
         if (e != cudaSuccess) return e;
     }
-    if (!warp_direct()) return flow_tile_launch(as_tile_args(a), 2, s);
+    // SCATTER_PRIV: d_input through a block-private footprint accumulator (one red per
+    // touched input element per tile) instead of per-tap global reds
+    if (algo == 2 || !warp_direct()) return flow_tile_launch(as_tile_args(a), 2, algo == 2, s);
     warp_bwd_kernel<<<dim3((unsigned)((HW + kThreads - 1) / kThreads), a.N), kThreads, 0, s>>>(a, 1.0 / a.W);
     note_launch();
     return cudaGetLastError();

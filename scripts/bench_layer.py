@@ -27,3 +27,17 @@ for name, fn in calls:
     t = e0.elapsed_time(e1) / reps * 1e-3
     res[name] = {"ms": round(t * 1e3, 3), "frac": round(bench.CALL_BYTES[name] * P / t / 1e9 / peak, 3)}
     print(f"{name:12s} {t*1e3:8.3f} ms  roofline {res[name]['frac']:.3f}", flush=True)
+
+if os.environ.get("RS_BENCH_ALGOS"):
+    # d_input algorithm comparison per layer (AUTO vs SCATTER_PRIV vs SCATTER_ATOMIC)
+    for algo in ("auto", "scatter_priv", "scatter_atomic"):
+        for name, fn in [("stn_bwd", lambda: rs.stn_bwd(s["x"], s["theta"], s["dy"], algo=algo, out=(o["stn_dx"], o["stn_dth"]))),
+                         ("warp_bwd", lambda: rs.warp_bwd(w["x"], w["flow"], w["dy"], algo=algo, out=(o["warp_dx"], o["warp_df"])))]:
+            fn(); torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                fn()
+            e1.record(); torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) / reps * 1e-3
+            print(f"{name:10s} {algo:15s} {t*1e3:8.3f} ms  roofline {bench.CALL_BYTES[name] * P / t / 1e9 / peak:.3f}", flush=True)

@@ -54,13 +54,48 @@ def test_stn_parity(cuda_device, shape, ac, padding):
     assert_close(_np(dth), rdth, "grad", "dtheta")
 
 
-@pytest.mark.parametrize("algo", ["gather", "scatter_atomic"])
+@pytest.mark.parametrize("algo", ["gather", "scatter_priv", "scatter_atomic"])
 def test_stn_algos_agree_with_oracle(cuda_device, algo):
     inp = synth.stn_inputs(2, 8, 48, 40, cfg=1)
     g = _cuda(inp, cuda_device)
     dx, _ = rsgrad.stn_bwd(g["x"], g["theta"], g["dy"], algo=algo, need_dtheta=False)
-    rdx, _ = oracle.stn_bwd(*(inp[k].double().numpy() for k in ("x", "theta", "dy")))
+    rdx, rdth = oracle.stn_bwd(*(inp[k].double().numpy() for k in ("x", "theta", "dy")))
     assert_close(_np(dx), rdx, "grad", f"dx[{algo}]")
+    dx2, dth2 = rsgrad.stn_bwd(g["x"], g["theta"], g["dy"], algo=algo)
+    assert_close(_np(dx2), rdx, "grad", f"dx[{algo}] with dtheta")
+    assert_close(_np(dth2), rdth, "grad", f"dtheta[{algo}]")
+
+
+@pytest.mark.parametrize("shape", [(2, 5, 37, 53, 41, 29), (1, 16, 64, 96, 64, 96), (2, 3, 20, 24, 20, 24)])
+@pytest.mark.parametrize("padding", ["zeros", "border"])
+@pytest.mark.parametrize("ac", [True, False])
+def test_stn_scatter_priv_parity(cuda_device, shape, padding, ac):
+    """SCATTER_PRIV: d_input via the block-private footprint accumulator, every sample."""
+    N, C, H, W, Ho, Wo = shape
+    inp = synth.stn_inputs(N, C, H, W, Ho, Wo, cfg=1)
+    g = _cuda(inp, cuda_device)
+    dx, dth = rsgrad.stn_bwd(g["x"], g["theta"], g["dy"], align_corners=ac, padding=padding,
+                             algo="scatter_priv")
+    rdx, rdth = oracle.stn_bwd(*(inp[k].double().numpy() for k in ("x", "theta", "dy")), ac,
+                               padding == "border")
+    assert_close(_np(dx), rdx, "grad", "dx")
+    assert_close(_np(dth), rdth, "grad", "dtheta")
+
+
+def test_stn_fallback_samples_priv_and_atomic(cuda_device):
+    """Fallback samples (singular / huge preimage) inside an AUTO batch: privatised dX,
+    alone (need_dtheta=False) and with d_theta; and the SCATTER_ATOMIC route."""
+    inp = synth.stn_inputs(4, 6, 40, 44, cfg=1)
+    inp["theta"][1] = torch.tensor([[0.5, 0.5, 0.1], [0.5, 0.5, -0.2]])
+    inp["theta"][3] = torch.tensor([[0.02, 0.0, 0.1], [0.0, 0.03, 0.0]])
+    g = _cuda(inp, cuda_device)
+    rdx, rdth = oracle.stn_bwd(*(inp[k].double().numpy() for k in ("x", "theta", "dy")))
+    dx, _ = rsgrad.stn_bwd(g["x"], g["theta"], g["dy"], need_dtheta=False)
+    assert_close(_np(dx), rdx, "grad", "dx (AUTO, no dtheta)")
+    for algo in ("auto", "scatter_atomic"):
+        dx, dth = rsgrad.stn_bwd(g["x"], g["theta"], g["dy"], algo=algo)
+        assert_close(_np(dx), rdx, "grad", f"dx [{algo}]")
+        assert_close(_np(dth), rdth, "grad", f"dtheta [{algo}]")
 
 
 def test_stn_singular_theta_falls_back(cuda_device):
@@ -129,6 +164,21 @@ def test_warp_parity(cuda_device, shape, flow, padding):
     border = padding == "border"
     assert_close(_np(y), oracle.warp_fwd(x, fl, border), "fwd", "y")
     rdx, rdf = oracle.warp_bwd(x, fl, dy, border)
+    assert_close(_np(dx), rdx, "grad", "dx")
+    assert_close(_np(df), rdf, "grad", "dflow")
+
+
+@pytest.mark.parametrize("shape", [(1, 3, 16, 16), (2, 3, 37, 61), (1, 7, 5, 130), (1, 20, 33, 40)])
+@pytest.mark.parametrize("flow", ["smooth", "stress", "zero"])
+@pytest.mark.parametrize("padding", ["zeros", "border"])
+def test_warp_scatter_priv_parity(cuda_device, shape, flow, padding):
+    """SCATTER_PRIV: block-private footprint accumulation, flushed with one red per touched
+    element (stress flows overflow the footprint and take per-tap reds inside the tile)."""
+    N, C, H, W = shape
+    inp = synth.warp_inputs(N, C, H, W, cfg=1, flow=flow)
+    g = _cuda(inp, cuda_device)
+    dx, df = rsgrad.warp_bwd(g["x"], g["flow"], g["dy"], padding=padding, algo="scatter_priv")
+    rdx, rdf = oracle.warp_bwd(*(inp[k].double().numpy() for k in ("x", "flow", "dy")), padding == "border")
     assert_close(_np(dx), rdx, "grad", "dx")
     assert_close(_np(df), rdf, "grad", "dflow")
 
