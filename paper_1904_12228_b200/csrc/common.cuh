@@ -171,9 +171,24 @@ RS_DEV bool mbar_try_wait(unsigned long long *bar, unsigned parity) {
         : "memory");
     return ok != 0;
 }
+// try_wait with a suspend-time hint: the thread sleeps until the phase completes (or
+// the hint expires) instead of spinning through issue slots
+RS_DEV bool mbar_try_wait_sleep(unsigned long long *bar, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+    return ok != 0;
+}
 RS_DEV void mbar_wait(unsigned long long *bar, unsigned parity) {
-    while (!mbar_try_wait(bar, parity)) {
+    while (!mbar_try_wait_sleep(bar, parity)) {
     }
+}
+// 16-B cp.async to a shared-window address (no generic->shared conversion per copy)
+RS_DEV void cp_async16_s(unsigned s, const void *g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(g) : "memory");
 }
 
 // One bulk copy per (channel, row) segment (16-B aligned rows, widths multiple of

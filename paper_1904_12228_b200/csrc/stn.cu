@@ -368,32 +368,35 @@ __global__ void __launch_bounds__(kThreads, 3)
                 for (int e = threadIdx.x; e < kNS * NC * 4; e += kThreads)
                     stage[(e / (4 * NC)) * kFSt + ((e >> 2) % NC) * kS + F + (e & 3)] = 0.f;
                 __syncthreads();
+                const unsigned sstage = smem_u32(stage);
                 // every thread issues its share of chunk kc's 16-B cp.async copies and arrives
                 // on full[slot] when they have landed (TMA bulk copies are request-rate bound
                 // at these 60-130 B row segments: measured 2.7 TB/s at 64 B, scripts/micro)
                 auto issue = [&](int kc) {
                     const int slot = kc % kNS, c0s = kc * NC, ncp = min(NC, a.C - c0s);
-                    float *dst = stage + slot * kFSt;
+                    const unsigned dst = sstage + (unsigned)(slot * kFSt) * 4u;
                     const float *xs = xbase + (long long)c0s * HW;
                     // X: four lanes per footprint row, channels innermost
                     for (int r = threadIdx.x >> 2; r < R; r += kThreads / 4) {
                         const int w = rcnt[r];
                         const float *src = xs + (long long)(ylo + r) * a.W + rxa[r];
-                        float *d = dst + roff[r];
+                        unsigned d = dst + (unsigned)roff[r] * 4u;
                         for (int c = 0; c < ncp; c++) {
-                            for (int q = (threadIdx.x & 3) * 4; q < w; q += 16) cp_async16(d + q, src + q);
+                            for (int q = (threadIdx.x & 3) * 4; q < w; q += 16) cp_async16_s(d + q * 4u, src + q);
                             src += HW;
-                            d += kS;
+                            d += kS * 4u;
                         }
                     }
-                    if (MODE != MODE_FWD) {  // dY tile: eight lanes per row
+                    if (MODE != MODE_FWD) {  // dY tile: eight lanes per row, channel loop outside
                         const int per = vrows * 8;
-                        for (int e = threadIdx.x; e < ncp * per; e += kThreads) {
-                            const int c = e / per, rem = e - c * per, r = rem >> 3, q = (rem & 7) * 4;
-                            if (q < vcols)
-                                cp_async16(dst + NC * kS + c * GT + r * kFJ + q,
-                                           a.dy + ((long long)n * a.C + c0s + c) * P +
-                                               (long long)(ti * kFI + r) * a.Wo + jb + q);
+                        const float *gs = a.dy + ((long long)n * a.C + c0s) * P + (long long)(ti * kFI) * a.Wo + jb;
+                        for (int c = 0; c < ncp; c++, gs += P) {
+                            for (int rem = threadIdx.x; rem < per; rem += kThreads) {
+                                const int r = rem >> 3, q = (rem & 7) * 4;
+                                if (q < vcols)
+                                    cp_async16_s(dst + (unsigned)(NC * kS + c * GT + r * kFJ + q) * 4u,
+                                                 gs + (long long)r * a.Wo + q);
+                            }
                         }
                     }
                     cp_async_arrive(&full[slot]);
