@@ -151,7 +151,8 @@ def test_stn_paper_shape_full(cuda_device):
 
 
 # ============================================================================ warp
-@pytest.mark.parametrize("shape", [(1, 3, 16, 16), (2, 3, 37, 61), (1, 7, 5, 130), (1, 1, 1, 1)])
+@pytest.mark.parametrize("shape", [(1, 3, 16, 16), (2, 3, 37, 61), (1, 7, 5, 130), (1, 1, 1, 1),
+                                   (2, 3, 37, 64), (1, 5, 9, 132), (1, 2, 3, 4)])
 @pytest.mark.parametrize("flow", ["smooth", "stress", "zero"])
 @pytest.mark.parametrize("padding", ["zeros", "border"])
 def test_warp_parity(cuda_device, shape, flow, padding):
