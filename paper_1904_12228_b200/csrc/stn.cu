@@ -372,32 +372,61 @@ __global__ void __launch_bounds__(kThreads, 3)
                 // every thread issues its share of chunk kc's 16-B cp.async copies and arrives
                 // on full[slot] when they have landed (TMA bulk copies are request-rate bound
                 // at these 60-130 B row segments: measured 2.7 TB/s at 64 B, scripts/micro)
+                // per-thread copy plan, identical for every chunk: four lanes per footprint
+                // row (rows tid/4 and tid/4 + 64), eight lanes per dY tile row
+                const int q0 = (threadIdx.x & 3) * 4;
+                int xnp[2];
+                long long xsrc[2];
+                unsigned xdst[2];
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const int r = MODE == MODE_FWD ? R : (threadIdx.x >> 2) + (kThreads / 4) * h;
+                    xnp[h] = 0;
+                    xsrc[h] = 0;
+                    xdst[h] = 0;
+                    if (r < R) {
+                        const int w = rcnt[r];
+                        xnp[h] = w > q0 ? (w - q0 + 15) >> 4 : 0;
+                        xsrc[h] = (long long)(ylo + r) * a.W + rxa[r] + q0;
+                        xdst[h] = (unsigned)(roff[r] + q0) * 4u;
+                    }
+                }
+                const int gr = threadIdx.x >> 3, gq = (threadIdx.x & 7) * 4;
+                const bool gok = MODE != MODE_FWD && gr < vrows && gq < vcols;
+                const long long gsrc = (long long)(ti * kFI + gr) * a.Wo + jb + gq;
+                const unsigned gdst = (unsigned)(NC * kS + gr * kFJ + gq) * 4u;
+                static_assert(kFI * 8 <= kThreads || MODE == MODE_FWD, "one dY copy per thread and channel");
                 auto issue = [&](int kc) {
                     const int slot = kc % kNS, c0s = kc * NC, ncp = min(NC, a.C - c0s);
                     const unsigned dst = sstage + (unsigned)(slot * kFSt) * 4u;
                     const float *xs = xbase + (long long)c0s * HW;
-                    // X: four lanes per footprint row, channels innermost
-                    for (int r = threadIdx.x >> 2; r < R; r += kThreads / 4) {
-                        const int w = rcnt[r];
-                        const float *src = xs + (long long)(ylo + r) * a.W + rxa[r];
-                        unsigned d = dst + (unsigned)roff[r] * 4u;
-                        for (int c = 0; c < ncp; c++) {
-                            for (int q = (threadIdx.x & 3) * 4; q < w; q += 16) cp_async16_s(d + q * 4u, src + q);
-                            src += HW;
-                            d += kS * 4u;
-                        }
-                    }
-                    if (MODE != MODE_FWD) {  // dY tile: eight lanes per row, channel loop outside
-                        const int per = vrows * 8;
-                        const float *gs = a.dy + ((long long)n * a.C + c0s) * P + (long long)(ti * kFI) * a.Wo + jb;
-                        for (int c = 0; c < ncp; c++, gs += P) {
-                            for (int rem = threadIdx.x; rem < per; rem += kThreads) {
-                                const int r = rem >> 3, q = (rem & 7) * 4;
-                                if (q < vcols)
-                                    cp_async16_s(dst + (unsigned)(NC * kS + c * GT + r * kFJ + q) * 4u,
-                                                 gs + (long long)r * a.Wo + q);
+                    if (MODE == MODE_FWD) {  // (measured faster here than the plan below)
+                        for (int r = threadIdx.x >> 2; r < R; r += kThreads / 4) {
+                            const int w = rcnt[r];
+                            const float *src = xs + (long long)(ylo + r) * a.W + rxa[r];
+                            unsigned d = dst + (unsigned)roff[r] * 4u;
+                            for (int c = 0; c < ncp; c++) {
+                                for (int q = q0; q < w; q += 16) cp_async16_s(d + q * 4u, src + q);
+                                src += HW;
+                                d += kS * 4u;
                             }
                         }
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < 2; h++) {
+                            if (xnp[h] == 0) continue;
+                            const float *src = xs + xsrc[h];
+                            unsigned d = dst + xdst[h];
+                            for (int c = 0; c < ncp; c++) {
+                                for (int pc = 0; pc < xnp[h]; pc++) cp_async16_s(d + pc * 64u, src + pc * 16);
+                                src += HW;
+                                d += kS * 4u;
+                            }
+                        }
+                    }
+                    if (gok) {
+                        const float *gs = a.dy + ((long long)n * a.C + c0s) * P + gsrc;
+                        for (int c = 0; c < ncp; c++) cp_async16_s(dst + gdst + (unsigned)(c * GT) * 4u, gs + (long long)c * P);
                     }
                     cp_async_arrive(&full[slot]);
                 };
