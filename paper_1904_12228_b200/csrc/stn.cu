@@ -141,6 +141,14 @@ RS_DEV bool stn_gatherable(const Affine &A, int Ho, int Wo) {
 #ifndef RS_FIDF
 #define RS_FIDF 32
 #endif
+#ifndef RS_OT
+#define RS_OT 256
+#endif
+#ifndef RS_OTB
+#define RS_OTB 3
+#endif
+constexpr int kOTFast = RS_OT;     // FAST: threads per output-tile block
+constexpr int kOTFastMinB = RS_OTB;
 constexpr int kNS = RS_NS;     // FAST: stages in the ring
 constexpr int kFSt = RS_FST;   // FAST: floats per stage
 constexpr int kFIdf = RS_FIDF; // FAST: d_theta tile rows
@@ -179,11 +187,12 @@ RS_DEV void dispatch_slice(int need, Fn &&fn) {
 // touched footprint element (PAPER.md:733's atomics, made block-local first).
 template <int MODE, bool VEC, bool FLOW = false, int kFI = (MODE == 0 ? kFIfwd : kFIdth), bool FAST = false,
           bool PRIV = false>
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(FAST ? kOTFast : kThreads, FAST ? kOTFastMinB : 3)
     stn_out_tile(StnArgs a, const double *__restrict__ xtab, const double *__restrict__ ytab,
                  const int *__restrict__ fb_list, const int *__restrict__ fb_count,
                  double *__restrict__ partials, int tiles_j, int tiles_i) {
-    constexpr int kFP = kFI / 8;  // output pixels per thread
+    constexpr int kOT = FAST ? kOTFast : kThreads, kOW = kOT / 32;  // threads, warps
+    constexpr int kFP = kFI / kOW;  // output pixels per thread
     extern __shared__ __align__(16) float4 sm4[];
     int *rlo = (int *)sm4;
     int *rhi = rlo + kFRMax;
@@ -192,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, 3)
     int *rcnt = roff + kFRMax;
     int *ctl = rcnt + kFRMax;                // 16 ints
     float *stage = (float *)(ctl + 16);      // 2 * kFStage (16-B aligned: 656 ints)
-    __shared__ float red[kThreads / 32][6];
+    __shared__ float red[kOT / 32][6];
 
     __shared__ double ntab[kFJ + kFI];  // normalised coordinates of the tile's columns / rows
     // FAST (single tile per block, fb_list == nullptr): full[s] = TMA bytes landed,
@@ -201,8 +210,8 @@ __global__ void __launch_bounds__(kThreads, 3)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (FAST && threadIdx.x == 0) {
         for (int b = 0; b < kNS; b++) {
-            mbar_init(&full[b], kThreads);
-            mbar_init(&empty[b], kThreads / 32);
+            mbar_init(&full[b], kOT);
+            mbar_init(&empty[b], kOT / 32);
         }
         fence_mbar_init();
     }
@@ -226,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 3)
         int ymin = INT_MAX, ymax = INT_MIN;
 #pragma unroll
         for (int k = 0; k < kFP; k++) {
-            const int i = ti * kFI + warp + 8 * k, j = tj * kFJ + lane;
+            const int i = ti * kFI + warp + kOW * k, j = tj * kFJ + lane;
             in[k] = i < a.Ho && j < a.Wo;
             x0[k] = y0[k] = 0;
             fx[k] = fy[k] = 0.f;
@@ -240,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                     ix = __dadd_rn((double)j, (double)ldg_stream(fp));
                     iy = __dadd_rn((double)i, (double)ldg_stream(fp + P));
                 } else {
-                    const double xt = ntab[lane], yt = ntab[kFJ + warp + 8 * k];
+                    const double xt = ntab[lane], yt = ntab[kFJ + warp + kOW * k];
                     xtf[k] = (float)xt;
                     ytf[k] = (float)yt;
                     stn_coord(T, xt, yt, a.H, a.W, a.ac, ix, iy);
@@ -268,7 +277,7 @@ __global__ void __launch_bounds__(kThreads, 3)
             ctl[0] = INT_MAX;
             ctl[1] = INT_MIN;
         }
-        for (int r = threadIdx.x; r < kFRMax; r += kThreads) {
+        for (int r = threadIdx.x; r < kFRMax; r += kOT) {
             rlo[r] = INT_MAX;
             rhi[r] = INT_MIN;
         }
@@ -312,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 3)
 #pragma unroll
             for (int k = 0; k < kFP; k++) {
                 if (!in[k]) continue;
-                const int i = ti * kFI + warp + 8 * k, j = tj * kFJ + lane;
+                const int i = ti * kFI + warp + kOW * k, j = tj * kFJ + lane;
                 const long long o00 = (long long)y0[k] * a.W + x0[k];
                 const float w00 = (1.f - fy[k]) * (1.f - fx[k]), w01 = (1.f - fy[k]) * fx[k];
                 const float w10 = fy[k] * (1.f - fx[k]), w11 = fy[k] * fx[k];
@@ -365,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                 constexpr int NC0 = kFSt / (kS + GT);
                 constexpr int NC = NC0 < 8 ? NC0 : 8;
                 const int nch = (a.C + NC - 1) / NC;
-                for (int e = threadIdx.x; e < kNS * NC * 4; e += kThreads)
+                for (int e = threadIdx.x; e < kNS * NC * 4; e += kOT)
                     stage[(e / (4 * NC)) * kFSt + ((e >> 2) % NC) * kS + F + (e & 3)] = 0.f;
                 __syncthreads();
                 const unsigned sstage = smem_u32(stage);
@@ -380,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                 unsigned xdst[2];
 #pragma unroll
                 for (int h = 0; h < 2; h++) {
-                    const int r = MODE == MODE_FWD ? R : (threadIdx.x >> 2) + (kThreads / 4) * h;
+                    const int r = MODE == MODE_FWD ? R : (threadIdx.x >> 2) + (kOT / 4) * h;
                     xnp[h] = 0;
                     xsrc[h] = 0;
                     xdst[h] = 0;
@@ -395,13 +404,13 @@ __global__ void __launch_bounds__(kThreads, 3)
                 const bool gok = MODE != MODE_FWD && gr < vrows && gq < vcols;
                 const long long gsrc = (long long)(ti * kFI + gr) * a.Wo + jb + gq;
                 const unsigned gdst = (unsigned)(NC * kS + gr * kFJ + gq) * 4u;
-                static_assert(kFI * 8 <= kThreads || MODE == MODE_FWD, "one dY copy per thread and channel");
+                static_assert(kFI * 8 <= kOT || MODE == MODE_FWD, "one dY copy per thread and channel");
                 auto issue = [&](int kc) {
                     const int slot = kc % kNS, c0s = kc * NC, ncp = min(NC, a.C - c0s);
                     const unsigned dst = sstage + (unsigned)(slot * kFSt) * 4u;
                     const float *xs = xbase + (long long)c0s * HW;
                     if (MODE == MODE_FWD) {  // (measured faster here than the plan below)
-                        for (int r = threadIdx.x >> 2; r < R; r += kThreads / 4) {
+                        for (int r = threadIdx.x >> 2; r < R; r += kOT / 4) {
                             const int w = rcnt[r];
                             const float *src = xs + (long long)(ylo + r) * a.W + rxa[r];
                             unsigned d = dst + (unsigned)roff[r] * 4u;
@@ -448,7 +457,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                             if (!in[k]) continue;
                             const float w00 = (1.f - fy[k]) * (1.f - fx[k]), w01 = (1.f - fy[k]) * fx[k];
                             const float w10 = fy[k] * (1.f - fx[k]), w11 = fy[k] * fx[k];
-                            const int i = ti * kFI + warp + 8 * k, j = jb + lane;
+                            const int i = ti * kFI + warp + kOW * k, j = jb + lane;
                             float *yp = a.y + ((long long)n * a.C + c0) * P + (long long)i * a.Wo + j;
 #pragma unroll
                             for (int c = 0; c < NC; c++) {
@@ -458,7 +467,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                                 yp[(long long)c * P] = v;
                             }
                         } else {
-                            const float *gp = S + NC * kS + (warp + 8 * k) * kFJ + lane;
+                            const float *gp = S + NC * kS + (warp + kOW * k) * kFJ + lane;
 #pragma unroll
                             for (int c = 0; c < NC; c++) {
                                 if (!fullc && c0 + c >= a.C) break;
@@ -498,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                 if (MODE == MODE_FWD) return;
                 const int jb = tj * kFJ;
                 if (gvec) {
-                    for (int e = threadIdx.x; e < ncp * kFI * (kFJ / 4); e += kThreads) {
+                    for (int e = threadIdx.x; e < ncp * kFI * (kFJ / 4); e += kOT) {
                         const int c = e / (kFI * (kFJ / 4)), rem = e - c * (kFI * (kFJ / 4));
                         const int r = rem / (kFJ / 4), q4 = (rem - r * (kFJ / 4)) * 4;
                         const int i = ti * kFI + r;
@@ -507,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                                        a.dy + ((long long)n * a.C + c0s + c) * P + (long long)i * a.Wo + jb + q4);
                     }
                 } else {
-                    for (int e = threadIdx.x; e < ncp * kFI * kFJ; e += kThreads) {
+                    for (int e = threadIdx.x; e < ncp * kFI * kFJ; e += kOT) {
                         const int c = e / (kFI * kFJ), rem = e - c * (kFI * kFJ);
                         const int r = rem / kFJ, q = rem - r * kFJ;
                         const int i = ti * kFI + r;
@@ -519,7 +528,7 @@ __global__ void __launch_bounds__(kThreads, 3)
             };
             float *pacc = stage + 2 * kFStage;  // PRIV: CH x F accumulator (CH * F <= kFStage)
             if (PRIV && a.dx)
-                for (int e = threadIdx.x; e < CH * F; e += kThreads) pacc[e] = 0.f;
+                for (int e = threadIdx.x; e < CH * F; e += kOT) pacc[e] = 0.f;
             if (F > 0) stage_rows<VEC>(stage, F, xbase, HW, min(CH, a.C), R, a.W, ylo, rxa, roff, rcnt);
             stage_g(stage + CH * F, 0, min(CH, a.C));
             cp_async_commit();
@@ -541,7 +550,7 @@ __global__ void __launch_bounds__(kThreads, 3)
 #pragma unroll
                 for (int k = 0; k < kFP; k++) {
                     if (!in[k]) continue;
-                    const int i = ti * kFI + warp + 8 * k, j = tj * kFJ + lane;
+                    const int i = ti * kFI + warp + kOW * k, j = tj * kFJ + lane;
                     const bool k00 = yv0[k] && xv0[k], k01 = yv0[k] && xv1[k];
                     const bool k10 = yv1[k] && xv0[k], k11 = yv1[k] && xv1[k];
                     const float w00 = (1.f - fy[k]) * (1.f - fx[k]), w01 = (1.f - fy[k]) * fx[k];
@@ -555,7 +564,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                         if (MODE == MODE_FWD) {
                             a.y[ob + c * P] = fmaf(w00, v00, fmaf(w01, v01, fmaf(w10, v10, w11 * v11)));
                         } else {
-                            const float g = S[CH * F + c * GT + (warp + 8 * k) * kFJ + lane];
+                            const float g = S[CH * F + c * GT + (warp + kOW * k) * kFJ + lane];
                             dix[k] = fmaf(g, fmaf(1.f - fy[k], v01 - v00, fy[k] * (v11 - v10)), dix[k]);
                             diy[k] = fmaf(g, fmaf(1.f - fx[k], v10 - v00, fx[k] * (v11 - v01)), diy[k]);
                             if (PRIV && a.dx) {  // block-private accumulator (shared atomics)
@@ -579,7 +588,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                 if (PRIV && a.dx) {
                     // flush: one red per touched footprint element, then re-zero (8 lanes per row)
                     float *dxc = a.dx + ((long long)n * a.C + c0) * HW;
-                    for (int r = (threadIdx.x >> 3); r < R; r += kThreads / 8) {
+                    for (int r = (threadIdx.x >> 3); r < R; r += kOT / 8) {
                         const int wdt = rcnt[r];
                         float *gr = dxc + (long long)(ylo + r) * a.W + rxa[r];
                         for (int c = 0; c < cn; c++) {
@@ -601,7 +610,7 @@ __global__ void __launch_bounds__(kThreads, 3)
 #pragma unroll
             for (int k = 0; k < kFP; k++) {
                 if (!in[k]) continue;
-                const int i = ti * kFI + warp + 8 * k, j = tj * kFJ + lane;
+                const int i = ti * kFI + warp + kOW * k, j = tj * kFJ + lane;
                 float *dfp = a.dflow + (long long)n * 2 * P + (long long)i * a.Wo + j;
                 dfp[0] = dix[k] * cgx[k];
                 dfp[P] = diy[k] * cgy[k];
@@ -630,7 +639,7 @@ __global__ void __launch_bounds__(kThreads, 3)
             __syncthreads();
             if (threadIdx.x < 6) {
                 double s = 0.0;
-                for (int w = 0; w < kThreads / 32; w++) s += (double)red[w][threadIdx.x];
+                for (int w = 0; w < kOT / 32; w++) s += (double)red[w][threadIdx.x];
                 partials[((long long)n * tiles_j * tiles_i + blockIdx.x) * 6 + threadIdx.x] = s;
             }
         }
@@ -1756,7 +1765,7 @@ cudaError_t stn_fwd_launch(const StnArgs &a, cudaStream_t s) {
     if (vec && !stn_slow_tiles()) {
         auto k = stn_out_tile<MODE_FWD, true, false, kFIfwd, true>;
         set_smem(k, sm);
-        k<<<grid, kThreads, sm, s>>>(a, nullptr, nullptr, nullptr, nullptr, nullptr, g.fj, g.fi_fwd);
+        k<<<grid, kOTFast, sm, s>>>(a, nullptr, nullptr, nullptr, nullptr, nullptr, g.fj, g.fi_fwd);
     } else if (vec) {
         set_smem(stn_out_tile<MODE_FWD, true>, sm);
         stn_out_tile<MODE_FWD, true><<<grid, kThreads, sm, s>>>(a, nullptr, nullptr, nullptr, nullptr,
@@ -1891,7 +1900,7 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
             auto k = stn_out_tile<MODE_DTHETA, true, false, kFIdf, true>;
             set_smem(k, sm);
             grid.x = g.fj * fi_df;
-            k<<<grid, kThreads, sm, s>>>(a, w.xtab, w.ytab, nullptr, w.fb_count, w.pf, g.fj, fi_df);
+            k<<<grid, kOTFast, sm, s>>>(a, w.xtab, w.ytab, nullptr, w.fb_count, w.pf, g.fj, fi_df);
         } else if (priv && !dth_all) {  // fallback samples: d_theta and privatised d_input
             auto k = vin ? stn_out_tile<MODE_DTHETA, true, false, kFIdth, false, true>
                          : stn_out_tile<MODE_DTHETA, false, false, kFIdth, false, true>;
