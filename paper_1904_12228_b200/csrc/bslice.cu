@@ -75,6 +75,35 @@ struct Tile {
     int ys, ye, xs, xe;  // pixel ranges [ys, ye) x [xs, xe)
 };
 
+// Block-wide tile descriptor: the four exact dual-cell bounds (fp64 searches with
+// divisions) are computed once, by threads 0-3, and shared through `sh` (4 ints).
+// Contains a __syncthreads: call from every thread of the block.
+RS_DEV Tile tile_of_block(int b, int Gh, int Gw, int SY, int SX, int H, int W, int *sh) {
+    Tile t;
+    const int sx = b % SX;
+    int bb = b / SX;
+    const int sy = bb % SY;
+    bb /= SY;
+    const int kk = bb % (Gw + 1);
+    bb /= (Gw + 1);
+    const int jj = bb % (Gh + 1);
+    t.n = bb / (Gh + 1);
+    t.j = jj - 1;
+    t.k = kk - 1;
+    if (threadIdx.x < 4) {
+        const int v = threadIdx.x;
+        sh[v] = v < 2 ? dual_begin(t.j + v, H, Gh) : dual_begin(t.k + v - 2, W, Gw);
+    }
+    __syncthreads();
+    const int yb = sh[0], yend = sh[1], xb = sh[2], xend = sh[3];
+    const int hh = yend - yb, ww = xend - xb;
+    t.ys = yb + (int)(((long long)hh * sy) / SY);
+    t.ye = yb + (int)(((long long)hh * (sy + 1)) / SY);
+    t.xs = xb + (int)(((long long)ww * sx) / SX);
+    t.xe = xb + (int)(((long long)ww * (sx + 1)) / SX);
+    return t;
+}
+
 RS_DEV Tile tile_of(int b, int Gh, int Gw, int SY, int SX, int H, int W) {
     Tile t;
     const int sx = b % SX;
@@ -138,7 +167,8 @@ __global__ void __launch_bounds__(kThreads)
     float4 *gdz = glo + (a.D + 1) * kPlaneStride;              // (D+1) * 13
     float *fxt = (float *)(gdz + (a.D + 1) * kPlaneStride);    // kTileXS
     float *fyt = fxt + kTileXS;                                // kTileYS
-    const Tile t = tile_of(blockIdx.x, a.Gh, a.Gw, SY, SX, a.H, a.W);
+    __shared__ int tsh[4];
+    const Tile t = tile_of_block(blockIdx.x, a.Gh, a.Gw, SY, SX, a.H, a.W, tsh);
     const int TW = t.xe - t.xs, TH = t.ye - t.ys;
     if (TW <= 0 || TH <= 0) return;
     stage_corners(glo, gdz, a.grid, t, a.D, a.Gh, a.Gw);
