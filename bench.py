@@ -513,7 +513,8 @@ def run_e2e(rs, s, w, b, args, world):
     return {"value": round(v, 1), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "samples_per_rank": nb, "steps": steps,
             "note": "pinned host buffers passed as host pointers to the C ABI: the library stages "
-                    "them in sample chunks on two internal streams (H2D / kernels / D2H overlap); "
+                    "them in up to 32 sample chunks on three internal streams (H2D / kernels / D2H overlap; "
+                    "temporaries from a private stream-ordered pool kept reserved); "
                     "one stream sync per step; wall clock, max over ranks"}
 
 

@@ -16,8 +16,8 @@
  *   Tensors   fp32, C-contiguous (NCHW), no aliasing between inputs and outputs.
  *   Pointers  device pointers (cudaMalloc / torch CUDA tensors) OR host pointers
  *             (pinned or pageable).  All-device calls run entirely on `stream`.
- *             If any pointer is host memory the batch is processed in sample
- *             chunks on two library-internal streams that are ordered after
+ *             If any pointer is host memory the batch is processed in up to 32
+ *             sample chunks on three library-internal streams that are ordered after
  *             `stream` (event wait) and before its later work (event wait back):
  *             per chunk, host inputs are copied H2D into stream-ordered
  *             temporaries (cudaMallocAsync), the kernels run, host outputs are
@@ -27,8 +27,10 @@
  *   Outputs   always OVERWRITTEN, never accumulated.  A NULL gradient pointer
  *             skips that gradient's work.
  *   Ownership the caller owns every buffer.  The library keeps no state except
- *             the thread-local error string; it allocates only stream-ordered
- *             temporaries (workspace, host staging) released in stream order.
+ *             the thread-local error string and one private stream-ordered memory
+ *             pool per device: its temporaries (workspace, host staging) are freed in
+ *             stream order but the pool keeps the memory reserved for later calls
+ *             (the caller's default pool is untouched).
  *   Workspace *_bwd take an optional device workspace (size from
  *             rsgrad_bwd_workspace_bytes); NULL/too small => the library takes
  *             a stream-ordered temporary of that size itself.

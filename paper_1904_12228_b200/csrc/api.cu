@@ -7,6 +7,9 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <string>
+#include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "../../include/rsgrad.h"
@@ -58,6 +61,50 @@ rs_status check_opts(const rs_opts &o) {
     return RS_OK;
 }
 
+constexpr int kMaxHostStreams = 4;
+
+// Library temporaries (workspace, host-path staging) come from a private stream-ordered
+// pool per device whose memory is kept reserved between calls (release threshold = max):
+// re-mapping freed memory on every call made the host-buffer path's timing erratic.  The
+// caller's default pool is left untouched.
+cudaError_t lib_malloc(void **p, size_t bytes, cudaStream_t s) {
+    static cudaMemPool_t pools[64] = {};
+    static std::mutex mu;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return cudaMallocAsync(p, bytes, s);
+    cudaMemPool_t pool;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!pools[dev]) {
+            cudaMemPoolProps props = {};
+            props.allocType = cudaMemAllocationTypePinned;
+            props.location.type = cudaMemLocationTypeDevice;
+            props.location.id = dev;
+            cudaMemPool_t np;
+            if (cudaMemPoolCreate(&np, &props) != cudaSuccess) {
+                cudaGetLastError();
+                return cudaMallocAsync(p, bytes, s);
+            }
+            unsigned long long thr = ~0ull;
+            cudaMemPoolSetAttribute(np, cudaMemPoolAttrReleaseThreshold, &thr);
+            pools[dev] = np;
+        }
+        pool = pools[dev];
+    }
+    return cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
+
+// integer tuning knob from the environment (A/B measurements), clamped to [1, hi]
+int env_int(const char *name, int dflt, int hi = 64) {
+    const char *e = getenv(name);
+    int v = e ? atoi(e) : dflt;
+    if (v < 1) v = 1;
+    if (v > hi) v = hi;
+    if (std::string(name) == "RSGRAD_HOST_STREAMS" && v > kMaxHostStreams) v = kMaxHostStreams;
+    return v;
+}
+
 // One tensor argument of an entry point: pointer (device, host or NULL), bytes per
 // sample, direction.
 struct TArg {
@@ -99,7 +146,7 @@ rs_status run_batched(int N, std::vector<TArg> &args, cudaStream_t s, void *work
         void *ws = workspace;
         bool own = false;
         if (need && (!ws || ws_bytes < need)) {
-            cudaError_t e = cudaMallocAsync(&ws, need, s);
+            cudaError_t e = lib_malloc(&ws, need, s);
             if (e != cudaSuccess) return fail(RS_ERR_WORKSPACE, "workspace cudaMallocAsync(%zu): %s", need, cudaGetErrorString(e));
             own = true;
         }
@@ -108,26 +155,30 @@ rs_status run_batched(int N, std::vector<TArg> &args, cudaStream_t s, void *work
         if (e != cudaSuccess) return fail(RS_ERR_CUDA, "launch: %s", cudaGetErrorString(e));
         return ok();
     }
-    const int nchunk = N < 8 ? N : 8;
+    // more, smaller chunks shorten the pipeline's fill and drain (the first chunk's H2D
+    // and the last chunk's D2H are not overlapped); three streams let chunk c+1's H2D,
+    // chunk c's kernels and chunk c-1's D2H run at once (H2D and D2H engines in parallel)
+    const int maxchunk = env_int("RSGRAD_HOST_CHUNKS", 32), NS = env_int("RSGRAD_HOST_STREAMS", 3);
+    const int nchunk = N < maxchunk ? N : maxchunk;
     const int cs = (N + nchunk - 1) / nchunk;
-    cudaStream_t st[2];
-    cudaEvent_t ev0, evs[2];
-    for (int k = 0; k < 2; k++) cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking);
+    cudaStream_t st[kMaxHostStreams];
+    cudaEvent_t ev0, evs[kMaxHostStreams];
+    for (int k = 0; k < NS; k++) cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
     cudaEventRecord(ev0, s);
-    std::vector<void *> buf[2];
-    void *wsk[2] = {nullptr, nullptr};
+    std::vector<void *> buf[kMaxHostStreams];
+    void *wsk[kMaxHostStreams] = {};
     cudaError_t err = cudaSuccess;
-    for (int k = 0; k < 2; k++) {
+    for (int k = 0; k < NS; k++) {
         cudaStreamWaitEvent(st[k], ev0, 0);
         buf[k].assign(na, nullptr);
         for (int i = 0; i < na; i++)
-            if (host[i] && err == cudaSuccess) err = cudaMallocAsync(&buf[k][i], args[i].per_sample * cs, st[k]);
+            if (host[i] && err == cudaSuccess) err = lib_malloc(&buf[k][i], args[i].per_sample * cs, st[k]);
         const size_t need = ws_need(cs);
-        if (need && err == cudaSuccess) err = cudaMallocAsync(&wsk[k], need, st[k]);
+        if (need && err == cudaSuccess) err = lib_malloc(&wsk[k], need, st[k]);
     }
     for (int c = 0, n0 = 0; n0 < N && err == cudaSuccess; c++, n0 += cs) {
-        const int nc = N - n0 < cs ? N - n0 : cs, k = c & 1;
+        const int nc = N - n0 < cs ? N - n0 : cs, k = c % NS;
         for (int i = 0; i < na && err == cudaSuccess; i++) {
             const size_t off = args[i].per_sample * (size_t)n0, bytes = args[i].per_sample * (size_t)nc;
             if (!args[i].p) {
@@ -146,7 +197,7 @@ rs_status run_batched(int N, std::vector<TArg> &args, cudaStream_t s, void *work
                 err = cudaMemcpyAsync((char *)const_cast<void *>(args[i].p) + args[i].per_sample * (size_t)n0, ptr[i],
                                       args[i].per_sample * (size_t)nc, cudaMemcpyDeviceToHost, st[k]);
     }
-    for (int k = 0; k < 2; k++) {
+    for (int k = 0; k < NS; k++) {
         for (int i = 0; i < na; i++)
             if (buf[k][i]) cudaFreeAsync(buf[k][i], st[k]);
         if (wsk[k]) cudaFreeAsync(wsk[k], st[k]);
