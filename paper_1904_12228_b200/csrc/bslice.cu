@@ -126,6 +126,37 @@ RS_DEV Tile tile_of(int b, int Gh, int Gw, int SY, int SX, int H, int W) {
     return t;
 }
 
+// Dual-cell bounds table: tab[jj] = dual_begin(jj - 1, H, Gh) for jj in [0, Gh+1],
+// tab[Gh + 2 + kk] = dual_begin(kk - 1, W, Gw) for kk in [0, Gw+1] (one tiny launch per
+// backward call, so the tiles read their bounds instead of re-running fp64 searches).
+__global__ void bslice_bounds_kernel(int *tab, int H, int W, int Gh, int Gw) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < Gh + 2) tab[t] = dual_begin(t - 1, H, Gh);
+    if (t < Gw + 2) tab[Gh + 2 + t] = dual_begin(t - 1, W, Gw);
+}
+
+RS_DEV Tile tile_of_tab(int b, int Gh, int Gw, int SY, int SX, const int *__restrict__ tab) {
+    Tile t;
+    const int sx = b % SX;
+    b /= SX;
+    const int sy = b % SY;
+    b /= SY;
+    const int kk = b % (Gw + 1);
+    b /= (Gw + 1);
+    const int jj = b % (Gh + 1);
+    t.n = b / (Gh + 1);
+    t.j = jj - 1;
+    t.k = kk - 1;
+    const int yb = __ldg(tab + jj), yend = __ldg(tab + jj + 1);
+    const int xb = __ldg(tab + Gh + 2 + kk), xend = __ldg(tab + Gh + 2 + kk + 1);
+    const int hh = yend - yb, ww = xend - xb;
+    t.ys = yb + (int)(((long long)hh * sy) / SY);
+    t.ye = yb + (int)(((long long)hh * (sy + 1)) / SY);
+    t.xs = xb + (int)(((long long)ww * sx) / SX);
+    t.xe = xb + (int)(((long long)ww * (sx + 1)) / SX);
+    return t;
+}
+
 // Stage, for every z-bin b in [0, D] and coefficient q, the bilinear-lerp terms
 // S(fx, fy) = a + fx b + fy (c + fx d) of (i) the low plane clamp(b-1) and (ii)
 // the plane DIFFERENCE clamp(b) - clamp(b-1).  Slicing the difference directly
@@ -286,7 +317,7 @@ RS_DEV void flush_acc(float *acc, float *wacc, int bin, int D, int lane) {
 }
 
 __global__ void __launch_bounds__(kThreads, 2)
-    bslice_bwd_tiled(BsliceArgs a, int SY, int SX, float *__restrict__ partials) {
+    bslice_bwd_tiled(BsliceArgs a, int SY, int SX, float *__restrict__ partials, const int *__restrict__ tab) {
     extern __shared__ float4 smem4[];
     const int D = a.D, NB = D + 1;
     float4 *glo = smem4;                                    // (D+1)*13 float4
@@ -302,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     float *fzv = (float *)(((uintptr_t)(sorted + max_chunks * kChunk) + 15) & ~(uintptr_t)15);  // kTileXS*kTileYS
     unsigned char *binv = (unsigned char *)(fzv + kTileXS * kTileYS);    // kTileXS*kTileYS
 
-    const Tile t = tile_of(blockIdx.x, a.Gh, a.Gw, SY, SX, a.H, a.W);
+    const Tile t = tile_of_tab(blockIdx.x, a.Gh, a.Gw, SY, SX, tab);
     const int TW = t.xe - t.xs, TH = t.ye - t.ys;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const long long HW = (long long)a.H * a.W;
@@ -691,7 +722,7 @@ size_t bwd_smem(int D) {
 size_t bslice_ws_bytes(int N, int H, int W, int D, int Gh, int Gw) {
     const TileGeom g = tile_geom(N, H, W, D, Gh, Gw);
     if (!g.ok) return 0;
-    return sizeof(float) * (size_t)g.blocks * 4 * D * 12;
+    return sizeof(float) * (size_t)g.blocks * 4 * D * 12 + sizeof(int) * (size_t)(Gh + Gw + 4);
 }
 
 cudaError_t bslice_fwd_launch(const BsliceArgs &a, cudaStream_t s) {
@@ -724,7 +755,11 @@ cudaError_t bslice_bwd_launch(const BsliceArgs &a, int algo, int deterministic, 
             attr_set = true;
         }
         float *partials = (float *)ws;
-        bslice_bwd_tiled<<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX, partials);
+        int *tab = (int *)(partials + (size_t)g.blocks * 4 * a.D * 12);
+        const int nt = (a.Gh > a.Gw ? a.Gh : a.Gw) + 2;
+        bslice_bounds_kernel<<<(nt + 127) / 128, 128, 0, s>>>(tab, a.H, a.W, a.Gh, a.Gw);
+        note_launch();
+        bslice_bwd_tiled<<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX, partials, tab);
         note_launch();
         const long long total = (long long)a.N * 12 * a.D * a.Gh * a.Gw;
         bslice_dgrid_gather<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(
