@@ -91,9 +91,10 @@ def test_workspace_sizes():
     # STN: per-block fp64 d_theta partials + coordinate tables
     assert rsgrad.workspace_bytes(0, 4, 16, 512, 512, 512, 512) > 0
     assert rsgrad.workspace_bytes(1, 8, 3, 384, 512) == 0
-    # bslice tiled path: one partial per (dual cell, corner, z, q)
+    # bslice tiled path: one partial per (dual cell, corner, z, q) + the per-call
+    # dual-cell bounds table (Gh + Gw + 4 ints)
     ws = rsgrad.workspace_bytes(2, 4, 3, 1024, 1024, D=8, Gh=16, Gw=16)
-    assert ws == 4 * 17 * 17 * 4 * 8 * 12 * 4
+    assert ws == 4 * 17 * 17 * 4 * 8 * 12 * 4 + 4 * (16 + 16 + 4)
     # too-fine grid => atomic path, no workspace
     assert rsgrad.workspace_bytes(2, 1, 3, 16, 16, D=8, Gh=16, Gw=16) == 0
     assert rsgrad.workspace_bytes(9, 1) == 0
