@@ -465,3 +465,40 @@ def test_bslice_many_planes_and_coarse_grid(cuda_device):
     assert_close(_np(dgr), rgr, "grad", "dgrid")
     assert_close(_np(dgd), rgd, "grad", "dguide")
     assert_close(_np(dx), rdx, "grad", "dx")
+
+
+@pytest.mark.parametrize("variant", ["win8,4,4", "win4,8,2", "win8,8,1", "win4,4,3", "direct"])
+@pytest.mark.parametrize("shape", [(2, 3, 70, 100), (1, 7, 45, 61), (1, 1, 33, 36), (2, 2, 130, 68)])
+@pytest.mark.parametrize("flow", ["smooth", "stress", "collapse"])
+@pytest.mark.parametrize("padding", ["zeros", "border"])
+def test_warp_bwd_window_variants(cuda_device, monkeypatch, variant, shape, flow, padding):
+    """warp_bwd d_input through per-warp shared windows flushed by vector reds
+    (RSGRAD_WARP_BWD=winR,NW,IT; AUTO keeps the per-tap reds, "direct"):
+    every (rows, warps, iterations) instantiation, ragged strips, W % 4 != 0 (scalar
+    flush), C > 3 (channel chunks), taps leaving the window (stress: direct reds) and a
+    collapsing flow (every pixel of a row on the same few cells: 32-lane duplicate
+    groups combined by shuffles)."""
+    monkeypatch.setenv("RSGRAD_WARP_BWD", variant)
+    N, C, H, W = shape
+    inp = synth.warp_inputs(N, C, H, W, cfg=1, flow="stress" if flow == "collapse" else flow)
+    if flow == "collapse":
+        yy, xx = torch.meshgrid(torch.arange(H, dtype=torch.float32), torch.arange(W, dtype=torch.float32),
+                                indexing="ij")
+        inp["flow"] = torch.stack([-xx * 0.97 + 3.3, -yy * 0.9 + 2.6]).expand(N, 2, H, W).contiguous()
+    g = _cuda(inp, cuda_device)
+    dx, df = rsgrad.warp_bwd(g["x"], g["flow"], g["dy"], padding=padding)
+    rdx, rdf = oracle.warp_bwd(*(inp[k].double().numpy() for k in ("x", "flow", "dy")), padding == "border")
+    assert_close(_np(dx), rdx, "grad", f"dx[{variant}]")
+    assert_close(_np(df), rdf, "grad", f"dflow[{variant}]")
+
+
+def test_warp_bwd_scatter_atomic_algo(cuda_device):
+    """SCATTER_ATOMIC = the per-tap red kernel; it agrees with AUTO and the oracle."""
+    inp = synth.warp_inputs(2, 3, 64, 96, cfg=1)
+    g = _cuda(inp, cuda_device)
+    a = rsgrad.warp_bwd(g["x"], g["flow"], g["dy"], algo="scatter_atomic")
+    b = rsgrad.warp_bwd(g["x"], g["flow"], g["dy"])
+    rdx, rdf = oracle.warp_bwd(*(inp[k].double().numpy() for k in ("x", "flow", "dy")))
+    for dx, df in (a, b):
+        assert_close(_np(dx), rdx, "grad", "dx")
+        assert_close(_np(df), rdf, "grad", "dflow")
