@@ -1,3 +1,5 @@
-bash scripts/gpurun_prof.sh warpd warp_bwd 4 RSGRAD_WARP_BWD=direct
-bash scripts/gpurun_prof.sh warpw warp_bwd 4 RSGRAD_WARP_BWD=win8,4,2
-cat gpurun_out/warpd.md gpurun_out/warpw.md; head -c 3000 gpurun_out/warpd.hot.txt; head -c 5000 gpurun_out/warpw.hot.txt
+timeout 600 python -m pytest tests -m gpu -x -q -k "bslice" > gpurun_out/pytest_bs.log 2>&1; echo pytest=$?
+for v in tiled staged; do echo "== $v"; RSGRAD_BSLICE_BWD=$v python scripts/bench_layer.py 16 5 bslice_bwd; done > gpurun_out/bs_ab.txt 2>&1
+cat gpurun_out/bs_ab.txt; tail -3 gpurun_out/pytest_bs.log
+bash scripts/gpurun_prof.sh bss bslice_bwd_staged 4
+rm -f gpurun_out/*.ncu-rep

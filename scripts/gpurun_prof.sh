@@ -12,7 +12,7 @@ r=list(csv.reader(sys.stdin)); i=r[0].index('Kernel Name')
 print(' '.join(sorted({re.sub(r'[(<].*','',x[i]).split('::')[-1] for x in r[2:]})))"); do
   ncu -i gpurun_out/$TAG.ncu-rep --page source --csv --print-source cuda,sass -k "regex:$k" > /tmp/src_$k.csv 2>/dev/null
   echo "=== $k" >> gpurun_out/$TAG.hot.txt
-  python scripts/src_hot.py /tmp/src_$k.csv 25 >> gpurun_out/$TAG.hot.txt 2>&1
+  python scripts/src_hot.py /tmp/src_$k.csv 60 >> gpurun_out/$TAG.hot.txt 2>&1
   ncu -i gpurun_out/$TAG.ncu-rep --page source --csv --print-source sass -k "regex:$k" > /tmp/sass_$k.csv 2>/dev/null
   python scripts/sass_hot.py /tmp/sass_$k.csv >> gpurun_out/$TAG.hot.txt 2>&1
 done

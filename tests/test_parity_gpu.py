@@ -502,3 +502,23 @@ def test_warp_bwd_scatter_atomic_algo(cuda_device):
     for dx, df in (a, b):
         assert_close(_np(dx), rdx, "grad", "dx")
         assert_close(_np(df), rdf, "grad", "dflow")
+
+
+@pytest.mark.parametrize("shape", [(1, 70, 66, 16, 1, 1), (1, 64, 96, 1, 2, 3)])
+@pytest.mark.parametrize("guide", ["uniform", "wide"])
+def test_bslice_bwd_single_cell_and_null_outputs(cuda_device, shape, guide):
+    """Dual-cell backward on a single 70 x 66 cell (D = 16) and with D = 1; a NULL
+    dX / d_guide skips that output and leaves d_grid bitwise unchanged."""
+    N, H, W, D, Gh, Gw = shape
+    inp = synth.bslice_inputs(N, H, W, D, Gh, Gw, cfg=1, grid="iid", guide=guide)
+    g = _cuda(inp, cuda_device)
+    dgr, dgd, dx = rsgrad.bslice_bwd(g["grid"], g["guide"], g["x"], g["dy"])
+    gr, gd, x, dy = (inp[k].double().numpy() for k in ("grid", "guide", "x", "dy"))
+    rgr, rgd, rdx = oracle.bslice_bwd(gr, gd, x, dy)
+    assert_close(_np(dx), rdx, "grad", "dx")
+    assert_close(_np(dgd), rgd, "grad", "dguide")
+    assert_close(_np(dgr), rgr, "grad", "dgrid")
+    a = rsgrad.bslice_bwd(g["grid"], g["guide"], g["x"], g["dy"], deterministic=True)
+    assert torch.equal(a[0], dgr) and torch.equal(a[1], dgd) and torch.equal(a[2], dx)
+    b = rsgrad.bslice_bwd(g["grid"], g["guide"], g["x"], g["dy"], need_dguide=False, need_dx=False)
+    assert b[1] is None and b[2] is None and torch.equal(b[0], dgr)
