@@ -49,6 +49,8 @@ def _load():
         lib.oracle_warp_bwd.argtypes = [P, P, P, I, I, I, I, I, P, P]
         lib.oracle_bslice_fwd.argtypes = [P, P, P, I, I, I, I, I, I, P]
         lib.oracle_bslice_bwd.argtypes = [P, P, P, P, I, I, I, I, I, I, P, P, P]
+        lib.oracle_conv_fwd.argtypes = [P, P, I, I, I, I, I, I, I, P]
+        lib.oracle_conv_bwd.argtypes = [P, P, P, I, I, I, I, I, I, I, P, P]
         lib.oracle_set_threads.argtypes = [I]
         lib.oracle_get_threads.restype = I
         _lib = lib
@@ -133,3 +135,26 @@ def bslice_bwd(grid, guide, x, dy, need_dgrid=True, need_dguide=True, need_dx=Tr
     _load().oracle_bslice_bwd(_p(grid), _p(guide), _p(x), _p(dy), N, H, W, D, Gh, Gw,
                               _p(dgrid), _p(dguide), _p(dx))
     return dgrid, dguide, dx
+
+
+# ----------------------------------------------------------------------------- conv (§8(f) f1)
+def conv_fwd(x, k):
+    """y = sum_{ci,ry,rx} x[n,ci,y-ry+kh//2,x-rx+kw//2] k[co,ci,ry,rx] (PAPER.md:703-707, 2-D)."""
+    x, k = _f64(x), _f64(k)
+    N, Ci, H, W = x.shape
+    Co, Ci2, kh, kw = k.shape
+    assert Ci2 == Ci
+    y = np.empty((N, Co, H, W), np.float64)
+    _load().oracle_conv_fwd(_p(x), _p(k), N, Ci, Co, H, W, kh, kw, _p(y))
+    return y
+
+
+def conv_bwd(x, k, dy, need_dx=True, need_dk=True):
+    """dx by the naive scatter, dk by its definition."""
+    x, k, dy = _f64(x), _f64(k), _f64(dy)
+    N, Ci, H, W = x.shape
+    Co, _, kh, kw = k.shape
+    dx = np.empty_like(x) if need_dx else None
+    dk = np.empty_like(k) if need_dk else None
+    _load().oracle_conv_bwd(_p(x), _p(k), _p(dy), N, Ci, Co, H, W, kh, kw, _p(dx), _p(dk))
+    return dx, dk

@@ -450,3 +450,83 @@ void oracle_bslice_bwd(const double *grid, const double *guide, const double *x,
         }
     }
 }
+
+/* ------------------------------------------------------------------ */
+/* 2-D convolution layer        */
+/* ------------------------------------------------------------------ */
+/* The paper's gather ("output(x) = input(x - r.x) *
+ * kernel(r.x)") extended to 2-D and channels, centred so the output has the
+ * input's size (reading R10):
+ *   y[n,co,y,x] = sum_{ci<Ci, ry<kh, rx<kw} x[n,ci, y-ry+ph, x-rx+pw] * k[co,ci,ry,rx]
+ * with ph = kh/2, pw = kw/2 (integer division) and zero outside [0,H)x[0,W).
+ * x: N x Ci x H x W, k: Co x Ci x kh x kw, y: N x Co x H x W.                */
+static double conv_in(const double *xc, int H, int W, long u, long v) {
+    return (u >= 0 && u < H && v >= 0 && v < W) ? xc[u * W + v] : 0.0;
+}
+
+void oracle_conv_fwd(const double *x, const double *k, int N, int Ci, int Co, int H, int W,
+                     int kh, int kw, double *y) {
+    const long HW = (long)H * W;
+    const int ph = kh / 2, pw = kw / 2;
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int n = 0; n < N; n++)
+        for (int co = 0; co < Co; co++)
+            for (int yy = 0; yy < H; yy++)
+                for (int xx = 0; xx < W; xx++) {
+                    double s = 0.0;
+                    for (int ci = 0; ci < Ci; ci++)
+                        for (int ry = 0; ry < kh; ry++)
+                            for (int rx = 0; rx < kw; rx++)
+                                s += conv_in(x + ((long)n * Ci + ci) * HW, H, W, yy - ry + ph, xx - rx + pw) *
+                                     k[(((long)co * Ci + ci) * kh + ry) * kw + rx];
+                    y[((long)n * Co + co) * HW + (long)yy * W + xx] = s;
+                }
+}
+
+/* Adjoints (VJP) of the layer above.
+ *   dx: the NAIVE SCATTER of PAPER.md:709-713, "d_input(ro.y - ro.x) +=
+ *       d_output(ro.y) * kernel(ro.x)": every output element adds g*k into the
+ *       input elements it read (the form before scatter-to-gather conversion).
+ *       Race-free: OpenMP over samples, each writes only its own dx slice.
+ *   dk: the plain definition dk[co,ci,ry,rx] = sum_{n,y,x} dy[n,co,y,x] *
+ *       x[n,ci,y-ry+ph,x-rx+pw] (the layer is bilinear in x and k).           */
+void oracle_conv_bwd(const double *x, const double *k, const double *dy, int N, int Ci, int Co,
+                     int H, int W, int kh, int kw, double *dx, double *dk) {
+    const long HW = (long)H * W;
+    const int ph = kh / 2, pw = kw / 2;
+    if (dx) {
+#pragma omp parallel for schedule(static)
+        for (int n = 0; n < N; n++) {
+            double *dxn = dx + (long)n * Ci * HW;
+            memset(dxn, 0, sizeof(double) * (size_t)(Ci * HW));
+            for (int co = 0; co < Co; co++)
+                for (int yy = 0; yy < H; yy++)
+                    for (int xx = 0; xx < W; xx++) {
+                        const double g = dy[((long)n * Co + co) * HW + (long)yy * W + xx];
+                        for (int ci = 0; ci < Ci; ci++)
+                            for (int ry = 0; ry < kh; ry++)
+                                for (int rx = 0; rx < kw; rx++) {
+                                    const long u = yy - ry + ph, v = xx - rx + pw;
+                                    if (u >= 0 && u < H && v >= 0 && v < W)
+                                        dxn[(long)ci * HW + u * W + v] +=
+                                            g * k[(((long)co * Ci + ci) * kh + ry) * kw + rx];
+                                }
+                    }
+        }
+    }
+    if (dk) {
+#pragma omp parallel for collapse(2) schedule(static)
+        for (int co = 0; co < Co; co++)
+            for (int ci = 0; ci < Ci; ci++)
+                for (int ry = 0; ry < kh; ry++)
+                    for (int rx = 0; rx < kw; rx++) {
+                        double s = 0.0;
+                        for (int n = 0; n < N; n++)
+                            for (int yy = 0; yy < H; yy++)
+                                for (int xx = 0; xx < W; xx++)
+                                    s += dy[((long)n * Co + co) * HW + (long)yy * W + xx] *
+                                         conv_in(x + ((long)n * Ci + ci) * HW, H, W, yy - ry + ph, xx - rx + pw);
+                        dk[(((long)co * Ci + ci) * kh + ry) * kw + rx] = s;
+                    }
+    }
+}

@@ -370,3 +370,89 @@ def test_fd_negative_control_at_kink():
     fm[0, 0, 0, 1] -= h
     fd = (np.vdot(oracle.warp_fwd(x, fp), g) - np.vdot(oracle.warp_fwd(x, fm), g)) / (2 * h)
     assert abs(fd - 2.5) < 1e-6            # central: (4 + 1)/2
+
+
+# --------------------------------------------------------------------------- conv layer (§8(f) f1)
+def _conv_case(N, Ci, Co, H, W, kh, kw, seed=0):
+    g = np.random.default_rng(seed)
+    return (g.standard_normal((N, Ci, H, W)), g.standard_normal((Co, Ci, kh, kw)),
+            g.standard_normal((N, Co, H, W)))
+
+
+@pytest.mark.parametrize("dims", [(2, 3, 4, 9, 11, 3, 3), (1, 2, 2, 12, 10, 1, 5), (1, 1, 3, 8, 8, 3, 5),
+                                  (2, 4, 1, 6, 7, 5, 1)])
+def test_conv_vs_torch(dims):
+    """Odd kernels: the layer is torch's conv2d (a cross-correlation) with the kernel
+    flipped in both axes and padding k//2; dx and dk from torch autograd (fp64)."""
+    N, Ci, Co, H, W, kh, kw = dims
+    x, k, dy = _conv_case(*dims)
+    xt = torch.tensor(x, requires_grad=True)
+    kt = torch.tensor(k, requires_grad=True)
+    yt = F.conv2d(xt, kt.flip(-1, -2), padding=(kh // 2, kw // 2))
+    yt.backward(torch.tensor(dy))
+    np.testing.assert_allclose(oracle.conv_fwd(x, k), _np(yt), rtol=1e-12, atol=1e-12)
+    dx, dk = oracle.conv_bwd(x, k, dy)
+    np.testing.assert_allclose(dx, _np(xt.grad), rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(dk, _np(kt.grad), rtol=1e-12, atol=1e-11)
+
+
+def test_conv_1d_is_numpy_convolve():
+    """The paper's 1-D listing output(x) = input(x - r.x) * kernel(r.x)
+    on one row: numpy's full convolution, shifted by the centring offset kw//2."""
+    g = np.random.default_rng(3)
+    sig, ker = g.standard_normal(23), g.standard_normal(5)
+    y = oracle.conv_fwd(sig.reshape(1, 1, 1, -1), ker.reshape(1, 1, 1, -1)).ravel()
+    np.testing.assert_allclose(y, np.convolve(sig, ker, "full")[2:2 + 23], rtol=1e-13, atol=1e-13)
+
+
+def test_conv_closed_forms():
+    """Delta kernel (identity across channels at the centre tap): y = x, dx = dy,
+    dk[co,ci,centre] = <dy_co, x_ci>.  A one-tap kernel at r = (0, 0) reads x at
+    (y + ph, x + pw) and at r = (2, 2) at (y - 1, x - 1), with zero fill."""
+    N, C, H, W = 2, 3, 7, 8
+    x, _, dy = _conv_case(N, C, C, H, W, 3, 3, seed=5)
+    k = np.zeros((C, C, 3, 3))
+    for c in range(C):
+        k[c, c, 1, 1] = 1.0
+    np.testing.assert_allclose(oracle.conv_fwd(x, k), x, rtol=0, atol=1e-15)
+    dx, dk = oracle.conv_bwd(x, k, dy)
+    np.testing.assert_allclose(dx, dy, rtol=0, atol=1e-15)
+    np.testing.assert_allclose(dk[:, :, 1, 1], np.einsum("nohw,nihw->oi", dy, x), rtol=1e-12, atol=1e-12)
+    k1 = np.zeros((1, 1, 3, 3))
+    k1[0, 0, 0, 0] = 1.0
+    y = oracle.conv_fwd(x[:, :1], k1)
+    np.testing.assert_allclose(y[:, 0, :-1, :-1], x[:, 0, 1:, 1:], rtol=0, atol=0)
+    assert np.all(y[:, 0, -1, :] == 0) and np.all(y[:, 0, :, -1] == 0)
+    k2 = np.zeros((1, 1, 3, 3))
+    k2[0, 0, 2, 2] = 1.0
+    y = oracle.conv_fwd(x[:, :1], k2)
+    np.testing.assert_allclose(y[:, 0, 1:, 1:], x[:, 0, :-1, :-1], rtol=0, atol=0)
+    assert np.all(y[:, 0, 0, :] == 0) and np.all(y[:, 0, :, 0] == 0)
+
+
+@pytest.mark.parametrize("ks", [(2, 2), (4, 3), (3, 3)])
+def test_conv_adjoint_identity_and_bilinearity(ks):
+    """<conv(x, k), g> = <x, dx(g)> = <k, dk(g)> (the layer is linear in x and in k),
+    including even kernel sizes, which no library pin covers."""
+    kh, kw = ks
+    x, k, dy = _conv_case(2, 3, 2, 9, 6, kh, kw, seed=7)
+    y = oracle.conv_fwd(x, k)
+    dx, dk = oracle.conv_bwd(x, k, dy)
+    lhs = float((y * dy).sum())
+    assert abs(lhs - float((x * dx).sum())) <= 1e-12 * max(1.0, abs(lhs))
+    assert abs(lhs - float((k * dk).sum())) <= 1e-12 * max(1.0, abs(lhs))
+
+
+def test_conv_brute_force_operator_matrix():
+    """dx = M^T dy with M built column by column from forward calls on basis inputs
+    (even 2 x 4 kernel, non-square image, 2 -> 3 channels)."""
+    N, Ci, Co, H, W, kh, kw = 1, 2, 3, 4, 5, 2, 4
+    _, k, dy = _conv_case(N, Ci, Co, H, W, kh, kw, seed=9)
+    n_in = Ci * H * W
+    M = np.zeros((Co * H * W, n_in))
+    for j in range(n_in):
+        e = np.zeros(n_in)
+        e[j] = 1.0
+        M[:, j] = oracle.conv_fwd(e.reshape(1, Ci, H, W), k).ravel()
+    dx, _ = oracle.conv_bwd(np.zeros((N, Ci, H, W)), k, dy)
+    np.testing.assert_allclose(dx.ravel(), M.T @ dy.ravel(), rtol=1e-13, atol=1e-13)
