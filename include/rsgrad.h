@@ -7,6 +7,8 @@
  *   stn_*    spatial transformer: affine_grid + bilinear grid_sample
  *   warp_*   FlowNet 2.0 per-pixel warp
  *   bslice_* HDRNet bilateral slice-apply
+ * plus, from the §8(f) NEXT rows, the 2-D convolution layer of the paper's
+ * scatter-to-gather example (conv_*).
  * Each *_bwd takes "a buffer representing the adjoints" of the layer output
  * and returns the adjoints of the inputs, i.e. df(x, dy) of
  * PAPER.md:2239-2241.  The exact definitions (the paper prints none; its
@@ -154,9 +156,35 @@ rs_status bslice_bwd(const float *grid, const float *guide, const float *x, cons
                      float *dgrid, float *dguide, float *dx, void *workspace, size_t ws_bytes,
                      rs_stream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * 2-D convolution layer: the scatter-vs-gather example of
+ * PAPER.md:703-733, "output(x) = input(x - r.x) * kernel(r.x)" in 2-D with
+ * channels, centred (R10):
+ *   y[n,co,y,x] = sum_{ci<Ci,ry<kh,rx<kw} x[n,ci, y-ry+kh/2, x-rx+kw/2] * k[co,ci,ry,rx]
+ *   x N x Ci x H x W, k Co x Ci x kh x kw, y N x Co x H x W, zero outside the image.
+ * DEVICE pointers only (k and dk are shared by the whole batch); 1 <= kh, kw <= 7
+ * and Ci small enough that one 32 x 16 tile's Ci input windows fit in shared
+ * memory (Ci <= ~190 at 3x3), else RS_ERR_SHAPE.  opts.padding/align_corners ignored.
+ * ------------------------------------------------------------------------- */
+rs_status conv_fwd(const float *x, const float *k, int N, int Ci, int Co, int H, int W, int kh,
+                   int kw, const rs_opts *opts, float *y, rs_stream_t stream);
+
+/*   dx N x Ci x H x W (nullable): AUTO/GATHER = the converted, sheared gather
+ *   "d_input(x) += d_output(x + r.x) * kernel(r.x)" over zero-padded d_output
+ *   (PAPER.md:721-724), deterministic; SCATTER_ATOMIC = the unconverted scatter
+ *   "d_input(ro.y - ro.x) += d_output(ro.y) * kernel(ro.x)" with atomics
+ *   (memset + red.global.add, not deterministic).
+ *   SCATTER_PRIV is refused (RS_ERR_FLAG).
+ *   dk Co x Ci x kh x kw (nullable): sum over the batch and pixels of dy x shifted x,
+ *   per-block partials in the workspace + a fixed-order sum (deterministic). */
+rs_status conv_bwd(const float *x, const float *k, const float *dy, int N, int Ci, int Co, int H,
+                   int W, int kh, int kw, const rs_opts *opts, float *dx, float *dk,
+                   void *workspace, size_t ws_bytes, rs_stream_t stream);
+
 /* Workspace (bytes) *_bwd wants for these shapes.  layer: 0 = STN (uses
- * N,C,H,W,Ho,Wo), 1 = warp (N,C,H,W), 2 = bslice (N,H,W,D,Gh,Gw); unused
- * arguments are ignored.  Returns 0 for an unknown layer.  DESIGN.md "Workspace". */
+ * N,C,H,W,Ho,Wo), 1 = warp (N,C,H,W), 2 = bslice (N,H,W,D,Gh,Gw), 3 = conv
+ * (N, C = Ci, H, W, D = Co, Gh = kh, Gw = kw); unused arguments are ignored.
+ * Returns 0 for an unknown layer.  DESIGN.md "Workspace". */
 size_t rsgrad_bwd_workspace_bytes(int layer, int N, int C, int H, int W, int Ho, int Wo, int D,
                                   int Gh, int Gw, const rs_opts *opts);
 

@@ -245,6 +245,9 @@ size_t rsgrad_bwd_workspace_bytes(int layer, int N, int C, int H, int W, int Ho,
         case 2:
             if (!pos(N) || !pos(H) || !pos(W) || !pos(D) || !pos(Gh) || !pos(Gw)) return 0;
             return rs::bslice_ws_bytes(N, H, W, D, Gh, Gw);
+        case 3:
+            if (!pos(N) || !pos(C) || !pos(H) || !pos(W) || !pos(D) || !pos(Gh) || !pos(Gw)) return 0;
+            return rs::conv_ws_bytes(N, C, D, H, W, Gh, Gw);
         default:
             return 0;
     }
@@ -462,6 +465,68 @@ rs_status bslice_bwd(const float *grid, const float *guide, const float *x, cons
                            return rs::bslice_bwd_launch(a, o.algo, o.deterministic, ws,
                                                         rs::bslice_ws_bytes(nc, H, W, D, Gh, Gw), t);
                        });
+}
+
+
+// ------------------------------------------------------------------------------ conv
+static rs_status conv_validate(const float *x, const float *k, int N, int Ci, int Co, int H, int W,
+                               int kh, int kw, const rs_opts &o) {
+    if (!x || !k) return fail(RS_ERR_NULL, "conv: x and k are required");
+    if (!pos(N) || !pos(Ci) || !pos(Co) || !pos(H) || !pos(W) || !pos(kh) || !pos(kw))
+        return fail(RS_ERR_SHAPE, "conv: dims must be positive (N=%d Ci=%d Co=%d H=%d W=%d kh=%d kw=%d)", N,
+                    Ci, Co, H, W, kh, kw);
+    if (N > 65535 || (long long)H * W >= (1LL << 31) || (long long)Co * H * W >= (1LL << 40))
+        return fail(RS_ERR_SHAPE, "conv: N <= 65535 and H*W < 2^31");
+    if (!rs::conv_shape_ok(Ci, Co, kh, kw))
+        return fail(RS_ERR_SHAPE, "conv: kh, kw must be <= 7 and Ci input windows must fit in shared memory");
+    if (!is_device_ptr(x) || !is_device_ptr(k))
+        return fail(RS_ERR_FLAG, "conv: device pointers only");
+    return check_opts(o);
+}
+
+rs_status conv_fwd(const float *x, const float *k, int N, int Ci, int Co, int H, int W, int kh, int kw,
+                   const rs_opts *opts, float *y, rs_stream_t stream) {
+    const rs_opts o = resolve(opts);
+    rs_status st = conv_validate(x, k, N, Ci, Co, H, W, kh, kw, o);
+    if (st != RS_OK) return st;
+    if (!y) return fail(RS_ERR_NULL, "conv_fwd: y is required");
+    if (!is_device_ptr(y)) return fail(RS_ERR_FLAG, "conv: device pointers only");
+    rs::ConvArgs a{};
+    a.x = x; a.k = k; a.y = y;
+    a.N = N; a.Ci = Ci; a.Co = Co; a.H = H; a.W = W; a.kh = kh; a.kw = kw;
+    return launched(rs::conv_fwd_launch(a, (cudaStream_t)stream), "conv_fwd");
+}
+
+rs_status conv_bwd(const float *x, const float *k, const float *dy, int N, int Ci, int Co, int H, int W,
+                   int kh, int kw, const rs_opts *opts, float *dx, float *dk, void *workspace, size_t ws_bytes,
+                   rs_stream_t stream) {
+    const rs_opts o = resolve(opts);
+    rs_status st = conv_validate(x, k, N, Ci, Co, H, W, kh, kw, o);
+    if (st != RS_OK) return st;
+    if (!dy) return fail(RS_ERR_NULL, "conv_bwd: dy is required");
+    if (dx && o.algo == RS_ALGO_SCATTER_PRIV)
+        return fail(RS_ERR_FLAG, "conv_bwd: SCATTER_PRIV is not implemented for the conv layer");
+    if (dx && o.algo == RS_ALGO_SCATTER_ATOMIC && o.deterministic)
+        return fail(RS_ERR_FLAG, "conv_bwd: the atomic scatter is not deterministic");
+    if (!is_device_ptr(dy) || (dx && !is_device_ptr(dx)) || (dk && !is_device_ptr(dk)))
+        return fail(RS_ERR_FLAG, "conv: device pointers only");
+    if (!dx && !dk) return ok();
+    cudaStream_t s = (cudaStream_t)stream;
+    rs::ConvArgs a{};
+    a.x = x; a.k = k; a.dy = dy; a.dx = dx; a.dk = dk;
+    a.N = N; a.Ci = Ci; a.Co = Co; a.H = H; a.W = W; a.kh = kh; a.kw = kw;
+    const size_t need = dk ? rs::conv_ws_bytes(N, Ci, Co, H, W, kh, kw) : 0;
+    void *ws = workspace;
+    bool own = false;
+    if (need && (!ws || ws_bytes < need)) {
+        cudaError_t e = lib_malloc(&ws, need, s);
+        if (e != cudaSuccess) return fail(RS_ERR_WORKSPACE, "workspace cudaMallocAsync(%zu): %s", need, cudaGetErrorString(e));
+        own = true;
+        ws_bytes = need;
+    }
+    cudaError_t e = rs::conv_bwd_launch(a, o.algo, ws, ws_bytes, s);
+    if (own) cudaFreeAsync(ws, s);
+    return launched(e, "conv_bwd");
 }
 
 }  // extern "C"

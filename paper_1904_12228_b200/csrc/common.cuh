@@ -296,6 +296,12 @@ struct BsliceArgs {
     int N, H, W, D, Gh, Gw;
 };
 
+struct ConvArgs {
+    const float *x, *k, *dy;
+    float *y, *dx, *dk;
+    int N, Ci, Co, H, W, kh, kw;
+};
+
 // each returns a cudaError_t from the launches; algo is an rs_algo value
 cudaError_t stn_fwd_launch(const StnArgs &a, cudaStream_t s);
 cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *ws, size_t ws_bytes,
@@ -313,4 +319,9 @@ cudaError_t bslice_fwd_launch(const BsliceArgs &a, cudaStream_t s);
 cudaError_t bslice_bwd_launch(const BsliceArgs &a, int algo, int deterministic, void *ws,
                               size_t ws_bytes, cudaStream_t s);
 size_t bslice_ws_bytes(int N, int H, int W, int D, int Gh, int Gw);
+
+bool conv_shape_ok(int Ci, int Co, int kh, int kw);
+cudaError_t conv_fwd_launch(const ConvArgs &a, cudaStream_t s);
+cudaError_t conv_bwd_launch(const ConvArgs &a, int algo, void *ws, size_t ws_bytes, cudaStream_t s);
+size_t conv_ws_bytes(int N, int Ci, int Co, int H, int W, int kh, int kw);
 }  // namespace rs

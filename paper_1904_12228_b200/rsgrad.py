@@ -20,7 +20,7 @@ from . import _build
 
 _PADDING = {"zeros": 0, "border": 1}
 _ALGO = {"auto": 0, "gather": 1, "scatter_priv": 2, "scatter_atomic": 3}
-LAYER_STN, LAYER_WARP, LAYER_BSLICE = 0, 1, 2
+LAYER_STN, LAYER_WARP, LAYER_BSLICE, LAYER_CONV = 0, 1, 2, 3
 
 
 class RsOpts(ctypes.Structure):
@@ -54,7 +54,9 @@ def lib():
         L.warp_bwd.argtypes = [P, P, P, I, I, I, I, O, P, P, P, S, P]
         L.bslice_fwd.argtypes = [P, P, P, I, I, I, I, I, I, O, P, P]
         L.bslice_bwd.argtypes = [P, P, P, P, I, I, I, I, I, I, O, P, P, P, P, S, P]
-        for f in ("stn_fwd", "stn_bwd", "warp_fwd", "warp_bwd", "bslice_fwd", "bslice_bwd"):
+        L.conv_fwd.argtypes = [P, P, I, I, I, I, I, I, I, O, P, P]
+        L.conv_bwd.argtypes = [P, P, P, I, I, I, I, I, I, I, O, P, P, P, S, P]
+        for f in ("stn_fwd", "stn_bwd", "warp_fwd", "warp_bwd", "bslice_fwd", "bslice_bwd", "conv_fwd", "conv_bwd"):
             getattr(L, f).restype = ctypes.c_int
         L.rsgrad_bwd_workspace_bytes.argtypes = [I, I, I, I, I, I, I, I, I, I, O]
         L.rsgrad_bwd_workspace_bytes.restype = S
@@ -280,3 +282,37 @@ class BilateralSlice(torch.autograd.Function):
         dgr, dgd, dx = bslice_bwd(grid, guide, x, dy.contiguous(), need_dgrid=n[0],
                                   need_dguide=n[1], need_dx=n[2])
         return dgr, dgd, dx
+
+
+# ----------------------------------------------------------------------------- conv (§8(f) f1)
+def conv_fwd(x, k, *, out=None):
+    """y = 2-D convolution layer of PAPER.md:703-707 (include/rsgrad.h conv_fwd).
+    CUDA tensors only (the kernel is shared by the batch)."""
+    N, Ci, H, W = x.shape
+    Co, Ci2, kh, kw = k.shape
+    if Ci2 != Ci:
+        raise ValueError("k must be Co x Ci x kh x kw")
+    y = out if out is not None else _like(x, (N, Co, H, W))
+    dev = _device_of(x, k, y)
+    o = _opts()
+    _check(lib().conv_fwd(_ptr(x), _ptr(k), N, Ci, Co, H, W, kh, kw, ctypes.byref(o), _ptr(y), _stream(dev)),
+           "conv_fwd")
+    return y
+
+
+def conv_bwd(x, k, dy, *, algo="auto", deterministic=False, need_dx=True, need_dk=True, out=None):
+    """(dx, dk): dx by the sheared gather (auto/gather) or the atomic scatter
+    (scatter_atomic); dk by per-block partials + fixed-order sum."""
+    N, Ci, H, W = x.shape
+    Co, _, kh, kw = k.shape
+    if out is not None:
+        dx, dk = out
+    else:
+        dx = _like(x, (N, Ci, H, W)) if need_dx else None
+        dk = _like(x, (Co, Ci, kh, kw)) if need_dk else None
+    dev = _device_of(x, k, dy, dx, dk)
+    o = _opts(True, "zeros", algo, deterministic)
+    ws, nws = _workspace(dev, workspace_bytes(LAYER_CONV, N, Ci, H, W, D=Co, Gh=kh, Gw=kw, opts=o))
+    _check(lib().conv_bwd(_ptr(x), _ptr(k), _ptr(dy), N, Ci, Co, H, W, kh, kw, ctypes.byref(o), _ptr(dx), _ptr(dk),
+                          ws, nws, _stream(dev)), "conv_bwd")
+    return dx, dk

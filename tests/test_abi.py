@@ -109,3 +109,16 @@ def test_no_cpu_fallback_without_gpu():
     th = torch.zeros(1, 2, 3)
     with pytest.raises(rsgrad.RsgradError):
         rsgrad.stn_fwd(x, th)
+
+
+def test_conv_validation():
+    """conv_* argument checks that need no GPU: NULLs, non-positive dims, kernel size."""
+    L = rsgrad.lib()
+    fake = ctypes.c_void_p(0x1000)
+    o = _o()
+    assert L.conv_fwd(None, fake, 1, 1, 1, 4, 4, 3, 3, ctypes.byref(o), fake, None) == -1
+    assert L.conv_fwd(fake, fake, 1, 0, 1, 4, 4, 3, 3, ctypes.byref(o), fake, None) == -2
+    assert L.conv_fwd(fake, fake, 1, 1, 1, 4, 4, 9, 3, ctypes.byref(o), fake, None) == -2
+    assert L.conv_bwd(fake, fake, fake, 1, 1, 1, 4, 4, 3, 8, ctypes.byref(o), fake, None, None, 0, None) == -2
+    # d_kernel partials: one per persistent block (<= 296) x Co x Ci x kh x kw floats
+    assert rsgrad.workspace_bytes(3, 16, 16, 256, 256, D=16, Gh=3, Gw=3) == 296 * 16 * 16 * 9 * 4

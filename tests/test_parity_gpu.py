@@ -522,3 +522,59 @@ def test_bslice_bwd_single_cell_and_null_outputs(cuda_device, shape, guide):
     assert torch.equal(a[0], dgr) and torch.equal(a[1], dgd) and torch.equal(a[2], dx)
     b = rsgrad.bslice_bwd(g["grid"], g["guide"], g["x"], g["dy"], need_dguide=False, need_dx=False)
     assert b[1] is None and b[2] is None and torch.equal(b[0], dgr)
+
+
+# ============================================================================ conv (§8(f) f1)
+def _conv_inputs(N, Ci, Co, H, W, kh, kw, seed=0):
+    g = torch.Generator().manual_seed(seed)
+    return (torch.randn(N, Ci, H, W, generator=g, dtype=torch.float64).float(),
+            (torch.randn(Co, Ci, kh, kw, generator=g, dtype=torch.float64) / (Ci * kh * kw) ** 0.5).float(),
+            torch.randn(N, Co, H, W, generator=g, dtype=torch.float64).float())
+
+
+@pytest.mark.parametrize("dims", [(2, 3, 5, 37, 45, 3, 3), (1, 16, 16, 40, 70, 3, 3), (2, 20, 17, 19, 33, 5, 1),
+                                  (1, 1, 1, 1, 1, 3, 3), (1, 9, 3, 16, 40, 1, 5), (1, 4, 6, 23, 29, 2, 4),
+                                  (1, 2, 33, 17, 16, 7, 7)])
+@pytest.mark.parametrize("algo", ["auto", "scatter_atomic"])
+def test_conv_parity(cuda_device, dims, algo):
+    """Forward, d_input (sheared gather = AUTO, or the atomic scatter) and d_kernel vs the
+    fp64 oracle: ragged tiles, channel chunks (Ci > 8), output-channel groups (Co > 16),
+    even and non-square kernels, a 1 x 1 image."""
+    x, k, dy = _conv_inputs(*dims)
+    g = [t.to(cuda_device) for t in (x, k, dy)]
+    y = rsgrad.conv_fwd(g[0], g[1])
+    dx, dk = rsgrad.conv_bwd(g[0], g[1], g[2], algo=algo)
+    xn, kn, dyn = (t.double().numpy() for t in (x, k, dy))
+    assert_close(_np(y), oracle.conv_fwd(xn, kn), "fwd", "y")
+    rdx, rdk = oracle.conv_bwd(xn, kn, dyn)
+    assert_close(_np(dx), rdx, "grad", f"dx[{algo}]")
+    assert_close(_np(dk), rdk, "grad", "dk")
+
+
+def test_conv_gather_deterministic_and_null_outputs(cuda_device):
+    x, k, dy = (t.to(cuda_device) for t in _conv_inputs(2, 16, 16, 64, 64, 3, 3, seed=1))
+    a = rsgrad.conv_bwd(x, k, dy, deterministic=True)
+    b = rsgrad.conv_bwd(x, k, dy, deterministic=True)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+    only_dk = rsgrad.conv_bwd(x, k, dy, need_dx=False)
+    assert only_dk[0] is None and torch.equal(only_dk[1], a[1])
+    only_dx = rsgrad.conv_bwd(x, k, dy, need_dk=False)
+    assert only_dx[1] is None and torch.equal(only_dx[0], a[0])
+    with pytest.raises(rsgrad.RsgradError):
+        rsgrad.conv_bwd(x, k, dy, algo="scatter_priv")
+
+
+def test_conv_paper_shape_sampled(cuda_device):
+    """The paper's 16 x 16 x 256 x 256 conv layer, 3 x 3 kernel: dx from the
+    gather and from the atomic scatter agree everywhere; sampled elements and dk vs the
+    oracle on a 2-sample slice (dk rescaled: it sums over the batch)."""
+    x, k, dy = _conv_inputs(16, 16, 16, 256, 256, 3, 3, seed=2)
+    g = [t.to(cuda_device) for t in (x, k, dy)]
+    dxg, dkg = rsgrad.conv_bwd(*g)
+    dxa, _ = rsgrad.conv_bwd(*g, algo="scatter_atomic", need_dk=False)
+    assert_close(_np(dxa), _np(dxg).astype(np.float64), "grad", "dx atomic vs gather")
+    xs, dys = x[:2].double().numpy(), dy[:2].double().numpy()
+    rdx, _ = oracle.conv_bwd(xs, k.double().numpy(), dys, need_dk=False)
+    assert_close(_np(dxg[:2]), rdx, "grad", "dx[:2]")
+    _, rdk = oracle.conv_bwd(x.double().numpy(), k.double().numpy(), dy.double().numpy(), need_dx=False)
+    assert_close(_np(dkg), rdk, "grad", "dk")
