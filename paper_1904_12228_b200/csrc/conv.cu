@@ -18,9 +18,9 @@
 //                    kernel(ro.x) with red.global.add: the
 //                    "general scatter with atomics" fallback.
 //   conv_dk_partial  d_kernel = sum over pixels of dy x shifted x: persistent blocks,
-//                    per-block fp32 partials in registers (thread = 4 output channels
-//                    x one (ci, ry) x all rx), then
-//   conv_dk_finalize fixed-order sum of the block partials (deterministic).
+//                    per-block partials in registers (thread = 4 output channels x one
+//                    (ci, ry) x all rx; fp32 per 32-px tile row, fp64 across rows), then
+//   conv_dk_finalize fixed-order fp64 sum of the block partials (deterministic).
 #include "common.cuh"
 
 namespace rs {
@@ -152,7 +152,7 @@ constexpr int kKMax = 7;  // kw bound of the d_kernel register block
 // Persistent blocks over (sample, 32 x 16 tile); task = (4 output channels, ci, ry):
 // 4 x kw sums in registers across all the block's tiles, one partial per block.
 __global__ void __launch_bounds__(kCT)
-    conv_dk_partial(const float *__restrict__ x, const float *__restrict__ dy, float *__restrict__ part, int N, int Ci,
+    conv_dk_partial(const float *__restrict__ x, const float *__restrict__ dy, double *__restrict__ part, int N, int Ci,
                     int Co, int H, int W, int kh, int kw, int tiles_x, int tiles) {
     extern __shared__ __align__(16) float csm[];
     const int SH = kTY + kh - 1, SW = kTX + kw - 1, SP = SW + 1;
@@ -166,11 +166,13 @@ __global__ void __launch_bounds__(kCT)
     const bool act = task < ntask;
     const int cog = act ? task % CO4 : 0, rest = act ? task / CO4 : 0;
     const int ry = rest % kh, ci = rest / kh;
-    float acc[4][kKMax];
+    // fp32 sums over one tile row (32 px), folded into fp64 sums per row: the rounding
+    // of a 10^6-term sum stays far below the rms-scaled tolerance (Q14)
+    double accd[4][kKMax];
 #pragma unroll
     for (int t = 0; t < 4; t++)
 #pragma unroll
-        for (int r = 0; r < kKMax; r++) acc[t][r] = 0.f;
+        for (int r = 0; r < kKMax; r++) accd[t][r] = 0.0;
     const int per_sample = tiles;
     for (int tt = blockIdx.x; tt < N * per_sample; tt += gridDim.x) {
         const int n = tt / per_sample, tl = tt - n * per_sample;
@@ -198,42 +200,52 @@ __global__ void __launch_bounds__(kCT)
         if (act) {
             // pixel (yl, xl) reads x at window (yl + kh-1-ry, xl + kw-1-rx)
             const float *xr = sx + (ci * SH + (kh - 1 - ry)) * SP + (kw - 1);
-            for (int p = 0; p < kTY * kTX; p++) {
-                const int yl = p / kTX, xl = p % kTX;
-                const float4 g = sg[p * CO4 + cog];
-                const float *xp = xr + yl * SP + xl;
+            for (int yl = 0; yl < kTY; yl++) {
+                float acc[4][kKMax];
 #pragma unroll
-                for (int rx = 0; rx < kKMax; rx++) {
-                    if (rx < kw) {
-                        const float v = xp[-rx];
-                        acc[0][rx] = fmaf(g.x, v, acc[0][rx]);
-                        acc[1][rx] = fmaf(g.y, v, acc[1][rx]);
-                        acc[2][rx] = fmaf(g.z, v, acc[2][rx]);
-                        acc[3][rx] = fmaf(g.w, v, acc[3][rx]);
+                for (int t = 0; t < 4; t++)
+#pragma unroll
+                    for (int r = 0; r < kKMax; r++) acc[t][r] = 0.f;
+                for (int xl = 0; xl < kTX; xl++) {
+                    const float4 g = sg[(yl * kTX + xl) * CO4 + cog];
+                    const float *xp = xr + yl * SP + xl;
+#pragma unroll
+                    for (int rx = 0; rx < kKMax; rx++) {
+                        if (rx < kw) {
+                            const float v = xp[-rx];
+                            acc[0][rx] = fmaf(g.x, v, acc[0][rx]);
+                            acc[1][rx] = fmaf(g.y, v, acc[1][rx]);
+                            acc[2][rx] = fmaf(g.z, v, acc[2][rx]);
+                            acc[3][rx] = fmaf(g.w, v, acc[3][rx]);
+                        }
                     }
                 }
+#pragma unroll
+                for (int t = 0; t < 4; t++)
+#pragma unroll
+                    for (int r = 0; r < kKMax; r++) accd[t][r] += (double)acc[t][r];
             }
         }
     }
     if (!act) return;
     const long long E = (long long)Co * Ci * kh * kw;
-    float *pb = part + (long long)blockIdx.x * E;
+    double *pb = part + (long long)blockIdx.x * E;
 #pragma unroll
     for (int t = 0; t < 4; t++) {
         const int co = 4 * cog + t;
         if (co >= Co) continue;
 #pragma unroll
         for (int rx = 0; rx < kKMax; rx++)
-            if (rx < kw) pb[(((long long)co * Ci + ci) * kh + ry) * kw + rx] = acc[t][rx];
+            if (rx < kw) pb[(((long long)co * Ci + ci) * kh + ry) * kw + rx] = accd[t][rx];
     }
 }
 
-__global__ void conv_dk_finalize(const float *__restrict__ part, float *__restrict__ dk, int nb, long long E) {
+__global__ void conv_dk_finalize(const double *__restrict__ part, float *__restrict__ dk, int nb, long long E) {
     const long long e = (long long)blockIdx.x * kCT + threadIdx.x;
     if (e >= E) return;
-    float s = 0.f;
+    double s = 0.0;
     for (int b = 0; b < nb; b++) s += part[(long long)b * E + e];
-    dk[e] = s;
+    dk[e] = (float)s;
 }
 
 size_t direct_smem(int kh, int kw) {
@@ -269,7 +281,7 @@ bool conv_shape_ok(int Ci, int Co, int kh, int kw) {
 }
 
 size_t conv_ws_bytes(int N, int Ci, int Co, int H, int W, int kh, int kw) {
-    return sizeof(float) * (size_t)dk_blocks(N, H, W) * Co * Ci * kh * kw;
+    return sizeof(double) * (size_t)dk_blocks(N, H, W) * Co * Ci * kh * kw;
 }
 
 cudaError_t conv_fwd_launch(const ConvArgs &a, cudaStream_t s) {
@@ -304,7 +316,7 @@ cudaError_t conv_bwd_launch(const ConvArgs &a, int algo, void *ws, size_t ws_byt
         const int ntask = ((a.Co + 3) / 4) * a.Ci * a.kh;
         const size_t sm = dk_smem(a.Ci, a.Co, a.kh, a.kw);
         if (sm > 48 * 1024) cudaFuncSetAttribute(conv_dk_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        float *part = (float *)ws;
+        double *part = (double *)ws;
         conv_dk_partial<<<dim3(nb, 1, (ntask + kCT - 1) / kCT), kCT, sm, s>>>(a.x, a.dy, part, a.N, a.Ci, a.Co, a.H,
                                                                               a.W, a.kh, a.kw, tiles_x, tiles);
         note_launch();

@@ -314,5 +314,5 @@ def conv_bwd(x, k, dy, *, algo="auto", deterministic=False, need_dx=True, need_d
     o = _opts(True, "zeros", algo, deterministic)
     ws, nws = _workspace(dev, workspace_bytes(LAYER_CONV, N, Ci, H, W, D=Co, Gh=kh, Gw=kw, opts=o))
     _check(lib().conv_bwd(_ptr(x), _ptr(k), _ptr(dy), N, Ci, Co, H, W, kh, kw, ctypes.byref(o), _ptr(dx), _ptr(dk),
-                          ws, nws, _stream(dev)), "conv_bwd")
+                          None if ws is None else ctypes.c_void_p(ws.data_ptr()), nws, _stream(dev)), "conv_bwd")
     return dx, dk

@@ -1,5 +1,3 @@
-timeout 600 python -m pytest tests -m gpu -x -q -k "bslice" > gpurun_out/pytest_bs.log 2>&1; echo pytest=$?
-for v in tiled staged; do echo "== $v"; RSGRAD_BSLICE_BWD=$v python scripts/bench_layer.py 16 5 bslice_bwd; done > gpurun_out/bs_ab.txt 2>&1
-cat gpurun_out/bs_ab.txt; tail -3 gpurun_out/pytest_bs.log
-bash scripts/gpurun_prof.sh bss bslice_bwd_staged 4
-rm -f gpurun_out/*.ncu-rep
+timeout 600 python -m pytest tests -m gpu -x -q -k "conv" > gpurun_out/pytest_conv.log 2>&1; echo pytest=$?
+tail -15 gpurun_out/pytest_conv.log
+python scripts/bench_next.py > gpurun_out/next.json 2>&1; cat gpurun_out/next.json
