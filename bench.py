@@ -237,6 +237,9 @@ def paper_shapes(rs, peak):
          synth.bslice_inputs(4, 1024, 1024, 8, 16, 16, cfg=4, device=dev)),
         ("bslice_4x1024x1024_g32x32x8", "bslice", 3,
          synth.bslice_inputs(4, 1024, 1024, 8, 32, 32, cfg=4, device=dev)),
+        # §8(f) f2: the paper's high-resolution case (batch unstated, 4 as above)
+        ("bslice_4x2048x2048_g64x64x8", "bslice", 3,
+         synth.bslice_inputs(4, 2048, 2048, 8, 64, 64, cfg=4, device=dev)),
     ]
     for name, layer, C, i in cases:
         if layer == "stn":
@@ -256,7 +259,7 @@ def paper_shapes(rs, peak):
             y = torch.empty_like(i["x"])
             fwd = lambda: rs.bslice_fwd(i["grid"], i["guide"], i["x"], out=y)  # noqa: E731
             bwd = lambda: rs.bslice_bwd(i["grid"], i["guide"], i["x"], i["dy"], out=o)  # noqa: E731
-            P = 4 * 1024 * 1024
+            P = i["x"].shape[0] * i["x"].shape[2] * i["x"].shape[3]
         times = {"fwd": [], "bwd": []}
         for rep in range(25):
             for kind, fn in (("fwd", fwd), ("bwd", bwd)):
@@ -279,6 +282,67 @@ def paper_shapes(rs, peak):
         }
     del fl
     return {"l2": "flushed (256 MB write) before every call; median of 20", "cases": out}
+
+
+# --------------------------------------------------------------------------- §8(f) NEXT rows
+def fp32_peak_tflops():
+    """FP32 FMA peak from the unit counts and clock (B200_PROFILING.md: 148 SMs x 128
+    FP32 lanes x 2 flop/FMA x max SM clock)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f)["sm_max_mhz"])
+    except Exception:  # noqa: BLE001
+        mhz = 1965.0
+    return 148 * 128 * 2 * mhz * 1e6 / 1e12
+
+
+def next_rows(rs, peak):
+    """SURVEY §8(f) rows at the paper's shapes, each call timed alone after an L2 flush
+    (median of 10).  f1: the conv layer of PAPER.md:733 (16 x 16 x 256 x 256, 3 x 3
+    chosen: the paper does not state the kernel size), d_input by the converted gather
+    vs the atomic scatter; the paper's 68 ms / 6 ms (GPU unstated) are context only."""
+    dev = torch.device("cuda")
+    fl = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+
+    def med(fn, reps=10):
+        fn()
+        ts = []
+        for _ in range(reps):
+            flush_l2(fl)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e-3)
+        return statistics.median(ts)
+
+    out = {}
+    g = torch.Generator(device=dev).manual_seed(733)
+    N, C, H, W, k = 16, 16, 256, 256, 3
+    x = torch.randn(N, C, H, W, device=dev, generator=g)
+    kk = torch.randn(C, C, k, k, device=dev, generator=g) / (C * k * k) ** 0.5
+    dy = torch.randn(N, C, H, W, device=dev, generator=g)
+    y, dx, dk = torch.empty_like(x), torch.empty_like(x), torch.empty_like(kk)
+    tf = med(lambda: rs.conv_fwd(x, kk, out=y))
+    tg = med(lambda: rs.conv_bwd(x, kk, dy, out=(dx, dk)))
+    tdx = med(lambda: rs.conv_bwd(x, kk, dy, need_dk=False, out=(dx, None)))
+    tdk = med(lambda: rs.conv_bwd(x, kk, dy, need_dx=False, out=(None, dk)))
+    ta = med(lambda: rs.conv_bwd(x, kk, dy, algo="scatter_atomic", need_dk=False, out=(dx, None)), reps=5)
+    flops = 2.0 * N * H * W * C * C * k * k
+    fp = fp32_peak_tflops()
+    out["f1_conv_16x16x256x256_k3"] = {
+        "fwd_us": round(tf * 1e6, 1), "bwd_us": round(tg * 1e6, 1),
+        "bwd_dx_gather_us": round(tdx * 1e6, 1), "bwd_dx_atomic_us": round(ta * 1e6, 1),
+        "bwd_dk_us": round(tdk * 1e6, 1), "atomic_over_gather": round(ta / tdx, 2),
+        "paper_atomic_over_gather": round(68.0 / 6.0, 2),
+        "roofline": {"bound": "alu", "unit": "TFLOP/s", "peak": round(fp, 1),
+                     "peak_source": "148 SMs x 128 FP32 FMA/clk x 2 x sm_max_mhz (B200_PROFILING.md unit counts)",
+                     "fwd_frac": round(flops / tf / 1e12 / fp, 3), "dx_gather_frac": round(flops / tdx / 1e12 / fp, 3),
+                     "dk_frac": round(flops / tdk / 1e12 / fp, 3)},
+    }
+    del x, dy, y, dx, fl
+    return {"l2": "flushed (256 MB write) before every call; median of 10", "rows": out}
 
 
 # --------------------------------------------------------------------------- cpu baseline
@@ -359,6 +423,7 @@ def main():
     ap.add_argument("--no-paper-shapes", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-next", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup(args)
@@ -450,6 +515,8 @@ def main():
         line["cpu_baseline"] = cpu_baseline(s, w, b)
     if world == 1 and not args.no_paper_shapes:
         line["paper_shapes"] = paper_shapes(rs, peak)
+    if world == 1 and not args.no_next:
+        line["next_rows"] = next_rows(rs, peak)
     print(json.dumps(line), flush=True)
 
 

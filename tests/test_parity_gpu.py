@@ -272,6 +272,21 @@ def test_bslice_paper_grid_32(cuda_device):
     assert_close(_np(dgd), rgd, "grad", "dguide")
 
 
+def test_bslice_paper_highres_2048_g64(cuda_device):
+    """the paper's high-resolution case, 2048^2 with a 64x64x8 grid
+    (PAPER.md:42), one sample, every element of the forward and all gradients."""
+    inp = synth.bslice_inputs(1, 2048, 2048, 8, 64, 64, cfg=4)
+    g = _cuda(inp, cuda_device)
+    y = rsgrad.bslice_fwd(g["grid"], g["guide"], g["x"])
+    dgr, dgd, dx = rsgrad.bslice_bwd(g["grid"], g["guide"], g["x"], g["dy"])
+    gr, gd, x, dy = (inp[k].double().numpy() for k in ("grid", "guide", "x", "dy"))
+    assert_close(_np(y), oracle.bslice_fwd(gr, gd, x), "fwd", "y")
+    rgr, rgd, rdx = oracle.bslice_bwd(gr, gd, x, dy)
+    assert_close(_np(dgr), rgr, "grad", "dgrid")
+    assert_close(_np(dgd), rgd, "grad", "dguide")
+    assert_close(_np(dx), rdx, "grad", "dx")
+
+
 # ============================================================================ configs[4] sampled
 def test_sweep_config_sampled(cuda_device):
     """configs[4]: batch 64 @ 1024^2 per layer in the bench launch configuration;
