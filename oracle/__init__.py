@@ -51,6 +51,9 @@ def _load():
         lib.oracle_bslice_bwd.argtypes = [P, P, P, P, I, I, I, I, I, I, P, P, P]
         lib.oracle_conv_fwd.argtypes = [P, P, I, I, I, I, I, I, I, P]
         lib.oracle_conv_bwd.argtypes = [P, P, P, I, I, I, I, I, I, I, P, P]
+        lib.oracle_convloss_grad.argtypes = [P, P, P, I, I, I, I, I, P]
+        lib.oracle_upsample4_fwd.argtypes = [P, I, I, I, I, P]
+        lib.oracle_upsample4_bwd.argtypes = [P, I, I, I, I, P]
         lib.oracle_set_threads.argtypes = [I]
         lib.oracle_get_threads.restype = I
         _lib = lib
@@ -158,3 +161,30 @@ def conv_bwd(x, k, dy, need_dx=True, need_dk=True):
     dk = np.empty_like(k) if need_dk else None
     _load().oracle_conv_bwd(_p(x), _p(k), _p(dy), N, Ci, Co, H, W, kh, kw, _p(dx), _p(dk))
     return dx, dk
+
+
+# ----------------------------------------------------------------------------- §8(f) f4
+def convloss_grad(inp, k, target):
+    """d_in of loss = sum (conv(in, k) - target)^2, single channel."""
+    inp, k, target = _f64(inp), _f64(k), _f64(target)
+    N, H, W = inp.shape
+    kh, kw = k.shape
+    d = np.empty_like(inp)
+    _load().oracle_convloss_grad(_p(inp), _p(k), _p(target), N, H, W, kh, kw, _p(d))
+    return d
+
+
+def upsample4_fwd(x):
+    x = _f64(x)
+    N, C, H, W = x.shape
+    y = np.empty((N, C, 4 * H, 4 * W), np.float64)
+    _load().oracle_upsample4_fwd(_p(x), N, C, H, W, _p(y))
+    return y
+
+
+def upsample4_bwd(dy):
+    dy = _f64(dy)
+    N, C, Ho, Wo = dy.shape
+    dx = np.empty((N, C, Ho // 4, Wo // 4), np.float64)
+    _load().oracle_upsample4_bwd(_p(dy), N, C, Ho // 4, Wo // 4, _p(dx))
+    return dx

@@ -530,3 +530,42 @@ void oracle_conv_bwd(const double *x, const double *k, const double *dy, int N, 
                     }
     }
 }
+
+/* ------------------------------------------------------------------ */
+/* Checkpointing study          */
+/* ------------------------------------------------------------------ */
+/* convolved = in (*) kernel, loss = sum (convolved - target)^2,
+ * d_in = "a cross correlation of 2*(convolved-target) with kernel".
+ * Single channel, the layer of oracle_conv_fwd with Ci = Co = 1 (zero padding,
+ * centred; R11).  Written as its definition: the residual
+ * r = 2 (conv(in) - target), then the naive-scatter adjoint of the convolution.
+ * in, target, d_in: N x H x W; k: kh x kw.                                    */
+void oracle_convloss_grad(const double *in, const double *k, const double *target, int N, int H,
+                          int W, int kh, int kw, double *d_in) {
+    const long HW = (long)H * W;
+    double *r = (double *)malloc(sizeof(double) * (size_t)(N * HW));
+    oracle_conv_fwd(in, k, N, 1, 1, H, W, kh, kw, r);
+    for (long i = 0; i < N * HW; i++) r[i] = 2.0 * (r[i] - target[i]);
+    oracle_conv_bwd(in, k, r, N, 1, 1, H, W, kh, kw, d_in, NULL);
+    free(r);
+}
+
+/* Upsampling by 4: output(x, y) = input(x/4, y/4), integer
+ * division; x: N x C x H x W, y: N x C x 4H x 4W.  Adjoint as the naive scatter
+ * d_input(x/4, y/4) += d_output(x, y).                                        */
+void oracle_upsample4_fwd(const double *x, int N, int C, int H, int W, double *y) {
+    const long Wo = 4L * W, Ho = 4L * H;
+    for (long nc = 0; nc < (long)N * C; nc++)
+        for (long yy = 0; yy < Ho; yy++)
+            for (long xx = 0; xx < Wo; xx++)
+                y[(nc * Ho + yy) * Wo + xx] = x[(nc * H + yy / 4) * W + xx / 4];
+}
+
+void oracle_upsample4_bwd(const double *dy, int N, int C, int H, int W, double *dx) {
+    const long Wo = 4L * W, Ho = 4L * H;
+    memset(dx, 0, sizeof(double) * (size_t)N * C * H * W);
+    for (long nc = 0; nc < (long)N * C; nc++)
+        for (long yy = 0; yy < Ho; yy++)
+            for (long xx = 0; xx < Wo; xx++)
+                dx[(nc * H + yy / 4) * W + xx / 4] += dy[(nc * Ho + yy) * Wo + xx];
+}

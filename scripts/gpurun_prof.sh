@@ -2,9 +2,11 @@
 # ncu --set full of the matching kernels of one bench_layer pass (NB samples), then
 # the summary table, per-line and per-SASS hot spots, written to gpurun_out/ (the
 # .ncu-rep itself is removed when large so the merge back stays small)
+# (PROF_CMD overrides the profiled command, e.g. "python scripts/bench_next.py")
 TAG=$1; KR=$2; NB=$3; shift 3
+CMD=${PROF_CMD:-python scripts/bench_layer.py $NB 1}
 env "$@" ncu --set full --import-source on --clock-control none -k "regex:$KR" -c 4 -f -o gpurun_out/$TAG \
-    python scripts/bench_layer.py $NB 1 > gpurun_out/$TAG.log 2>&1
+    $CMD > gpurun_out/$TAG.log 2>&1
 python scripts/ncu_summary.py gpurun_out/$TAG.ncu-rep gpurun_out/$TAG.md >> gpurun_out/$TAG.log 2>&1
 for k in $(ncu -i gpurun_out/$TAG.ncu-rep --page raw --csv 2>/dev/null | python -c "
 import csv,sys,re

@@ -456,3 +456,35 @@ def test_conv_brute_force_operator_matrix():
         M[:, j] = oracle.conv_fwd(e.reshape(1, Ci, H, W), k).ravel()
     dx, _ = oracle.conv_bwd(np.zeros((N, Ci, H, W)), k, dy)
     np.testing.assert_allclose(dx.ravel(), M.T @ dy.ravel(), rtol=1e-13, atol=1e-13)
+
+
+# --------------------------------------------------------------------------- checkpointing study (§8(f) f4)
+@pytest.mark.parametrize("ks", [(1, 5), (3, 5), (2, 2)])
+def test_convloss_grad_vs_torch_autograd(ks):
+    """d_in of sum (conv(in, k) - target)^2 = torch autograd of the
+    same loss built from conv2d with the flipped kernel (even kernels: asymmetric pad)."""
+    kh, kw = ks
+    g = np.random.default_rng(11)
+    N, H, W = 2, 13, 17
+    inp, k, tgt = g.standard_normal((N, H, W)), g.standard_normal((kh, kw)), g.standard_normal((N, H, W))
+    it = torch.tensor(inp[:, None], requires_grad=True)
+    # y[y,x] = sum_r in[y - ry + kh//2, x - rx + kw//2] k[r]: pad top kh//2, bottom kh-1-kh//2
+    pt = F.pad(it, (kw - 1 - kw // 2, kw // 2, kh - 1 - kh // 2, kh // 2))
+    conv = F.conv2d(pt, torch.tensor(k).flip(0, 1)[None, None])
+    loss = ((conv[:, 0] - torch.tensor(tgt)) ** 2).sum()
+    loss.backward()
+    np.testing.assert_allclose(oracle.convloss_grad(inp, k, tgt), _np(it.grad)[:, 0], rtol=1e-12, atol=1e-11)
+
+
+def test_upsample4_vs_torch():
+    """output(x) = input(x/4) is nearest upsampling by 4; its adjoint
+    sums each 4 x 4 block (torch autograd)."""
+    g = np.random.default_rng(12)
+    x, dy = g.standard_normal((2, 3, 5, 7)), g.standard_normal((2, 3, 20, 28))
+    xt = torch.tensor(x, requires_grad=True)
+    yt = F.interpolate(xt, scale_factor=4, mode="nearest")
+    yt.backward(torch.tensor(dy))
+    np.testing.assert_array_equal(oracle.upsample4_fwd(x), _np(yt))
+    np.testing.assert_allclose(oracle.upsample4_bwd(dy), _np(xt.grad), rtol=1e-14, atol=1e-14)
+    np.testing.assert_allclose(oracle.upsample4_bwd(dy), dy.reshape(2, 3, 5, 4, 7, 4).sum(axis=(3, 5)),
+                               rtol=1e-14, atol=1e-14)
