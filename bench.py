@@ -341,7 +341,34 @@ def next_rows(rs, peak):
                      "fwd_frac": round(flops / tf / 1e12 / fp, 3), "dx_gather_frac": round(flops / tdx / 1e12 / fp, 3),
                      "dk_frac": round(flops / tdk / 1e12 / fp, 3)},
     }
-    del x, dy, y, dx, fl
+    del x, dy, y, dx
+    # f4: the checkpointing study, 2560 x 1600, kernels 1 x 5 and 3 x 5;
+    # the paper's CPU times (ms: inline / root / compute_at) are context only
+    paper_ms = {(1, 5): (5.6, 10.1, 9.7), (3, 5): (66.2, 18.7, 12.3)}
+    H, W = 1600, 2560
+    inp = torch.rand(1, H, W, device=dev, generator=g)
+    tgt = torch.rand(1, H, W, device=dev, generator=g)
+    d = torch.empty_like(inp)
+    for kh, kw in ((1, 5), (3, 5)):
+        kk = torch.randn(kh, kw) / (kh * kw) ** 0.5
+        r = {}
+        for sch in ("inline", "root", "at"):
+            t = med(lambda: rs.convloss_grad(inp, kk, tgt, schedule=sch, out=d))  # noqa: B023
+            r[f"{sch}_us"] = round(t * 1e6, 1)
+            # compulsory bytes: in + target read, d_in written (root adds R write + read)
+            r[f"{sch}_hbm_frac"] = round(12.0 * H * W / t / 1e9 / peak, 3)
+        r["paper_cpu_ms_inline_root_at"] = paper_ms[(kh, kw)]
+        out[f"f4_convloss_2560x1600_k{kh}x{kw}"] = r
+    xu = torch.randn(1, 3, 400, 640, device=dev, generator=g)
+    yu = torch.empty(1, 3, 1600, 2560, device=dev)
+    dxu = torch.empty_like(xu)
+    tu_f = med(lambda: rs.upsample4_fwd(xu, out=yu))
+    tu_b = med(lambda: rs.upsample4_bwd(yu, out=dxu))
+    bu = 4.0 * xu.numel() * 17  # 1 + 16 floats per input element
+    out["f4_upsample4_1x3x400x640"] = {"fwd_us": round(tu_f * 1e6, 1), "bwd_us": round(tu_b * 1e6, 1),
+                                       "fwd_hbm_frac": round(bu / tu_f / 1e9 / peak, 3),
+                                       "bwd_hbm_frac": round(bu / tu_b / 1e9 / peak, 3)}
+    del fl
     return {"l2": "flushed (256 MB write) before every call; median of 10", "rows": out}
 
 

@@ -181,9 +181,34 @@ rs_status conv_bwd(const float *x, const float *k, const float *dy, int N, int C
                    int W, int kh, int kw, const rs_opts *opts, float *dx, float *dk,
                    void *workspace, size_t ws_bytes, rs_stream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * Checkpointing study: the gradient of
+ *   loss = sum (conv(in, k) - target)^2,  conv = the conv_* layer with Ci = Co = 1,
+ *   d_in(u) = sum_r k(r) R(u + r - p),  R = 2 (conv(in) - target), zero outside,
+ * "a cross correlation of 2*(convolved-target) with kernel".
+ *   in, target, d_in  N x H x W (device);  k  kh x kw, HOST pointer (copied into the
+ *   kernel parameters; 1 <= kh, kw <= 7).
+ *   schedule  RS_SCHED_ROOT   R written to the workspace, then gathered (compute_root)
+ *             RS_SCHED_INLINE R recomputed at every tap (compute_inline)
+ *             RS_SCHED_AT     R per 32 x 32 tile of d_in in shared memory (compute_at)
+ * The paper's 2560 x 1600 image with 1 x 5 and 3 x 5 kernels.
+ * ------------------------------------------------------------------------- */
+typedef enum { RS_SCHED_ROOT = 0, RS_SCHED_INLINE = 1, RS_SCHED_AT = 2 } rs_schedule;
+rs_status convloss_grad(const float *in, const float *k, const float *target, int N, int H, int W,
+                        int kh, int kw, rs_schedule schedule, float *d_in, void *workspace,
+                        size_t ws_bytes, rs_stream_t stream);
+
+/* Upsampling by 4, output(x, y) = input(x/4, y/4):
+ *   x N x C x H x W -> y N x C x 4H x 4W;  the adjoint is the converted gather
+ *   d_input(x) = sum_{r < 4 x 4} d_output(4x + r), deterministic.
+ * Device pointers only. */
+rs_status upsample4_fwd(const float *x, int N, int C, int H, int W, float *y, rs_stream_t stream);
+rs_status upsample4_bwd(const float *dy, int N, int C, int H, int W, float *dx, rs_stream_t stream);
+
 /* Workspace (bytes) *_bwd wants for these shapes.  layer: 0 = STN (uses
  * N,C,H,W,Ho,Wo), 1 = warp (N,C,H,W), 2 = bslice (N,H,W,D,Gh,Gw), 3 = conv
- * (N, C = Ci, H, W, D = Co, Gh = kh, Gw = kw); unused arguments are ignored.
+ * (N, C = Ci, H, W, D = Co, Gh = kh, Gw = kw), 4 = convloss_grad (N, H, W: the
+ * RS_SCHED_ROOT residual); unused arguments are ignored.
  * Returns 0 for an unknown layer.  DESIGN.md "Workspace". */
 size_t rsgrad_bwd_workspace_bytes(int layer, int N, int C, int H, int W, int Ho, int Wo, int D,
                                   int Gh, int Gw, const rs_opts *opts);

@@ -248,6 +248,9 @@ size_t rsgrad_bwd_workspace_bytes(int layer, int N, int C, int H, int W, int Ho,
         case 3:
             if (!pos(N) || !pos(C) || !pos(H) || !pos(W) || !pos(D) || !pos(Gh) || !pos(Gw)) return 0;
             return rs::conv_ws_bytes(N, C, D, H, W, Gh, Gw);
+        case 4:
+            if (!pos(N) || !pos(H) || !pos(W)) return 0;
+            return rs::convloss_ws_bytes(N, H, W);
         default:
             return 0;
     }
@@ -527,6 +530,53 @@ rs_status conv_bwd(const float *x, const float *k, const float *dy, int N, int C
     cudaError_t e = rs::conv_bwd_launch(a, o.algo, ws, ws_bytes, s);
     if (own) cudaFreeAsync(ws, s);
     return launched(e, "conv_bwd");
+}
+
+// ------------------------------------------------------------------------------ f4
+rs_status convloss_grad(const float *in, const float *k, const float *target, int N, int H, int W, int kh,
+                        int kw, rs_schedule schedule, float *d_in, void *workspace, size_t ws_bytes,
+                        rs_stream_t stream) {
+    if (!in || !k || !target || !d_in) return fail(RS_ERR_NULL, "convloss_grad: in, k, target, d_in are required");
+    if (!pos(N) || !pos(H) || !pos(W) || !pos(kh) || !pos(kw) || kh > 7 || kw > 7)
+        return fail(RS_ERR_SHAPE, "convloss_grad: positive dims, 1 <= kh, kw <= 7 (N=%d H=%d W=%d kh=%d kw=%d)", N,
+                    H, W, kh, kw);
+    if (N > 65535 || (long long)H * W >= (1LL << 31)) return fail(RS_ERR_SHAPE, "convloss_grad: H*W < 2^31");
+    if (schedule != RS_SCHED_ROOT && schedule != RS_SCHED_INLINE && schedule != RS_SCHED_AT)
+        return fail(RS_ERR_FLAG, "convloss_grad: unknown schedule %d", (int)schedule);
+    if (!is_device_ptr(in) || !is_device_ptr(target) || !is_device_ptr(d_in))
+        return fail(RS_ERR_FLAG, "convloss_grad: in, target, d_in must be device pointers");
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t need = schedule == RS_SCHED_ROOT ? rs::convloss_ws_bytes(N, H, W) : 0;
+    void *ws = workspace;
+    bool own = false;
+    if (need && (!ws || ws_bytes < need)) {
+        cudaError_t e = lib_malloc(&ws, need, s);
+        if (e != cudaSuccess) return fail(RS_ERR_WORKSPACE, "workspace cudaMallocAsync(%zu): %s", need, cudaGetErrorString(e));
+        own = true;
+    }
+    cudaError_t e = rs::convloss_grad_launch(in, k, target, N, H, W, kh, kw, (int)schedule, d_in, ws, s);
+    if (own) cudaFreeAsync(ws, s);
+    return launched(e, "convloss_grad");
+}
+
+static rs_status up4_check(const void *a, const void *b, int N, int C, int H, int W) {
+    if (!a || !b) return fail(RS_ERR_NULL, "upsample4: both tensors are required");
+    if (!pos(N) || !pos(C) || !pos(H) || !pos(W) || 16LL * N * C * H * W >= (1LL << 40))
+        return fail(RS_ERR_SHAPE, "upsample4: positive dims");
+    if (!is_device_ptr(a) || !is_device_ptr(b)) return fail(RS_ERR_FLAG, "upsample4: device pointers only");
+    return RS_OK;
+}
+
+rs_status upsample4_fwd(const float *x, int N, int C, int H, int W, float *y, rs_stream_t stream) {
+    rs_status st = up4_check(x, y, N, C, H, W);
+    if (st != RS_OK) return st;
+    return launched(rs::upsample4_launch(x, y, N, C, H, W, false, (cudaStream_t)stream), "upsample4_fwd");
+}
+
+rs_status upsample4_bwd(const float *dy, int N, int C, int H, int W, float *dx, rs_stream_t stream) {
+    rs_status st = up4_check(dy, dx, N, C, H, W);
+    if (st != RS_OK) return st;
+    return launched(rs::upsample4_launch(dy, dx, N, C, H, W, true, (cudaStream_t)stream), "upsample4_bwd");
 }
 
 }  // extern "C"

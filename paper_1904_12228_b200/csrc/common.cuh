@@ -324,4 +324,9 @@ bool conv_shape_ok(int Ci, int Co, int kh, int kw);
 cudaError_t conv_fwd_launch(const ConvArgs &a, cudaStream_t s);
 cudaError_t conv_bwd_launch(const ConvArgs &a, int algo, void *ws, size_t ws_bytes, cudaStream_t s);
 size_t conv_ws_bytes(int N, int Ci, int Co, int H, int W, int kh, int kw);
+
+size_t convloss_ws_bytes(int N, int H, int W);
+cudaError_t convloss_grad_launch(const float *in, const float *hk, const float *tg, int N, int H, int W, int kh,
+                                 int kw, int schedule, float *din, void *ws, cudaStream_t s);
+cudaError_t upsample4_launch(const float *src, float *dst, int N, int C, int H, int W, bool bwd, cudaStream_t s);
 }  // namespace rs

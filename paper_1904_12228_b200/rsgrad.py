@@ -55,8 +55,12 @@ def lib():
         L.bslice_fwd.argtypes = [P, P, P, I, I, I, I, I, I, O, P, P]
         L.bslice_bwd.argtypes = [P, P, P, P, I, I, I, I, I, I, O, P, P, P, P, S, P]
         L.conv_fwd.argtypes = [P, P, I, I, I, I, I, I, I, O, P, P]
+        L.convloss_grad.argtypes = [P, P, P, I, I, I, I, I, I, P, P, S, P]
+        L.upsample4_fwd.argtypes = [P, I, I, I, I, P, P]
+        L.upsample4_bwd.argtypes = [P, I, I, I, I, P, P]
         L.conv_bwd.argtypes = [P, P, P, I, I, I, I, I, I, I, O, P, P, P, S, P]
-        for f in ("stn_fwd", "stn_bwd", "warp_fwd", "warp_bwd", "bslice_fwd", "bslice_bwd", "conv_fwd", "conv_bwd"):
+        for f in ("stn_fwd", "stn_bwd", "warp_fwd", "warp_bwd", "bslice_fwd", "bslice_bwd", "conv_fwd", "conv_bwd",
+                  "convloss_grad", "upsample4_fwd", "upsample4_bwd"):
             getattr(L, f).restype = ctypes.c_int
         L.rsgrad_bwd_workspace_bytes.argtypes = [I, I, I, I, I, I, I, I, I, I, O]
         L.rsgrad_bwd_workspace_bytes.restype = S
@@ -316,3 +320,40 @@ def conv_bwd(x, k, dy, *, algo="auto", deterministic=False, need_dx=True, need_d
     _check(lib().conv_bwd(_ptr(x), _ptr(k), _ptr(dy), N, Ci, Co, H, W, kh, kw, ctypes.byref(o), _ptr(dx), _ptr(dk),
                           None if ws is None else ctypes.c_void_p(ws.data_ptr()), nws, _stream(dev)), "conv_bwd")
     return dx, dk
+
+
+# ----------------------------------------------------------------------------- §8(f) f4
+_SCHED = {"root": 0, "inline": 1, "at": 2}
+LAYER_CONVLOSS = 4
+
+
+def convloss_grad(inp, k, target, *, schedule="root", out=None):
+    """d_in of sum (conv(in, k) - target)^2; inp/target N x H x W CUDA
+    tensors, k a kh x kw CPU tensor; schedule root / inline / at."""
+    N, H, W = inp.shape
+    kh, kw = k.shape
+    kc = k.detach().to("cpu", torch.float32).contiguous()
+    d = out if out is not None else torch.empty_like(inp)
+    dev = _device_of(inp, target, d)
+    ws, nws = _workspace(dev, workspace_bytes(LAYER_CONVLOSS, N, 1, H, W) if schedule == "root" else 0)
+    _check(lib().convloss_grad(_ptr(inp), _ptr(kc), _ptr(target), N, H, W, kh, kw, _SCHED[schedule], _ptr(d),
+                               None if ws is None else ctypes.c_void_p(ws.data_ptr()), nws, _stream(dev)),
+           "convloss_grad")
+    return d
+
+
+def upsample4_fwd(x, *, out=None):
+    N, C, H, W = x.shape
+    y = out if out is not None else torch.empty((N, C, 4 * H, 4 * W), dtype=torch.float32, device=x.device)
+    _check(lib().upsample4_fwd(_ptr(x), N, C, H, W, _ptr(y), _stream(_device_of(x, y))), "upsample4_fwd")
+    return y
+
+
+def upsample4_bwd(dy, *, out=None):
+    N, C, Ho, Wo = dy.shape
+    if Ho % 4 or Wo % 4:
+        raise ValueError("upsample4_bwd: d_output must be 4H x 4W")
+    dx = out if out is not None else torch.empty((N, C, Ho // 4, Wo // 4), dtype=torch.float32, device=dy.device)
+    _check(lib().upsample4_bwd(_ptr(dy), N, C, Ho // 4, Wo // 4, _ptr(dx), _stream(_device_of(dy, dx))),
+           "upsample4_bwd")
+    return dx

@@ -593,3 +593,47 @@ def test_conv_paper_shape_sampled(cuda_device):
     assert_close(_np(dxg[:2]), rdx, "grad", "dx[:2]")
     _, rdk = oracle.conv_bwd(x.double().numpy(), k.double().numpy(), dy.double().numpy(), need_dx=False)
     assert_close(_np(dkg), rdk, "grad", "dk")
+
+
+# ============================================================================ checkpointing study (§8(f) f4)
+@pytest.mark.parametrize("ks", [(1, 5), (3, 5), (2, 2), (7, 7)])
+@pytest.mark.parametrize("schedule", ["root", "inline", "at"])
+def test_convloss_grad_schedules(cuda_device, ks, schedule):
+    """d_in of the conv loss under the three schedules the paper times
+    (compute_root / compute_inline / compute_at) vs the oracle; ragged
+    32 x 32 tiles and a 2-sample batch."""
+    kh, kw = ks
+    g = torch.Generator().manual_seed(17)
+    inp = torch.randn(2, 45, 70, generator=g, dtype=torch.float64).float()
+    tgt = torch.randn(2, 45, 70, generator=g, dtype=torch.float64).float()
+    k = (torch.randn(kh, kw, generator=g, dtype=torch.float64) / (kh * kw) ** 0.5).float()
+    d = rsgrad.convloss_grad(inp.to(cuda_device), k, tgt.to(cuda_device), schedule=schedule)
+    ref = oracle.convloss_grad(inp.double().numpy(), k.double().numpy(), tgt.double().numpy())
+    assert_close(_np(d), ref, "grad", f"d_in[{schedule}]")
+
+
+def test_convloss_paper_shape_schedules_agree(cuda_device):
+    """2560 x 1600 with the paper's 3 x 5 kernel: the three schedules agree
+    with each other everywhere and with the oracle."""
+    g = torch.Generator().manual_seed(18)
+    inp = torch.rand(1, 1600, 2560, generator=g, dtype=torch.float64).float()
+    tgt = torch.rand(1, 1600, 2560, generator=g, dtype=torch.float64).float()
+    k = (torch.randn(3, 5, generator=g, dtype=torch.float64) / 15 ** 0.5).float()
+    ref = oracle.convloss_grad(inp.double().numpy(), k.double().numpy(), tgt.double().numpy())
+    for sch in ("root", "inline", "at"):
+        d = rsgrad.convloss_grad(inp.to(cuda_device), k, tgt.to(cuda_device), schedule=sch)
+        assert_close(_np(d), ref, "grad", f"d_in[{sch}]")
+
+
+@pytest.mark.parametrize("shape", [(2, 3, 5, 7), (1, 1, 1, 1), (1, 4, 33, 65)])
+def test_upsample4_pair(cuda_device, shape):
+    """output(x) = input(x/4) and its converted gather adjoint (PAPER.md:725-731);
+    the forward is exact, the adjoint a 16-term sum."""
+    g = torch.Generator().manual_seed(19)
+    N, C, H, W = shape
+    x = torch.randn(N, C, H, W, generator=g, dtype=torch.float64).float()
+    dy = torch.randn(N, C, 4 * H, 4 * W, generator=g, dtype=torch.float64).float()
+    y = rsgrad.upsample4_fwd(x.to(cuda_device))
+    assert torch.equal(y.cpu(), torch.from_numpy(oracle.upsample4_fwd(x.double().numpy())).float())
+    dx = rsgrad.upsample4_bwd(dy.to(cuda_device))
+    assert_close(_np(dx), oracle.upsample4_bwd(dy.double().numpy()), "grad", "upsample dx")
