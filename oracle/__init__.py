@@ -54,6 +54,10 @@ def _load():
         lib.oracle_convloss_grad.argtypes = [P, P, P, I, I, I, I, I, P]
         lib.oracle_upsample4_fwd.argtypes = [P, I, I, I, I, P]
         lib.oracle_upsample4_bwd.argtypes = [P, I, I, I, I, P]
+        lib.oracle_stn_bicubic_fwd.argtypes = [P, P, I, I, I, I, I, I, I, P]
+        lib.oracle_stn_bicubic_bwd.argtypes = [P, P, P, I, I, I, I, I, I, I, P, P]
+        lib.oracle_stn3d_fwd.argtypes = [P, P, I, I, I, I, I, I, I, I, I, P]
+        lib.oracle_stn3d_bwd.argtypes = [P, P, P, I, I, I, I, I, I, I, I, I, P, P]
         lib.oracle_set_threads.argtypes = [I]
         lib.oracle_get_threads.restype = I
         _lib = lib
@@ -188,3 +192,43 @@ def upsample4_bwd(dy):
     dx = np.empty((N, C, Ho // 4, Wo // 4), np.float64)
     _load().oracle_upsample4_bwd(_p(dy), N, C, Ho // 4, Wo // 4, _p(dx))
     return dx
+
+
+# ----------------------------------------------------------------------------- §8(f) f3
+def stn_bicubic_fwd(x, theta, Ho=None, Wo=None, align_corners=True):
+    x, theta = _f64(x), _f64(theta)
+    N, C, H, W = x.shape
+    Ho = H if Ho is None else Ho
+    Wo = W if Wo is None else Wo
+    y = np.empty((N, C, Ho, Wo), np.float64)
+    _load().oracle_stn_bicubic_fwd(_p(x), _p(theta), N, C, H, W, Ho, Wo, int(align_corners), _p(y))
+    return y
+
+
+def stn_bicubic_bwd(x, theta, dy, align_corners=True):
+    x, theta, dy = _f64(x), _f64(theta), _f64(dy)
+    N, C, H, W = x.shape
+    Ho, Wo = dy.shape[2:]
+    dx, dth = np.empty_like(x), np.empty((N, 2, 3), np.float64)
+    _load().oracle_stn_bicubic_bwd(_p(x), _p(theta), _p(dy), N, C, H, W, Ho, Wo, int(align_corners), _p(dx),
+                                   _p(dth))
+    return dx, dth
+
+
+def stn3d_fwd(x, theta, out_size=None, align_corners=True):
+    x, theta = _f64(x), _f64(theta)
+    N, C, D, H, W = x.shape
+    Do, Ho, Wo = (D, H, W) if out_size is None else out_size
+    y = np.empty((N, C, Do, Ho, Wo), np.float64)
+    _load().oracle_stn3d_fwd(_p(x), _p(theta), N, C, D, H, W, Do, Ho, Wo, int(align_corners), _p(y))
+    return y
+
+
+def stn3d_bwd(x, theta, dy, align_corners=True):
+    x, theta, dy = _f64(x), _f64(theta), _f64(dy)
+    N, C, D, H, W = x.shape
+    Do, Ho, Wo = dy.shape[2:]
+    dx, dth = np.empty_like(x), np.empty((N, 3, 4), np.float64)
+    _load().oracle_stn3d_bwd(_p(x), _p(theta), _p(dy), N, C, D, H, W, Do, Ho, Wo, int(align_corners), _p(dx),
+                             _p(dth))
+    return dx, dth

@@ -569,3 +569,169 @@ void oracle_upsample4_bwd(const double *dy, int N, int C, int H, int W, double *
             for (long xx = 0; xx < Wo; xx++)
                 dx[(nc * H + yy / 4) * W + xx / 4] += dy[(nc * Ho + yy) * Wo + xx];
 }
+
+/* ------------------------------------------------------------------ */
+/* STN variants ("changing the        */
+/* interpolation scheme ... or interpolating over more dimensions")    */
+/* ------------------------------------------------------------------ */
+/* Bicubic: Keys' cubic convolution with A = -0.75 over the 4 x 4 taps
+ * floor(i) - 1 .. floor(i) + 2 per axis, zeros outside (the convention of
+ * PyTorch grid_sample(mode='bicubic'), R12).  Coordinates as R1.   */
+static const double CUBIC_A = -0.75;
+static double cubic1(double x) { return ((CUBIC_A + 2.0) * x - (CUBIC_A + 3.0)) * x * x + 1.0; }
+static double cubic2(double x) { return ((CUBIC_A * x - 5.0 * CUBIC_A) * x + 8.0 * CUBIC_A) * x - 4.0 * CUBIC_A; }
+static double dcubic1(double x) { return (3.0 * (CUBIC_A + 2.0) * x - 2.0 * (CUBIC_A + 3.0)) * x; }
+static double dcubic2(double x) { return (3.0 * CUBIC_A * x - 10.0 * CUBIC_A) * x + 8.0 * CUBIC_A; }
+static void cubic_w(double t, double w[4], double dw[4]) {
+    w[0] = cubic2(t + 1.0); w[1] = cubic1(t); w[2] = cubic1(1.0 - t); w[3] = cubic2(2.0 - t);
+    dw[0] = dcubic2(t + 1.0); dw[1] = dcubic1(t); dw[2] = -dcubic1(1.0 - t); dw[3] = -dcubic2(2.0 - t);
+}
+
+void oracle_stn_bicubic_fwd(const double *x, const double *theta, int N, int C, int H, int W,
+                            int Ho, int Wo, int ac, double *y) {
+    const long HW = (long)H * W, P = (long)Ho * Wo;
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int n = 0; n < N; n++)
+        for (int c = 0; c < C; c++)
+            for (int i = 0; i < Ho; i++)
+                for (int j = 0; j < Wo; j++) {
+                    double xt, yt, ix, iy, wx[4], wy[4], d[4];
+                    stn_coord(theta + 6L * n, H, W, Ho, Wo, ac, i, j, &xt, &yt, &ix, &iy);
+                    const double x0 = floor(ix), y0 = floor(iy);
+                    cubic_w(ix - x0, wx, d);
+                    cubic_w(iy - y0, wy, d);
+                    const double *p = x + ((long)n * C + c) * HW;
+                    double s = 0.0;
+                    for (int a = 0; a < 4; a++)
+                        for (int b = 0; b < 4; b++)
+                            s += wy[a] * wx[b] * tap(p, H, W, (long)y0 - 1 + a, (long)x0 - 1 + b);
+                    y[((long)n * C + c) * P + (long)i * Wo + j] = s;
+                }
+}
+
+/* Adjoint: d_input by the naive scatter of every tap, d_theta by the chain rule
+ * through d(weights)/dt and the un-normalisation scale, summed over pixels. */
+void oracle_stn_bicubic_bwd(const double *x, const double *theta, const double *dy, int N, int C,
+                            int H, int W, int Ho, int Wo, int ac, double *dx, double *dtheta) {
+    const long HW = (long)H * W, P = (long)Ho * Wo;
+    const double sx = stn_unnorm_scale(W, ac), sy = stn_unnorm_scale(H, ac);
+#pragma omp parallel for schedule(static)
+    for (int n = 0; n < N; n++) {
+        if (dx) memset(dx + (long)n * C * HW, 0, sizeof(double) * (size_t)(C * HW));
+        double dth[6] = {0, 0, 0, 0, 0, 0};
+        for (int i = 0; i < Ho; i++)
+            for (int j = 0; j < Wo; j++) {
+                double xt, yt, ix, iy, wx[4], wy[4], dwx[4], dwy[4];
+                stn_coord(theta + 6L * n, H, W, Ho, Wo, ac, i, j, &xt, &yt, &ix, &iy);
+                const double x0 = floor(ix), y0 = floor(iy);
+                cubic_w(ix - x0, wx, dwx);
+                cubic_w(iy - y0, wy, dwy);
+                double gix = 0.0, giy = 0.0;
+                for (int c = 0; c < C; c++) {
+                    const double g = dy[((long)n * C + c) * P + (long)i * Wo + j];
+                    const double *p = x + ((long)n * C + c) * HW;
+                    for (int a = 0; a < 4; a++)
+                        for (int b = 0; b < 4; b++) {
+                            const long yy = (long)y0 - 1 + a, xx = (long)x0 - 1 + b;
+                            if (yy < 0 || yy >= H || xx < 0 || xx >= W) continue;
+                            const double v = p[yy * W + xx];
+                            if (dx) dx[((long)n * C + c) * HW + yy * W + xx] += g * wy[a] * wx[b];
+                            gix += g * wy[a] * dwx[b] * v;
+                            giy += g * dwy[a] * wx[b] * v;
+                        }
+                }
+                const double gx = gix * sx, gy = giy * sy;
+                dth[0] += gx * xt; dth[1] += gx * yt; dth[2] += gx;
+                dth[3] += gy * xt; dth[4] += gy * yt; dth[5] += gy;
+            }
+        if (dtheta)
+            for (int k = 0; k < 6; k++) dtheta[6L * n + k] = dth[k];
+    }
+}
+
+/* Volumetric STN: theta N x 3 x 4, x N x C x D x H x W, output N x C x Do x Ho x Wo;
+ * normalised (x_t, y_t, z_t) per R1 on each axis, (g_x, g_y, g_z) = theta [x_t, y_t, z_t, 1],
+ * trilinear tent over the 8 taps, zeros outside (PyTorch 5-D affine_grid + grid_sample). */
+static double tap3(const double *p, int D, int H, int W, long zz, long yy, long xx) {
+    if (zz < 0 || zz >= D || yy < 0 || yy >= H || xx < 0 || xx >= W) return 0.0;
+    return p[(zz * H + yy) * (long)W + xx];
+}
+
+static void stn3_coord(const double *th, int D, int H, int W, int Do, int Ho, int Wo, int ac, int k,
+                       int i, int j, double t[3], double pix[3]) {
+    t[0] = stn_norm(j, Wo, ac);
+    t[1] = stn_norm(i, Ho, ac);
+    t[2] = stn_norm(k, Do, ac);
+    const int L[3] = {W, H, D};
+    for (int r = 0; r < 3; r++) {
+        const double g = th[4 * r] * t[0] + th[4 * r + 1] * t[1] + th[4 * r + 2] * t[2] + th[4 * r + 3];
+        pix[r] = stn_unnorm(g, L[r], ac);
+    }
+}
+
+void oracle_stn3d_fwd(const double *x, const double *theta, int N, int C, int D, int H, int W, int Do,
+                      int Ho, int Wo, int ac, double *y) {
+    const long V = (long)D * H * W, Po = (long)Do * Ho * Wo;
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int n = 0; n < N; n++)
+        for (int c = 0; c < C; c++)
+            for (int k = 0; k < Do; k++)
+                for (int i = 0; i < Ho; i++)
+                    for (int j = 0; j < Wo; j++) {
+                        double t[3], q[3];
+                        stn3_coord(theta + 12L * n, D, H, W, Do, Ho, Wo, ac, k, i, j, t, q);
+                        const double x0 = floor(q[0]), y0 = floor(q[1]), z0 = floor(q[2]);
+                        const double f[3] = {q[0] - x0, q[1] - y0, q[2] - z0};
+                        const double *p = x + ((long)n * C + c) * V;
+                        double s = 0.0;
+                        for (int e = 0; e < 8; e++) {
+                            const int a = e & 1, b = (e >> 1) & 1, d = e >> 2;
+                            const double w = (a ? f[0] : 1.0 - f[0]) * (b ? f[1] : 1.0 - f[1]) * (d ? f[2] : 1.0 - f[2]);
+                            s += w * tap3(p, D, H, W, (long)z0 + d, (long)y0 + b, (long)x0 + a);
+                        }
+                        y[((long)n * C + c) * Po + ((long)k * Ho + i) * Wo + j] = s;
+                    }
+}
+
+void oracle_stn3d_bwd(const double *x, const double *theta, const double *dy, int N, int C, int D, int H,
+                      int W, int Do, int Ho, int Wo, int ac, double *dx, double *dtheta) {
+    const long V = (long)D * H * W, Po = (long)Do * Ho * Wo;
+    const double sc[3] = {stn_unnorm_scale(W, ac), stn_unnorm_scale(H, ac), stn_unnorm_scale(D, ac)};
+#pragma omp parallel for schedule(static)
+    for (int n = 0; n < N; n++) {
+        if (dx) memset(dx + (long)n * C * V, 0, sizeof(double) * (size_t)(C * V));
+        double dth[12] = {0};
+        for (int k = 0; k < Do; k++)
+            for (int i = 0; i < Ho; i++)
+                for (int j = 0; j < Wo; j++) {
+                    double t[3], q[3];
+                    stn3_coord(theta + 12L * n, D, H, W, Do, Ho, Wo, ac, k, i, j, t, q);
+                    const double x0 = floor(q[0]), y0 = floor(q[1]), z0 = floor(q[2]);
+                    const double f[3] = {q[0] - x0, q[1] - y0, q[2] - z0};
+                    double gq[3] = {0, 0, 0};
+                    for (int c = 0; c < C; c++) {
+                        const double g = dy[((long)n * C + c) * Po + ((long)k * Ho + i) * Wo + j];
+                        const double *p = x + ((long)n * C + c) * V;
+                        for (int e = 0; e < 8; e++) {
+                            const int a = e & 1, b = (e >> 1) & 1, d = e >> 2;
+                            const double wx = a ? f[0] : 1.0 - f[0], wy = b ? f[1] : 1.0 - f[1],
+                                         wz = d ? f[2] : 1.0 - f[2];
+                            const long zz = (long)z0 + d, yy = (long)y0 + b, xx = (long)x0 + a;
+                            if (zz < 0 || zz >= D || yy < 0 || yy >= H || xx < 0 || xx >= W) continue;
+                            const double v = p[(zz * H + yy) * W + xx];
+                            if (dx) dx[((long)n * C + c) * V + (zz * H + yy) * W + xx] += g * wx * wy * wz;
+                            gq[0] += g * (a ? 1.0 : -1.0) * wy * wz * v;
+                            gq[1] += g * wx * (b ? 1.0 : -1.0) * wz * v;
+                            gq[2] += g * wx * wy * (d ? 1.0 : -1.0) * v;
+                        }
+                    }
+                    for (int r = 0; r < 3; r++) {
+                        const double gg = gq[r] * sc[r];
+                        dth[4 * r] += gg * t[0]; dth[4 * r + 1] += gg * t[1];
+                        dth[4 * r + 2] += gg * t[2]; dth[4 * r + 3] += gg;
+                    }
+                }
+        if (dtheta)
+            for (int r = 0; r < 12; r++) dtheta[12L * n + r] = dth[r];
+    }
+}

@@ -488,3 +488,72 @@ def test_upsample4_vs_torch():
     np.testing.assert_allclose(oracle.upsample4_bwd(dy), _np(xt.grad), rtol=1e-14, atol=1e-14)
     np.testing.assert_allclose(oracle.upsample4_bwd(dy), dy.reshape(2, 3, 5, 4, 7, 4).sum(axis=(3, 5)),
                                rtol=1e-14, atol=1e-14)
+
+
+# --------------------------------------------------------------------------- STN variants (§8(f) f3)
+def _rand_theta(N, rows, seed):
+    g = np.random.default_rng(seed)
+    th = np.zeros((N, rows, rows + 1))
+    for n in range(N):
+        th[n, :, :rows] = np.eye(rows) * g.uniform(0.8, 1.2) + g.uniform(-0.25, 0.25, (rows, rows))
+        th[n, :, rows] = g.uniform(-0.2, 0.2, rows)
+    return th
+
+
+@pytest.mark.parametrize("ac", [True, False])
+def test_stn_bicubic_vs_torch(ac):
+    """Bicubic STN = torch affine_grid + grid_sample(mode='bicubic', zeros) in fp64,
+    forward and autograd d_input / d_theta ("changing the interpolation
+    scheme")."""
+    g = np.random.default_rng(21)
+    N, C, H, W, Ho, Wo = 2, 3, 11, 13, 9, 10
+    x, dy = g.standard_normal((N, C, H, W)), g.standard_normal((N, C, Ho, Wo))
+    th = _rand_theta(N, 2, 22)
+    xt, tt = torch.tensor(x, requires_grad=True), torch.tensor(th, requires_grad=True)
+    grid = F.affine_grid(tt, (N, C, Ho, Wo), align_corners=ac)
+    yt = F.grid_sample(xt, grid, mode="bicubic", padding_mode="zeros", align_corners=ac)
+    yt.backward(torch.tensor(dy))
+    np.testing.assert_allclose(oracle.stn_bicubic_fwd(x, th, Ho, Wo, ac), _np(yt), rtol=1e-11, atol=1e-12)
+    dx, dth = oracle.stn_bicubic_bwd(x, th, dy, ac)
+    np.testing.assert_allclose(dx, _np(xt.grad), rtol=1e-11, atol=1e-12)
+    np.testing.assert_allclose(dth, _np(tt.grad), rtol=1e-10, atol=1e-10)
+
+
+def test_stn_bicubic_identity_interpolates():
+    """Keys' kernel interpolates: identity theta (align_corners=1) reproduces x up to the
+    rounding of the normalisation round trip."""
+    x = np.random.default_rng(23).standard_normal((1, 2, 8, 9))
+    th = np.array([[[1.0, 0, 0], [0, 1.0, 0]]])
+    np.testing.assert_allclose(oracle.stn_bicubic_fwd(x, th), x, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("ac", [True, False])
+def test_stn3d_vs_torch(ac):
+    """Volumetric STN = torch 5-D affine_grid + trilinear grid_sample (zeros) in fp64,
+    forward and autograd ("interpolating over more dimensions")."""
+    g = np.random.default_rng(24)
+    N, C, D, H, W, Do, Ho, Wo = 2, 2, 5, 6, 7, 4, 6, 5
+    x, dy = g.standard_normal((N, C, D, H, W)), g.standard_normal((N, C, Do, Ho, Wo))
+    th = _rand_theta(N, 3, 25)
+    xt, tt = torch.tensor(x, requires_grad=True), torch.tensor(th, requires_grad=True)
+    grid = F.affine_grid(tt, (N, C, Do, Ho, Wo), align_corners=ac)
+    yt = F.grid_sample(xt, grid, mode="bilinear", padding_mode="zeros", align_corners=ac)
+    yt.backward(torch.tensor(dy))
+    np.testing.assert_allclose(oracle.stn3d_fwd(x, th, (Do, Ho, Wo), ac), _np(yt), rtol=1e-11, atol=1e-12)
+    dx, dth = oracle.stn3d_bwd(x, th, dy, ac)
+    np.testing.assert_allclose(dx, _np(xt.grad), rtol=1e-11, atol=1e-12)
+    np.testing.assert_allclose(dth, _np(tt.grad), rtol=1e-10, atol=1e-10)
+
+
+def test_stn3d_reduces_to_2d_on_one_slice():
+    """On a one-slice volume (align_corners=0) a 3-D theta that leaves z alone samples
+    the slice exactly (f_z = 0): the 2-D STN of that slice (cross-layer invariant)."""
+    g = np.random.default_rng(26)
+    x = g.standard_normal((1, 2, 1, 9, 11))
+    th2 = _rand_theta(1, 2, 27)
+    th3 = np.zeros((1, 3, 4))
+    th3[0, :2, :2], th3[0, :2, 3] = th2[0, :, :2], th2[0, :, 2]
+    th3[0, 2, 2] = 1.0
+    y3 = oracle.stn3d_fwd(x, th3, (1, 9, 11), align_corners=False)
+    y2 = oracle.stn_fwd(x[:, :, 0], th2, align_corners=False)
+    np.testing.assert_allclose(y3[:, :, 0], y2, rtol=1e-13, atol=1e-13)
