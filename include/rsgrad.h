@@ -205,10 +205,35 @@ rs_status convloss_grad(const float *in, const float *k, const float *target, in
 rs_status upsample4_fwd(const float *x, int N, int C, int H, int W, float *y, rs_stream_t stream);
 rs_status upsample4_bwd(const float *dy, int N, int C, int H, int W, float *dx, rs_stream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * STN variants ("changing the interpolation scheme
+ * ... or interpolating over more dimensions").  Device pointers only; zeros padding
+ * only (opts.padding = RS_PAD_BORDER => RS_ERR_FLAG); opts.align_corners as stn_*.
+ * d_input is the atomic scatter (memset + red.global.add; SCATTER_ATOMIC semantics,
+ * not deterministic; GATHER / SCATTER_PRIV / deterministic=1 => RS_ERR_FLAG); d_theta
+ * is a fixed-order fp64 sum of per-block partials.
+ *   stn_bicubic_*  theta N x 2 x 3, x N x C x H x W, y N x C x Ho x Wo: Keys' cubic
+ *                  convolution (A = -0.75) over the 4 x 4 taps floor(i)-1 .. floor(i)+2
+ *                  (= torch grid_sample mode='bicubic', zeros; R12).
+ *   stn3d_*        theta N x 3 x 4, x N x C x D x H x W, y N x C x Do x Ho x Wo:
+ *                  5-D affine_grid + trilinear grid_sample (zeros).
+ * ------------------------------------------------------------------------- */
+rs_status stn_bicubic_fwd(const float *x, const float *theta, int N, int C, int H, int W, int Ho,
+                          int Wo, const rs_opts *opts, float *y, rs_stream_t stream);
+rs_status stn_bicubic_bwd(const float *x, const float *theta, const float *dy, int N, int C, int H,
+                          int W, int Ho, int Wo, const rs_opts *opts, float *dx, float *dtheta,
+                          void *workspace, size_t ws_bytes, rs_stream_t stream);
+rs_status stn3d_fwd(const float *x, const float *theta, int N, int C, int D, int H, int W, int Do,
+                    int Ho, int Wo, const rs_opts *opts, float *y, rs_stream_t stream);
+rs_status stn3d_bwd(const float *x, const float *theta, const float *dy, int N, int C, int D, int H,
+                    int W, int Do, int Ho, int Wo, const rs_opts *opts, float *dx, float *dtheta,
+                    void *workspace, size_t ws_bytes, rs_stream_t stream);
+
 /* Workspace (bytes) *_bwd wants for these shapes.  layer: 0 = STN (uses
  * N,C,H,W,Ho,Wo), 1 = warp (N,C,H,W), 2 = bslice (N,H,W,D,Gh,Gw), 3 = conv
  * (N, C = Ci, H, W, D = Co, Gh = kh, Gw = kw), 4 = convloss_grad (N, H, W: the
- * RS_SCHED_ROOT residual); unused arguments are ignored.
+ * RS_SCHED_ROOT residual), 5 = stn_bicubic (N, Ho, Wo), 6 = stn3d (N, Ho, Wo, D = Do);
+ * unused arguments are ignored.
  * Returns 0 for an unknown layer.  DESIGN.md "Workspace". */
 size_t rsgrad_bwd_workspace_bytes(int layer, int N, int C, int H, int W, int Ho, int Wo, int D,
                                   int Gh, int Gw, const rs_opts *opts);

@@ -10,6 +10,7 @@
 #include <string>
 #include <cstdlib>
 #include <mutex>
+#include <initializer_list>
 #include <vector>
 
 #include "../../include/rsgrad.h"
@@ -251,6 +252,12 @@ size_t rsgrad_bwd_workspace_bytes(int layer, int N, int C, int H, int W, int Ho,
         case 4:
             if (!pos(N) || !pos(H) || !pos(W)) return 0;
             return rs::convloss_ws_bytes(N, H, W);
+        case 5:
+            if (!pos(N) || !pos(Ho) || !pos(Wo)) return 0;
+            return rs::stn_var_ws_bytes(N, Ho * Wo, 6);
+        case 6:
+            if (!pos(N) || !pos(Ho) || !pos(Wo) || !pos(D)) return 0;
+            return rs::stn_var_ws_bytes(N, D * Ho * Wo, 12);
         default:
             return 0;
     }
@@ -577,6 +584,106 @@ rs_status upsample4_bwd(const float *dy, int N, int C, int H, int W, float *dx, 
     rs_status st = up4_check(dy, dx, N, C, H, W);
     if (st != RS_OK) return st;
     return launched(rs::upsample4_launch(dy, dx, N, C, H, W, true, (cudaStream_t)stream), "upsample4_bwd");
+}
+
+// ------------------------------------------------------------------------------ f3
+static rs_status var_check(const rs_opts &o, bool bwd, bool has_dx, std::initializer_list<const void *> ptrs) {
+    rs_status st = check_opts(o);
+    if (st != RS_OK) return st;
+    if (o.padding != RS_PAD_ZEROS) return fail(RS_ERR_FLAG, "stn variants: zeros padding only");
+    if (bwd && has_dx && (o.algo == RS_ALGO_GATHER || o.algo == RS_ALGO_SCATTER_PRIV || o.deterministic))
+        return fail(RS_ERR_FLAG, "stn variants: d_input is the atomic scatter only (not deterministic)");
+    for (const void *p : ptrs)
+        if (p && !is_device_ptr(p)) return fail(RS_ERR_FLAG, "stn variants: device pointers only");
+    return RS_OK;
+}
+
+extern "C++" {
+template <class F>
+rs_status with_ws(size_t need, void *workspace, size_t ws_bytes, cudaStream_t s, F &&f, const char *what) {
+    void *ws = workspace;
+    bool own = false;
+    if (need && (!ws || ws_bytes < need)) {
+        cudaError_t e = lib_malloc(&ws, need, s);
+        if (e != cudaSuccess) return fail(RS_ERR_WORKSPACE, "workspace cudaMallocAsync(%zu): %s", need, cudaGetErrorString(e));
+        own = true;
+    }
+    cudaError_t e = f(ws);
+    if (own) cudaFreeAsync(ws, s);
+    return launched(e, what);
+}
+}  // extern "C++"
+
+rs_status stn_bicubic_fwd(const float *x, const float *theta, int N, int C, int H, int W, int Ho, int Wo,
+                          const rs_opts *opts, float *y, rs_stream_t stream) {
+    const rs_opts o = resolve(opts);
+    rs_status st = stn_validate(x, theta, N, C, H, W, Ho, Wo, o);
+    if (st != RS_OK) return st;
+    if (!y) return fail(RS_ERR_NULL, "stn_bicubic_fwd: y is required");
+    if ((st = var_check(o, false, false, {x, theta, y})) != RS_OK) return st;
+    rs::StnArgs a{};
+    a.x = x; a.theta = theta; a.y = y;
+    a.N = N; a.C = C; a.H = H; a.W = W; a.Ho = Ho; a.Wo = Wo; a.ac = o.align_corners;
+    return launched(rs::stn_bicubic_launch(a, false, nullptr, (cudaStream_t)stream), "stn_bicubic_fwd");
+}
+
+rs_status stn_bicubic_bwd(const float *x, const float *theta, const float *dy, int N, int C, int H, int W, int Ho,
+                          int Wo, const rs_opts *opts, float *dx, float *dtheta, void *workspace, size_t ws_bytes,
+                          rs_stream_t stream) {
+    const rs_opts o = resolve(opts);
+    rs_status st = stn_validate(x, theta, N, C, H, W, Ho, Wo, o);
+    if (st != RS_OK) return st;
+    if (!dy) return fail(RS_ERR_NULL, "stn_bicubic_bwd: dy is required");
+    if ((st = var_check(o, true, dx != nullptr, {x, theta, dy, dx, dtheta})) != RS_OK) return st;
+    if (!dx && !dtheta) return ok();
+    rs::StnArgs a{};
+    a.x = x; a.theta = theta; a.dy = dy; a.dx = dx; a.dtheta = dtheta;
+    a.N = N; a.C = C; a.H = H; a.W = W; a.Ho = Ho; a.Wo = Wo; a.ac = o.align_corners;
+    cudaStream_t s = (cudaStream_t)stream;
+    return with_ws(dtheta ? rs::stn_var_ws_bytes(N, Ho * Wo, 6) : 0, workspace, ws_bytes, s,
+                   [&](void *ws) { return rs::stn_bicubic_launch(a, true, ws, s); }, "stn_bicubic_bwd");
+}
+
+static rs_status stn3d_validate(const float *x, const float *theta, int N, int C, int D, int H, int W, int Do, int Ho,
+                                int Wo, const rs_opts &o) {
+    if (!x || !theta) return fail(RS_ERR_NULL, "stn3d: x and theta are required");
+    if (!pos(N) || !pos(C) || !pos(D) || !pos(H) || !pos(W) || !pos(Do) || !pos(Ho) || !pos(Wo))
+        return fail(RS_ERR_SHAPE, "stn3d: dims must be positive");
+    if (o.align_corners && (Do < 2 || Ho < 2 || Wo < 2))
+        return fail(RS_ERR_SHAPE, "stn3d: align_corners=1 needs Do, Ho, Wo >= 2");
+    if (N > 65535 || (long long)Do * Ho * Wo >= (1LL << 31) || (long long)D * H * W >= (1LL << 40))
+        return fail(RS_ERR_SHAPE, "stn3d: N <= 65535 and Do*Ho*Wo < 2^31");
+    return RS_OK;
+}
+
+rs_status stn3d_fwd(const float *x, const float *theta, int N, int C, int D, int H, int W, int Do, int Ho, int Wo,
+                    const rs_opts *opts, float *y, rs_stream_t stream) {
+    const rs_opts o = resolve(opts);
+    rs_status st = stn3d_validate(x, theta, N, C, D, H, W, Do, Ho, Wo, o);
+    if (st != RS_OK) return st;
+    if (!y) return fail(RS_ERR_NULL, "stn3d_fwd: y is required");
+    if ((st = var_check(o, false, false, {x, theta, y})) != RS_OK) return st;
+    return launched(rs::stn3d_launch(x, theta, nullptr, y, nullptr, nullptr, N, C, D, H, W, Do, Ho, Wo,
+                                     o.align_corners, false, nullptr, (cudaStream_t)stream),
+                    "stn3d_fwd");
+}
+
+rs_status stn3d_bwd(const float *x, const float *theta, const float *dy, int N, int C, int D, int H, int W, int Do,
+                    int Ho, int Wo, const rs_opts *opts, float *dx, float *dtheta, void *workspace, size_t ws_bytes,
+                    rs_stream_t stream) {
+    const rs_opts o = resolve(opts);
+    rs_status st = stn3d_validate(x, theta, N, C, D, H, W, Do, Ho, Wo, o);
+    if (st != RS_OK) return st;
+    if (!dy) return fail(RS_ERR_NULL, "stn3d_bwd: dy is required");
+    if ((st = var_check(o, true, dx != nullptr, {x, theta, dy, dx, dtheta})) != RS_OK) return st;
+    if (!dx && !dtheta) return ok();
+    cudaStream_t s = (cudaStream_t)stream;
+    return with_ws(dtheta ? rs::stn_var_ws_bytes(N, Do * Ho * Wo, 12) : 0, workspace, ws_bytes, s,
+                   [&](void *ws) {
+                       return rs::stn3d_launch(x, theta, dy, nullptr, dx, dtheta, N, C, D, H, W, Do, Ho, Wo,
+                                               o.align_corners, true, ws, s);
+                   },
+                   "stn3d_bwd");
 }
 
 }  // extern "C"

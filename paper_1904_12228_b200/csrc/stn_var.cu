@@ -1,0 +1,307 @@
+// stn_var.cu — STN variants the paper names (PAPER.md:28:
+// "changing the interpolation scheme ... or interpolating over more dimensions"), sm_100a.
+//
+//   bicubic STN   Keys' cubic convolution (A = -0.75) over the 4 x 4 taps around the
+//                 affine sample point, zeros outside (R12).
+//   3-D STN       volumetric affine_grid (theta 3 x 4) + trilinear sampling.
+// Coordinates are evaluated in fp64 in the oracle's order (P1); tap weights and their
+// derivatives in fp64, rounded to fp32 for the per-channel data arithmetic.
+// Forward: thread per output pixel, taps through L1.  Adjoint: d_input by the
+// general scatter with atomics (no converted gather yet: PAPER.md:733's fallback),
+// d_theta per pixel -> warp -> block (fp32) -> fp64 block partials -> fixed-order sum.
+#include "common.cuh"
+
+namespace rs {
+namespace {
+
+constexpr int kVT = 256;
+
+RS_DEV void cubic_w(double t, float w[4], float dw[4]) {
+    const double A = -0.75;
+    auto c1 = [&](double x) { return __dadd_rn(__dmul_rn(__dmul_rn(__dsub_rn(__dmul_rn(A + 2.0, x), A + 3.0), x), x), 1.0); };
+    auto c2 = [&](double x) {
+        return __dsub_rn(__dmul_rn(__dadd_rn(__dmul_rn(__dsub_rn(__dmul_rn(A, x), 5.0 * A), x), 8.0 * A), x), 4.0 * A);
+    };
+    auto d1 = [&](double x) { return __dmul_rn(__dsub_rn(__dmul_rn(3.0 * (A + 2.0), x), 2.0 * (A + 3.0)), x); };
+    auto d2 = [&](double x) { return __dadd_rn(__dmul_rn(__dsub_rn(__dmul_rn(3.0 * A, x), 10.0 * A), x), 8.0 * A); };
+    w[0] = (float)c2(t + 1.0);
+    w[1] = (float)c1(t);
+    w[2] = (float)c1(1.0 - t);
+    w[3] = (float)c2(2.0 - t);
+    dw[0] = (float)d2(t + 1.0);
+    dw[1] = (float)d1(t);
+    dw[2] = (float)-d1(1.0 - t);
+    dw[3] = (float)-d2(2.0 - t);
+}
+
+struct Bicubic {
+    int x0, y0;  // floor of the sample point
+    float wx[4], wy[4], dwx[4], dwy[4];
+    double xt, yt;
+};
+
+RS_DEV Bicubic bicubic_at(const float *theta, int n, int i, int j, int H, int W, int Ho, int Wo, int ac) {
+    Bicubic b;
+    b.xt = stn_norm(j, Wo, ac);
+    b.yt = stn_norm(i, Ho, ac);
+    const float *t = theta + 6 * n;
+    const double ix = stn_unnorm(affine3(__ldg(t), __ldg(t + 1), __ldg(t + 2), b.xt, b.yt), W, ac);
+    const double iy = stn_unnorm(affine3(__ldg(t + 3), __ldg(t + 4), __ldg(t + 5), b.xt, b.yt), H, ac);
+    const Cell cx = cell_of(ix), cy = cell_of(iy);
+    b.x0 = cx.i0;
+    b.y0 = cy.i0;
+    cubic_w(__dsub_rn(ix, floor(ix)), b.wx, b.dwx);
+    cubic_w(__dsub_rn(iy, floor(iy)), b.wy, b.dwy);
+    return b;
+}
+
+__global__ void __launch_bounds__(kVT) bicubic_fwd(StnArgs a) {
+    const int P = a.Ho * a.Wo, HW = a.H * a.W;
+    const int q = blockIdx.x * kVT + threadIdx.x;
+    if (q >= P) return;
+    const int n = blockIdx.y, i = q / a.Wo, j = q - i * a.Wo;
+    const Bicubic b = bicubic_at(a.theta, n, i, j, a.H, a.W, a.Ho, a.Wo, a.ac);
+    for (int c = 0; c < a.C; c++) {
+        const float *p = a.x + ((long long)n * a.C + c) * HW;
+        float s = 0.f;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int yy = b.y0 - 1 + u;
+            if (yy < 0 || yy >= a.H) continue;
+            float r = 0.f;
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+                const int xx = b.x0 - 1 + v;
+                if (xx >= 0 && xx < a.W) r = fmaf(b.wx[v], __ldg(p + yy * a.W + xx), r);
+            }
+            s = fmaf(b.wy[u], r, s);
+        }
+        a.y[((long long)n * a.C + c) * P + q] = s;
+    }
+}
+
+// block reduction of NV fp32 values into fp64 partial slot `out` (thread 0 writes)
+template <int NV>
+RS_DEV void block_partial(float (&v)[NV], double *out) {
+    __shared__ float red[kVT / 32][NV];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; k++) {
+        const float s = warp_sum(v[k]);
+        if (lane == 0) red[w][k] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < NV) {
+        double s = 0.0;
+        for (int ww = 0; ww < kVT / 32; ww++) s += (double)red[ww][threadIdx.x];
+        out[threadIdx.x] = s;
+    }
+}
+
+__global__ void __launch_bounds__(kVT) bicubic_bwd(StnArgs a, double *part) {
+    const int P = a.Ho * a.Wo, HW = a.H * a.W;
+    const int q = blockIdx.x * kVT + threadIdx.x;
+    const int n = blockIdx.y;
+    float dth[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (q < P) {
+        const int i = q / a.Wo, j = q - i * a.Wo;
+        const Bicubic b = bicubic_at(a.theta, n, i, j, a.H, a.W, a.Ho, a.Wo, a.ac);
+        float gix = 0.f, giy = 0.f;
+        for (int c = 0; c < a.C; c++) {
+            const float g = __ldg(a.dy + ((long long)n * a.C + c) * P + q);
+            const float *p = a.x + ((long long)n * a.C + c) * HW;
+            float *d = a.dx ? a.dx + ((long long)n * a.C + c) * HW : nullptr;
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int yy = b.y0 - 1 + u;
+                if (yy < 0 || yy >= a.H) continue;
+#pragma unroll
+                for (int v = 0; v < 4; v++) {
+                    const int xx = b.x0 - 1 + v;
+                    if (xx < 0 || xx >= a.W) continue;
+                    if (d) red_add(d + yy * a.W + xx, g * b.wy[u] * b.wx[v]);
+                    if (a.dtheta) {
+                        const float val = __ldg(p + yy * a.W + xx);
+                        gix = fmaf(g * b.wy[u] * b.dwx[v], val, gix);
+                        giy = fmaf(g * b.dwy[u] * b.wx[v], val, giy);
+                    }
+                }
+            }
+        }
+        const float sx = a.ac ? 0.5f * (a.W - 1) : 0.5f * a.W, sy = a.ac ? 0.5f * (a.H - 1) : 0.5f * a.H;
+        const float gx = gix * sx, gy = giy * sy, xt = (float)b.xt, yt = (float)b.yt;
+        dth[0] = gx * xt; dth[1] = gx * yt; dth[2] = gx;
+        dth[3] = gy * xt; dth[4] = gy * yt; dth[5] = gy;
+    }
+    if (a.dtheta) block_partial<6>(dth, part + ((long long)n * gridDim.x + blockIdx.x) * 6);
+}
+
+// ----------------------------------------------------------------- 3-D
+struct Vol {
+    int N, C, D, H, W, Do, Ho, Wo, ac;
+    const float *x, *theta, *dy;
+    float *y, *dx, *dtheta;
+};
+
+struct Tri {
+    int x0, y0, z0;
+    float f[3];
+    double t[3];
+};
+
+RS_DEV Tri tri_at(const Vol &a, int n, int k, int i, int j) {
+    Tri r;
+    r.t[0] = stn_norm(j, a.Wo, a.ac);
+    r.t[1] = stn_norm(i, a.Ho, a.ac);
+    r.t[2] = stn_norm(k, a.Do, a.ac);
+    const float *th = a.theta + 12 * n;
+    const int L[3] = {a.W, a.H, a.D};
+    int c0[3];
+#pragma unroll
+    for (int d = 0; d < 3; d++) {
+        // ((t0 x + t1 y) + t2 z) + t3, the oracle's order
+        const double g = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(__ldg(th + 4 * d), r.t[0]),
+                                                       __dmul_rn(__ldg(th + 4 * d + 1), r.t[1])),
+                                             __dmul_rn(__ldg(th + 4 * d + 2), r.t[2])),
+                                   (double)__ldg(th + 4 * d + 3));
+        const double pcoord = stn_unnorm(g, L[d], a.ac);
+        const Cell cc = cell_of(pcoord);
+        c0[d] = cc.i0;
+        r.f[d] = cc.f;
+    }
+    r.x0 = c0[0];
+    r.y0 = c0[1];
+    r.z0 = c0[2];
+    return r;
+}
+
+__global__ void __launch_bounds__(kVT) stn3d_fwd_k(Vol a) {
+    const int P = a.Do * a.Ho * a.Wo;
+    const long long V = (long long)a.D * a.H * a.W;
+    const int q = blockIdx.x * kVT + threadIdx.x;
+    if (q >= P) return;
+    const int n = blockIdx.y;
+    const int k = q / (a.Ho * a.Wo), rem = q - k * a.Ho * a.Wo, i = rem / a.Wo, j = rem - i * a.Wo;
+    const Tri r = tri_at(a, n, k, i, j);
+    for (int c = 0; c < a.C; c++) {
+        const float *p = a.x + ((long long)n * a.C + c) * V;
+        float s = 0.f;
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+            const int ax = e & 1, by = (e >> 1) & 1, dz = e >> 2;
+            const int xx = r.x0 + ax, yy = r.y0 + by, zz = r.z0 + dz;
+            if (xx < 0 || xx >= a.W || yy < 0 || yy >= a.H || zz < 0 || zz >= a.D) continue;
+            const float w = (ax ? r.f[0] : 1.f - r.f[0]) * (by ? r.f[1] : 1.f - r.f[1]) * (dz ? r.f[2] : 1.f - r.f[2]);
+            s = fmaf(w, __ldg(p + ((long long)zz * a.H + yy) * a.W + xx), s);
+        }
+        a.y[((long long)n * a.C + c) * P + q] = s;
+    }
+}
+
+__global__ void __launch_bounds__(kVT) stn3d_bwd_k(Vol a, double *part) {
+    const int P = a.Do * a.Ho * a.Wo;
+    const long long V = (long long)a.D * a.H * a.W;
+    const int q = blockIdx.x * kVT + threadIdx.x;
+    const int n = blockIdx.y;
+    float dth[12];
+#pragma unroll
+    for (int e = 0; e < 12; e++) dth[e] = 0.f;
+    if (q < P) {
+        const int k = q / (a.Ho * a.Wo), rem = q - k * a.Ho * a.Wo, i = rem / a.Wo, j = rem - i * a.Wo;
+        const Tri r = tri_at(a, n, k, i, j);
+        float gq[3] = {0.f, 0.f, 0.f};
+        for (int c = 0; c < a.C; c++) {
+            const float g = __ldg(a.dy + ((long long)n * a.C + c) * P + q);
+            const float *p = a.x + ((long long)n * a.C + c) * V;
+            float *d = a.dx ? a.dx + ((long long)n * a.C + c) * V : nullptr;
+#pragma unroll
+            for (int e = 0; e < 8; e++) {
+                const int ax = e & 1, by = (e >> 1) & 1, dz = e >> 2;
+                const int xx = r.x0 + ax, yy = r.y0 + by, zz = r.z0 + dz;
+                if (xx < 0 || xx >= a.W || yy < 0 || yy >= a.H || zz < 0 || zz >= a.D) continue;
+                const float wx = ax ? r.f[0] : 1.f - r.f[0], wy = by ? r.f[1] : 1.f - r.f[1],
+                            wz = dz ? r.f[2] : 1.f - r.f[2];
+                const long long o = ((long long)zz * a.H + yy) * a.W + xx;
+                if (d) red_add(d + o, g * wx * wy * wz);
+                if (a.dtheta) {
+                    const float gv = g * __ldg(p + o);
+                    gq[0] = fmaf(gv * (ax ? 1.f : -1.f), wy * wz, gq[0]);
+                    gq[1] = fmaf(gv * (by ? 1.f : -1.f), wx * wz, gq[1]);
+                    gq[2] = fmaf(gv * (dz ? 1.f : -1.f), wx * wy, gq[2]);
+                }
+            }
+        }
+        const int L[3] = {a.W, a.H, a.D};
+#pragma unroll
+        for (int d = 0; d < 3; d++) {
+            const float gg = gq[d] * (a.ac ? 0.5f * (L[d] - 1) : 0.5f * L[d]);
+            dth[4 * d] = gg * (float)r.t[0];
+            dth[4 * d + 1] = gg * (float)r.t[1];
+            dth[4 * d + 2] = gg * (float)r.t[2];
+            dth[4 * d + 3] = gg;
+        }
+    }
+    if (a.dtheta) block_partial<12>(dth, part + ((long long)n * gridDim.x + blockIdx.x) * 12);
+}
+
+// dtheta[n][e] = fixed-order fp64 sum over the sample's block partials
+__global__ void theta_finalize(const double *part, int nb, int ne, float *dtheta) {
+    const int n = blockIdx.x, e = threadIdx.x;
+    if (e >= ne) return;
+    double s = 0.0;
+    for (int b = 0; b < nb; b++) s += part[((long long)n * nb + b) * ne + e];
+    dtheta[n * ne + e] = (float)s;
+}
+
+}  // namespace
+
+size_t stn_var_ws_bytes(int N, int P, int ne) {
+    return sizeof(double) * (size_t)N * ((P + kVT - 1) / kVT) * ne;
+}
+
+cudaError_t stn_bicubic_launch(const StnArgs &a, bool bwd, void *ws, cudaStream_t s) {
+    const int P = a.Ho * a.Wo;
+    const dim3 grid((P + kVT - 1) / kVT, a.N);
+    if (!bwd) {
+        bicubic_fwd<<<grid, kVT, 0, s>>>(a);
+        note_launch();
+        return cudaGetLastError();
+    }
+    if (a.dx) {
+        cudaError_t e = cudaMemsetAsync(a.dx, 0, sizeof(float) * (size_t)a.N * a.C * a.H * a.W, s);
+        if (e != cudaSuccess) return e;
+    }
+    bicubic_bwd<<<grid, kVT, 0, s>>>(a, (double *)ws);
+    note_launch();
+    if (a.dtheta) {
+        theta_finalize<<<a.N, 32, 0, s>>>((const double *)ws, grid.x, 6, a.dtheta);
+        note_launch();
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t stn3d_launch(const float *x, const float *theta, const float *dy, float *y, float *dx, float *dtheta,
+                         int N, int C, int D, int H, int W, int Do, int Ho, int Wo, int ac, bool bwd, void *ws,
+                         cudaStream_t s) {
+    Vol a{N, C, D, H, W, Do, Ho, Wo, ac, x, theta, dy, y, dx, dtheta};
+    const int P = Do * Ho * Wo;
+    const dim3 grid((P + kVT - 1) / kVT, N);
+    if (!bwd) {
+        stn3d_fwd_k<<<grid, kVT, 0, s>>>(a);
+        note_launch();
+        return cudaGetLastError();
+    }
+    if (dx) {
+        cudaError_t e = cudaMemsetAsync(dx, 0, sizeof(float) * (size_t)N * C * D * H * W, s);
+        if (e != cudaSuccess) return e;
+    }
+    stn3d_bwd_k<<<grid, kVT, 0, s>>>(a, (double *)ws);
+    note_launch();
+    if (dtheta) {
+        theta_finalize<<<N, 32, 0, s>>>((const double *)ws, grid.x, 12, dtheta);
+        note_launch();
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace rs

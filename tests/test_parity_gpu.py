@@ -637,3 +637,58 @@ def test_upsample4_pair(cuda_device, shape):
     assert torch.equal(y.cpu(), torch.from_numpy(oracle.upsample4_fwd(x.double().numpy())).float())
     dx = rsgrad.upsample4_bwd(dy.to(cuda_device))
     assert_close(_np(dx), oracle.upsample4_bwd(dy.double().numpy()), "grad", "upsample dx")
+
+
+# ============================================================================ STN variants (§8(f) f3)
+def _var_theta(N, rows, seed):
+    g = torch.Generator().manual_seed(seed)
+    th = torch.zeros(N, rows, rows + 1, dtype=torch.float64)
+    for n in range(N):
+        s = 0.8 + 0.4 * torch.rand(1, generator=g, dtype=torch.float64)
+        th[n, :, :rows] = torch.eye(rows, dtype=torch.float64) * s + \
+            (torch.rand(rows, rows, generator=g, dtype=torch.float64) - 0.5) * 0.5
+        th[n, :, rows] = (torch.rand(rows, generator=g, dtype=torch.float64) - 0.5) * 0.4
+    return th.float()
+
+
+@pytest.mark.parametrize("dims", [(2, 3, 37, 45, 30, 52), (1, 16, 64, 64, 64, 64), (1, 1, 5, 4, 3, 7)])
+@pytest.mark.parametrize("ac", [True, False])
+def test_stn_bicubic_parity(cuda_device, dims, ac):
+    N, C, H, W, Ho, Wo = dims
+    g = torch.Generator().manual_seed(31)
+    x = torch.randn(N, C, H, W, generator=g, dtype=torch.float64).float()
+    dy = torch.randn(N, C, Ho, Wo, generator=g, dtype=torch.float64).float()
+    th = _var_theta(N, 2, 32)
+    y = rsgrad.stn_bicubic_fwd(x.to(cuda_device), th.to(cuda_device), Ho, Wo, align_corners=ac)
+    dx, dth = rsgrad.stn_bicubic_bwd(x.to(cuda_device), th.to(cuda_device), dy.to(cuda_device), align_corners=ac)
+    xn, tn, dn = x.double().numpy(), th.double().numpy(), dy.double().numpy()
+    assert_close(_np(y), oracle.stn_bicubic_fwd(xn, tn, Ho, Wo, ac), "fwd", "y")
+    rdx, rdth = oracle.stn_bicubic_bwd(xn, tn, dn, ac)
+    assert_close(_np(dx), rdx, "grad", "dx")
+    assert_close(_np(dth), rdth, "grad", "dtheta")
+
+
+@pytest.mark.parametrize("dims", [(2, 2, 9, 11, 13, 8, 12, 10), (1, 4, 32, 32, 32, 32, 32, 32), (1, 1, 2, 3, 4, 2, 2, 2)])
+@pytest.mark.parametrize("ac", [True, False])
+def test_stn3d_parity(cuda_device, dims, ac):
+    N, C, D, H, W, Do, Ho, Wo = dims
+    g = torch.Generator().manual_seed(33)
+    x = torch.randn(N, C, D, H, W, generator=g, dtype=torch.float64).float()
+    dy = torch.randn(N, C, Do, Ho, Wo, generator=g, dtype=torch.float64).float()
+    th = _var_theta(N, 3, 34)
+    y = rsgrad.stn3d_fwd(x.to(cuda_device), th.to(cuda_device), (Do, Ho, Wo), align_corners=ac)
+    dx, dth = rsgrad.stn3d_bwd(x.to(cuda_device), th.to(cuda_device), dy.to(cuda_device), align_corners=ac)
+    xn, tn, dn = x.double().numpy(), th.double().numpy(), dy.double().numpy()
+    assert_close(_np(y), oracle.stn3d_fwd(xn, tn, (Do, Ho, Wo), ac), "fwd", "y")
+    rdx, rdth = oracle.stn3d_bwd(xn, tn, dn, ac)
+    assert_close(_np(dx), rdx, "grad", "dx")
+    assert_close(_np(dth), rdth, "grad", "dtheta")
+
+
+def test_stn_variants_refuse_border_and_gather(cuda_device):
+    x = torch.zeros(1, 1, 8, 8, device=cuda_device)
+    th = torch.zeros(1, 2, 3, device=cuda_device)
+    o = rsgrad._opts(True, "border")
+    y = torch.empty_like(x)
+    assert rsgrad.lib().stn_bicubic_fwd(rsgrad._ptr(x), rsgrad._ptr(th), 1, 1, 8, 8, 8, 8,
+                                        __import__("ctypes").byref(o), rsgrad._ptr(y), None) == -4
