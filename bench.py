@@ -368,6 +368,31 @@ def next_rows(rs, peak):
     out["f4_upsample4_1x3x400x640"] = {"fwd_us": round(tu_f * 1e6, 1), "bwd_us": round(tu_b * 1e6, 1),
                                        "fwd_hbm_frac": round(bu / tu_f / 1e9 / peak, 3),
                                        "bwd_hbm_frac": round(bu / tu_b / 1e9 / peak, 3)}
+    # f3: bicubic STN at the paper's STN shape (4 x 16 x 512^2) and a volumetric STN
+    import synth
+    si = synth.stn_inputs(4, 16, 512, 512, cfg=2, device=dev)
+    yb, dxb, dtb = torch.empty_like(si["dy"]), torch.empty_like(si["x"]), torch.empty_like(si["theta"])
+    tbf = med(lambda: rs.stn_bicubic_fwd(si["x"], si["theta"], out=yb))
+    tbb = med(lambda: rs.stn_bicubic_bwd(si["x"], si["theta"], si["dy"], out=(dxb, dtb)))
+    P = 4 * 512 * 512
+    out["f3_stn_bicubic_4x16x512x512"] = {
+        "fwd_us": round(tbf * 1e6, 1), "bwd_us": round(tbb * 1e6, 1),
+        "fwd_bwd_mpix_s": round(P / (tbf + tbb) / 1e6, 1),
+        "fwd_roofline_frac": round(BYTES[("stn", "fwd")](16) * P / tbf / 1e9 / peak, 3),
+        "bwd_roofline_frac": round(BYTES[("stn", "bwd")](16) * P / tbb / 1e9 / peak, 3)}
+    del si, yb, dxb
+    x3 = torch.randn(2, 4, 96, 96, 96, device=dev, generator=g)
+    d3 = torch.randn(2, 4, 96, 96, 96, device=dev, generator=g)
+    th3 = torch.eye(3, 4, device=dev).expand(2, 3, 4).contiguous() + 0.05 * torch.randn(2, 3, 4, device=dev, generator=g)
+    y3, dx3, dt3 = torch.empty_like(x3), torch.empty_like(x3), torch.empty_like(th3)
+    t3f = med(lambda: rs.stn3d_fwd(x3, th3, out=y3))
+    t3b = med(lambda: rs.stn3d_bwd(x3, th3, d3, out=(dx3, dt3)))
+    P3 = 2 * 96 ** 3
+    out["f3_stn3d_2x4x96^3"] = {
+        "fwd_us": round(t3f * 1e6, 1), "bwd_us": round(t3b * 1e6, 1),
+        "fwd_bwd_mvox_s": round(P3 / (t3f + t3b) / 1e6, 1),
+        "fwd_roofline_frac": round(8.0 * 4 * P3 / t3f / 1e9 / peak, 3),
+        "bwd_roofline_frac": round(12.0 * 4 * P3 / t3b / 1e9 / peak, 3)}
     del fl
     return {"l2": "flushed (256 MB write) before every call; median of 10", "rows": out}
 

@@ -1,7 +1,5 @@
-timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -3 gpurun_out/pytest_gpu.log
-python -c "import __graft_entry__ as g; g.smoke(); print('SMOKE OK')" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
-python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench=$?
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 > gpurun_out/b_ncu.log 2>&1; echo ncu=$?
-PROF_CMD="python scripts/bench_next.py" bash scripts/gpurun_prof.sh convp "conv_direct|conv_dk_partial|conv_dx_atomic" 2 RS_X=1
-rm -f gpurun_out/*.ncu-rep
-cat gpurun_out/bench.json
+timeout 900 python -m pytest tests -m gpu -q -k "conv or upsample or bicubic or stn3d or variants" > gpurun_out/pytest_f.log 2>&1; echo pytest=$?; tail -15 gpurun_out/pytest_f.log
+python -c "
+import bench, json
+from paper_1904_12228_b200 import rsgrad as rs
+print(json.dumps(bench.next_rows(rs, bench.peak_hbm()[0]), indent=1))" > gpurun_out/next.json 2>&1; cat gpurun_out/next.json
