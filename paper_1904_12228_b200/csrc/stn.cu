@@ -45,7 +45,10 @@ constexpr int kThreads = 256;
 
 // forward tiles
 constexpr int kFJ = 32;                   // output tile width (px)
-constexpr int kFIfwd = 32, kFIdth = 16;   // output tile rows: forward / d_theta (measured)
+#ifndef RS_FIFWD
+#define RS_FIFWD 32
+#endif
+constexpr int kFIfwd = RS_FIFWD, kFIdth = 16;  // output tile rows: forward / d_theta (measured)
 constexpr int kFRMax = 128;               // max staged input rows
 constexpr int kFStage = 6144;             // floats per pipeline stage
 
@@ -193,6 +196,7 @@ __global__ void __launch_bounds__(FAST ? kOTFast : kThreads, FAST ? kOTFastMinB 
                  double *__restrict__ partials, int tiles_j, int tiles_i) {
     constexpr int kOT = FAST ? kOTFast : kThreads, kOW = kOT / 32;  // threads, warps
     constexpr int kFP = kFI / kOW;  // output pixels per thread
+    static_assert(kFI % kOW == 0, "every tile row needs a warp: tile rows must be a multiple of the warps");
     extern __shared__ __align__(16) float4 sm4[];
     int *rlo = (int *)sm4;
     int *rhi = rlo + kFRMax;
