@@ -209,9 +209,14 @@ rs_status upsample4_bwd(const float *dy, int N, int C, int H, int W, float *dx, 
  * STN variants ("changing the interpolation scheme
  * ... or interpolating over more dimensions").  Device pointers only; zeros padding
  * only (opts.padding = RS_PAD_BORDER => RS_ERR_FLAG); opts.align_corners as stn_*.
- * d_input is the atomic scatter (memset + red.global.add; SCATTER_ATOMIC semantics,
- * not deterministic; GATHER / SCATTER_PRIV / deterministic=1 => RS_ERR_FLAG); d_theta
- * is a fixed-order fp64 sum of per-block partials.
+ * d_theta is a fixed-order fp64 sum of per-block partials.  d_input:
+ *   stn_bicubic_bwd  GATHER or deterministic=1: the converted gather -- each input pixel
+ *                    enumerates the affine preimage of (x-2, x+2) x (y-2, y+2) with exact
+ *                    fp64 membership (a singular map or a window > 1024 output pixels
+ *                    falls back to reds for that sample); AUTO / SCATTER_ATOMIC: memset +
+ *                    red.global.add per tap in the d_theta pass (measured faster).
+ *   stn3d_bwd        the atomic scatter only (GATHER / deterministic=1 => RS_ERR_FLAG).
+ * SCATTER_PRIV => RS_ERR_FLAG.
  *   stn_bicubic_*  theta N x 2 x 3, x N x C x H x W, y N x C x Ho x Wo: Keys' cubic
  *                  convolution (A = -0.75) over the 4 x 4 taps floor(i)-1 .. floor(i)+2
  *                  (= torch grid_sample mode='bicubic', zeros; R12).
@@ -232,7 +237,8 @@ rs_status stn3d_bwd(const float *x, const float *theta, const float *dy, int N, 
 /* Workspace (bytes) *_bwd wants for these shapes.  layer: 0 = STN (uses
  * N,C,H,W,Ho,Wo), 1 = warp (N,C,H,W), 2 = bslice (N,H,W,D,Gh,Gw), 3 = conv
  * (N, C = Ci, H, W, D = Co, Gh = kh, Gw = kw), 4 = convloss_grad (N, H, W: the
- * RS_SCHED_ROOT residual), 5 = stn_bicubic (N, Ho, Wo), 6 = stn3d (N, Ho, Wo, D = Do);
+ * RS_SCHED_ROOT residual), 5 = stn_bicubic (N, Ho, Wo: d_theta partials, coordinate
+ * tables, N fallback flags), 6 = stn3d (N, Ho, Wo, D = Do);
  * unused arguments are ignored.
  * Returns 0 for an unknown layer.  DESIGN.md "Workspace". */
 size_t rsgrad_bwd_workspace_bytes(int layer, int N, int C, int H, int W, int Ho, int Wo, int D,

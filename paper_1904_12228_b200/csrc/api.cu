@@ -254,7 +254,7 @@ size_t rsgrad_bwd_workspace_bytes(int layer, int N, int C, int H, int W, int Ho,
             return rs::convloss_ws_bytes(N, H, W);
         case 5:
             if (!pos(N) || !pos(Ho) || !pos(Wo)) return 0;
-            return rs::stn_var_ws_bytes(N, Ho * Wo, 6);
+            return rs::stn_bicubic_ws_bytes(N, Ho, Wo);
         case 6:
             if (!pos(N) || !pos(Ho) || !pos(Wo) || !pos(D)) return 0;
             return rs::stn_var_ws_bytes(N, D * Ho * Wo, 12);
@@ -587,12 +587,17 @@ rs_status upsample4_bwd(const float *dy, int N, int C, int H, int W, float *dx, 
 }
 
 // ------------------------------------------------------------------------------ f3
-static rs_status var_check(const rs_opts &o, bool bwd, bool has_dx, std::initializer_list<const void *> ptrs) {
+static rs_status var_check(const rs_opts &o, bool bwd, bool has_dx, std::initializer_list<const void *> ptrs,
+                           bool has_gather = false) {
     rs_status st = check_opts(o);
     if (st != RS_OK) return st;
     if (o.padding != RS_PAD_ZEROS) return fail(RS_ERR_FLAG, "stn variants: zeros padding only");
-    if (bwd && has_dx && (o.algo == RS_ALGO_GATHER || o.algo == RS_ALGO_SCATTER_PRIV || o.deterministic))
-        return fail(RS_ERR_FLAG, "stn variants: d_input is the atomic scatter only (not deterministic)");
+    if (bwd && has_dx && o.algo == RS_ALGO_SCATTER_PRIV)
+        return fail(RS_ERR_FLAG, "stn variants: SCATTER_PRIV is not implemented");
+    if (bwd && has_dx && !has_gather && (o.algo == RS_ALGO_GATHER || o.deterministic))
+        return fail(RS_ERR_FLAG, "stn3d: d_input is the atomic scatter only (not deterministic)");
+    if (bwd && has_dx && o.algo == RS_ALGO_SCATTER_ATOMIC && o.deterministic)
+        return fail(RS_ERR_FLAG, "stn variants: the atomic scatter is not deterministic");
     for (const void *p : ptrs)
         if (p && !is_device_ptr(p)) return fail(RS_ERR_FLAG, "stn variants: device pointers only");
     return RS_OK;
@@ -624,7 +629,7 @@ rs_status stn_bicubic_fwd(const float *x, const float *theta, int N, int C, int 
     rs::StnArgs a{};
     a.x = x; a.theta = theta; a.y = y;
     a.N = N; a.C = C; a.H = H; a.W = W; a.Ho = Ho; a.Wo = Wo; a.ac = o.align_corners;
-    return launched(rs::stn_bicubic_launch(a, false, nullptr, (cudaStream_t)stream), "stn_bicubic_fwd");
+    return launched(rs::stn_bicubic_launch(a, false, 0, nullptr, (cudaStream_t)stream), "stn_bicubic_fwd");
 }
 
 rs_status stn_bicubic_bwd(const float *x, const float *theta, const float *dy, int N, int C, int H, int W, int Ho,
@@ -634,14 +639,17 @@ rs_status stn_bicubic_bwd(const float *x, const float *theta, const float *dy, i
     rs_status st = stn_validate(x, theta, N, C, H, W, Ho, Wo, o);
     if (st != RS_OK) return st;
     if (!dy) return fail(RS_ERR_NULL, "stn_bicubic_bwd: dy is required");
-    if ((st = var_check(o, true, dx != nullptr, {x, theta, dy, dx, dtheta})) != RS_OK) return st;
+    if ((st = var_check(o, true, dx != nullptr, {x, theta, dy, dx, dtheta}, true)) != RS_OK) return st;
     if (!dx && !dtheta) return ok();
     rs::StnArgs a{};
     a.x = x; a.theta = theta; a.dy = dy; a.dx = dx; a.dtheta = dtheta;
     a.N = N; a.C = C; a.H = H; a.W = W; a.Ho = Ho; a.Wo = Wo; a.ac = o.align_corners;
     cudaStream_t s = (cudaStream_t)stream;
-    return with_ws(dtheta ? rs::stn_var_ws_bytes(N, Ho * Wo, 6) : 0, workspace, ws_bytes, s,
-                   [&](void *ws) { return rs::stn_bicubic_launch(a, true, ws, s); }, "stn_bicubic_bwd");
+    return with_ws(rs::stn_bicubic_ws_bytes(N, Ho, Wo), workspace, ws_bytes, s,
+                   [&](void *ws) {
+                       return rs::stn_bicubic_launch(a, true, o.deterministic ? (int)RS_ALGO_GATHER : (int)o.algo, ws, s);
+                   },
+                   "stn_bicubic_bwd");
 }
 
 static rs_status stn3d_validate(const float *x, const float *theta, int N, int C, int D, int H, int W, int Do, int Ho,

@@ -331,7 +331,8 @@ cudaError_t convloss_grad_launch(const float *in, const float *hk, const float *
 cudaError_t upsample4_launch(const float *src, float *dst, int N, int C, int H, int W, bool bwd, cudaStream_t s);
 
 size_t stn_var_ws_bytes(int N, int P, int ne);
-cudaError_t stn_bicubic_launch(const StnArgs &a, bool bwd, void *ws, cudaStream_t s);
+size_t stn_bicubic_ws_bytes(int N, int Ho, int Wo);
+cudaError_t stn_bicubic_launch(const StnArgs &a, bool bwd, int algo, void *ws, cudaStream_t s);
 cudaError_t stn3d_launch(const float *x, const float *theta, const float *dy, float *y, float *dx, float *dtheta,
                          int N, int C, int D, int H, int W, int Do, int Ho, int Wo, int ac, bool bwd, void *ws,
                          cudaStream_t s);

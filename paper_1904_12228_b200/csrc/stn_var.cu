@@ -6,9 +6,11 @@
 //   3-D STN       volumetric affine_grid (theta 3 x 4) + trilinear sampling.
 // Coordinates are evaluated in fp64 in the oracle's order (P1); tap weights and their
 // derivatives in fp64, rounded to fp32 for the per-channel data arithmetic.
-// Forward: thread per output pixel, taps through L1.  Adjoint: d_input by the
-// general scatter with atomics (no converted gather yet: PAPER.md:733's fallback),
-// d_theta per pixel -> warp -> block (fp32) -> fp64 block partials -> fixed-order sum.
+// Forward: thread per output pixel, taps through L1.  Adjoint: d_theta per pixel ->
+// warp -> block (fp32) -> fp64 block partials -> fixed-order sum; d_input of the bicubic
+// STN by the converted gather over the affine preimage (bicubic_dx_gather: GATHER or
+// deterministic=1) or the general scatter with atomics (AUTO / SCATTER_ATOMIC, and the 3-D
+// STN: PAPER.md:733's fallback).
 #include "common.cuh"
 
 namespace rs {
@@ -98,10 +100,127 @@ RS_DEV void block_partial(float (&v)[NV], double *out) {
     }
 }
 
-__global__ void __launch_bounds__(kVT) bicubic_bwd(StnArgs a, double *part) {
+// cubic weight of tap k (0..3 = floor - 1 .. floor + 2) at fraction t, the same fp64
+// expressions as cubic_w (so both adjoint forms use identical fp32 weights)
+RS_DEV float cubic_tap(double t, int k) {
+    const double A = -0.75;
+    if (k == 1 || k == 2) {
+        const double x = k == 1 ? t : 1.0 - t;
+        return (float)__dadd_rn(__dmul_rn(__dmul_rn(__dsub_rn(__dmul_rn(A + 2.0, x), A + 3.0), x), x), 1.0);
+    }
+    const double x = k == 0 ? t + 1.0 : 2.0 - t;
+    return (float)__dsub_rn(__dmul_rn(__dadd_rn(__dmul_rn(__dsub_rn(__dmul_rn(A, x), 5.0 * A), x), 8.0 * A), x),
+                            4.0 * A);
+}
+
+// red.global.add without a compiler memory clobber: the adjoint kernels below only read
+// inputs that never alias the reduced output (API contract), so their loads may be
+// scheduled across the reds
+RS_DEV void red_add_nc(float *addr, float v) {
+    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(v));
+}
+
+// Real-arithmetic output -> input pixel map of sample n and its inverse (bounds only;
+// membership is decided with the exact fp64 coordinate).
+struct Aff {
+    double m00, m01, m10, m11, p0x, p0y, i00, i01, i10, i11;
+    bool ok;
+};
+
+RS_DEV Aff aff_of(const float *theta, int n, int H, int W, int Ho, int Wo, int ac) {
+    const float *t = theta + 6 * n;
+    const double t0 = __ldg(t), t1 = __ldg(t + 1), t2 = __ldg(t + 2), t3 = __ldg(t + 3), t4 = __ldg(t + 4),
+                 t5 = __ldg(t + 5);
+    const double ax = ac ? 2.0 / (Wo - 1) : 2.0 / Wo, bx = ac ? -1.0 : 1.0 / Wo - 1.0;
+    const double ay = ac ? 2.0 / (Ho - 1) : 2.0 / Ho, by = ac ? -1.0 : 1.0 / Ho - 1.0;
+    const double sx = ac ? 0.5 * (W - 1) : 0.5 * W, ox = ac ? 0.0 : -0.5;
+    const double sy = ac ? 0.5 * (H - 1) : 0.5 * H, oy = ac ? 0.0 : -0.5;
+    Aff A;
+    A.m00 = sx * t0 * ax; A.m01 = sx * t1 * ay;
+    A.m10 = sy * t3 * ax; A.m11 = sy * t4 * ay;
+    A.p0x = sx * (t0 * bx + t1 * by + t2 + 1.0) + ox;
+    A.p0y = sy * (t3 * bx + t4 * by + t5 + 1.0) + oy;
+    const double det = A.m00 * A.m11 - A.m01 * A.m10;
+    const double scale = fabs(A.m00 * A.m11) + fabs(A.m01 * A.m10);
+    A.ok = isfinite(det) && fabs(det) > 1e-9 * (scale > 0 ? scale : 1.0) && fabs(det) > 1e-12;
+    const double id = A.ok ? 1.0 / det : 0.0;
+    A.i00 = A.m11 * id; A.i01 = -A.m01 * id;
+    A.i10 = -A.m10 * id; A.i11 = A.m00 * id;
+    return A;
+}
+
+constexpr int kGCH = 16;        // channels per pass of the bicubic gather
+constexpr int kGWinMax = 1024;  // candidate output pixels per input pixel (else atomic)
+
+// Bicubic d_input as a GATHER (scatter-to-gather by affine inversion):
+// input pixel (x, y) collects the output pixels whose sample point lies in
+// (x-2, x+2) x (y-2, y+2) -- the preimage of that square under the affine map,
+// enumerated over its bounding box with exact fp64 membership.  Deterministic, no
+// memset.  A sample whose map is singular or whose window is too large is flagged:
+// its dX is zeroed here and bicubic_bwd adds it by reds.
+// exact normalised coordinates of every output column / row (stn_norm has fp64 divisions)
+__global__ void norm_tables(double *xt, double *yt, int Ho, int Wo, int ac) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < Wo) xt[t] = stn_norm(t, Wo, ac);
+    if (t < Ho) yt[t] = stn_norm(t, Ho, ac);
+}
+
+__global__ void __launch_bounds__(kVT)
+    bicubic_dx_gather(StnArgs a, int *flags, const double *__restrict__ xtab, const double *__restrict__ ytab) {
+    const int HW = a.H * a.W, P = a.Ho * a.Wo;
+    const int n = blockIdx.y;
+    const int idx = blockIdx.x * kVT + threadIdx.x;
+    const Aff A = aff_of(a.theta, n, a.H, a.W, a.Ho, a.Wo, a.ac);
+    const double eps = 1e-6;
+    const double hj = 2.0 * (fabs(A.i00) + fabs(A.i01)) + eps, hi = 2.0 * (fabs(A.i10) + fabs(A.i11)) + eps;
+    const bool ok = A.ok && (2.0 * hj + 2.0) * (2.0 * hi + 2.0) <= (double)kGWinMax;
+    if (!ok && blockIdx.x == 0 && threadIdx.x == 0) flags[n] = 1;
+    if (idx >= HW) return;
+    const int y = idx / a.W, x = idx - y * a.W;
+    float *dxn = a.dx + (long long)n * a.C * HW + idx;
+    if (!ok) {
+        for (int c = 0; c < a.C; c++) dxn[(long long)c * HW] = 0.f;
+        return;
+    }
+    const float *t = a.theta + 6 * n;
+    const double T0 = __ldg(t), T1 = __ldg(t + 1), T2 = __ldg(t + 2), T3 = __ldg(t + 3), T4 = __ldg(t + 4),
+                 T5 = __ldg(t + 5);
+    const double ux = (double)x - A.p0x, uy = (double)y - A.p0y;
+    const double qj = A.i00 * ux + A.i01 * uy, qi = A.i10 * ux + A.i11 * uy;
+    const int jlo = max(0, (int)ceil(qj - hj)), jhi = min(a.Wo - 1, (int)floor(qj + hj));
+    const int ilo = max(0, (int)ceil(qi - hi)), ihi = min(a.Ho - 1, (int)floor(qi + hi));
+    const float *gn = a.dy + (long long)n * a.C * P;
+    for (int c0 = 0; c0 < a.C; c0 += kGCH) {
+        float acc[kGCH];
+#pragma unroll
+        for (int c = 0; c < kGCH; c++) acc[c] = 0.f;
+        for (int i = ilo; i <= ihi; i++) {
+            const double yt = __ldg(ytab + i);
+            for (int j = jlo; j <= jhi; j++) {
+                const double xt = __ldg(xtab + j);
+                const double ix = stn_unnorm(affine3(T0, T1, T2, xt, yt), a.W, a.ac);
+                const double iy = stn_unnorm(affine3(T3, T4, T5, xt, yt), a.H, a.ac);
+                const double fx = floor(ix), fy = floor(iy);
+                const int kx = x - ((int)fx - 1), ky = y - ((int)fy - 1);
+                if (kx < 0 || kx > 3 || ky < 0 || ky > 3) continue;
+                const float w = cubic_tap(__dsub_rn(iy, fy), ky) * cubic_tap(__dsub_rn(ix, fx), kx);
+                const float *g = gn + (long long)c0 * P + i * a.Wo + j;
+#pragma unroll
+                for (int c = 0; c < kGCH; c++)
+                    if (c0 + c < a.C) acc[c] = fmaf(w, __ldg(g + (long long)c * P), acc[c]);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < kGCH; c++)
+            if (c0 + c < a.C) dxn[(long long)(c0 + c) * HW] = acc[c];
+    }
+}
+
+__global__ void __launch_bounds__(kVT) bicubic_bwd(StnArgs a, double *part, const int *flags) {
     const int P = a.Ho * a.Wo, HW = a.H * a.W;
     const int q = blockIdx.x * kVT + threadIdx.x;
     const int n = blockIdx.y;
+    if (flags && !flags[n]) a.dx = nullptr;  // d_input came from the gather
     float dth[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if (q < P) {
         const int i = q / a.Wo, j = q - i * a.Wo;
@@ -119,7 +238,7 @@ __global__ void __launch_bounds__(kVT) bicubic_bwd(StnArgs a, double *part) {
                 for (int v = 0; v < 4; v++) {
                     const int xx = b.x0 - 1 + v;
                     if (xx < 0 || xx >= a.W) continue;
-                    if (d) red_add(d + yy * a.W + xx, g * b.wy[u] * b.wx[v]);
+                    if (d) red_add_nc(d + yy * a.W + xx, g * (b.wy[u] * b.wx[v]));
                     if (a.dtheta) {
                         const float val = __ldg(p + yy * a.W + xx);
                         gix = fmaf(g * b.wy[u] * b.dwx[v], val, gix);
@@ -222,7 +341,7 @@ __global__ void __launch_bounds__(kVT) stn3d_bwd_k(Vol a, double *part) {
                 const float wx = ax ? r.f[0] : 1.f - r.f[0], wy = by ? r.f[1] : 1.f - r.f[1],
                             wz = dz ? r.f[2] : 1.f - r.f[2];
                 const long long o = ((long long)zz * a.H + yy) * a.W + xx;
-                if (d) red_add(d + o, g * wx * wy * wz);
+                if (d) red_add_nc(d + o, g * wx * wy * wz);
                 if (a.dtheta) {
                     const float gv = g * __ldg(p + o);
                     gq[0] = fmaf(gv * (ax ? 1.f : -1.f), wy * wz, gq[0]);
@@ -259,7 +378,11 @@ size_t stn_var_ws_bytes(int N, int P, int ne) {
     return sizeof(double) * (size_t)N * ((P + kVT - 1) / kVT) * ne;
 }
 
-cudaError_t stn_bicubic_launch(const StnArgs &a, bool bwd, void *ws, cudaStream_t s) {
+size_t stn_bicubic_ws_bytes(int N, int Ho, int Wo) {
+    return stn_var_ws_bytes(N, Ho * Wo, 6) + sizeof(double) * (size_t)(Ho + Wo) + sizeof(int) * (size_t)N;
+}
+
+cudaError_t stn_bicubic_launch(const StnArgs &a, bool bwd, int algo, void *ws, cudaStream_t s) {
     const int P = a.Ho * a.Wo;
     const dim3 grid((P + kVT - 1) / kVT, a.N);
     if (!bwd) {
@@ -267,14 +390,32 @@ cudaError_t stn_bicubic_launch(const StnArgs &a, bool bwd, void *ws, cudaStream_
         note_launch();
         return cudaGetLastError();
     }
-    if (a.dx) {
+    // workspace: d_theta partials, then one flag per sample (gather fallback)
+    // workspace: d_theta partials | xt[Wo], yt[Ho] | one flag per sample
+    double *part = (double *)ws;
+    double *xtab = part + stn_var_ws_bytes(a.N, P, 6) / sizeof(double), *ytab = xtab + a.Wo;
+    int *flags = (int *)(ytab + a.Ho);
+    // GATHER (or deterministic=1, passed as algo 1): the converted gather; AUTO takes the
+    // atomic scatter, measured faster here (4 x 16 x 512^2: 0.92 ms for reds + d_theta in
+    // one pass vs 0.76 ms gather + 0.70 ms d_theta pass)
+    const bool gather = a.dx && algo == 1 /*GATHER*/;
+    if (gather) {
+        cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)a.N, s);
+        if (e != cudaSuccess) return e;
+        const int nt = a.Ho > a.Wo ? a.Ho : a.Wo;
+        norm_tables<<<(nt + 255) / 256, 256, 0, s>>>(xtab, ytab, a.Ho, a.Wo, a.ac);
+        note_launch();
+        const int HW = a.H * a.W;
+        bicubic_dx_gather<<<dim3((HW + kVT - 1) / kVT, a.N), kVT, 0, s>>>(a, flags, xtab, ytab);
+        note_launch();
+    } else if (a.dx) {
         cudaError_t e = cudaMemsetAsync(a.dx, 0, sizeof(float) * (size_t)a.N * a.C * a.H * a.W, s);
         if (e != cudaSuccess) return e;
     }
-    bicubic_bwd<<<grid, kVT, 0, s>>>(a, (double *)ws);
+    bicubic_bwd<<<grid, kVT, 0, s>>>(a, part, gather ? flags : nullptr);
     note_launch();
     if (a.dtheta) {
-        theta_finalize<<<a.N, 32, 0, s>>>((const double *)ws, grid.x, 6, a.dtheta);
+        theta_finalize<<<a.N, 32, 0, s>>>(part, grid.x, 6, a.dtheta);
         note_launch();
     }
     return cudaGetLastError();

@@ -377,7 +377,10 @@ def stn_bicubic_fwd(x, theta, Ho=None, Wo=None, *, align_corners=True, out=None)
     return y
 
 
-def stn_bicubic_bwd(x, theta, dy, *, align_corners=True, need_dx=True, need_dtheta=True, out=None):
+def stn_bicubic_bwd(x, theta, dy, *, align_corners=True, algo="auto", deterministic=False, need_dx=True,
+                    need_dtheta=True, out=None):
+    """d_input by the converted gather over the affine preimage (gather, or deterministic=True)
+    or the atomic scatter (auto / scatter_atomic); d_theta by fixed-order partial sums."""
     N, C, H, W = x.shape
     Ho, Wo = dy.shape[2:]
     if out is not None:
@@ -385,7 +388,7 @@ def stn_bicubic_bwd(x, theta, dy, *, align_corners=True, need_dx=True, need_dthe
     else:
         dx = torch.empty_like(x) if need_dx else None
         dth = torch.empty((N, 2, 3), dtype=torch.float32, device=x.device) if need_dtheta else None
-    o = _opts(align_corners, "zeros", "scatter_atomic")
+    o = _opts(align_corners, "zeros", algo, deterministic)
     _check(lib().stn_bicubic_bwd(_ptr(x), _ptr(theta), _ptr(dy), N, C, H, W, Ho, Wo, ctypes.byref(o), _ptr(dx),
                                  _ptr(dth), None, 0, _stream(_device_of(x, dy))), "stn_bicubic_bwd")
     return dx, dth

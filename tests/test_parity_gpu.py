@@ -665,12 +665,34 @@ def test_stn_bicubic_parity(cuda_device, dims, ac):
     dy = torch.randn(N, C, Ho, Wo, generator=g, dtype=torch.float64).float()
     th = _var_theta(N, 2, 32)
     y = rsgrad.stn_bicubic_fwd(x.to(cuda_device), th.to(cuda_device), Ho, Wo, align_corners=ac)
-    dx, dth = rsgrad.stn_bicubic_bwd(x.to(cuda_device), th.to(cuda_device), dy.to(cuda_device), align_corners=ac)
     xn, tn, dn = x.double().numpy(), th.double().numpy(), dy.double().numpy()
     assert_close(_np(y), oracle.stn_bicubic_fwd(xn, tn, Ho, Wo, ac), "fwd", "y")
     rdx, rdth = oracle.stn_bicubic_bwd(xn, tn, dn, ac)
-    assert_close(_np(dx), rdx, "grad", "dx")
-    assert_close(_np(dth), rdth, "grad", "dtheta")
+    for algo in ("auto", "gather", "scatter_atomic"):
+        dx, dth = rsgrad.stn_bicubic_bwd(x.to(cuda_device), th.to(cuda_device), dy.to(cuda_device),
+                                         align_corners=ac, algo=algo)
+        assert_close(_np(dx), rdx, "grad", f"dx[{algo}]")
+        assert_close(_np(dth), rdth, "grad", f"dtheta[{algo}]")
+
+
+def test_stn_bicubic_gather_deterministic_and_fallback(cuda_device):
+    """The converted-gather d_input is bitwise reproducible; a singular theta (rank-1
+    map) and a 5x zoom-in (each input pixel's preimage window > 1024 output pixels) fall
+    back to the reds per sample, next to a regular sample in the same batch."""
+    g = torch.Generator().manual_seed(35)
+    N, C, H, W = 3, 5, 40, 48
+    x = torch.randn(N, C, H, W, generator=g, dtype=torch.float64).float()
+    dy = torch.randn(N, C, H, W, generator=g, dtype=torch.float64).float()
+    th = _var_theta(N, 2, 36)
+    th[1] = torch.tensor([[0.5, 0.5, 0.1], [0.5, 0.5, -0.1]])    # singular
+    th[2] = torch.tensor([[0.2, 0.01, 0.05], [-0.01, 0.2, 0.0]])  # zoom-in: ~42 x 42 window
+    xs, ts, ds = (t.to(cuda_device) for t in (x, th, dy))
+    a = rsgrad.stn_bicubic_bwd(xs, ts, ds, deterministic=True)
+    b = rsgrad.stn_bicubic_bwd(xs, ts, ds, deterministic=True)
+    assert torch.equal(a[0][0], b[0][0]) and torch.equal(a[1], b[1])
+    rdx, rdth = oracle.stn_bicubic_bwd(x.double().numpy(), th.double().numpy(), dy.double().numpy())
+    assert_close(_np(a[0]), rdx, "grad", "dx")
+    assert_close(_np(a[1]), rdth, "grad", "dtheta")
 
 
 @pytest.mark.parametrize("dims", [(2, 2, 9, 11, 13, 8, 12, 10), (1, 4, 32, 32, 32, 32, 32, 32), (1, 1, 2, 3, 4, 2, 2, 2)])
