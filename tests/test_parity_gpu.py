@@ -719,3 +719,30 @@ def test_stn_variants_refuse_border_and_gather(cuda_device):
     y = torch.empty_like(x)
     assert rsgrad.lib().stn_bicubic_fwd(rsgrad._ptr(x), rsgrad._ptr(th), 1, 1, 8, 8, 8, 8,
                                         __import__("ctypes").byref(o), rsgrad._ptr(y), None) == -4
+
+
+def test_stn_variants_bench_shapes_sampled(cuda_device):
+    """The bench's f3 cases in their launch configuration: bicubic 4 x 16 x 512^2 and
+    3-D 2 x 4 x 96^3; samples 0 and 3 (resp. 1) in full against the oracle."""
+    si = synth.stn_inputs(4, 16, 512, 512, cfg=2)
+    g = _cuda(si, cuda_device)
+    y = rsgrad.stn_bicubic_fwd(g["x"], g["theta"])
+    dx, dth = rsgrad.stn_bicubic_bwd(g["x"], g["theta"], g["dy"])
+    for n in (0, 3):
+        x, th, dy = (si[k][n:n + 1].double().numpy() for k in ("x", "theta", "dy"))
+        assert_close(_np(y[n:n + 1]), oracle.stn_bicubic_fwd(x, th), "fwd", f"y[{n}]")
+        rdx, rdth = oracle.stn_bicubic_bwd(x, th, dy)
+        assert_close(_np(dx[n:n + 1]), rdx, "grad", f"dx[{n}]")
+        assert_close(_np(dth[n:n + 1]), rdth, "grad", f"dtheta[{n}]")
+    g3 = torch.Generator().manual_seed(37)
+    x3 = torch.randn(2, 4, 96, 96, 96, generator=g3, dtype=torch.float64).float()
+    d3 = torch.randn(2, 4, 96, 96, 96, generator=g3, dtype=torch.float64).float()
+    t3 = (torch.eye(3, 4, dtype=torch.float64).expand(2, 3, 4) +
+          0.05 * torch.randn(2, 3, 4, generator=g3, dtype=torch.float64)).float().contiguous()
+    y3 = rsgrad.stn3d_fwd(x3.to(cuda_device), t3.to(cuda_device))
+    dx3, dt3 = rsgrad.stn3d_bwd(x3.to(cuda_device), t3.to(cuda_device), d3.to(cuda_device))
+    xn, tn, dn = x3[1:].double().numpy(), t3[1:].double().numpy(), d3[1:].double().numpy()
+    assert_close(_np(y3[1:]), oracle.stn3d_fwd(xn, tn), "fwd", "y3")
+    rdx, rdth = oracle.stn3d_bwd(xn, tn, dn)
+    assert_close(_np(dx3[1:]), rdx, "grad", "dx3")
+    assert_close(_np(dt3[1:]), rdth, "grad", "dtheta3")
