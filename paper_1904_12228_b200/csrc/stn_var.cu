@@ -225,8 +225,9 @@ __global__ void __launch_bounds__(kVT, 3) bicubic_bwd(StnArgs a, double *part, c
     if (q < P) {
         const int i = q / a.Wo, j = q - i * a.Wo;
         const Bicubic b = bicubic_at(a.theta, n, i, j, a.H, a.W, a.Ho, a.Wo, a.ac);
-        // branch-free taps: out-of-image taps read a clamped in-image address with zero
-        // weights, so all 16 loads of a channel are issued together
+        // branch-free taps: out-of-image taps load from a clamped in-image address and the
+        // value is then replaced by 0 (a select, so a non-finite neighbour cannot leak in),
+        // so all 16 loads of a channel are issued together
         int ro[4], co[4];
         bool vy[4], vx[4];
         float wy[4], dwy[4], wx[4], dwx[4];
@@ -251,7 +252,10 @@ __global__ void __launch_bounds__(kVT, 3) bicubic_bwd(StnArgs a, double *part, c
 #pragma unroll
                 for (int u = 0; u < 4; u++)
 #pragma unroll
-                    for (int v = 0; v < 4; v++) val[u][v] = __ldg(p + ro[u] + co[v]);
+                    for (int v = 0; v < 4; v++) {
+                        const float t = __ldg(p + ro[u] + co[v]);
+                        val[u][v] = (vy[u] && vx[v]) ? t : 0.f;
+                    }
                 float sx_ = 0.f, sy_ = 0.f;
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
