@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(kVT) stn3d_fwd_k(Vol a) {
     }
 }
 
-__global__ void __launch_bounds__(kVT) stn3d_bwd_k(Vol a, double *part) {
+__global__ void __launch_bounds__(kVT, 3) stn3d_bwd_k(Vol a, double *part) {
     const int P = a.Do * a.Ho * a.Wo;
     const long long V = (long long)a.D * a.H * a.W;
     const int q = blockIdx.x * kVT + threadIdx.x;
@@ -361,26 +361,48 @@ __global__ void __launch_bounds__(kVT) stn3d_bwd_k(Vol a, double *part) {
     if (q < P) {
         const int k = q / (a.Ho * a.Wo), rem = q - k * a.Ho * a.Wo, i = rem / a.Wo, j = rem - i * a.Wo;
         const Tri r = tri_at(a, n, k, i, j);
+        // branch-free taps (as bicubic_bwd): clamped loads, out-of-volume values selected to 0
+        long long off[8];
+        bool ok[8];
+        float w[8];
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+            const int ax = e & 1, by = (e >> 1) & 1, dz = e >> 2;
+            const int xx = r.x0 + ax, yy = r.y0 + by, zz = r.z0 + dz;
+            ok[e] = xx >= 0 && xx < a.W && yy >= 0 && yy < a.H && zz >= 0 && zz < a.D;
+            const int xc = min(max(xx, 0), a.W - 1), yc = min(max(yy, 0), a.H - 1), zc = min(max(zz, 0), a.D - 1);
+            off[e] = ((long long)zc * a.H + yc) * a.W + xc;
+            w[e] = (ax ? r.f[0] : 1.f - r.f[0]) * (by ? r.f[1] : 1.f - r.f[1]) * (dz ? r.f[2] : 1.f - r.f[2]);
+        }
         float gq[3] = {0.f, 0.f, 0.f};
         for (int c = 0; c < a.C; c++) {
             const float g = __ldg(a.dy + ((long long)n * a.C + c) * P + q);
             const float *p = a.x + ((long long)n * a.C + c) * V;
-            float *d = a.dx ? a.dx + ((long long)n * a.C + c) * V : nullptr;
+            if (a.dtheta) {
+                float v[8];
 #pragma unroll
-            for (int e = 0; e < 8; e++) {
-                const int ax = e & 1, by = (e >> 1) & 1, dz = e >> 2;
-                const int xx = r.x0 + ax, yy = r.y0 + by, zz = r.z0 + dz;
-                if (xx < 0 || xx >= a.W || yy < 0 || yy >= a.H || zz < 0 || zz >= a.D) continue;
-                const float wx = ax ? r.f[0] : 1.f - r.f[0], wy = by ? r.f[1] : 1.f - r.f[1],
-                            wz = dz ? r.f[2] : 1.f - r.f[2];
-                const long long o = ((long long)zz * a.H + yy) * a.W + xx;
-                if (d) red_add_nc(d + o, g * wx * wy * wz);
-                if (a.dtheta) {
-                    const float gv = g * __ldg(p + o);
-                    gq[0] = fmaf(gv * (ax ? 1.f : -1.f), wy * wz, gq[0]);
-                    gq[1] = fmaf(gv * (by ? 1.f : -1.f), wx * wz, gq[1]);
-                    gq[2] = fmaf(gv * (dz ? 1.f : -1.f), wx * wy, gq[2]);
+                for (int e = 0; e < 8; e++) {
+                    const float t = __ldg(p + off[e]);
+                    v[e] = ok[e] ? t : 0.f;
                 }
+                const float wx0 = 1.f - r.f[0], wx1 = r.f[0], wy0 = 1.f - r.f[1], wy1 = r.f[1];
+                const float wz0 = 1.f - r.f[2], wz1 = r.f[2];
+                // e = ax + 2 by + 4 dz: d/dx pairs (e, e+1), d/dy (e, e+2), d/dz (e, e+4)
+                const float gx_ = wz0 * (wy0 * (v[1] - v[0]) + wy1 * (v[3] - v[2])) +
+                                  wz1 * (wy0 * (v[5] - v[4]) + wy1 * (v[7] - v[6]));
+                const float gy_ = wz0 * (wx0 * (v[2] - v[0]) + wx1 * (v[3] - v[1])) +
+                                  wz1 * (wx0 * (v[6] - v[4]) + wx1 * (v[7] - v[5]));
+                const float gz_ = wy0 * (wx0 * (v[4] - v[0]) + wx1 * (v[5] - v[1])) +
+                                  wy1 * (wx0 * (v[6] - v[2]) + wx1 * (v[7] - v[3]));
+                gq[0] = fmaf(g, gx_, gq[0]);
+                gq[1] = fmaf(g, gy_, gq[1]);
+                gq[2] = fmaf(g, gz_, gq[2]);
+            }
+            if (a.dx) {
+                float *d = a.dx + ((long long)n * a.C + c) * V;
+#pragma unroll
+                for (int e = 0; e < 8; e++)
+                    if (ok[e]) red_add_nc(d + off[e], g * w[e]);
             }
         }
         const int L[3] = {a.W, a.H, a.D};

@@ -1,5 +1,6 @@
-timeout 900 python -m pytest tests -m gpu -q -x -k "warp or bicubic" > gpurun_out/pytest_w.log 2>&1; echo pytest=$?; tail -2 gpurun_out/pytest_w.log
-for i in 1 2; do
-echo "== new"; python scripts/bench_layer.py 16 5 warp
-echo "== old"; python scripts/ab_lib.py abtmp/lib_old.so 16 5 warp
-done
+timeout 900 python -m pytest tests -m gpu -q -x -k "stn3d or bench_shapes_sampled" > gpurun_out/pytest_3d.log 2>&1; echo pytest=$?; tail -2 gpurun_out/pytest_3d.log
+python -c "
+import bench, json
+from paper_1904_12228_b200 import rsgrad as rs
+r = bench.next_rows(rs, bench.peak_hbm()[0])['rows']
+print(json.dumps({k: v for k, v in r.items() if k.startswith('f3')}, indent=1))"
