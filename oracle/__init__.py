@@ -58,6 +58,12 @@ def _load():
         lib.oracle_stn_bicubic_bwd.argtypes = [P, P, P, I, I, I, I, I, I, I, P, P]
         lib.oracle_stn3d_fwd.argtypes = [P, P, I, I, I, I, I, I, I, I, I, P]
         lib.oracle_stn3d_bwd.argtypes = [P, P, P, I, I, I, I, I, I, I, I, I, P, P]
+        lib.oracle_stn_kinks.argtypes = [P, I, I, I, I, I, I, ctypes.c_double]
+        lib.oracle_stn_kinks.restype = ctypes.c_long
+        lib.oracle_warp_kinks.argtypes = [P, I, I, I, ctypes.c_double]
+        lib.oracle_warp_kinks.restype = ctypes.c_long
+        lib.oracle_bslice_kinks.argtypes = [P, I, I, I, I, ctypes.c_double]
+        lib.oracle_bslice_kinks.restype = ctypes.c_long
         lib.oracle_set_threads.argtypes = [I]
         lib.oracle_get_threads.restype = I
         _lib = lib
@@ -232,3 +238,24 @@ def stn3d_bwd(x, theta, dy, align_corners=True):
     _load().oracle_stn3d_bwd(_p(x), _p(theta), _p(dy), N, C, D, H, W, Do, Ho, Wo, int(align_corners), _p(dx),
                              _p(dth))
     return dx, dth
+
+
+# ----------------------------------------------------------------------------- diagnostics
+def stn_kinks(theta, H, W, Ho=None, Wo=None, align_corners=True, tol=1e-6):
+    """Sample coordinates (per axis) within tol px of an integer (SURVEY 8(c) diagnostic)."""
+    theta = _f64(theta)
+    Ho = H if Ho is None else Ho
+    Wo = W if Wo is None else Wo
+    return int(_load().oracle_stn_kinks(_p(theta), theta.shape[0], H, W, Ho, Wo, int(align_corners), tol))
+
+
+def warp_kinks(flow, tol=1e-6):
+    flow = _f64(flow)
+    N, _, H, W = flow.shape
+    return int(_load().oracle_warp_kinks(_p(flow), N, H, W, tol))
+
+
+def bslice_kinks(guide, D, tol=1e-6):
+    guide = _f64(guide)
+    N, H, W = guide.shape
+    return int(_load().oracle_bslice_kinks(_p(guide), N, H, W, D, tol))

@@ -735,3 +735,47 @@ void oracle_stn3d_bwd(const double *x, const double *theta, const double *dy, in
             for (int r = 0; r < 12; r++) dtheta[12L * n + r] = dth[r];
     }
 }
+
+/* ------------------------------------------------------------------ */
+/* Diagnostics: kink-straddling sample coordinates       */
+/* ------------------------------------------------------------------ */
+/* Number of sample coordinates (each axis counted separately) within tol px of an
+ * integer, where the floor cell -- and so the one-sided derivative (R8) --
+ * is decided by the last bits of the coordinate.  Reported next to parity results. */
+static int near_int(double v, double tol) { return fabs(v - floor(v + 0.5)) <= tol; }
+
+long oracle_stn_kinks(const double *theta, int N, int H, int W, int Ho, int Wo, int ac, double tol) {
+    long cnt = 0;
+#pragma omp parallel for reduction(+ : cnt) schedule(static)
+    for (int n = 0; n < N; n++)
+        for (int i = 0; i < Ho; i++)
+            for (int j = 0; j < Wo; j++) {
+                double xt, yt, ix, iy;
+                stn_coord(theta + 6L * n, H, W, Ho, Wo, ac, i, j, &xt, &yt, &ix, &iy);
+                cnt += near_int(ix, tol) + near_int(iy, tol);
+            }
+    return cnt;
+}
+
+long oracle_warp_kinks(const double *flow, int N, int H, int W, double tol) {
+    const long HW = (long)H * W;
+    long cnt = 0;
+#pragma omp parallel for reduction(+ : cnt) schedule(static)
+    for (int n = 0; n < N; n++)
+        for (long p = 0; p < HW; p++) {
+            const double ix = (double)(p % W) + flow[(2L * n) * HW + p];
+            const double iy = (double)(p / W) + flow[(2L * n + 1) * HW + p];
+            cnt += near_int(ix, tol) + near_int(iy, tol);
+        }
+    return cnt;
+}
+
+/* bilateral slice: the guide axis c_z = guide * D - 1/2 (the spatial cell coordinates
+ * are fixed by the shapes) */
+long oracle_bslice_kinks(const double *guide, int N, int H, int W, int D, double tol) {
+    const long T = (long)N * H * W;
+    long cnt = 0;
+#pragma omp parallel for reduction(+ : cnt) schedule(static)
+    for (long p = 0; p < T; p++) cnt += near_int(guide[p] * (double)D - 0.5, tol);
+    return cnt;
+}

@@ -557,3 +557,19 @@ def test_stn3d_reduces_to_2d_on_one_slice():
     y3 = oracle.stn3d_fwd(x, th3, (1, 9, 11), align_corners=False)
     y2 = oracle.stn_fwd(x[:, :, 0], th2, align_corners=False)
     np.testing.assert_allclose(y3[:, :, 0], y2, rtol=1e-13, atol=1e-13)
+
+
+# --------------------------------------------------------------------------- kink diagnostics
+def test_kink_counts():
+    """SURVEY 8(c) diagnostic: identity theta (align_corners=1) and zero flow put every
+    sample exactly on the grid (2 axes x pixels); the quarter-pixel theta puts none there;
+    guide values k/D + 1/(2D) sit exactly on the guide-axis kink."""
+    th = np.array([[[1.0, 0, 0], [0, 1.0, 0]]] * 2)
+    assert oracle.stn_kinks(th, 8, 9) == 2 * 2 * 8 * 9
+    q = np.array([[[1.0, 0, 0.5 / 8], [0, 1.0, 0.5 / 7]]])
+    assert oracle.stn_kinks(q, 8, 9) == 0
+    assert oracle.warp_kinks(np.zeros((1, 2, 5, 6))) == 2 * 30
+    assert oracle.warp_kinks(np.full((1, 2, 5, 6), 0.25)) == 0
+    g = (np.arange(8)[None, None, :] + 0.5) / 8 * np.ones((1, 3, 8))
+    assert oracle.bslice_kinks(g, 8) == 24
+    assert oracle.bslice_kinks(g + 0.01, 8) == 0
