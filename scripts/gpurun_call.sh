@@ -1,7 +1,6 @@
-timeout 900 python -m pytest tests -m gpu -q -x -k "stn" > gpurun_out/pytest_stn.log 2>&1; echo pytest=$?; tail -2 gpurun_out/pytest_stn.log
+timeout 900 python -m pytest tests -m gpu -q -x -k "bslice" > gpurun_out/pytest_bs.log 2>&1; echo pytest=$?; tail -2 gpurun_out/pytest_bs.log
 for i in 1 2; do
-echo "== concurrent"; python scripts/bench_layer.py 16 5 stn_bwd
-echo "== serial"; RSGRAD_STN_CONCURRENT=0 python scripts/bench_layer.py 16 5 stn_bwd
+echo "== dyn smem, minb2"; python scripts/bench_layer.py 16 5 bslice_bwd
+echo "== dyn smem, minb3"; python scripts/ab_lib.py abtmp/lib_b3.so 16 5 bslice_bwd
+echo "== old"; python scripts/ab_lib.py abtmp/lib_old.so 16 5 bslice_bwd
 done
-echo "== concurrent 64"; python scripts/bench_layer.py 64 3 stn_bwd
-echo "== serial 64"; RSGRAD_STN_CONCURRENT=0 python scripts/bench_layer.py 64 3 stn_bwd
