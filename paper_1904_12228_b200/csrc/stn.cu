@@ -359,8 +359,11 @@ __global__ void __launch_bounds__(FAST ? kOTFast : kThreads, FAST ? kOTFastMinB 
             int t00[kFP], t01[kFP], t10[kFP], t11[kFP];
 #pragma unroll
             for (int k = 0; k < kFP; k++) {
-                const int s0 = (in[k] && yv0[k]) ? roff[y0[k] - ylo] + (x0[k] - rxa[y0[k] - ylo]) : 0;
-                const int s1 = (in[k] && yv1[k]) ? roff[y0[k] + 1 - ylo] + (x0[k] - rxa[y0[k] + 1 - ylo]) : 0;
+                // a row has a table entry only if one of the pixel's taps in it is in the image
+                // (ylo / R come from those): never index the tables otherwise
+                const bool xany = xv0[k] || xv1[k];
+                const int s0 = (in[k] && yv0[k] && xany) ? roff[y0[k] - ylo] + (x0[k] - rxa[y0[k] - ylo]) : 0;
+                const int s1 = (in[k] && yv1[k] && xany) ? roff[y0[k] + 1 - ylo] + (x0[k] - rxa[y0[k] + 1 - ylo]) : 0;
                 t00[k] = (in[k] && yv0[k] && xv0[k]) ? s0 : F;
                 t01[k] = (in[k] && yv0[k] && xv1[k]) ? s0 + 1 : F;
                 t10[k] = (in[k] && yv1[k] && xv0[k]) ? s1 : F;
@@ -499,8 +502,9 @@ __global__ void __launch_bounds__(FAST ? kOTFast : kThreads, FAST ? kOTFastMinB 
             int s0[kFP], s1[kFP];
 #pragma unroll
             for (int k = 0; k < kFP; k++) {
-                s0[k] = (in[k] && yv0[k]) ? roff[y0[k] - ylo] + (x0[k] - rxa[y0[k] - ylo]) : 0;
-                s1[k] = (in[k] && yv1[k]) ? roff[y0[k] + 1 - ylo] + (x0[k] - rxa[y0[k] + 1 - ylo]) : 0;
+                const bool xany = xv0[k] || xv1[k];  // as above: only rows with a table entry
+                s0[k] = (in[k] && yv0[k] && xany) ? roff[y0[k] - ylo] + (x0[k] - rxa[y0[k] - ylo]) : 0;
+                s1[k] = (in[k] && yv1[k] && xany) ? roff[y0[k] + 1 - ylo] + (x0[k] - rxa[y0[k] + 1 - ylo]) : 0;
             }
             // d_theta also stages the tile's dY rows (kFI x kFJ per channel) after the X footprint
             constexpr int GT = (MODE != MODE_FWD) ? kFI * kFJ : 0;
