@@ -380,6 +380,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
             const unsigned m = __match_any_sync(0xffffffffu, bin);
             if (bin >= 0 && lane == __ffs(m) - 1) cnt[w * NB + bin] += __popc(m);
+            __syncwarp();  // the next iteration's leader may update the same counter
         }
     }
     __syncthreads();
