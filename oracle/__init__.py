@@ -64,6 +64,12 @@ def _load():
         lib.oracle_warp_kinks.restype = ctypes.c_long
         lib.oracle_bslice_kinks.argtypes = [P, I, I, I, I, ctypes.c_double]
         lib.oracle_bslice_kinks.restype = ctypes.c_long
+        lib.oracle_stn_lanczos_fwd.argtypes = [P, P, I, I, I, I, I, I, I, P]
+        lib.oracle_stn_lanczos_bwd.argtypes = [P, P, P, I, I, I, I, I, I, I, P, P]
+        lib.oracle_lanczos3.argtypes = [ctypes.c_double]
+        lib.oracle_lanczos3.restype = ctypes.c_double
+        lib.oracle_dlanczos3.argtypes = [ctypes.c_double]
+        lib.oracle_dlanczos3.restype = ctypes.c_double
         lib.oracle_set_threads.argtypes = [I]
         lib.oracle_get_threads.restype = I
         _lib = lib
@@ -259,3 +265,31 @@ def bslice_kinks(guide, D, tol=1e-6):
     guide = _f64(guide)
     N, H, W = guide.shape
     return int(_load().oracle_bslice_kinks(_p(guide), N, H, W, D, tol))
+
+
+def lanczos3(x):
+    return float(_load().oracle_lanczos3(float(x)))
+
+
+def dlanczos3(x):
+    return float(_load().oracle_dlanczos3(float(x)))
+
+
+def stn_lanczos_fwd(x, theta, Ho=None, Wo=None, align_corners=True):
+    x, theta = _f64(x), _f64(theta)
+    N, C, H, W = x.shape
+    Ho = H if Ho is None else Ho
+    Wo = W if Wo is None else Wo
+    y = np.empty((N, C, Ho, Wo), np.float64)
+    _load().oracle_stn_lanczos_fwd(_p(x), _p(theta), N, C, H, W, Ho, Wo, int(align_corners), _p(y))
+    return y
+
+
+def stn_lanczos_bwd(x, theta, dy, align_corners=True):
+    x, theta, dy = _f64(x), _f64(theta), _f64(dy)
+    N, C, H, W = x.shape
+    Ho, Wo = dy.shape[2:]
+    dx, dth = np.empty_like(x), np.empty((N, 2, 3), np.float64)
+    _load().oracle_stn_lanczos_bwd(_p(x), _p(theta), _p(dy), N, C, H, W, Ho, Wo, int(align_corners), _p(dx),
+                                   _p(dth))
+    return dx, dth

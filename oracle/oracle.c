@@ -779,3 +779,86 @@ long oracle_bslice_kinks(const double *guide, int N, int H, int W, int D, double
     for (long p = 0; p < T; p++) cnt += near_int(guide[p] * (double)D - 0.5, tol);
     return cnt;
 }
+
+/* Lanczos-3 STN ("changing the interpolation scheme", PAPER.md:28;
+ * DESIGN.md R13): 6 x 6 taps floor(i)-2 .. floor(i)+3 per axis with the (unnormalised)
+ * Lanczos kernel L(x) = sinc(x) sinc(x/3) for |x| < 3, sinc(x) = sin(pi x)/(pi x),
+ * zeros outside the image; coordinates as R1.                                  */
+static const double PI_ = 3.14159265358979323846;
+static double lanczos3(double x) {
+    if (x == 0.0) return 1.0;
+    if (fabs(x) >= 3.0) return 0.0;
+    const double px = PI_ * x;
+    return 3.0 * sin(px) * sin(px / 3.0) / (px * px);
+}
+static double dlanczos3(double x) {
+    if (x == 0.0 || fabs(x) >= 3.0) return 0.0;
+    const double px = PI_ * x, s1 = sin(px), s3 = sin(px / 3.0), c1 = cos(px), c3 = cos(px / 3.0);
+    return 3.0 * (PI_ * c1 * s3 + (PI_ / 3.0) * s1 * c3) / (px * px) - 6.0 * s1 * s3 / (px * px * x);
+}
+static void lanczos_w(double t, double w[6], double dw[6]) {
+    for (int m = 0; m < 6; m++) { w[m] = lanczos3(t + 2.0 - m); dw[m] = dlanczos3(t + 2.0 - m); }
+}
+
+void oracle_stn_lanczos_fwd(const double *x, const double *theta, int N, int C, int H, int W,
+                            int Ho, int Wo, int ac, double *y) {
+    const long HW = (long)H * W, P = (long)Ho * Wo;
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int n = 0; n < N; n++)
+        for (int c = 0; c < C; c++)
+            for (int i = 0; i < Ho; i++)
+                for (int j = 0; j < Wo; j++) {
+                    double xt, yt, ix, iy, wx[6], wy[6], d[6];
+                    stn_coord(theta + 6L * n, H, W, Ho, Wo, ac, i, j, &xt, &yt, &ix, &iy);
+                    const double x0 = floor(ix), y0 = floor(iy);
+                    lanczos_w(ix - x0, wx, d);
+                    lanczos_w(iy - y0, wy, d);
+                    const double *p = x + ((long)n * C + c) * HW;
+                    double s = 0.0;
+                    for (int a = 0; a < 6; a++)
+                        for (int b = 0; b < 6; b++)
+                            s += wy[a] * wx[b] * tap(p, H, W, (long)y0 - 2 + a, (long)x0 - 2 + b);
+                    y[((long)n * C + c) * P + (long)i * Wo + j] = s;
+                }
+}
+
+void oracle_stn_lanczos_bwd(const double *x, const double *theta, const double *dy, int N, int C,
+                            int H, int W, int Ho, int Wo, int ac, double *dx, double *dtheta) {
+    const long HW = (long)H * W, P = (long)Ho * Wo;
+    const double sx = stn_unnorm_scale(W, ac), sy = stn_unnorm_scale(H, ac);
+#pragma omp parallel for schedule(static)
+    for (int n = 0; n < N; n++) {
+        if (dx) memset(dx + (long)n * C * HW, 0, sizeof(double) * (size_t)(C * HW));
+        double dth[6] = {0, 0, 0, 0, 0, 0};
+        for (int i = 0; i < Ho; i++)
+            for (int j = 0; j < Wo; j++) {
+                double xt, yt, ix, iy, wx[6], wy[6], dwx[6], dwy[6];
+                stn_coord(theta + 6L * n, H, W, Ho, Wo, ac, i, j, &xt, &yt, &ix, &iy);
+                const double x0 = floor(ix), y0 = floor(iy);
+                lanczos_w(ix - x0, wx, dwx);
+                lanczos_w(iy - y0, wy, dwy);
+                double gix = 0.0, giy = 0.0;
+                for (int c = 0; c < C; c++) {
+                    const double g = dy[((long)n * C + c) * P + (long)i * Wo + j];
+                    const double *p = x + ((long)n * C + c) * HW;
+                    for (int a = 0; a < 6; a++)
+                        for (int b = 0; b < 6; b++) {
+                            const long yy = (long)y0 - 2 + a, xx = (long)x0 - 2 + b;
+                            if (yy < 0 || yy >= H || xx < 0 || xx >= W) continue;
+                            const double v = p[yy * W + xx];
+                            if (dx) dx[((long)n * C + c) * HW + yy * W + xx] += g * wy[a] * wx[b];
+                            gix += g * wy[a] * dwx[b] * v;
+                            giy += g * dwy[a] * wx[b] * v;
+                        }
+                }
+                const double gx = gix * sx, gy = giy * sy;
+                dth[0] += gx * xt; dth[1] += gx * yt; dth[2] += gx;
+                dth[3] += gy * xt; dth[4] += gy * yt; dth[5] += gy;
+            }
+        if (dtheta)
+            for (int k = 0; k < 6; k++) dtheta[6L * n + k] = dth[k];
+    }
+}
+
+double oracle_lanczos3(double x) { return lanczos3(x); }
+double oracle_dlanczos3(double x) { return dlanczos3(x); }

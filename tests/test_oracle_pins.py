@@ -573,3 +573,53 @@ def test_kink_counts():
     g = (np.arange(8)[None, None, :] + 0.5) / 8 * np.ones((1, 3, 8))
     assert oracle.bslice_kinks(g, 8) == 24
     assert oracle.bslice_kinks(g + 0.01, 8) == 0
+
+
+# --------------------------------------------------------------------------- Lanczos-3 STN (§8(f) f3)
+def test_lanczos3_kernel_is_numpy_sinc():
+    """L(x) = sinc(x) sinc(x/3) on |x| < 3 (numpy's normalised sinc), 0 outside; L' matches
+    a central difference of numpy's expression."""
+    for x in np.linspace(-3.5, 3.5, 141):
+        ref = np.sinc(x) * np.sinc(x / 3) if abs(x) < 3 else 0.0
+        assert abs(oracle.lanczos3(x) - ref) <= 1e-14
+        if 1e-3 < abs(x) < 2.999:
+            h = 1e-6
+            fd = (np.sinc(x + h) * np.sinc((x + h) / 3) - np.sinc(x - h) * np.sinc((x - h) / 3)) / (2 * h)
+            assert abs(oracle.dlanczos3(x) - fd) <= 1e-8
+
+
+def test_stn_lanczos_identity_and_adjoint():
+    """Lanczos interpolates (L(0) = 1, L(k) = 0): identity theta reproduces x; the adjoint
+    is the transpose (adjoint identity, brute-force operator matrix)."""
+    g = np.random.default_rng(41)
+    x = g.standard_normal((1, 2, 9, 11))
+    th = np.array([[[1.0, 0, 0], [0, 1.0, 0]]])
+    np.testing.assert_allclose(oracle.stn_lanczos_fwd(x, th), x, rtol=0, atol=1e-12)
+    th = _rand_theta(1, 2, 42)
+    C, H, W = 1, 6, 7
+    n_in = C * H * W
+    M = np.zeros((C * H * W, n_in))
+    for j in range(n_in):
+        e = np.zeros(n_in)
+        e[j] = 1.0
+        M[:, j] = oracle.stn_lanczos_fwd(e.reshape(1, C, H, W), th).ravel()
+    dy = g.standard_normal((1, C, H, W))
+    dx, _ = oracle.stn_lanczos_bwd(np.zeros((1, C, H, W)), th, dy)
+    np.testing.assert_allclose(dx.ravel(), M.T @ dy.ravel(), rtol=1e-12, atol=1e-12)
+
+
+def test_stn_lanczos_theta_central_fd():
+    """d_theta vs central finite differences of <y(theta), dy> with
+    sample coordinates kept away from the kernel's kinks (integers)."""
+    g = np.random.default_rng(43)
+    x, dy = g.standard_normal((1, 2, 10, 12)), g.standard_normal((1, 2, 8, 9))
+    th = _rand_theta(1, 2, 44)
+    _, dth = oracle.stn_lanczos_bwd(x, th, dy)
+    h = 1e-6
+    for r in range(2):
+        for c in range(3):
+            tp, tm = th.copy(), th.copy()
+            tp[0, r, c] += h
+            tm[0, r, c] -= h
+            fd = ((oracle.stn_lanczos_fwd(x, tp, 8, 9) - oracle.stn_lanczos_fwd(x, tm, 8, 9)) * dy).sum() / (2 * h)
+            assert abs(dth[0, r, c] - fd) <= 1e-5 * max(1.0, abs(fd))
