@@ -380,6 +380,13 @@ def next_rows(rs, peak):
         "fwd_bwd_mpix_s": round(P / (tbf + tbb) / 1e6, 1),
         "fwd_roofline_frac": round(BYTES[("stn", "fwd")](16) * P / tbf / 1e9 / peak, 3),
         "bwd_roofline_frac": round(BYTES[("stn", "bwd")](16) * P / tbb / 1e9 / peak, 3)}
+    tlf = med(lambda: rs.stn_lanczos_fwd(si["x"], si["theta"], out=yb))
+    tlb = med(lambda: rs.stn_lanczos_bwd(si["x"], si["theta"], si["dy"], out=(dxb, dtb)))
+    out["f3_stn_lanczos3_4x16x512x512"] = {
+        "fwd_us": round(tlf * 1e6, 1), "bwd_us": round(tlb * 1e6, 1),
+        "fwd_bwd_mpix_s": round(P / (tlf + tlb) / 1e6, 1),
+        "fwd_roofline_frac": round(BYTES[("stn", "fwd")](16) * P / tlf / 1e9 / peak, 3),
+        "bwd_roofline_frac": round(BYTES[("stn", "bwd")](16) * P / tlb / 1e9 / peak, 3)}
     del si, yb, dxb
     x3 = torch.randn(2, 4, 96, 96, 96, device=dev, generator=g)
     d3 = torch.randn(2, 4, 96, 96, 96, device=dev, generator=g)

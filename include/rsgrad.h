@@ -228,6 +228,15 @@ rs_status stn_bicubic_fwd(const float *x, const float *theta, int N, int C, int 
 rs_status stn_bicubic_bwd(const float *x, const float *theta, const float *dy, int N, int C, int H,
                           int W, int Ho, int Wo, const rs_opts *opts, float *dx, float *dtheta,
                           void *workspace, size_t ws_bytes, rs_stream_t stream);
+/*   stn_lanczos_*  as stn_bicubic_* with 6 x 6 taps floor(i)-2 .. floor(i)+3 and the
+ *                  Lanczos-3 kernel L(x) = sinc(x) sinc(x/3), |x| < 3 (R13);
+ *                  d_input by the atomic scatter only (GATHER / deterministic=1 =>
+ *                  RS_ERR_FLAG); workspace layer 7 (N, Ho, Wo). */
+rs_status stn_lanczos_fwd(const float *x, const float *theta, int N, int C, int H, int W, int Ho,
+                          int Wo, const rs_opts *opts, float *y, rs_stream_t stream);
+rs_status stn_lanczos_bwd(const float *x, const float *theta, const float *dy, int N, int C, int H,
+                          int W, int Ho, int Wo, const rs_opts *opts, float *dx, float *dtheta,
+                          void *workspace, size_t ws_bytes, rs_stream_t stream);
 rs_status stn3d_fwd(const float *x, const float *theta, int N, int C, int D, int H, int W, int Do,
                     int Ho, int Wo, const rs_opts *opts, float *y, rs_stream_t stream);
 rs_status stn3d_bwd(const float *x, const float *theta, const float *dy, int N, int C, int D, int H,
@@ -238,7 +247,7 @@ rs_status stn3d_bwd(const float *x, const float *theta, const float *dy, int N, 
  * N,C,H,W,Ho,Wo), 1 = warp (N,C,H,W), 2 = bslice (N,H,W,D,Gh,Gw), 3 = conv
  * (N, C = Ci, H, W, D = Co, Gh = kh, Gw = kw), 4 = convloss_grad (N, H, W: the
  * RS_SCHED_ROOT residual), 5 = stn_bicubic (N, Ho, Wo: d_theta partials, coordinate
- * tables, N fallback flags), 6 = stn3d (N, Ho, Wo, D = Do);
+ * tables, N fallback flags), 6 = stn3d (N, Ho, Wo, D = Do), 7 = stn_lanczos (N, Ho, Wo);
  * unused arguments are ignored.
  * Returns 0 for an unknown layer.  DESIGN.md "Workspace". */
 size_t rsgrad_bwd_workspace_bytes(int layer, int N, int C, int H, int W, int Ho, int Wo, int D,

@@ -258,6 +258,9 @@ size_t rsgrad_bwd_workspace_bytes(int layer, int N, int C, int H, int W, int Ho,
         case 6:
             if (!pos(N) || !pos(Ho) || !pos(Wo) || !pos(D)) return 0;
             return rs::stn_var_ws_bytes(N, D * Ho * Wo, 12);
+        case 7:
+            if (!pos(N) || !pos(Ho) || !pos(Wo)) return 0;
+            return rs::stn_var_ws_bytes(N, Ho * Wo, 6);
         default:
             return 0;
     }
@@ -595,7 +598,7 @@ static rs_status var_check(const rs_opts &o, bool bwd, bool has_dx, std::initial
     if (bwd && has_dx && o.algo == RS_ALGO_SCATTER_PRIV)
         return fail(RS_ERR_FLAG, "stn variants: SCATTER_PRIV is not implemented");
     if (bwd && has_dx && !has_gather && (o.algo == RS_ALGO_GATHER || o.deterministic))
-        return fail(RS_ERR_FLAG, "stn3d: d_input is the atomic scatter only (not deterministic)");
+        return fail(RS_ERR_FLAG, "stn3d / lanczos: d_input is the atomic scatter only (not deterministic)");
     if (bwd && has_dx && o.algo == RS_ALGO_SCATTER_ATOMIC && o.deterministic)
         return fail(RS_ERR_FLAG, "stn variants: the atomic scatter is not deterministic");
     for (const void *p : ptrs)
@@ -692,6 +695,36 @@ rs_status stn3d_bwd(const float *x, const float *theta, const float *dy, int N, 
                                                o.align_corners, true, ws, s);
                    },
                    "stn3d_bwd");
+}
+
+rs_status stn_lanczos_fwd(const float *x, const float *theta, int N, int C, int H, int W, int Ho, int Wo,
+                          const rs_opts *opts, float *y, rs_stream_t stream) {
+    const rs_opts o = resolve(opts);
+    rs_status st = stn_validate(x, theta, N, C, H, W, Ho, Wo, o);
+    if (st != RS_OK) return st;
+    if (!y) return fail(RS_ERR_NULL, "stn_lanczos_fwd: y is required");
+    if ((st = var_check(o, false, false, {x, theta, y})) != RS_OK) return st;
+    rs::StnArgs a{};
+    a.x = x; a.theta = theta; a.y = y;
+    a.N = N; a.C = C; a.H = H; a.W = W; a.Ho = Ho; a.Wo = Wo; a.ac = o.align_corners;
+    return launched(rs::stn_lanczos_launch(a, false, nullptr, (cudaStream_t)stream), "stn_lanczos_fwd");
+}
+
+rs_status stn_lanczos_bwd(const float *x, const float *theta, const float *dy, int N, int C, int H, int W, int Ho,
+                          int Wo, const rs_opts *opts, float *dx, float *dtheta, void *workspace, size_t ws_bytes,
+                          rs_stream_t stream) {
+    const rs_opts o = resolve(opts);
+    rs_status st = stn_validate(x, theta, N, C, H, W, Ho, Wo, o);
+    if (st != RS_OK) return st;
+    if (!dy) return fail(RS_ERR_NULL, "stn_lanczos_bwd: dy is required");
+    if ((st = var_check(o, true, dx != nullptr, {x, theta, dy, dx, dtheta})) != RS_OK) return st;
+    if (!dx && !dtheta) return ok();
+    rs::StnArgs a{};
+    a.x = x; a.theta = theta; a.dy = dy; a.dx = dx; a.dtheta = dtheta;
+    a.N = N; a.C = C; a.H = H; a.W = W; a.Ho = Ho; a.Wo = Wo; a.ac = o.align_corners;
+    cudaStream_t s = (cudaStream_t)stream;
+    return with_ws(dtheta ? rs::stn_var_ws_bytes(N, Ho * Wo, 6) : 0, workspace, ws_bytes, s,
+                   [&](void *ws) { return rs::stn_lanczos_launch(a, true, ws, s); }, "stn_lanczos_bwd");
 }
 
 }  // extern "C"

@@ -288,6 +288,140 @@ __global__ void __launch_bounds__(kVT, 3) bicubic_bwd(StnArgs a, double *part, c
     if (a.dtheta) block_partial<6>(dth, part + ((long long)n * gridDim.x + blockIdx.x) * 6);
 }
 
+// ----------------------------------------------------------------- Lanczos-3
+// 6 x 6 taps floor(i)-2 .. floor(i)+3, L(x) = sinc(x) sinc(x/3) (R13), weights
+// and derivatives in fp64 (sinpi / cospi) rounded to fp32; same structure as the bicubic
+// kernels with branch-free taps (clamped loads, out-of-image values selected to 0).
+RS_DEV void lanczos_w(double t, float w[6], float dw[6]) {
+    const double pi = 3.14159265358979323846;
+#pragma unroll
+    for (int m = 0; m < 6; m++) {
+        const double x = t + 2.0 - m;
+        if (x == 0.0) {
+            w[m] = 1.f;
+            dw[m] = 0.f;
+        } else if (fabs(x) >= 3.0) {
+            w[m] = 0.f;
+            dw[m] = 0.f;
+        } else {
+            const double px = pi * x, s1 = sinpi(x), s3 = sinpi(x / 3.0), c1 = cospi(x), c3 = cospi(x / 3.0);
+            w[m] = (float)(3.0 * s1 * s3 / (px * px));
+            dw[m] = (float)(3.0 * (pi * c1 * s3 + (pi / 3.0) * s1 * c3) / (px * px) - 6.0 * s1 * s3 / (px * px * x));
+        }
+    }
+}
+
+struct Lz {
+    int x0, y0;
+    float wx[6], wy[6], dwx[6], dwy[6];
+    double xt, yt;
+};
+
+RS_DEV Lz lanczos_at(const float *theta, int n, int i, int j, int H, int W, int Ho, int Wo, int ac) {
+    Lz b;
+    b.xt = stn_norm(j, Wo, ac);
+    b.yt = stn_norm(i, Ho, ac);
+    const float *t = theta + 6 * n;
+    const double ix = stn_unnorm(affine3(__ldg(t), __ldg(t + 1), __ldg(t + 2), b.xt, b.yt), W, ac);
+    const double iy = stn_unnorm(affine3(__ldg(t + 3), __ldg(t + 4), __ldg(t + 5), b.xt, b.yt), H, ac);
+    const Cell cx = cell_of(ix), cy = cell_of(iy);
+    b.x0 = cx.i0;
+    b.y0 = cy.i0;
+    lanczos_w(__dsub_rn(ix, floor(ix)), b.wx, b.dwx);
+    lanczos_w(__dsub_rn(iy, floor(iy)), b.wy, b.dwy);
+    return b;
+}
+
+__global__ void __launch_bounds__(kVT) lanczos_fwd(StnArgs a) {
+    const int P = a.Ho * a.Wo, HW = a.H * a.W;
+    const int q = blockIdx.x * kVT + threadIdx.x;
+    if (q >= P) return;
+    const int n = blockIdx.y, i = q / a.Wo, j = q - i * a.Wo;
+    const Lz b = lanczos_at(a.theta, n, i, j, a.H, a.W, a.Ho, a.Wo, a.ac);
+    int ro[6], co[6];
+    bool vy[6], vx[6];
+#pragma unroll
+    for (int u = 0; u < 6; u++) {
+        const int yy = b.y0 - 2 + u, xx = b.x0 - 2 + u;
+        vy[u] = yy >= 0 && yy < a.H;
+        vx[u] = xx >= 0 && xx < a.W;
+        ro[u] = min(max(yy, 0), a.H - 1) * a.W;
+        co[u] = min(max(xx, 0), a.W - 1);
+    }
+    for (int c = 0; c < a.C; c++) {
+        const float *p = a.x + ((long long)n * a.C + c) * HW;
+        float s = 0.f;
+#pragma unroll
+        for (int u = 0; u < 6; u++) {
+            float r = 0.f;
+#pragma unroll
+            for (int v = 0; v < 6; v++) {
+                const float t = __ldg(p + ro[u] + co[v]);
+                r = fmaf(b.wx[v], (vy[u] && vx[v]) ? t : 0.f, r);
+            }
+            s = fmaf(b.wy[u], r, s);
+        }
+        a.y[((long long)n * a.C + c) * P + q] = s;
+    }
+}
+
+__global__ void __launch_bounds__(kVT) lanczos_bwd(StnArgs a, double *part) {
+    const int P = a.Ho * a.Wo, HW = a.H * a.W;
+    const int q = blockIdx.x * kVT + threadIdx.x;
+    const int n = blockIdx.y;
+    float dth[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (q < P) {
+        const int i = q / a.Wo, j = q - i * a.Wo;
+        const Lz b = lanczos_at(a.theta, n, i, j, a.H, a.W, a.Ho, a.Wo, a.ac);
+        int ro[6], co[6];
+        bool vy[6], vx[6];
+#pragma unroll
+        for (int u = 0; u < 6; u++) {
+            const int yy = b.y0 - 2 + u, xx = b.x0 - 2 + u;
+            vy[u] = yy >= 0 && yy < a.H;
+            vx[u] = xx >= 0 && xx < a.W;
+            ro[u] = min(max(yy, 0), a.H - 1) * a.W;
+            co[u] = min(max(xx, 0), a.W - 1);
+        }
+        float gix = 0.f, giy = 0.f;
+        for (int c = 0; c < a.C; c++) {
+            const float g = __ldg(a.dy + ((long long)n * a.C + c) * P + q);
+            const float *p = a.x + ((long long)n * a.C + c) * HW;
+            if (a.dtheta) {
+                float sx_ = 0.f, sy_ = 0.f;
+#pragma unroll
+                for (int u = 0; u < 6; u++) {
+                    float rx = 0.f, ry = 0.f;
+#pragma unroll
+                    for (int v = 0; v < 6; v++) {
+                        const float t = __ldg(p + ro[u] + co[v]);
+                        const float val = (vy[u] && vx[v]) ? t : 0.f;
+                        rx = fmaf(b.dwx[v], val, rx);
+                        ry = fmaf(b.wx[v], val, ry);
+                    }
+                    sx_ = fmaf(b.wy[u], rx, sx_);
+                    sy_ = fmaf(b.dwy[u], ry, sy_);
+                }
+                gix = fmaf(g, sx_, gix);
+                giy = fmaf(g, sy_, giy);
+            }
+            if (a.dx) {
+                float *d = a.dx + ((long long)n * a.C + c) * HW;
+#pragma unroll
+                for (int u = 0; u < 6; u++)
+#pragma unroll
+                    for (int v = 0; v < 6; v++)
+                        if (vy[u] && vx[v]) red_add_nc(d + ro[u] + co[v], g * (b.wy[u] * b.wx[v]));
+            }
+        }
+        const float sx = a.ac ? 0.5f * (a.W - 1) : 0.5f * a.W, sy = a.ac ? 0.5f * (a.H - 1) : 0.5f * a.H;
+        const float gx = gix * sx, gy = giy * sy, xt = (float)b.xt, yt = (float)b.yt;
+        dth[0] = gx * xt; dth[1] = gx * yt; dth[2] = gx;
+        dth[3] = gy * xt; dth[4] = gy * yt; dth[5] = gy;
+    }
+    if (a.dtheta) block_partial<6>(dth, part + ((long long)n * gridDim.x + blockIdx.x) * 6);
+}
+
 // ----------------------------------------------------------------- 3-D
 struct Vol {
     int N, C, D, H, W, Do, Ho, Wo, ac;
@@ -471,6 +605,27 @@ cudaError_t stn_bicubic_launch(const StnArgs &a, bool bwd, int algo, void *ws, c
     note_launch();
     if (a.dtheta) {
         theta_finalize<<<a.N, 32, 0, s>>>(part, grid.x, 6, a.dtheta);
+        note_launch();
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t stn_lanczos_launch(const StnArgs &a, bool bwd, void *ws, cudaStream_t s) {
+    const int P = a.Ho * a.Wo;
+    const dim3 grid((P + kVT - 1) / kVT, a.N);
+    if (!bwd) {
+        lanczos_fwd<<<grid, kVT, 0, s>>>(a);
+        note_launch();
+        return cudaGetLastError();
+    }
+    if (a.dx) {
+        cudaError_t e = cudaMemsetAsync(a.dx, 0, sizeof(float) * (size_t)a.N * a.C * a.H * a.W, s);
+        if (e != cudaSuccess) return e;
+    }
+    lanczos_bwd<<<grid, kVT, 0, s>>>(a, (double *)ws);
+    note_launch();
+    if (a.dtheta) {
+        theta_finalize<<<a.N, 32, 0, s>>>((const double *)ws, grid.x, 6, a.dtheta);
         note_launch();
     }
     return cudaGetLastError();

@@ -59,13 +59,15 @@ def lib():
         L.upsample4_fwd.argtypes = [P, I, I, I, I, P, P]
         L.stn_bicubic_fwd.argtypes = [P, P, I, I, I, I, I, I, O, P, P]
         L.stn_bicubic_bwd.argtypes = [P, P, P, I, I, I, I, I, I, O, P, P, P, S, P]
+        L.stn_lanczos_fwd.argtypes = [P, P, I, I, I, I, I, I, O, P, P]
+        L.stn_lanczos_bwd.argtypes = [P, P, P, I, I, I, I, I, I, O, P, P, P, S, P]
         L.stn3d_fwd.argtypes = [P, P, I, I, I, I, I, I, I, I, O, P, P]
         L.stn3d_bwd.argtypes = [P, P, P, I, I, I, I, I, I, I, I, O, P, P, P, S, P]
         L.upsample4_bwd.argtypes = [P, I, I, I, I, P, P]
         L.conv_bwd.argtypes = [P, P, P, I, I, I, I, I, I, I, O, P, P, P, S, P]
         for f in ("stn_fwd", "stn_bwd", "warp_fwd", "warp_bwd", "bslice_fwd", "bslice_bwd", "conv_fwd", "conv_bwd",
                   "convloss_grad", "upsample4_fwd", "upsample4_bwd", "stn_bicubic_fwd", "stn_bicubic_bwd",
-                  "stn3d_fwd", "stn3d_bwd"):
+                  "stn3d_fwd", "stn3d_bwd", "stn_lanczos_fwd", "stn_lanczos_bwd"):
             getattr(L, f).restype = ctypes.c_int
         L.rsgrad_bwd_workspace_bytes.argtypes = [I, I, I, I, I, I, I, I, I, I, O]
         L.rsgrad_bwd_workspace_bytes.restype = S
@@ -416,4 +418,30 @@ def stn3d_bwd(x, theta, dy, *, align_corners=True, need_dx=True, need_dtheta=Tru
     o = _opts(align_corners, "zeros", "scatter_atomic")
     _check(lib().stn3d_bwd(_ptr(x), _ptr(theta), _ptr(dy), N, C, D, H, W, Do, Ho, Wo, ctypes.byref(o), _ptr(dx),
                            _ptr(dth), None, 0, _stream(_device_of(x, dy))), "stn3d_bwd")
+    return dx, dth
+
+
+def stn_lanczos_fwd(x, theta, Ho=None, Wo=None, *, align_corners=True, out=None):
+    """Lanczos-3 STN (6 x 6 taps, zeros); CUDA tensors."""
+    N, C, H, W = x.shape
+    Ho = H if Ho is None else int(Ho)
+    Wo = W if Wo is None else int(Wo)
+    y = out if out is not None else torch.empty((N, C, Ho, Wo), dtype=torch.float32, device=x.device)
+    o = _opts(align_corners)
+    _check(lib().stn_lanczos_fwd(_ptr(x), _ptr(theta), N, C, H, W, Ho, Wo, ctypes.byref(o), _ptr(y),
+                                 _stream(_device_of(x, y))), "stn_lanczos_fwd")
+    return y
+
+
+def stn_lanczos_bwd(x, theta, dy, *, align_corners=True, need_dx=True, need_dtheta=True, out=None):
+    N, C, H, W = x.shape
+    Ho, Wo = dy.shape[2:]
+    if out is not None:
+        dx, dth = out
+    else:
+        dx = torch.empty_like(x) if need_dx else None
+        dth = torch.empty((N, 2, 3), dtype=torch.float32, device=x.device) if need_dtheta else None
+    o = _opts(align_corners, "zeros", "scatter_atomic")
+    _check(lib().stn_lanczos_bwd(_ptr(x), _ptr(theta), _ptr(dy), N, C, H, W, Ho, Wo, ctypes.byref(o), _ptr(dx),
+                                 _ptr(dth), None, 0, _stream(_device_of(x, dy))), "stn_lanczos_bwd")
     return dx, dth

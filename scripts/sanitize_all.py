@@ -17,6 +17,8 @@ for shape in [(2, 5, 37, 53, 41, 29), (1, 16, 96, 128, 96, 128)]:
                      ("auto", "gather", "scatter_priv", "scatter_atomic")):
             rs.stn_bwd(s["x"], s["theta"], s["dy"], padding=pad, algo=algo)
     rs.stn_bicubic_fwd(s["x"], s["theta"], Ho, Wo)
+    rs.stn_lanczos_bwd(s["x"], s["theta"], s["dy"])
+    rs.stn_lanczos_fwd(s["x"], s["theta"], Ho, Wo)
     for algo in ("auto", "gather"):
         rs.stn_bicubic_bwd(s["x"], s["theta"], s["dy"], algo=algo)
 for flow in ("smooth", "stress"):
