@@ -293,7 +293,15 @@ __global__ void __launch_bounds__(kVT, 3) bicubic_bwd(StnArgs a, double *part, c
 // and derivatives in fp64 (sinpi / cospi) rounded to fp32; same structure as the bicubic
 // kernels with branch-free taps (clamped loads, out-of-image values selected to 0).
 RS_DEV void lanczos_w(double t, float w[6], float dw[6]) {
+    // x_m = t + 2 - m: sin(pi x_m) = (-1)^m sin(pi t) (likewise cos), and the x_m / 3 angles
+    // step by -pi/3, so one sincospi pair per argument family serves all six taps
     const double pi = 3.14159265358979323846;
+    const double cm[6] = {1.0, 0.5, -0.5, -1.0, -0.5, 0.5};  // cos(m pi / 3)
+    const double sm[6] = {0.0, 0.86602540378443864676, 0.86602540378443864676, 0.0, -0.86602540378443864676,
+                          -0.86602540378443864676};          // sin(m pi / 3)
+    double s1, c1, sa, ca;
+    sincospi(t, &s1, &c1);
+    sincospi((t + 2.0) / 3.0, &sa, &ca);
 #pragma unroll
     for (int m = 0; m < 6; m++) {
         const double x = t + 2.0 - m;
@@ -304,9 +312,12 @@ RS_DEV void lanczos_w(double t, float w[6], float dw[6]) {
             w[m] = 0.f;
             dw[m] = 0.f;
         } else {
-            const double px = pi * x, s1 = sinpi(x), s3 = sinpi(x / 3.0), c1 = cospi(x), c3 = cospi(x / 3.0);
-            w[m] = (float)(3.0 * s1 * s3 / (px * px));
-            dw[m] = (float)(3.0 * (pi * c1 * s3 + (pi / 3.0) * s1 * c3) / (px * px) - 6.0 * s1 * s3 / (px * px * x));
+            const double sg = (m & 1) ? -1.0 : 1.0;
+            const double sx1 = sg * s1, cx1 = sg * c1;
+            const double s3 = sa * cm[m] - ca * sm[m], c3 = ca * cm[m] + sa * sm[m];
+            const double px = pi * x;
+            w[m] = (float)(3.0 * sx1 * s3 / (px * px));
+            dw[m] = (float)(3.0 * (pi * cx1 * s3 + (pi / 3.0) * sx1 * c3) / (px * px) - 6.0 * sx1 * s3 / (px * px * x));
         }
     }
 }
