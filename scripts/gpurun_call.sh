@@ -1,3 +1,4 @@
+# scratch: the command list of the most recent gpurun call (see DESIGN.md 9a for the reproducible commands)
 timeout 900 python -m pytest tests -m gpu -q -k "lanczos" > gpurun_out/pytest_lz.log 2>&1; echo pytest=$?; tail -1 gpurun_out/pytest_lz.log
 python -c "
 import bench, json
