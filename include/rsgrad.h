@@ -163,8 +163,9 @@ rs_status bslice_bwd(const float *grid, const float *guide, const float *x, cons
  *   y[n,co,y,x] = sum_{ci<Ci,ry<kh,rx<kw} x[n,ci, y-ry+kh/2, x-rx+kw/2] * k[co,ci,ry,rx]
  *   x N x Ci x H x W, k Co x Ci x kh x kw, y N x Co x H x W, zero outside the image.
  * DEVICE pointers only (k and dk are shared by the whole batch); 1 <= kh, kw <= 7
- * and Ci small enough that one 32 x 16 tile's Ci input windows fit in shared
- * memory (Ci <= ~190 at 3x3), else RS_ERR_SHAPE.  opts.padding/align_corners ignored.
+ * and Ci small enough for the d_kernel tile to fit in shared memory,
+ * 4 * (Ci*(15+kh)*(32+kw) + 2048*ceil(Co/4)) <= 200 KB (Ci <= 68 at 3x3 with Co = 16),
+ * else RS_ERR_SHAPE.  opts.padding/align_corners ignored.
  * ------------------------------------------------------------------------- */
 rs_status conv_fwd(const float *x, const float *k, int N, int Ci, int Co, int H, int W, int kh,
                    int kw, const rs_opts *opts, float *y, rs_stream_t stream);

@@ -120,5 +120,8 @@ def test_conv_validation():
     assert L.conv_fwd(fake, fake, 1, 0, 1, 4, 4, 3, 3, ctypes.byref(o), fake, None) == -2
     assert L.conv_fwd(fake, fake, 1, 1, 1, 4, 4, 9, 3, ctypes.byref(o), fake, None) == -2
     assert L.conv_bwd(fake, fake, fake, 1, 1, 1, 4, 4, 3, 8, ctypes.byref(o), fake, None, None, 0, None) == -2
+    # d_kernel tile in shared memory: Ci <= 68 at 3x3 with Co = 16 (include/rsgrad.h)
+    assert L.conv_fwd(fake, fake, 1, 69, 16, 8, 8, 3, 3, ctypes.byref(o), fake, None) == -2
+    assert L.conv_fwd(fake, fake, 1, 68, 16, 8, 8, 3, 3, ctypes.byref(o), fake, None) != -2
     # d_kernel partials: one per persistent block (<= 296) x Co x Ci x kh x kw doubles
     assert rsgrad.workspace_bytes(3, 16, 16, 256, 256, D=16, Gh=3, Gw=3) == 296 * 16 * 16 * 9 * 8
