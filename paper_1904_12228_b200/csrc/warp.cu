@@ -7,7 +7,10 @@
 //                     taps); d_input is the reversed gather, which for an
 //                     arbitrary flow field has no bounded inverse, so it is
 //                     "a general scatter using atomics": fp32
-//                     red.global.add into a zero-filled dx.
+//                     red.global.add into a zero-filled dx (AUTO, SCATTER_ATOMIC).
+//   warp_bwd_win      variant (RSGRAD_WARP_BWD=winR,NW,IT): per-warp shared windows
+//                     flushed by red.v4 (measured slower).
+//   SCATTER_PRIV goes through the staged-footprint output tile of stn.cu (flow mode).
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
