@@ -360,10 +360,12 @@ __global__ void __launch_bounds__(FAST ? kOTFast : kThreads, FAST ? kOTFastMinB 
 #pragma unroll
             for (int k = 0; k < kFP; k++) {
                 // a row has a table entry only if one of the pixel's taps in it is in the image
-                // (ylo / R come from those): never index the tables otherwise
-                const bool xany = xv0[k] || xv1[k];
-                const int s0 = (in[k] && yv0[k] && xany) ? roff[y0[k] - ylo] + (x0[k] - rxa[y0[k] - ylo]) : 0;
-                const int s1 = (in[k] && yv1[k] && xany) ? roff[y0[k] + 1 - ylo] + (x0[k] - rxa[y0[k] + 1 - ylo]) : 0;
+                // (ylo / R come from those): other rows' indices are clamped into the tables
+                // (their value is never used) so no read leaves them
+                const int r0 = min(max(y0[k] - ylo, 0), kFRMax - 1);
+                const int r1 = min(max(y0[k] + 1 - ylo, 0), kFRMax - 1);
+                const int s0 = (in[k] && yv0[k]) ? roff[r0] + (x0[k] - rxa[r0]) : 0;
+                const int s1 = (in[k] && yv1[k]) ? roff[r1] + (x0[k] - rxa[r1]) : 0;
                 t00[k] = (in[k] && yv0[k] && xv0[k]) ? s0 : F;
                 t01[k] = (in[k] && yv0[k] && xv1[k]) ? s0 + 1 : F;
                 t10[k] = (in[k] && yv1[k] && xv0[k]) ? s1 : F;
@@ -502,9 +504,10 @@ __global__ void __launch_bounds__(FAST ? kOTFast : kThreads, FAST ? kOTFastMinB 
             int s0[kFP], s1[kFP];
 #pragma unroll
             for (int k = 0; k < kFP; k++) {
-                const bool xany = xv0[k] || xv1[k];  // as above: only rows with a table entry
-                s0[k] = (in[k] && yv0[k] && xany) ? roff[y0[k] - ylo] + (x0[k] - rxa[y0[k] - ylo]) : 0;
-                s1[k] = (in[k] && yv1[k] && xany) ? roff[y0[k] + 1 - ylo] + (x0[k] - rxa[y0[k] + 1 - ylo]) : 0;
+                const int r0 = min(max(y0[k] - ylo, 0), kFRMax - 1);  // as above: clamped rows
+                const int r1 = min(max(y0[k] + 1 - ylo, 0), kFRMax - 1);
+                s0[k] = (in[k] && yv0[k]) ? roff[r0] + (x0[k] - rxa[r0]) : 0;
+                s1[k] = (in[k] && yv1[k]) ? roff[r1] + (x0[k] - rxa[r1]) : 0;
             }
             // d_theta also stages the tile's dY rows (kFI x kFJ per channel) after the X footprint
             constexpr int GT = (MODE != MODE_FWD) ? kFI * kFJ : 0;
