@@ -8,7 +8,7 @@ from paper_1904_12228_b200 import rsgrad as rs
 
 dev = torch.device("cuda")
 c = lambda d: {k: v.to(dev) for k, v in d.items()}  # noqa: E731
-for shape in [(2, 5, 37, 53, 41, 29), (1, 16, 96, 128, 96, 128)]:
+for shape in [(2, 5, 37, 53, 41, 29), (1, 16, 96, 128, 96, 128), (2, 4, 512, 512, 512, 512)]:
     N, C, H, W, Ho, Wo = shape
     s = c(synth.stn_inputs(N, C, H, W, Ho, Wo, cfg=1))
     for pad in ("zeros", "border"):
