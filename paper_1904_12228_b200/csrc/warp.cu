@@ -20,7 +20,10 @@
 namespace rs {
 namespace {
 
-constexpr int kThreads = 256;
+#ifndef RS_WARP_T
+#define RS_WARP_T 256
+#endif
+constexpr int kThreads = RS_WARP_T;  // threads per block of the per-pixel kernels
 
 #ifndef RS_TAP_HINT
 #define RS_TAP_HINT 1
