@@ -21,9 +21,9 @@ namespace rs {
 namespace {
 
 #ifndef RS_WARP_T
-#define RS_WARP_T 256
+#define RS_WARP_T 128
 #endif
-constexpr int kThreads = RS_WARP_T;  // threads per block of the per-pixel kernels
+constexpr int kThreads = RS_WARP_T;  // per-pixel kernels: 128 measured vs 256: fwd 0.771 vs 0.809 ms (64 samples)
 
 #ifndef RS_TAP_HINT
 #define RS_TAP_HINT 1
