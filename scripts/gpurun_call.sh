@@ -1,3 +1,5 @@
 # scratch: the command list of the most recent gpurun call (see DESIGN.md 9a for the reproducible commands)
-timeout 900 python -m pytest tests -m gpu -q -x -k "warp or sweep or host_pointer or null" > gpurun_out/pytest_w.log 2>&1; echo pytest=$?; tail -1 gpurun_out/pytest_w.log
-python scripts/bench_layer.py 64 3 warp
+for i in 1 2; do
+echo "== base"; python scripts/bench_layer.py 16 5 bslice
+for v in bt128 bt512; do echo "== $v"; python scripts/ab_lib.py abtmp/lib_$v.so 16 5 bslice; done
+done
