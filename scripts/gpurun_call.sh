@@ -1,6 +1,5 @@
 # scratch: the command list of the most recent gpurun call (see DESIGN.md 9a for the reproducible commands)
-timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -1 gpurun_out/pytest_gpu.log
-python -c "import __graft_entry__ as g; g.smoke(); print('SMOKE OK')" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
-python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench=$?
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 > gpurun_out/b_ncu.log 2>&1; echo ncu=$?
-cat gpurun_out/bench.json
+for i in 1 2; do
+echo "== base"; python scripts/bench_layer.py 16 5 stn
+for v in fi16 fi48 f8k; do echo "== $v"; python scripts/ab_lib.py abtmp/lib_$v.so 16 5 stn; done
+done
