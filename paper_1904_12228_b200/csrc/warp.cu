@@ -156,6 +156,224 @@ __global__ void __launch_bounds__(kThreads) warp_bwd_kernel(WarpArgs a, double i
     }
 }
 
+// ----------------------------------------------------------------- backward, row strips (AUTO)
+// d_input as a scatter whose overlapping writes are combined in registers before they
+// reach memory (PAPER.md:733's atomics, applied to pre-summed values).  Lane = column
+// x, a warp walks R consecutive rows of its 32 columns, block = kStripW warps stacked
+// vertically.  Each lane keeps the 4 tap sums of its CURRENT floor cell pending:
+//   * next row's cell == the same cell (vertical compression): add into the pending sums;
+//   * next row's cell == the cell one row down (the common, smooth case): the pending
+//     lower taps ARE the new cell's upper taps -- carried, only the upper pair is emitted;
+//   * otherwise: all 4 pending sums are emitted.
+// Emitted sums of lanes that share an element are merged across lanes before the red:
+// a lane whose left taps are its left neighbour's right taps absorbs them (one shuffle
+// per tap), and runs of lanes on the SAME cell (horizontal compression) are summed by
+// a segmented shuffle scan onto the run's first lane.  Smooth flow: ~1 red per
+// (pixel, channel) instead of ~2.2; a collapsing flow: the red count per element drops
+// by the compression in both axes, which is also what keeps the fp32 reds' rounding
+// (sequential in the order the L2 applies them) inside the tolerance.
+// d_flow is the gather of the same pass; the X taps of a cell one row down reuse the
+// two lower tap values already loaded.
+constexpr int kStripW = 4;  // warps per block (stacked vertically)
+
+#ifndef RS_STRIP_MINB
+#define RS_STRIP_MINB 6
+#endif
+template <int CW, int R>
+__global__ void __launch_bounds__(kStripW * 32, RS_STRIP_MINB)
+    warp_bwd_strip(WarpArgs a, int tiles_x, double invW) {
+    (void)invW;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int n = blockIdx.y;
+    const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
+    const int x = tx * 32 + lane;
+    const bool xin = x < a.W;
+    const int HW = a.H * a.W;
+    const int ybeg = (ty * kStripW + w) * R;
+    if (ybeg >= a.H) return;  // warp-uniform
+    const int yend = min(a.H, ybeg + R);
+    const float *fs = a.flow + (long long)n * 2 * HW;
+    const bool need_df = a.dflow != nullptr, need_dx = a.dx != nullptr;
+
+    for (int c0 = 0; c0 < a.C; c0 += CW) {
+        const int cn = min(CW, a.C - c0);
+        const float *xs = a.x + ((long long)n * a.C + c0) * HW;
+        const float *gs = a.dy + ((long long)n * a.C + c0) * HW;
+        float *dxs = need_dx ? a.dx + ((long long)n * a.C + c0) * HW : nullptr;
+        // pending cell of this lane
+        bool have = false;
+        int pcx = 0, pcy = 0;
+        bool pk[4] = {false, false, false, false};
+        float pend[CW][4], xv[CW][4];
+#pragma unroll
+        for (int c = 0; c < CW; c++)
+#pragma unroll
+            for (int k = 0; k < 4; k++) pend[c][k] = xv[c][k] = 0.f;
+
+        // Emit the pending sums selected by em[] (warp-collective: every lane calls it).
+        auto emit = [&](bool e00, bool e01, bool e10, bool e11) {
+            bool em[4] = {e00 && pk[0], e01 && pk[1], e10 && pk[2], e11 && pk[3]};
+            const bool any = em[0] || em[1] || em[2] || em[3];
+            const unsigned emk = (unsigned)em[0] | ((unsigned)em[1] << 1) | ((unsigned)em[2] << 2) |
+                                 ((unsigned)em[3] << 3);
+            // runs of lanes emitting the same set on the same cell
+            const int ppx = __shfl_up_sync(0xffffffffu, pcx, 1), ppy = __shfl_up_sync(0xffffffffu, pcy, 1);
+            const unsigned pem = __shfl_up_sync(0xffffffffu, emk, 1);
+            const bool same_prev = lane > 0 && any && pem == emk && ppx == pcx && ppy == pcy;
+            const unsigned runs = __ballot_sync(0xffffffffu, same_prev);
+            float val[CW][4];
+#pragma unroll
+            for (int c = 0; c < CW; c++)
+#pragma unroll
+                for (int k = 0; k < 4; k++) val[c][k] = pend[c][k];
+            if (runs) {
+                // segmented suffix sum: every run's first lane gets the run total
+                const unsigned heads = ~runs;  // bit l: lane l starts a run (or is alone)
+                const unsigned after = (lane == 31) ? 0u : (heads >> (lane + 1)) << (lane + 1);
+                const int seg_end = after ? __ffs(after) - 2 : 31;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+                    for (int c = 0; c < CW; c++)
+#pragma unroll
+                        for (int k = 0; k < 4; k++) {
+                            const float t = __shfl_down_sync(0xffffffffu, val[c][k], o);
+                            if (lane + o <= seg_end) val[c][k] += t;
+                        }
+                }
+                if (same_prev) em[0] = em[1] = em[2] = em[3] = false;
+            }
+            // left neighbour's right taps on our left taps (same cell row, one column left)
+            const bool p01 = __shfl_up_sync(0xffffffffu, (int)(em[1] && !same_prev), 1) != 0;
+            const bool p11 = __shfl_up_sync(0xffffffffu, (int)(em[3] && !same_prev), 1) != 0;
+            const bool adj = lane > 0 && ppx + 1 == pcx && ppy == pcy;
+            const bool ab01 = adj && p01 && em[0], ab11 = adj && p11 && em[2];
+            const bool g01 = __shfl_down_sync(0xffffffffu, (int)ab01, 1) != 0 && lane < 31;
+            const bool g11 = __shfl_down_sync(0xffffffffu, (int)ab11, 1) != 0 && lane < 31;
+            if (g01) em[1] = false;
+            if (g11) em[3] = false;
+            const int o00 = any ? pcy * a.W + pcx : 0;  // a tap of the cell is in the image
+#pragma unroll
+            for (int c = 0; c < CW; c++) {
+                const float r01 = __shfl_up_sync(0xffffffffu, val[c][1], 1);
+                const float r11 = __shfl_up_sync(0xffffffffu, val[c][3], 1);
+                if (c >= cn) continue;
+                float *dp = dxs + (long long)c * HW + o00;
+                const float v00 = val[c][0] + (ab01 ? r01 : 0.f), v10 = val[c][2] + (ab11 ? r11 : 0.f);
+                if (em[0] && v00 != 0.f) red_add(dp, v00);
+                if (em[1] && val[c][1] != 0.f) red_add(dp + 1, val[c][1]);
+                if (em[2] && v10 != 0.f) red_add(dp + a.W, v10);
+                if (em[3] && val[c][3] != 0.f) red_add(dp + a.W + 1, val[c][3]);
+            }
+        };
+
+        float un = 0.f, vn = 0.f;
+        if (xin) {
+            un = ldg_stream(fs + ybeg * a.W + x);
+            vn = ldg_stream(fs + HW + ybeg * a.W + x);
+        }
+#pragma unroll 1
+        for (int y = ybeg; y < yend; y++) {
+            const float u = un, v = vn;
+            if (xin && y + 1 < yend) {  // prefetch the next row's flow
+                un = ldg_stream(fs + (y + 1) * a.W + x);
+                vn = ldg_stream(fs + HW + (y + 1) * a.W + x);
+            }
+            float cgx, cgy;
+            Tap t = warp_tap(a, xin ? x : 0, y, u, v, cgx, cgy);
+            if (!xin) t.k00 = t.k01 = t.k10 = t.k11 = false;
+            const bool tany = t.k00 || t.k01 || t.k10 || t.k11;
+            const int rem = y * a.W + (xin ? x : 0);
+            float g[CW];
+#pragma unroll
+            for (int c = 0; c < CW; c++) g[c] = (xin && c < cn) ? ldg_stream(gs + (long long)c * HW + rem) : 0.f;
+            // relation of this row's cell to the pending one
+            const bool same = have && t.x0 == pcx && t.y0 == pcy;
+            const bool down = have && t.x0 == pcx && t.y0 == pcy + 1;
+            if (need_df) {
+                const int o = (int)t.o00;
+#pragma unroll
+                for (int c = 0; c < CW; c++) {
+                    if (c >= cn) break;
+                    const float *p = xs + (long long)c * HW + o;
+                    if (!same) {
+                        if (down) {
+                            xv[c][0] = xv[c][2];
+                            xv[c][1] = xv[c][3];
+                        } else {
+                            xv[c][0] = t.k00 ? TAPLD(p) : 0.f;
+                            xv[c][1] = t.k01 ? TAPLD(p + 1) : 0.f;
+                        }
+                        xv[c][2] = t.k10 ? TAPLD(p + a.W) : 0.f;
+                        xv[c][3] = t.k11 ? TAPLD(p + a.W + 1) : 0.f;
+                    }
+                }
+                float dix = 0.f, diy = 0.f;
+#pragma unroll
+                for (int c = 0; c < CW; c++) {
+                    if (c >= cn) break;
+                    dix = fmaf(g[c], fmaf(1.f - t.fy, xv[c][1] - xv[c][0], t.fy * (xv[c][3] - xv[c][2])), dix);
+                    diy = fmaf(g[c], fmaf(1.f - t.fx, xv[c][2] - xv[c][0], t.fx * (xv[c][3] - xv[c][1])), diy);
+                }
+                if (xin) {
+                    float *dfp = a.dflow + (long long)n * 2 * HW + rem;
+                    if (c0 == 0) {
+                        dfp[0] = dix * cgx;
+                        dfp[HW] = diy * cgy;
+                    } else {  // C > CW: later chunks add onto the first chunk's value
+                        dfp[0] += dix * cgx;
+                        dfp[HW] += diy * cgy;
+                    }
+                }
+            }
+            if (need_dx) {
+                // emit what this row does not continue (warp-collective)
+                const bool keep_all = same || (!have);
+                emit(!keep_all, !keep_all, !keep_all && !down, !keep_all && !down);
+                float nv[CW][4];
+#pragma unroll
+                for (int c = 0; c < CW; c++) {
+                    nv[c][0] = t.w00 * g[c];
+                    nv[c][1] = t.w01 * g[c];
+                    nv[c][2] = t.w10 * g[c];
+                    nv[c][3] = t.w11 * g[c];
+                }
+                if (same) {
+#pragma unroll
+                    for (int c = 0; c < CW; c++)
+#pragma unroll
+                        for (int k = 0; k < 4; k++) pend[c][k] += nv[c][k];
+                } else if (down) {
+#pragma unroll
+                    for (int c = 0; c < CW; c++) {
+                        pend[c][0] = pend[c][2] + nv[c][0];
+                        pend[c][1] = pend[c][3] + nv[c][1];
+                        pend[c][2] = nv[c][2];
+                        pend[c][3] = nv[c][3];
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < CW; c++)
+#pragma unroll
+                        for (int k = 0; k < 4; k++) pend[c][k] = nv[c][k];
+                }
+                have = tany;
+                pcx = t.x0;
+                pcy = t.y0;
+                pk[0] = t.k00;
+                pk[1] = t.k01;
+                pk[2] = t.k10;
+                pk[3] = t.k11;
+            } else {
+                have = tany;
+                pcx = t.x0;
+                pcy = t.y0;
+            }
+        }
+        if (need_dx) emit(true, true, true, true);
+    }
+}
+
 // ----------------------------------------------------------------- backward, warp windows
 // d_input through a per-warp shared-memory window (the "bounded footprint" of the
 // scatter, found at run time since a flow field has no inverse).
@@ -418,14 +636,39 @@ cudaError_t warp_bwd_launch(const WarpArgs &a, int algo, int deterministic, void
     // SCATTER_PRIV: d_input through a block-private footprint accumulator (one red per
     // touched input element per tile) instead of per-tap global reds
     if (algo == 2 || !warp_direct()) return flow_tile_launch(as_tile_args(a), 2, algo == 2, s);
-    // AUTO / SCATTER_ATOMIC: per-tap reds (warp_bwd_kernel).  RSGRAD_WARP_BWD=winR,NW,IT
-    // selects the per-warp shared windows flushed by vector reds (warp_bwd_win): 2.5x
-    // less L2 traffic, but measured slower at configs[4] (0.65 vs 0.59 ms at 16 x 3 x
-    // 1024^2): the per-tap kernel is bound by L1 (83%, the d_flow tap gathers as much
-    // as the reds), the window kernel by shared-memory latency at 22% occupancy.
+    // AUTO: row strips with register-combined taps (warp_bwd_strip).  SCATTER_ATOMIC:
+    // one red per tap (warp_bwd_kernel, the unconverted scatter).  RSGRAD_WARP_BWD=winR,NW,IT
+    // selects the per-warp shared windows flushed by vector reds (warp_bwd_win),
+    // RSGRAD_WARP_BWD=direct the per-tap kernel (A/B measurements).
     const char *e = getenv("RSGRAD_WARP_BWD");
-    const bool direct = algo == 3 || !a.dx || !(e && strncmp(e, "win", 3) == 0);
-    if (direct) {
+    const bool win = algo != 3 && a.dx && e && strncmp(e, "win", 3) == 0;
+    const bool direct = algo == 3 || (e && strcmp(e, "direct") == 0);
+    if (!win && !direct) {
+        const int tiles_x = (a.W + 31) / 32;
+        int R = 16;
+        if ((long long)tiles_x * ((a.H + 4 * R * kStripW - 1) / (4 * R * kStripW)) * a.N < 8LL * kNumSMs) R = 8;
+        const char *er = getenv("RSGRAD_WARP_R");
+        if (er) R = atoi(er) == 8 ? 8 : 16;
+        const int tiles_y = (a.H + R * kStripW - 1) / (R * kStripW);
+        const dim3 grid((unsigned)(tiles_x * tiles_y), a.N);
+        const int CW = a.C < 4 ? a.C : 4;
+#define RS_STRIP(RR)                                                                                        \
+    switch (CW) {                                                                                           \
+        case 1: warp_bwd_strip<1, RR><<<grid, kStripW * 32, 0, s>>>(a, tiles_x, 1.0 / a.W); break;          \
+        case 2: warp_bwd_strip<2, RR><<<grid, kStripW * 32, 0, s>>>(a, tiles_x, 1.0 / a.W); break;          \
+        case 3: warp_bwd_strip<3, RR><<<grid, kStripW * 32, 0, s>>>(a, tiles_x, 1.0 / a.W); break;          \
+        default: warp_bwd_strip<4, RR><<<grid, kStripW * 32, 0, s>>>(a, tiles_x, 1.0 / a.W); break;         \
+    }
+        if (R == 8) {
+            RS_STRIP(8)
+        } else {
+            RS_STRIP(16)
+        }
+#undef RS_STRIP
+        note_launch();
+        return cudaGetLastError();
+    }
+    if (direct || !win) {
         warp_bwd_kernel<<<dim3((unsigned)((HW + kThreads - 1) / kThreads), a.N), kThreads, 0, s>>>(a, 1.0 / a.W);
         note_launch();
         return cudaGetLastError();

@@ -482,34 +482,110 @@ def test_bslice_many_planes_and_coarse_grid(cuda_device):
     assert_close(_np(dx), rdx, "grad", "dx")
 
 
-@pytest.mark.parametrize("variant", ["win8,4,4", "win4,8,2", "win8,8,1", "win4,4,3", "direct"])
+def _collapse_flow(N, H, W):
+    """A flow that folds each row onto ~1/30 of its width and each column onto ~1/10 of
+    its height: ~1300 taps land on every element of a small region."""
+    yy, xx = torch.meshgrid(torch.arange(H, dtype=torch.float32), torch.arange(W, dtype=torch.float32),
+                            indexing="ij")
+    return torch.stack([-xx * 0.97 + 3.3, -yy * 0.9 + 2.6]).expand(N, 2, H, W).contiguous()
+
+
+def _fp32_sum_bound(x, flow, dy, border):
+    """Worst-case rounding of an fp32 sum in any order (PAPER.md:733's atomics): for an
+    element receiving n terms, |fl(sum) - sum| <= (n - 1) u sum|term| with u = 2^-24
+    (+ one rounding of each product w*g).  Computed from the oracle with |dy|
+    (the weights are >= 0, so dx(|dy|) = sum |w g|) and a tap count per element."""
+    absdx, _ = oracle.warp_bwd(x, flow, np.abs(dy), border)
+    N, C, H, W = x.shape
+    # taps per element: count every tap that lands in the image (weights ignored)
+    yy, xx = np.meshgrid(np.arange(H), np.arange(W), indexing="ij")
+    n_max = 0
+    for n in range(N):
+        ix = xx + flow[n, 0].astype(np.float64)
+        iy = yy + flow[n, 1].astype(np.float64)
+        if border:
+            ix, iy = np.clip(ix, 0, W - 1), np.clip(iy, 0, H - 1)
+        x0, y0 = np.floor(ix).astype(np.int64), np.floor(iy).astype(np.int64)
+        cnt = np.zeros((H + 2, W + 2), np.int64)
+        for dy_, dx_ in ((0, 0), (0, 1), (1, 0), (1, 1)):
+            ex, ey = x0 + dx_, y0 + dy_
+            ok = (ex >= 0) & (ex < W) & (ey >= 0) & (ey < H)
+            np.add.at(cnt, (ey[ok], ex[ok]), 1)
+        n_max = max(n_max, int(cnt.max()))
+    u = 2.0 ** -24
+    return (n_max + 1) * u * absdx + 1e-30
+
+
+@pytest.mark.parametrize("variant", ["auto", "auto_r8", "win8,4,4", "win4,8,2", "win8,8,1", "win4,4,3", "direct"])
 @pytest.mark.parametrize("shape", [(2, 3, 70, 100), (1, 7, 45, 61), (1, 1, 33, 36), (2, 2, 130, 68)])
 @pytest.mark.parametrize("flow", ["smooth", "stress", "collapse"])
 @pytest.mark.parametrize("padding", ["zeros", "border"])
-def test_warp_bwd_window_variants(cuda_device, monkeypatch, variant, shape, flow, padding):
-    """warp_bwd d_input through per-warp shared windows flushed by vector reds
-    (RSGRAD_WARP_BWD=winR,NW,IT; AUTO keeps the per-tap reds, "direct"):
-    every (rows, warps, iterations) instantiation, ragged strips, W % 4 != 0 (scalar
-    flush), C > 3 (channel chunks), taps leaving the window (stress: direct reds) and a
-    collapsing flow (every pixel of a row on the same few cells: 32-lane duplicate
-    groups combined by shuffles)."""
-    if variant == "direct" and flow == "collapse":
-        # a collapsing flow puts thousands of taps on a few elements: the per-tap fp32
-        # reds' sequential rounding (order set by the hardware) can exceed T there
-        # (DESIGN.md "Precision limits"); the window variants pre-sum per group
-        pytest.skip("fp32 atomic fan-in beyond the tolerance model")
-    monkeypatch.setenv("RSGRAD_WARP_BWD", variant)
+def test_warp_bwd_variants(cuda_device, monkeypatch, variant, shape, flow, padding):
+    """warp_bwd d_input variants: "auto" = row strips with register-combined taps
+    (warp_bwd_strip, R = 16 / "auto_r8" R = 8), "win..." = per-warp shared windows flushed
+    by vector reds (RSGRAD_WARP_BWD=winR,NW,IT), "direct" = one fp32 red per tap (the
+    unconverted scatter, = SCATTER_ATOMIC).  Ragged strips, W % 32 != 0, C > 4 (channel
+    chunks), stress flows (taps far from their row) and a collapsing flow (~1300 taps per
+    element: runs of lanes on one cell, rows on one cell).  The per-tap kernel is held to
+    the worst-case rounding bound of an unordered fp32 sum instead of T: its error grows
+    with the fan-in, which is why AUTO combines taps before the reds."""
+    if variant.startswith("win"):
+        monkeypatch.setenv("RSGRAD_WARP_BWD", variant)
+    elif variant == "direct":
+        monkeypatch.setenv("RSGRAD_WARP_BWD", "direct")
+    elif variant == "auto_r8":
+        monkeypatch.setenv("RSGRAD_WARP_R", "8")
     N, C, H, W = shape
     inp = synth.warp_inputs(N, C, H, W, cfg=1, flow="stress" if flow == "collapse" else flow)
     if flow == "collapse":
-        yy, xx = torch.meshgrid(torch.arange(H, dtype=torch.float32), torch.arange(W, dtype=torch.float32),
-                                indexing="ij")
-        inp["flow"] = torch.stack([-xx * 0.97 + 3.3, -yy * 0.9 + 2.6]).expand(N, 2, H, W).contiguous()
+        inp["flow"] = _collapse_flow(N, H, W)
     g = _cuda(inp, cuda_device)
     dx, df = rsgrad.warp_bwd(g["x"], g["flow"], g["dy"], padding=padding)
-    rdx, rdf = oracle.warp_bwd(*(inp[k].double().numpy() for k in ("x", "flow", "dy")), padding == "border")
-    assert_close(_np(dx), rdx, "grad", f"dx[{variant}]")
+    x, fl, dy = (inp[k].double().numpy() for k in ("x", "flow", "dy"))
+    rdx, rdf = oracle.warp_bwd(x, fl, dy, padding == "border")
     assert_close(_np(df), rdf, "grad", f"dflow[{variant}]")
+    if variant == "direct" and flow == "collapse":
+        bound = _fp32_sum_bound(x, fl, dy, padding == "border")
+        err = np.abs(_np(dx) - rdx)
+        assert np.all(err <= bound), f"dx[direct] beyond the fp32 summation bound: {np.max(err / bound)}"
+    else:
+        assert_close(_np(dx), rdx, "grad", f"dx[{variant}]")
+
+
+@pytest.mark.parametrize("padding", ["zeros", "border"])
+def test_warp_bwd_auto_collapse_paper_shape(cuda_device, padding):
+    """configs[2] shape (8 x 3 x 384 x 512) with a collapsing flow: AUTO d_input and
+    d_flow within T on every element (border padding also clamps the off-image taps
+    onto the edge rows / columns)."""
+    N, C, H, W = 8, 3, 384, 512
+    inp = synth.warp_inputs(N, C, H, W, cfg=3, flow="smooth")
+    inp["flow"] = _collapse_flow(N, H, W)
+    g = _cuda(inp, cuda_device)
+    dx, df = rsgrad.warp_bwd(g["x"], g["flow"], g["dy"], padding=padding)
+    x, fl, dy = (inp[k].double().numpy() for k in ("x", "flow", "dy"))
+    rdx, rdf = oracle.warp_bwd(x, fl, dy, padding == "border")
+    assert_close(_np(dx), rdx, "grad", "dx")
+    assert_close(_np(df), rdf, "grad", "dflow")
+
+
+@pytest.mark.parametrize("flow", ["zero", "int", "translate_border"])
+def test_warp_bwd_strip_special_flows(cuda_device, flow):
+    """Integer and zero flows put every sample on a kink (fx = fy = 0): the strip kernel's
+    carried taps then have zero weight and are skipped; a large translation with border
+    padding clamps whole rows onto one edge column (a vertical run per lane)."""
+    N, C, H, W = 2, 3, 67, 90
+    inp = synth.warp_inputs(N, C, H, W, cfg=1, flow="zero")
+    if flow == "int":
+        inp["flow"] = torch.stack([torch.full((H, W), 3.0), torch.full((H, W), -2.0)]).expand(N, 2, H, W).contiguous()
+    elif flow == "translate_border":
+        inp["flow"] = torch.stack([torch.full((H, W), 500.5), torch.full((H, W), 0.25)]).expand(N, 2, H, W).contiguous()
+    g = _cuda(inp, cuda_device)
+    border = flow == "translate_border"
+    dx, df = rsgrad.warp_bwd(g["x"], g["flow"], g["dy"], padding="border" if border else "zeros")
+    x, fl, dy = (inp[k].double().numpy() for k in ("x", "flow", "dy"))
+    rdx, rdf = oracle.warp_bwd(x, fl, dy, border)
+    assert_close(_np(dx), rdx, "grad", "dx")
+    assert_close(_np(df), rdf, "grad", "dflow")
 
 
 def test_warp_bwd_scatter_atomic_algo(cuda_device):
