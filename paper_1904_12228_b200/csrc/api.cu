@@ -236,13 +236,14 @@ unsigned long long rsgrad_launch_count(int reset) {
 
 size_t rsgrad_bwd_workspace_bytes(int layer, int N, int C, int H, int W, int Ho, int Wo, int D,
                                   int Gh, int Gw, const rs_opts *opts) {
-    (void)opts;
+    const bool det = opts && opts->deterministic == 1;
     switch (layer) {
         case 0:
-            if (!pos(N) || !pos(Ho) || !pos(Wo)) return 0;
-            return rs::stn_ws_bytes(N, C, H, W, Ho, Wo);
+            if (!pos(N) || !pos(C) || !pos(H) || !pos(W) || !pos(Ho) || !pos(Wo)) return 0;
+            return rs::stn_ws_bytes(N, C, H, W, Ho, Wo, det);
         case 1:
-            return rs::warp_ws_bytes(N, C, H, W);
+            if (!pos(N) || !pos(C) || !pos(H) || !pos(W)) return 0;
+            return rs::warp_ws_bytes(N, C, H, W, det);
         case 2:
             if (!pos(N) || !pos(H) || !pos(W) || !pos(D) || !pos(Gh) || !pos(Gw)) return 0;
             return rs::bslice_ws_bytes(N, H, W, D, Gh, Gw);
@@ -254,7 +255,8 @@ size_t rsgrad_bwd_workspace_bytes(int layer, int N, int C, int H, int W, int Ho,
             return rs::convloss_ws_bytes(N, H, W);
         case 5:
             if (!pos(N) || !pos(Ho) || !pos(Wo)) return 0;
-            return rs::stn_bicubic_ws_bytes(N, Ho, Wo);
+            if (!pos(C) || !pos(H) || !pos(W)) return 0;
+            return rs::stn_bicubic_ws_bytes(N, C, H, W, Ho, Wo, det);
         case 6:
             if (!pos(N) || !pos(Ho) || !pos(Wo) || !pos(D)) return 0;
             return rs::stn_var_ws_bytes(N, D * Ho * Wo, 12);
@@ -313,11 +315,10 @@ rs_status stn_bwd(const float *x, const float *theta, const float *dy, int N, in
     const bool border = o.padding == RS_PAD_BORDER;
     if (dx && border && o.algo == RS_ALGO_GATHER)
         return fail(RS_ERR_FLAG, "stn_bwd: GATHER needs zeros padding (border clamp has no bounded inverse)");
-    if (dx && border && o.deterministic)
-        return fail(RS_ERR_FLAG, "stn_bwd: no deterministic d_input path with border padding");
     if (dx && (o.algo == RS_ALGO_SCATTER_ATOMIC || o.algo == RS_ALGO_SCATTER_PRIV) && o.deterministic)
         return fail(RS_ERR_FLAG, "stn_bwd: scatter paths (atomics) are not deterministic");
     if (!dx && !dtheta) return ok();
+    const bool det = o.deterministic && dx;
     cudaStream_t s = (cudaStream_t)stream;
     std::vector<TArg> args = {{x, sizeof(float) * (size_t)C * H * W, true, false},
                               {theta, sizeof(float) * 6, true, false},
@@ -325,7 +326,7 @@ rs_status stn_bwd(const float *x, const float *theta, const float *dy, int N, in
                               {dx, sizeof(float) * (size_t)C * H * W, false, true},
                               {dtheta, sizeof(float) * 6, false, true}};
     return run_batched(N, args, s, workspace, ws_bytes,
-                       [&](int n) { return rs::stn_ws_bytes(n, C, H, W, Ho, Wo); },
+                       [&](int n) { return rs::stn_ws_bytes(n, C, H, W, Ho, Wo, det); },
                        [&](int, int nc, void **p, cudaStream_t t, void *ws) {
                            rs::StnArgs a{};
                            a.x = (const float *)p[0];
@@ -337,7 +338,7 @@ rs_status stn_bwd(const float *x, const float *theta, const float *dy, int N, in
                            a.ac = o.align_corners;
                            a.border = border;
                            return rs::stn_bwd_launch(a, o.algo, o.deterministic, ws,
-                                                     rs::stn_ws_bytes(nc, C, H, W, Ho, Wo), t);
+                                                     rs::stn_ws_bytes(nc, C, H, W, Ho, Wo, det), t);
                        });
 }
 
@@ -383,8 +384,8 @@ rs_status warp_bwd(const float *x, const float *flow, const float *dy, int N, in
     if (!dy) return fail(RS_ERR_NULL, "warp_bwd: dy is required");
     if (dx && o.algo == RS_ALGO_GATHER)
         return fail(RS_ERR_FLAG, "warp_bwd: GATHER invalid (arbitrary flow has no bounded inverse)");
-    if (dx && o.deterministic)
-        return fail(RS_ERR_FLAG, "warp_bwd: no deterministic d_input path (atomic scatter)");
+    if (dx && o.deterministic && (o.algo == RS_ALGO_SCATTER_ATOMIC || o.algo == RS_ALGO_SCATTER_PRIV))
+        return fail(RS_ERR_FLAG, "warp_bwd: SCATTER_ATOMIC / SCATTER_PRIV are atomic paths (not deterministic)");
     if (!dx && !dflow) return ok();
     cudaStream_t s = (cudaStream_t)stream;
     std::vector<TArg> args = {{x, sizeof(float) * (size_t)C * H * W, true, false},
@@ -392,7 +393,8 @@ rs_status warp_bwd(const float *x, const float *flow, const float *dy, int N, in
                               {dy, sizeof(float) * (size_t)C * H * W, true, false},
                               {dx, sizeof(float) * (size_t)C * H * W, false, true},
                               {dflow, sizeof(float) * 2 * (size_t)H * W, false, true}};
-    return run_batched(N, args, s, workspace, ws_bytes, [&](int n) { return rs::warp_ws_bytes(n, C, H, W); },
+    const bool det = o.deterministic && dx;
+    return run_batched(N, args, s, workspace, ws_bytes, [&](int n) { return rs::warp_ws_bytes(n, C, H, W, det); },
                        [&](int, int nc, void **p, cudaStream_t t, void *ws) {
                            rs::WarpArgs a{};
                            a.x = (const float *)p[0];
@@ -402,7 +404,8 @@ rs_status warp_bwd(const float *x, const float *flow, const float *dy, int N, in
                            a.dflow = (float *)p[4];
                            a.N = nc; a.C = C; a.H = H; a.W = W;
                            a.border = o.padding == RS_PAD_BORDER;
-                           return rs::warp_bwd_launch(a, o.algo, o.deterministic, ws, 0, t);
+                           return rs::warp_bwd_launch(a, o.algo, o.deterministic, ws,
+                                                      rs::warp_ws_bytes(nc, C, H, W, det), t);
                        });
 }
 
@@ -632,7 +635,7 @@ rs_status stn_bicubic_fwd(const float *x, const float *theta, int N, int C, int 
     rs::StnArgs a{};
     a.x = x; a.theta = theta; a.y = y;
     a.N = N; a.C = C; a.H = H; a.W = W; a.Ho = Ho; a.Wo = Wo; a.ac = o.align_corners;
-    return launched(rs::stn_bicubic_launch(a, false, 0, nullptr, (cudaStream_t)stream), "stn_bicubic_fwd");
+    return launched(rs::stn_bicubic_launch(a, false, 0, false, nullptr, (cudaStream_t)stream), "stn_bicubic_fwd");
 }
 
 rs_status stn_bicubic_bwd(const float *x, const float *theta, const float *dy, int N, int C, int H, int W, int Ho,
@@ -648,9 +651,10 @@ rs_status stn_bicubic_bwd(const float *x, const float *theta, const float *dy, i
     a.x = x; a.theta = theta; a.dy = dy; a.dx = dx; a.dtheta = dtheta;
     a.N = N; a.C = C; a.H = H; a.W = W; a.Ho = Ho; a.Wo = Wo; a.ac = o.align_corners;
     cudaStream_t s = (cudaStream_t)stream;
-    return with_ws(rs::stn_bicubic_ws_bytes(N, Ho, Wo), workspace, ws_bytes, s,
+    const bool det = o.deterministic && dx;
+    return with_ws(rs::stn_bicubic_ws_bytes(N, C, H, W, Ho, Wo, det), workspace, ws_bytes, s,
                    [&](void *ws) {
-                       return rs::stn_bicubic_launch(a, true, o.deterministic ? (int)RS_ALGO_GATHER : (int)o.algo, ws, s);
+                       return rs::stn_bicubic_launch(a, true, (int)o.algo, det, ws, s);
                    },
                    "stn_bicubic_bwd");
 }

@@ -306,14 +306,14 @@ struct ConvArgs {
 cudaError_t stn_fwd_launch(const StnArgs &a, cudaStream_t s);
 cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *ws, size_t ws_bytes,
                            cudaStream_t s);
-size_t stn_ws_bytes(int N, int C, int H, int W, int Ho, int Wo);
+size_t stn_ws_bytes(int N, int C, int H, int W, int Ho, int Wo, bool det = false);
 
 // output-tile kernel driven by a flow field (warp.cu): mode 0 = y, 2 = d_flow (+ dx reds)
 cudaError_t flow_tile_launch(const StnArgs &a, int mode, bool priv, cudaStream_t s);
 cudaError_t warp_fwd_launch(const WarpArgs &a, cudaStream_t s);
 cudaError_t warp_bwd_launch(const WarpArgs &a, int algo, int deterministic, void *ws,
                             size_t ws_bytes, cudaStream_t s);
-size_t warp_ws_bytes(int N, int C, int H, int W);
+size_t warp_ws_bytes(int N, int C, int H, int W, bool det = false);
 
 cudaError_t bslice_fwd_launch(const BsliceArgs &a, cudaStream_t s);
 cudaError_t bslice_bwd_launch(const BsliceArgs &a, int algo, int deterministic, void *ws,
@@ -331,8 +331,8 @@ cudaError_t convloss_grad_launch(const float *in, const float *hk, const float *
 cudaError_t upsample4_launch(const float *src, float *dst, int N, int C, int H, int W, bool bwd, cudaStream_t s);
 
 size_t stn_var_ws_bytes(int N, int P, int ne);
-size_t stn_bicubic_ws_bytes(int N, int Ho, int Wo);
-cudaError_t stn_bicubic_launch(const StnArgs &a, bool bwd, int algo, void *ws, cudaStream_t s);
+size_t stn_bicubic_ws_bytes(int N, int C, int H, int W, int Ho, int Wo, bool det);
+cudaError_t stn_bicubic_launch(const StnArgs &a, bool bwd, int algo, bool det, void *ws, cudaStream_t s);
 cudaError_t stn_lanczos_launch(const StnArgs &a, bool bwd, void *ws, cudaStream_t s);
 cudaError_t stn3d_launch(const float *x, const float *theta, const float *dy, float *y, float *dx, float *dtheta,
                          int N, int C, int D, int H, int W, int Do, int Ho, int Wo, int ac, bool bwd, void *ws,

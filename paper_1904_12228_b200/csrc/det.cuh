@@ -1,0 +1,170 @@
+// det.cuh — deterministic general scatter by fixed-point integer accumulation.
+//
+// where a scatter cannot be converted to a gather, "we fall back to a
+// general scattering operation" with atomics.  fp32 atomics sum in the order the
+// memory system applies them, so their result is not reproducible (and their rounding
+// grows with the fan-in of an element).  This path makes the same scatter bitwise
+// reproducible (rs_opts.deterministic = 1, SURVEY §8(b) "Deterministic when
+// deterministic=1"): every contribution w*g is formed exactly in fp64, scaled by 2^S
+// and rounded once to a 64-bit integer, and the integers are summed with 64-bit
+// atomics -- integer addition is associative, so the sum does not depend on the
+// order.  S is chosen per sample from max|dY| so that no partial sum can overflow:
+//   |sum| <= max|g| * sum_q |w_q| <= max|g| * P * kWmax  < 2^61 * 2^-S.
+// Each term carries at most 2^-(S+1) absolute rounding, so an element with n terms
+// is within n * 2^-(S+1) = n * max|g| * P * kWmax * 2^-62 of the exact sum (≈1e-11
+// for the bench shapes) -- far tighter than fp32 accumulation.
+//
+// One persistent cooperative kernel walks the selected samples one after another
+// (the int64 accumulator is one sample large): per sample, (A) zero the accumulator
+// and reduce max|dY| (order-free: atomicMax on the bit pattern), (B) scatter, (C)
+// convert to fp32 into dx; phases are separated by a grid barrier (all blocks are
+// co-resident: cudaLaunchCooperativeKernel).
+#pragma once
+
+#include "common.cuh"
+
+namespace rs {
+
+struct DetWs {
+    unsigned long long *acc;  // C*HW accumulators of one sample
+    unsigned *maxbits;        // per selected-sample slot: max |dY| bit pattern
+    unsigned *bar;            // grid barrier: count, generation
+};
+
+inline size_t det_align(size_t v) { return (v + 255) & ~(size_t)255; }
+
+// bytes of the deterministic-scatter workspace for N samples of C*HW input elements
+inline size_t det_ws_bytes(int N, long long CHW) {
+    return det_align(sizeof(unsigned long long) * (size_t)CHW) + det_align(sizeof(unsigned) * ((size_t)N + 2));
+}
+
+inline DetWs det_ws_layout(void *base, int N, long long CHW) {
+    (void)N;
+    DetWs w;
+    char *b = (char *)base;
+    w.acc = (unsigned long long *)b;
+    w.bar = (unsigned *)(b + det_align(sizeof(unsigned long long) * (size_t)CHW));
+    w.maxbits = w.bar + 2;
+    return w;
+}
+
+// Sense-free grid barrier: the generation is read before arriving; the last block
+// to arrive resets the count and bumps the generation.
+RS_DEV void det_grid_barrier(unsigned *bar, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned *gen = bar + 1;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == nblocks - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g) __nanosleep(100);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// Sampler concept (see the layer files):
+//   static constexpr int kMaxTaps;      taps per output pixel
+//   static constexpr double kWmax;      bound on sum over output pixels of |w| landing on one element, / P
+//   RS_DEV int taps(int n, long long q, long long *off, float *w) const;
+//     the in-image taps of output pixel q of sample n: element offsets within a
+//     channel plane and the fp32 weights the float path uses.
+// Sample selection: list/count (device list of samples), else flags (flags[n] != 0),
+// else every sample 0..N-1.
+template <class S, int kT = 256>
+__global__ void __launch_bounds__(kT)
+    det_scatter_kernel(S smp, const float *__restrict__ dy, float *__restrict__ dx, int N, int C, long long HW,
+                       long long P, const int *__restrict__ list, const int *__restrict__ count,
+                       const int *__restrict__ flags, DetWs ws) {
+    const unsigned nb = gridDim.x;
+    const long long tid = (long long)blockIdx.x * kT + threadIdx.x, nthr = (long long)nb * kT;
+    const int nsel = list ? *count : N;
+    const long long CHW = (long long)C * HW, CP = (long long)C * P;
+    __shared__ unsigned red[kT / 32];
+    for (int f = 0; f < nsel; f++) {
+        const int n = list ? list[f] : f;
+        if (!list && flags && !flags[n]) continue;  // uniform over the grid
+        const float *g = dy + (long long)n * CP;
+        // (A) zero the accumulator, max |dY| of the sample
+        for (long long e = tid; e < CHW; e += nthr) ws.acc[e] = 0ull;
+        unsigned m = 0u;
+        for (long long e = tid; e < CP; e += nthr) m = max(m, __float_as_uint(fabsf(__ldg(g + e))));
+        m = __reduce_max_sync(0xffffffffu, m);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned b = 0u;
+            for (int k = 0; k < kT / 32; k++) b = max(b, red[k]);
+            atomicMax(ws.maxbits + f, b);
+        }
+        det_grid_barrier(ws.bar, nb);
+        // (B) scatter: round(w*g * 2^S) into 64-bit integer sums
+        const float mx = __uint_as_float(__ldcg(ws.maxbits + f));
+        const bool finite = isfinite(mx);
+        int Sx = 0;
+        if (mx > 0.f && finite) {
+            const double bound = (double)mx * (double)P * S::kWmax;
+            Sx = 61 - ilogb(bound) - 1;  // bound < 2^(ilogb+1)  =>  bound * 2^S < 2^61
+        }
+        if (finite) {
+            for (long long q = tid; q < P; q += nthr) {
+                long long off[S::kMaxTaps];
+                float w[S::kMaxTaps];
+                const int nt = smp.taps(n, q, off, w);
+                if (nt == 0) continue;
+                for (int c = 0; c < C; c++) {
+                    const float gv = __ldg(g + (long long)c * P + q);
+                    if (gv == 0.f) continue;
+                    unsigned long long *ac = ws.acc + (long long)c * HW;
+#pragma unroll
+                    for (int k = 0; k < S::kMaxTaps; k++) {
+                        if (k >= nt) break;
+                        const double v = ldexp((double)w[k] * (double)gv, Sx);  // exact product, exact scaling
+                        const long long iv = __double2ll_rn(v);
+                        if (iv != 0) atomicAdd(ac + off[k], (unsigned long long)iv);
+                    }
+                }
+            }
+        }
+        det_grid_barrier(ws.bar, nb);
+        // (C) fixed point -> fp32 (non-finite dY: the sample's dx is NaN)
+        float *d = dx + (long long)n * CHW;
+        for (long long e = tid; e < CHW; e += nthr)
+            d[e] = finite ? (float)ldexp((double)(long long)__ldcg(ws.acc + e), -Sx) : __int_as_float(0x7fffffff);
+        det_grid_barrier(ws.bar, nb);
+    }
+}
+
+// Zero the barrier / max slots, then launch the cooperative kernel with every block
+// co-resident.
+template <class S>
+cudaError_t det_scatter_launch(const S &smp, const float *dy, float *dx, int N, int C, long long HW, long long P,
+                               const int *list, const int *count, const int *flags, void *ws, cudaStream_t s) {
+    constexpr int kT = 256;
+    const DetWs w = det_ws_layout(ws, N, (long long)C * HW);
+    cudaError_t e = cudaMemsetAsync(w.bar, 0, sizeof(unsigned) * ((size_t)N + 2), s);
+    if (e != cudaSuccess) return e;
+    int dev = 0, nsm = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    auto kern = det_scatter_kernel<S, kT>;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kT, 0);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    const int blocks = nsm * (occ < 4 ? occ : 4);
+    S sm = smp;
+    long long hw = HW, p = P;
+    int n = N, c = C;
+    DetWs wk = w;
+    void *args[] = {&sm, (void *)&dy, (void *)&dx, &n, &c, &hw, &p, (void *)&list, (void *)&count, (void *)&flags, &wk};
+    e = cudaLaunchCooperativeKernel((const void *)kern, dim3(blocks), dim3(kT), args, 0, s);
+    note_launch();
+    return e;
+}
+
+}  // namespace rs

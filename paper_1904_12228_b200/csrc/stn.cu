@@ -37,6 +37,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "det.cuh"
 
 namespace rs {
 namespace {
@@ -1669,6 +1670,36 @@ __global__ void __launch_bounds__(kThreads)
     }
 }
 
+// Bilinear STN taps for the deterministic fixed-point scatter (det.cuh): the same
+// exact fp64 coordinate and fp32 weights as stn_dx_scatter.
+struct StnTapSampler {
+    const float *theta;
+    int H, W, Ho, Wo, ac, border;
+    static constexpr int kMaxTaps = 4;
+    static constexpr double kWmax = 1.0;
+    RS_DEV int taps(int n, long long q, long long *off, float *w) const {
+        const int i = (int)(q / Wo), j = (int)(q - (long long)i * Wo);
+        const Theta T = load_theta(theta, n);
+        double ix, iy;
+        stn_coord(T, stn_norm(j, Wo, ac), stn_norm(i, Ho, ac), H, W, ac, ix, iy);
+        if (border) {
+            float d;
+            ix = clamp_coord(ix, W, d);
+            iy = clamp_coord(iy, H, d);
+        }
+        const Cell cx = cell_of(ix), cy = cell_of(iy);
+        const bool x0ok = cx.i0 >= 0 && cx.i0 < W, x1ok = cx.i0 + 1 >= 0 && cx.i0 + 1 < W;
+        const bool y0ok = cy.i0 >= 0 && cy.i0 < H, y1ok = cy.i0 + 1 >= 0 && cy.i0 + 1 < H;
+        const long long o00 = (long long)cy.i0 * W + cx.i0;
+        int k = 0;
+        if (y0ok && x0ok) { off[k] = o00; w[k++] = (1.f - cy.f) * (1.f - cx.f); }
+        if (y0ok && x1ok) { off[k] = o00 + 1; w[k++] = (1.f - cy.f) * cx.f; }
+        if (y1ok && x0ok) { off[k] = o00 + W; w[k++] = cy.f * (1.f - cx.f); }
+        if (y1ok && x1ok) { off[k] = o00 + W + 1; w[k++] = cy.f * cx.f; }
+        return k;
+    }
+};
+
 // ----------------------------------------------------------------- host helpers
 size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
@@ -1704,10 +1735,11 @@ int stn_bwd_variant() {
 struct StnWs {
     double *xtab, *ytab, *pb, *pf;
     int *flags, *fb_list, *fb_count;
+    void *det;  // deterministic fallback scatter (det.cuh), when requested
     size_t bytes;
 };
 
-StnWs stn_ws_layout(void *base, int N, int H, int W, int Ho, int Wo) {
+StnWs stn_ws_layout(void *base, int N, int C, int H, int W, int Ho, int Wo, bool det) {
     const StnGeom g = stn_geom(H, W, Ho, Wo);
     StnWs w;
     size_t off = 0;
@@ -1725,6 +1757,7 @@ StnWs stn_ws_layout(void *base, int N, int H, int W, int Ho, int Wo) {
     const size_t tb = (size_t)g.bx * g.by > (size_t)g.gx * g.gy ? (size_t)g.bx * g.by : (size_t)g.gx * g.gy;
     w.pb = (double *)take(sizeof(double) * 6 * (size_t)N * tb);
     w.pf = (double *)take(sizeof(double) * 6 * (size_t)N * g.fj * g.fi);
+    w.det = det ? take(det_ws_bytes(N, (long long)C * H * W)) : nullptr;
     w.bytes = off;
     return w;
 }
@@ -1765,9 +1798,8 @@ bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
 
 }  // namespace
 
-size_t stn_ws_bytes(int N, int C, int H, int W, int Ho, int Wo) {
-    (void)C;
-    return stn_ws_layout(nullptr, N, H, W, Ho, Wo).bytes;
+size_t stn_ws_bytes(int N, int C, int H, int W, int Ho, int Wo, bool det) {
+    return stn_ws_layout(nullptr, N, C, H, W, Ho, Wo, det).bytes;
 }
 
 cudaError_t stn_fwd_launch(const StnArgs &a, cudaStream_t s) {
@@ -1837,9 +1869,9 @@ cudaError_t flow_tile_launch(const StnArgs &a, int mode, bool priv, cudaStream_t
 cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *ws, size_t ws_bytes,
                            cudaStream_t s) {
     (void)ws_bytes;
-    (void)deterministic;
+    const bool det = deterministic && a.dx;
     const StnGeom g = stn_geom(a.H, a.W, a.Ho, a.Wo);
-    const StnWs w = stn_ws_layout(ws, a.N, a.H, a.W, a.Ho, a.Wo);
+    const StnWs w = stn_ws_layout(ws, a.N, a.C, a.H, a.W, a.Ho, a.Wo, det);
     const long long HW = (long long)a.H * a.W;
     const int tmax = a.Wo > a.Ho ? a.Wo : a.Ho;
     stn_tables_kernel<<<(tmax + 255) / 256, 256, 0, s>>>(w.xtab, w.ytab, a.Ho, a.Wo, a.ac);
@@ -1850,7 +1882,7 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
     const int variant = stn_bwd_variant();
     stn_classify_kernel<<<1, 256, 0, s>>>(a, allow_gather, variant, w.flags, w.fb_list, w.fb_count);
     note_launch();
-    if (!allow_gather && a.dx) {
+    if (!allow_gather && a.dx && !det) {
         cudaError_t e = cudaMemsetAsync(a.dx, 0, sizeof(float) * (size_t)a.N * a.C * HW, s);
         if (e != cudaSuccess) return e;
     }
@@ -1939,6 +1971,12 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
         set_smem(k, smp);
         k<<<dim3(g.fj * g.fi, 1), kThreads, smp, s>>>(b, w.xtab, w.ytab, w.fb_list, w.fb_count, nullptr, g.fj, g.fi);
         note_launch();
+    } else if (det) {
+        // deterministic=1: the fallback samples' d_input by the fixed-point scatter
+        const StnTapSampler smp{a.theta, a.H, a.W, a.Ho, a.Wo, a.ac, a.border};
+        cudaError_t e = det_scatter_launch(smp, a.dy, a.dx, a.N, a.C, HW, (long long)a.Ho * a.Wo, w.fb_list,
+                                           w.fb_count, nullptr, w.det, s);
+        if (e != cudaSuccess) return e;
     } else if (a.dx && !priv) {
         const long long P = (long long)a.Ho * a.Wo;
         long long blocks = (P + kThreads - 1) / kThreads;

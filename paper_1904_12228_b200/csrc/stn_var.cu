@@ -12,6 +12,7 @@
 // deterministic=1) or the general scatter with atomics (AUTO / SCATTER_ATOMIC, and the 3-D
 // STN: PAPER.md:733's fallback).
 #include "common.cuh"
+#include "det.cuh"
 
 namespace rs {
 namespace {
@@ -572,17 +573,48 @@ __global__ void theta_finalize(const double *part, int nb, int ne, float *dtheta
     dtheta[n * ne + e] = (float)s;
 }
 
+// Bicubic taps for the deterministic fixed-point scatter (det.cuh): the 16 in-image
+// taps of bicubic_bwd with its fp32 weights wy * wx (|w| <= 1 per tap).
+struct BicubicTapSampler {
+    const float *theta;
+    int H, W, Ho, Wo, ac;
+    static constexpr int kMaxTaps = 16;
+    static constexpr double kWmax = 1.0;
+    RS_DEV int taps(int n, long long q, long long *off, float *w) const {
+        const int i = (int)(q / Wo), j = (int)(q - (long long)i * Wo);
+        const Bicubic b = bicubic_at(theta, n, i, j, H, W, Ho, Wo, ac);
+        int k = 0;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int yy = b.y0 - 1 + u;
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+                const int xx = b.x0 - 1 + v;
+                if (yy >= 0 && yy < H && xx >= 0 && xx < W) {
+                    off[k] = (long long)yy * W + xx;
+                    w[k++] = b.wy[u] * b.wx[v];
+                }
+            }
+        }
+        return k;
+    }
+};
+
 }  // namespace
 
 size_t stn_var_ws_bytes(int N, int P, int ne) {
     return sizeof(double) * (size_t)N * ((P + kVT - 1) / kVT) * ne;
 }
 
-size_t stn_bicubic_ws_bytes(int N, int Ho, int Wo) {
-    return stn_var_ws_bytes(N, Ho * Wo, 6) + sizeof(double) * (size_t)(Ho + Wo) + sizeof(int) * (size_t)N;
+static size_t bicubic_base_bytes(int N, int Ho, int Wo) {
+    return det_align(stn_var_ws_bytes(N, Ho * Wo, 6) + sizeof(double) * (size_t)(Ho + Wo) + sizeof(int) * (size_t)N);
 }
 
-cudaError_t stn_bicubic_launch(const StnArgs &a, bool bwd, int algo, void *ws, cudaStream_t s) {
+size_t stn_bicubic_ws_bytes(int N, int C, int H, int W, int Ho, int Wo, bool det) {
+    return bicubic_base_bytes(N, Ho, Wo) + (det ? det_ws_bytes(N, (long long)C * H * W) : 0);
+}
+
+cudaError_t stn_bicubic_launch(const StnArgs &a, bool bwd, int algo, bool det, void *ws, cudaStream_t s) {
     const int P = a.Ho * a.Wo;
     const dim3 grid((P + kVT - 1) / kVT, a.N);
     if (!bwd) {
@@ -598,7 +630,7 @@ cudaError_t stn_bicubic_launch(const StnArgs &a, bool bwd, int algo, void *ws, c
     // GATHER (or deterministic=1, passed as algo 1): the converted gather; AUTO takes the
     // atomic scatter, measured faster here (4 x 16 x 512^2: 0.79 ms for reds + d_theta in
     // one pass vs 0.57 ms gather + 0.28 ms d_theta pass)
-    const bool gather = a.dx && algo == 1 /*GATHER*/;
+    const bool gather = a.dx && (algo == 1 /*GATHER*/ || det);
     if (gather) {
         cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)a.N, s);
         if (e != cudaSuccess) return e;
@@ -612,8 +644,23 @@ cudaError_t stn_bicubic_launch(const StnArgs &a, bool bwd, int algo, void *ws, c
         cudaError_t e = cudaMemsetAsync(a.dx, 0, sizeof(float) * (size_t)a.N * a.C * a.H * a.W, s);
         if (e != cudaSuccess) return e;
     }
-    bicubic_bwd<<<grid, kVT, 0, s>>>(a, part, gather ? flags : nullptr);
-    note_launch();
+    if (det && gather) {
+        // deterministic=1: d_theta for every sample here, the gather's fallback samples'
+        // d_input (flags[n] = 1) by the fixed-point scatter instead of reds
+        StnArgs b = a;
+        b.dx = nullptr;
+        if (a.dtheta) {
+            bicubic_bwd<<<grid, kVT, 0, s>>>(b, part, nullptr);
+            note_launch();
+        }
+        const BicubicTapSampler smp{a.theta, a.H, a.W, a.Ho, a.Wo, a.ac};
+        cudaError_t e = det_scatter_launch(smp, a.dy, a.dx, a.N, a.C, (long long)a.H * a.W, (long long)P, nullptr,
+                                           nullptr, flags, (char *)ws + bicubic_base_bytes(a.N, a.Ho, a.Wo), s);
+        if (e != cudaSuccess) return e;
+    } else {
+        bicubic_bwd<<<grid, kVT, 0, s>>>(a, part, gather ? flags : nullptr);
+        note_launch();
+    }
     if (a.dtheta) {
         theta_finalize<<<a.N, 32, 0, s>>>(part, grid.x, 6, a.dtheta);
         note_launch();

@@ -16,6 +16,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "det.cuh"
 
 namespace rs {
 namespace {
@@ -219,8 +220,13 @@ __global__ void __launch_bounds__(kStripW * 32, RS_STRIP_MINB)
             // runs of lanes emitting the same set on the same cell
             const int ppx = __shfl_up_sync(0xffffffffu, pcx, 1), ppy = __shfl_up_sync(0xffffffffu, pcy, 1);
             const unsigned pem = __shfl_up_sync(0xffffffffu, emk, 1);
-            const bool same_prev = lane > 0 && any && pem == emk && ppx == pcx && ppy == pcy;
-            const unsigned runs = __ballot_sync(0xffffffffu, same_prev);
+            const bool same_prev0 = lane > 0 && any && pem == emk && ppx == pcx && ppy == pcy;
+            const unsigned runs0 = __ballot_sync(0xffffffffu, same_prev0);
+            // combine only where it matters for the rounding: a run of >= 3 lanes on one
+            // cell somewhere in the warp (pairs of jittered samples just red twice)
+            const bool scan = (runs0 & (runs0 << 1)) != 0u;
+            const bool same_prev = scan && same_prev0;
+            const unsigned runs = scan ? runs0 : 0u;
             float val[CW][4];
 #pragma unroll
             for (int c = 0; c < CW; c++)
@@ -587,14 +593,31 @@ __global__ void __launch_bounds__(NW * 32)
     }
 }
 
+// Warp taps for the deterministic fixed-point scatter (det.cuh): the coordinate and
+// weights of warp_tap.
+struct WarpTapSampler {
+    WarpArgs a;
+    static constexpr int kMaxTaps = 4;
+    static constexpr double kWmax = 1.0;
+    RS_DEV int taps(int n, long long q, long long *off, float *w) const {
+        const int HW = a.H * a.W;
+        const int y = (int)(q / a.W), x = (int)(q - (long long)y * a.W);
+        const float *fp = a.flow + (long long)n * 2 * HW + q;
+        float cgx, cgy;
+        const Tap t = warp_tap(a, x, y, __ldg(fp), __ldg(fp + HW), cgx, cgy);
+        int k = 0;
+        if (t.k00) { off[k] = t.o00; w[k++] = t.w00; }
+        if (t.k01) { off[k] = t.o00 + 1; w[k++] = t.w01; }
+        if (t.k10) { off[k] = t.o00 + a.W; w[k++] = t.w10; }
+        if (t.k11) { off[k] = t.o00 + a.W + 1; w[k++] = t.w11; }
+        return k;
+    }
+};
+
 }  // namespace
 
-size_t warp_ws_bytes(int N, int C, int H, int W) {
-    (void)N;
-    (void)C;
-    (void)H;
-    (void)W;
-    return 0;
+size_t warp_ws_bytes(int N, int C, int H, int W, bool det) {
+    return det ? det_ws_bytes(N, (long long)C * H * W) : 0;
 }
 
 // Optional tiled path (RSGRAD_WARP=tiled): the staged-footprint output-tile kernel of
@@ -625,10 +648,19 @@ cudaError_t warp_fwd_launch(const WarpArgs &a, cudaStream_t s) {
 
 cudaError_t warp_bwd_launch(const WarpArgs &a, int algo, int deterministic, void *ws,
                             size_t ws_bytes, cudaStream_t s) {
-    (void)deterministic;
-    (void)ws;
     (void)ws_bytes;
     const long long HW = (long long)a.H * a.W;
+    if (deterministic && a.dx) {
+        // deterministic=1: d_flow by the strip kernel's gather alone, d_input by the
+        // fixed-point scatter (bitwise reproducible, det.cuh)
+        if (a.dflow) {
+            WarpArgs b = a;
+            b.dx = nullptr;
+            cudaError_t e = warp_bwd_launch(b, 0, 0, nullptr, 0, s);
+            if (e != cudaSuccess) return e;
+        }
+        return det_scatter_launch(WarpTapSampler{a}, a.dy, a.dx, a.N, a.C, HW, HW, nullptr, nullptr, nullptr, ws, s);
+    }
     if (a.dx) {
         cudaError_t e = cudaMemsetAsync(a.dx, 0, sizeof(float) * (size_t)a.N * a.C * HW, s);
         if (e != cudaSuccess) return e;

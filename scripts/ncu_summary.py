@@ -13,7 +13,8 @@ KEYS = [
     ("gpu__time_duration.sum", "time"),
     ("dram__bytes_read.sum", "dram rd"),
     ("dram__bytes_write.sum", "dram wr"),
-    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram %"),
+    (("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+      "dram__throughput.avg.pct_of_peak_sustained_elapsed"), "dram %"),
     ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 %"),
     ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1 %"),
     ("lts__t_sector_hit_rate.pct", "L2 hit %"),
@@ -24,7 +25,15 @@ KEYS = [
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "occ %"),
     ("launch__registers_per_thread", "regs"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem confl"),
+    ("smsp__inst_executed_op_global_red.sum", "red inst"),
+    ("lts__t_sectors_op_red.sum", "L2 red sect"),
+    ("lts__t_sectors_op_atom.sum", "L2 atom sect"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum", "smem atom wavefr"),
 ]
+# extra counters to request with --set full (scripts/gpurun_prof.sh)
+EXTRA_METRICS = ",".join(["smsp__inst_executed_op_global_red.sum", "lts__t_sectors_op_red.sum",
+                          "lts__t_sectors_op_atom.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum",
+                          "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"])
 
 
 def load(rep):
@@ -62,9 +71,11 @@ def main():
         short = re.sub(r"\(.*", "", name).replace("unnamed>::", "").replace("void ", "")
         cells = []
         for k, _ in KEYS:
-            if k in col:
-                u = units[col[k]]
-                cells.append(f"{r[col[k]]} {u}".strip())
+            ks = k if isinstance(k, tuple) else (k,)
+            hit = next((kk for kk in ks if kk in col), None)
+            if hit is not None:
+                u = units[col[hit]]
+                cells.append(f"{r[col[hit]]} {u}".strip())
             else:
                 cells.append("-")
         lines.append(f"| {short} | " + " | ".join(cells) + f" | {stalls(hdr, r)} |")

@@ -110,6 +110,69 @@ def test_stn_singular_theta_falls_back(cuda_device):
     assert_close(_np(dth), rdth, "grad", "dtheta")
 
 
+@pytest.mark.parametrize("padding", ["zeros", "border"])
+def test_stn_deterministic_every_sample(cuda_device, padding):
+    """deterministic=1 is bitwise reproducible for EVERY sample: regular samples take the
+    cell-owner gather, fallback samples (singular theta, huge preimage) and border padding
+    the fixed-point integer scatter (det.cuh) instead of fp32 atomics; all within T."""
+    inp = synth.stn_inputs(4, 6, 40, 44, cfg=1)
+    inp["theta"][1] = torch.tensor([[0.5, 0.5, 0.1], [0.5, 0.5, -0.2]])   # det = 0
+    inp["theta"][3] = torch.tensor([[0.02, 0.0, 0.1], [0.0, 0.03, 0.0]])  # huge preimage
+    g = _cuda(inp, cuda_device)
+    runs = [rsgrad.stn_bwd(g["x"], g["theta"], g["dy"], padding=padding, deterministic=True) for _ in range(3)]
+    for r in runs[1:]:
+        assert torch.equal(r[0], runs[0][0]) and torch.equal(r[1], runs[0][1])
+    rdx, rdth = oracle.stn_bwd(*(inp[k].double().numpy() for k in ("x", "theta", "dy")), True, padding == "border")
+    assert_close(_np(runs[0][0]), rdx, "grad", "dx")
+    assert_close(_np(runs[0][1]), rdth, "grad", "dtheta")
+    # without dtheta (the fallback list still drives the scatter)
+    dx, _ = rsgrad.stn_bwd(g["x"], g["theta"], g["dy"], padding=padding, deterministic=True, need_dtheta=False)
+    assert torch.equal(dx, runs[0][0])
+
+
+@pytest.mark.parametrize("flow", ["smooth", "stress", "collapse"])
+@pytest.mark.parametrize("padding", ["zeros", "border"])
+def test_warp_deterministic(cuda_device, flow, padding):
+    """warp_bwd deterministic=1: d_input by the fixed-point scatter (bitwise reproducible,
+    |error| <= fan-in * 2^-(S+1), so also the collapsing flow is well inside T), d_flow by
+    the strip kernel's gather (no atomics)."""
+    N, C, H, W = 2, 3, 70, 100
+    inp = synth.warp_inputs(N, C, H, W, cfg=1, flow="stress" if flow == "collapse" else flow)
+    if flow == "collapse":
+        inp["flow"] = _collapse_flow(N, H, W)
+    g = _cuda(inp, cuda_device)
+    a = rsgrad.warp_bwd(g["x"], g["flow"], g["dy"], padding=padding, deterministic=True)
+    b = rsgrad.warp_bwd(g["x"], g["flow"], g["dy"], padding=padding, deterministic=True)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+    rdx, rdf = oracle.warp_bwd(*(inp[k].double().numpy() for k in ("x", "flow", "dy")), padding == "border")
+    rep = assert_close(_np(a[0]), rdx, "grad", "dx")
+    # fixed point: the accumulation adds ~1e-11; what remains is the fp32 tap weights
+    # (~1e-7 relative per term), as in every other path -- far inside T even for the
+    # collapsing flow's ~1300 terms per element
+    assert rep["max_ratio"] < 0.25, rep
+    assert_close(_np(a[1]), rdf, "grad", "dflow")
+    dx_only, none = rsgrad.warp_bwd(g["x"], g["flow"], g["dy"], padding=padding, deterministic=True,
+                                    need_dflow=False)
+    assert none is None and torch.equal(dx_only, a[0])
+
+
+def test_warp_deterministic_nonfinite_and_zero(cuda_device):
+    """Fixed-point edge cases: an all-zero dY (scale exponent 0) gives exactly 0; a
+    non-finite dY makes that sample's dX NaN (the fp32 path would propagate it too)
+    and leaves the other sample exact."""
+    inp = synth.warp_inputs(2, 2, 20, 33, cfg=1)
+    inp["dy"][0].zero_()
+    g = _cuda(inp, cuda_device)
+    dx, _ = rsgrad.warp_bwd(g["x"], g["flow"], g["dy"], deterministic=True)
+    assert torch.count_nonzero(dx[0]) == 0
+    rdx, _ = oracle.warp_bwd(*(inp[k].double().numpy() for k in ("x", "flow", "dy")))
+    assert_close(_np(dx[1]), rdx[1], "grad", "dx sample 1")
+    bad = g["dy"].clone()
+    bad[0, 0, 3, 4] = float("inf")
+    dxb, _ = rsgrad.warp_bwd(g["x"], g["flow"], bad, deterministic=True)
+    assert torch.isnan(dxb[0]).all() and torch.equal(dxb[1], dx[1])
+
+
 def test_stn_identity_and_quarter_pixel(cuda_device):
     N, C, H, W = 2, 3, 32, 48
     inp = synth.stn_inputs(N, C, H, W, cfg=1, theta_kind="identity")
@@ -765,7 +828,8 @@ def test_stn_bicubic_gather_deterministic_and_fallback(cuda_device):
     xs, ts, ds = (t.to(cuda_device) for t in (x, th, dy))
     a = rsgrad.stn_bicubic_bwd(xs, ts, ds, deterministic=True)
     b = rsgrad.stn_bicubic_bwd(xs, ts, ds, deterministic=True)
-    assert torch.equal(a[0][0], b[0][0]) and torch.equal(a[1], b[1])
+    # every sample, the fallback ones included (fixed-point scatter, det.cuh)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
     rdx, rdth = oracle.stn_bicubic_bwd(x.double().numpy(), th.double().numpy(), dy.double().numpy())
     assert_close(_np(a[0]), rdx, "grad", "dx")
     assert_close(_np(a[1]), rdth, "grad", "dtheta")
