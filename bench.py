@@ -119,16 +119,39 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- distributed
+def spawn_ranks(args):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-exec this command under
+    torch.distributed.run with N ranks on this node (127.0.0.1 rendezvous), exactly
+    as the driver launches it.  Returns only when no re-exec is needed."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    elif torch.cuda.is_available():
+        if args.dry_run:  # CPU plumbing test: gloo, no device
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available() and not args.dry_run:
         torch.cuda.set_device(0)
     return world, rank, local
 
@@ -473,6 +496,72 @@ def run_reference(args, world, rank):
 
 
 # --------------------------------------------------------------------------- main
+class DeviceClock:
+    """Per-step device timing on the launching stream (CUDA events)."""
+
+    def __init__(self, steps, ncalls, stream):
+        self.stream = stream
+        self.ev = [[torch.cuda.Event(enable_timing=True) for _ in range(ncalls + 1)] for _ in range(steps)]
+
+    def mark(self, k, i):
+        self.ev[k][i].record(self.stream)
+
+    def finish(self):
+        torch.cuda.synchronize()
+
+    def seconds(self, k, i, j):
+        return self.ev[k][i].elapsed_time(self.ev[k][j]) * 1e-3
+
+
+class HostClock:
+    """--dry-run (CPU plumbing only): wall-clock marks."""
+
+    def __init__(self, steps, ncalls, stream=None):
+        self.t = [[0.0] * (ncalls + 1) for _ in range(steps)]
+
+    def mark(self, k, i):
+        self.t[k][i] = time.perf_counter()
+
+    def finish(self):
+        pass
+
+    def seconds(self, k, i, j):
+        return self.t[k][j] - self.t[k][i]
+
+
+def dry_calls(nb):
+    """--dry-run stand-in for the six calls: a little CPU work per call, no product code."""
+    a = torch.ones(nb, 256, 256)
+    return [(n, (lambda: a.mul_(1.0))) for n in
+            ("stn_fwd", "stn_bwd", "warp_fwd", "warp_bwd", "bslice_fwd", "bslice_bwd")]
+
+
+def timed_steps(calls, steps, world, clock):
+    """K timed steps.  Every step: events around each of the six calls on the launching
+    stream; between steps a barrier (outside the events).  Per step and per call the
+    MAX over ranks, then the median over steps; also the max-over-ranks
+    total of the K steps (the bracketed-region number)."""
+    barrier(world)
+    for k in range(steps):
+        clock.mark(k, 0)
+        for ci, (_, fn) in enumerate(calls):
+            fn()
+            clock.mark(k, ci + 1)
+        if world > 1:
+            clock.finish()
+            barrier(world)
+    clock.finish()
+    nc = len(calls)
+    per = [[clock.seconds(k, ci, ci + 1) for ci in range(nc)] for k in range(steps)]
+    tot = [clock.seconds(k, 0, nc) for k in range(steps)]
+    flat = max_over_ranks(world, tot + [v for row in per for v in row])
+    tot_max, per_max = flat[:steps], flat[steps:]
+    per_max = [per_max[k * nc:(k + 1) * nc] for k in range(steps)]
+    step_med = statistics.median(tot_max)
+    call_med = [statistics.median(per_max[k][ci] for k in range(steps)) for ci in range(nc)]
+    return step_med, call_med, sum(tot_max)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -483,60 +572,52 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-next", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU plumbing test of the rank loop (gloo, stand-in calls, no product code)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    spawn_ranks(args)
     world, rank, local = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, world, rank)
         return
-
-    from paper_1904_12228_b200 import rsgrad as rs
-
-    dev = torch.device("cuda", local if world > 1 else 0)
     n0, nb = shard(world, rank)
-    s, w, b = make_inputs(n0, nb, dev)
-    o = alloc_outputs(s, w, b)
-    calls = step_calls(rs, s, w, b, o)
-    stream = torch.cuda.current_stream()
+    if args.dry_run:
+        calls, clock_t, rs = dry_calls(nb), HostClock, None
+        stream = None
+    else:
+        from paper_1904_12228_b200 import rsgrad as rs
+
+        dev = torch.device("cuda", local if world > 1 else 0)
+        s, w, b = make_inputs(n0, nb, dev)
+        o = alloc_outputs(s, w, b)
+        calls = step_calls(rs, s, w, b, o)
+        stream = torch.cuda.current_stream()
+        clock_t = DeviceClock
     for _ in range(args.warmup):
         for _, fn in calls:
             fn()
-    torch.cuda.synchronize()
+    if not args.dry_run:
+        torch.cuda.synchronize()
 
-    # ---- timed region: K steps, events between the six calls on the launching stream
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(calls) + 1)] for _ in range(args.steps)]
-    clocks = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
+    # ---- timed region
+    clock = clock_t(args.steps, len(calls), stream)
+    clocks = ClockSampler(torch.cuda.current_device()) if (rank == 0 and not args.dry_run) else None
     if clocks:
         clocks.start()
         time.sleep(0.3)
-    barrier(world)
-    torch.cuda.synchronize()
-    rs.launch_count(reset=True)
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    t_start.record(stream)
-    for k in range(args.steps):
-        ev[k][0].record(stream)
-        for ci, (_, fn) in enumerate(calls):
-            fn()
-            ev[k][ci + 1].record(stream)
-    t_end.record(stream)
-    torch.cuda.synchronize()
-    launches = rs.launch_count()
+    if rs is not None:
+        rs.launch_count(reset=True)
+    t_step, per_call, total_s = timed_steps(calls, args.steps, world, clock)
+    launches = rs.launch_count() if rs is not None else 0
     barrier(world)
     clk = clocks.stop() if clocks else None
-    total_s = t_start.elapsed_time(t_end) * 1e-3
-    per_call = [sum(ev[k][ci].elapsed_time(ev[k][ci + 1]) for k in range(args.steps)) * 1e-3 / args.steps
-                for ci in range(len(calls))]
-    mx = max_over_ranks(world, [total_s] + per_call)
-    total_s, per_call = mx[0], mx[1:]
-    t_step = total_s / args.steps
     P_global = BATCH * H * W
     value = P_global / t_step / 1e6
 
     # ---- e2e: the same step through the C ABI with pinned host buffers
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not args.dry_run:
         e2e = run_e2e(rs, s, w, b, args, world)
 
     if rank != 0:
@@ -567,14 +648,21 @@ def main():
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (synth/: seeded per-sample recipe, generated on device)",
         "config": config_dict(world),
+        "timing": {"ms_per_step": "median over the K steps of the per-step max over ranks (CUDA events on the "
+                                  "launching stream; a barrier between steps, outside the events)",
+                   "total_ms_k_steps_max_over_ranks": round(total_s * 1e3, 4)},
         "layers": layers, "roofline": roof, "gpu_launches": launches,
         "clocks": clk, "e2e": e2e,
     }
-    if world == 1 and not args.no_cpu:
+    if args.dry_run:
+        line["dry_run"] = True
+        line["data"] = "none (--dry-run: CPU stand-in calls, plumbing only)"
+        line["per_rank_shards"] = [list(shard(world, r)) for r in range(world)]
+    if world == 1 and not args.no_cpu and not args.dry_run:
         line["cpu_baseline"] = cpu_baseline(s, w, b)
-    if world == 1 and not args.no_paper_shapes:
+    if world == 1 and not args.no_paper_shapes and not args.dry_run:
         line["paper_shapes"] = paper_shapes(rs, peak)
-    if world == 1 and not args.no_next:
+    if world == 1 and not args.no_next and not args.dry_run:
         line["next_rows"] = next_rows(rs, peak)
     print(json.dumps(line), flush=True)
 
@@ -617,6 +705,10 @@ def run_e2e(rs, s, w, b, args, world):
            + sum(hb[k].numel() for k in ("grid", "guide", "x"))
            + sum(hb[k].numel() for k in ("grid", "guide", "x", "dy"))) * 4
     d2h = sum(v.numel() for k, v in ho.items() if not k.startswith("_")) * 4
+    # a caller-owned staging buffer (3 streams x the largest chunk's host tensors +
+    # workspace: the library carves its per-chunk buffers from it, no per-call allocation)
+    stage = torch.empty(int(1.5 * 2**30), dtype=torch.uint8, device=s["x"].device)
+    rs.set_host_staging(stage)
     for _, fn in calls:  # warm-up
         fn()
     torch.cuda.synchronize()
@@ -633,6 +725,8 @@ def run_e2e(rs, s, w, b, args, world):
     e1.record()
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) / steps
+    rs.set_host_staging(None)
+    del stage
     dt = max(e0.elapsed_time(e1) * 1e-3 / steps, 1e-9)
     dt = max_over_ranks(world, [max(dt, wall)])[0]
     v = world * nb * H * W / dt / 1e6
@@ -640,7 +734,7 @@ def run_e2e(rs, s, w, b, args, world):
             "samples_per_rank": nb, "steps": steps,
             "note": "pinned host buffers passed as host pointers to the C ABI: the library stages "
                     "them in up to 32 sample chunks on three internal streams (H2D / kernels / D2H overlap; "
-                    "temporaries from a private stream-ordered pool kept reserved); "
+                    "staging carved from a caller-owned 1.5 GB device buffer, rsgrad_set_host_staging); "
                     "one stream sync per step; wall clock, max over ranks"}
 
 

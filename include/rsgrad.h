@@ -28,22 +28,39 @@
  *             memory: fully asynchronous; pageable: copies may block the caller).
  *   Outputs   always OVERWRITTEN, never accumulated.  A NULL gradient pointer
  *             skips that gradient's work.
- *   Ownership the caller owns every buffer.  The library keeps no state except
- *             the thread-local error string and one private stream-ordered memory
- *             pool per device: its temporaries (workspace, host staging) are freed in
- *             stream order but the pool keeps the memory reserved for later calls
- *             (the caller's default pool is untouched).
- *   Workspace *_bwd take an optional device workspace (size from
- *             rsgrad_bwd_workspace_bytes); NULL/too small => the library takes
- *             a stream-ordered temporary of that size itself.
+ *   Ownership the caller owns every buffer; the library allocates nothing that
+ *             outlives a call.  Its only state: the thread-local error string and,
+ *             per (thread, device), the internal streams/events of the host-pointer
+ *             path (created on first use, reused, released with the CUDA context).
+ *   Workspace *_bwd take an optional device workspace of
+ *             rsgrad_bwd_workspace_bytes(...) bytes (same opts: deterministic=1
+ *             adds the fixed-point accumulators).  NULL / ws_bytes too small (e.g.
+ *             0) => the library takes a stream-ordered temporary of that size from
+ *             the stream's device's DEFAULT memory pool (cudaMallocAsync) and frees it
+ *             in stream order (cudaFreeAsync): nothing is reserved by the library
+ *             after the call; caching is the pool's (the caller's) release policy.
+ *             (Reading of SURVEY 8(b) "ws_bytes=0 => workspace-free algorithm":
+ *             every backward here needs scratch for its fixed-order partial sums,
+ *             which is what makes it deterministic, so the free-standing variant is
+ *             a stream-ordered temporary rather than a different algorithm;
+ *             DESIGN.md "Boundary".)
+ *   Devices   every entry point runs on the device of `stream` (made current for
+ *             the call, the previous device restored); NULL stream = the current
+ *             device.  All pointers must belong to that device (or be host memory).
  *   Errors    no exceptions cross the ABI: a negative rs_status is returned and
  *             rsgrad_last_error() describes it.  Status reflects argument
  *             validation and launch errors (cudaGetLastError) only; kernel
  *             faults surface on the next synchronisation of `stream`.
  *   Threads   re-entrant; concurrent calls on different streams are safe.
- *   Determinism: with deterministic=1 every result is bitwise reproducible
- *             (AUTO then never picks an atomic-scatter path); gather paths are
- *             always deterministic.
+ *   Determinism: with deterministic=1 every result is bitwise reproducible, for
+ *             every sample: gathers and fixed-order partial sums as always, and where
+ *             a scatter cannot be converted (STN samples with a singular map or a huge
+ *             preimage, STN border padding, warp d_input, bicubic fallback samples)
+ *             the fixed-point integer scatter: each term w*g rounded once to a 64-bit
+ *             integer at a per-sample scale 2^S (S from max|dy|), summed with integer
+ *             atomics (order-free), converted once (absolute error <= n 2^-(S+1) for
+ *             n terms, n*max|dy|*P*2^-62).  SCATTER_ATOMIC / SCATTER_PRIV with
+ *             deterministic=1 => RS_ERR_FLAG; stn3d / lanczos (atomics only) likewise.
  */
 #ifndef RSGRAD_H
 #define RSGRAD_H
@@ -73,16 +90,21 @@ typedef enum { RS_PAD_ZEROS = 0, RS_PAD_BORDER = 1 } rs_padding;
  * to gathers where a bounded inverse exists, else "a general scattering operation"
  * with atomics).  What each layer accepts:
  *   stn_bwd  d_input  AUTO, GATHER: cell-owner gather over the affine preimage
- *                     (zeros padding; per-sample fallback to atomics for singular
- *                     theta); SCATTER_ATOMIC: per-tap global atomics;
+ *                     (zeros padding; per-sample fallback to atomics -- or, with
+ *                     deterministic=1, the fixed-point scatter -- for singular
+ *                     theta / huge preimages); SCATTER_ATOMIC: per-tap global atomics;
  *                     SCATTER_PRIV: per output tile, taps accumulate in a shared-
  *                     memory copy of the tile's input footprint, flushed with one
  *                     global atomic per touched element.  Border padding never
  *                     gathers (no bounded inverse).
- *   warp_bwd d_input  AUTO and SCATTER_ATOMIC: per-tap global atomics (adjacent
- *                     lanes' shared taps merged first); SCATTER_PRIV as for STN;
- *                     GATHER -> RS_ERR_FLAG (no bounded inverse).
- *                     AUTO picks the measured-faster path.
+ *   warp_bwd d_input  AUTO: row strips -- each lane walks rows of one column and keeps
+ *                     its current cell's 4 tap sums in registers (carried down a
+ *                     row, merged with the neighbour lane's shared taps and across
+ *                     runs of lanes on one cell) before fp32 global atomics;
+ *                     deterministic=1: the fixed-point scatter;
+ *                     SCATTER_ATOMIC: one fp32 atomic per tap (the unconverted
+ *                     scatter); SCATTER_PRIV as for STN; GATHER -> RS_ERR_FLAG (an
+ *                     arbitrary flow has no bounded inverse).
  *   bslice_bwd d_grid AUTO, GATHER, SCATTER_PRIV: dual-cell register-privatised
  *                     accumulation + fixed-order partial gather (deterministic;
  *                     cells >= 8 px); SCATTER_ATOMIC: global atomics.
@@ -119,7 +141,8 @@ rs_status stn_fwd(const float *x, const float *theta, int N, int C, int H, int W
 /*   dy      N x C x Ho x Wo     adjoint of y
  *   dx      N x C x H x W       adjoint of x (nullable)
  *   dtheta  N x 2 x 3           adjoint of theta (nullable)
- * GATHER is invalid with border padding (the clamp has no bounded inverse). */
+ * GATHER is invalid with border padding (the clamp has no bounded inverse);
+ * border padding with deterministic=1 takes the fixed-point scatter for d_input. */
 rs_status stn_bwd(const float *x, const float *theta, const float *dy, int N, int C, int H,
                   int W, int Ho, int Wo, const rs_opts *opts, float *dx, float *dtheta,
                   void *workspace, size_t ws_bytes, rs_stream_t stream);
@@ -214,7 +237,8 @@ rs_status upsample4_bwd(const float *dy, int N, int C, int H, int W, float *dx, 
  *   stn_bicubic_bwd  GATHER or deterministic=1: the converted gather -- each input pixel
  *                    enumerates the affine preimage of (x-2, x+2) x (y-2, y+2) with exact
  *                    fp64 membership (a singular map or a window > 1024 output pixels
- *                    falls back to reds for that sample); AUTO / SCATTER_ATOMIC: memset +
+ *                    falls back to reds for that sample, to the fixed-point scatter
+ *                    with deterministic=1); AUTO / SCATTER_ATOMIC: memset +
  *                    red.global.add per tap in the d_theta pass (measured faster).
  *   stn3d_bwd        the atomic scatter only (GATHER / deterministic=1 => RS_ERR_FLAG).
  * SCATTER_PRIV => RS_ERR_FLAG.
@@ -250,7 +274,8 @@ rs_status stn3d_bwd(const float *x, const float *theta, const float *dy, int N, 
  * RS_SCHED_ROOT residual), 5 = stn_bicubic (N, Ho, Wo: d_theta partials, coordinate
  * tables, N fallback flags), 6 = stn3d (N, Ho, Wo, D = Do), 7 = stn_lanczos (N, Ho, Wo);
  * unused arguments are ignored.
- * Returns 0 for an unknown layer.  DESIGN.md "Workspace". */
+ * opts->deterministic = 1 adds the fixed-point accumulators of one sample
+ * (8 * C * H * W bytes) for layers 0, 1 and 5.  Returns 0 for an unknown layer. */
 size_t rsgrad_bwd_workspace_bytes(int layer, int N, int C, int H, int W, int Ho, int Wo, int D,
                                   int Gh, int Gw, const rs_opts *opts);
 
@@ -259,6 +284,15 @@ const char *rsgrad_last_error(void);
 
 /* Library version string, e.g. "rsgrad 0.1.0 sm_100a". */
 const char *rsgrad_version(void);
+
+/* Caller-owned device staging buffer for the host-pointer path on the calling thread
+ * and the current device: when it holds 3 streams x (the host tensors of one sample
+ * chunk + that chunk's workspace), calls carve their staging from it instead of taking
+ * stream-ordered temporaries per call.  Calls that use it are serialised on an event
+ * (each waits until the previous user is done).  buf = NULL unregisters (waiting until
+ * the last user is done).  The caller keeps ownership and must not free `buf` while
+ * registered.  RS_ERR_FLAG if buf is not device memory. */
+rs_status rsgrad_set_host_staging(void *buf, size_t bytes);
 
 /* Number of kernels the library enqueued on this thread since the last reset
  * (launch accounting for bench.py's gpu_launches). */

@@ -64,36 +64,61 @@ rs_status check_opts(const rs_opts &o) {
 
 constexpr int kMaxHostStreams = 4;
 
-// Library temporaries (workspace, host-path staging) come from a private stream-ordered
-// pool per device whose memory is kept reserved between calls (release threshold = max):
-// re-mapping freed memory on every call made the host-buffer path's timing erratic.  The
-// caller's default pool is left untouched.
-cudaError_t lib_malloc(void **p, size_t bytes, cudaStream_t s) {
-    static cudaMemPool_t pools[64] = {};
-    static std::mutex mu;
+// Library temporaries (a workspace the caller did not provide, host-path staging) are
+// stream-ordered allocations from the device's default memory pool (cudaMallocAsync /
+// cudaFreeAsync on the call's stream): nothing is reserved by the library between
+// calls -- what the pool keeps cached is the pool's (i.e. the caller's) release
+// policy (SURVEY 8(b) "the library never allocates persistently").
+cudaError_t lib_malloc(void **p, size_t bytes, cudaStream_t s) { return cudaMallocAsync(p, bytes, s); }
+
+// Make the device of the caller's stream current for the duration of one entry point:
+// launches, stream-ordered allocations and cudaFuncSetAttribute act on the current
+// device, so a stream of another GPU would otherwise fail (or allocate on the wrong
+// device).  The legacy default stream (NULL) means the current device.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(cudaStream_t s) {
+        if (!s) return;
+        int d = 0, cur = 0;
+        if (cudaStreamGetDevice(s, &d) != cudaSuccess) {
+            cudaGetLastError();
+            return;
+        }
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != d && cudaSetDevice(d) == cudaSuccess) prev = cur;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// Internal streams / events of the host-pointer path, created once per (thread,
+// device) and reused by every later call on that thread (re-entrant: no sharing
+// between threads).  Released with the CUDA context.
+struct HostStreams {
+    bool made = false;
+    cudaStream_t st[4];
+    cudaEvent_t ev0, evs[4];
+    // caller-owned device staging buffer (rsgrad_set_host_staging), or none
+    char *stage = nullptr;
+    size_t stage_bytes = 0;
+    cudaEvent_t stage_free;  // recorded when the last call using `stage` is done with it
+    bool stage_used = false;
+};
+HostStreams &host_streams() {
+    static thread_local HostStreams hs[64];
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev < 0 || dev >= 64) return cudaMallocAsync(p, bytes, s);
-    cudaMemPool_t pool;
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        if (!pools[dev]) {
-            cudaMemPoolProps props = {};
-            props.allocType = cudaMemAllocationTypePinned;
-            props.location.type = cudaMemLocationTypeDevice;
-            props.location.id = dev;
-            cudaMemPool_t np;
-            if (cudaMemPoolCreate(&np, &props) != cudaSuccess) {
-                cudaGetLastError();
-                return cudaMallocAsync(p, bytes, s);
-            }
-            unsigned long long thr = ~0ull;
-            cudaMemPoolSetAttribute(np, cudaMemPoolAttrReleaseThreshold, &thr);
-            pools[dev] = np;
+    HostStreams &h = hs[dev >= 0 && dev < 64 ? dev : 0];
+    if (!h.made) {
+        for (int k = 0; k < 4; k++) {
+            cudaStreamCreateWithFlags(&h.st[k], cudaStreamNonBlocking);
+            cudaEventCreateWithFlags(&h.evs[k], cudaEventDisableTiming);
         }
-        pool = pools[dev];
+        cudaEventCreateWithFlags(&h.ev0, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&h.stage_free, cudaEventDisableTiming);
+        h.made = true;
     }
-    return cudaMallocFromPoolAsync(p, bytes, pool, s);
+    return h;
 }
 
 // integer tuning knob from the environment (A/B measurements), clamped to [1, hi]
@@ -162,21 +187,38 @@ rs_status run_batched(int N, std::vector<TArg> &args, cudaStream_t s, void *work
     const int maxchunk = env_int("RSGRAD_HOST_CHUNKS", 32), NS = env_int("RSGRAD_HOST_STREAMS", 3);
     const int nchunk = N < maxchunk ? N : maxchunk;
     const int cs = (N + nchunk - 1) / nchunk;
-    cudaStream_t st[kMaxHostStreams];
-    cudaEvent_t ev0, evs[kMaxHostStreams];
-    for (int k = 0; k < NS; k++) cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking);
-    cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
-    cudaEventRecord(ev0, s);
+    HostStreams &hs = host_streams();
+    cudaStream_t *st = hs.st;
+    cudaEventRecord(hs.ev0, s);
     std::vector<void *> buf[kMaxHostStreams];
     void *wsk[kMaxHostStreams] = {};
     cudaError_t err = cudaSuccess;
+    // staging: carve from the caller's registered buffer when it is large enough (no
+    // per-call allocation), else stream-ordered temporaries
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    size_t per_stream = al(ws_need(cs));
+    for (int i = 0; i < na; i++)
+        if (host[i]) per_stream += al(args[i].per_sample * cs);
+    const bool use_stage = hs.stage && per_stream * NS <= hs.stage_bytes;
     for (int k = 0; k < NS; k++) {
-        cudaStreamWaitEvent(st[k], ev0, 0);
+        cudaStreamWaitEvent(st[k], hs.ev0, 0);
+        if (use_stage && hs.stage_used) cudaStreamWaitEvent(st[k], hs.stage_free, 0);
         buf[k].assign(na, nullptr);
+        char *cur = use_stage ? hs.stage + per_stream * k : nullptr;
         for (int i = 0; i < na; i++)
-            if (host[i] && err == cudaSuccess) err = lib_malloc(&buf[k][i], args[i].per_sample * cs, st[k]);
+            if (host[i] && err == cudaSuccess) {
+                if (use_stage) {
+                    buf[k][i] = cur;
+                    cur += al(args[i].per_sample * cs);
+                } else {
+                    err = lib_malloc(&buf[k][i], args[i].per_sample * cs, st[k]);
+                }
+            }
         const size_t need = ws_need(cs);
-        if (need && err == cudaSuccess) err = lib_malloc(&wsk[k], need, st[k]);
+        if (need && err == cudaSuccess) {
+            if (use_stage) wsk[k] = cur;
+            else err = lib_malloc(&wsk[k], need, st[k]);
+        }
     }
     for (int c = 0, n0 = 0; n0 < N && err == cudaSuccess; c++, n0 += cs) {
         const int nc = N - n0 < cs ? N - n0 : cs, k = c % NS;
@@ -199,16 +241,18 @@ rs_status run_batched(int N, std::vector<TArg> &args, cudaStream_t s, void *work
                                       args[i].per_sample * (size_t)nc, cudaMemcpyDeviceToHost, st[k]);
     }
     for (int k = 0; k < NS; k++) {
-        for (int i = 0; i < na; i++)
-            if (buf[k][i]) cudaFreeAsync(buf[k][i], st[k]);
-        if (wsk[k]) cudaFreeAsync(wsk[k], st[k]);
-        cudaEventCreateWithFlags(&evs[k], cudaEventDisableTiming);
-        cudaEventRecord(evs[k], st[k]);
-        cudaStreamWaitEvent(s, evs[k], 0);
-        cudaEventDestroy(evs[k]);
-        cudaStreamDestroy(st[k]);  // released once its queued work completes
+        if (!use_stage) {
+            for (int i = 0; i < na; i++)
+                if (buf[k][i]) cudaFreeAsync(buf[k][i], st[k]);
+            if (wsk[k]) cudaFreeAsync(wsk[k], st[k]);
+        }
+        cudaEventRecord(hs.evs[k], st[k]);
+        cudaStreamWaitEvent(s, hs.evs[k], 0);
     }
-    cudaEventDestroy(ev0);
+    if (use_stage) {  // the next call that uses the staging buffer waits for this one
+        cudaEventRecord(hs.stage_free, s);
+        hs.stage_used = true;
+    }
     if (err != cudaSuccess) return fail(RS_ERR_CUDA, "host-staged path: %s", cudaGetErrorString(err));
     return ok();
 }
@@ -227,6 +271,16 @@ extern "C" {
 const char *rsgrad_last_error(void) { return rs::g_err; }
 
 const char *rsgrad_version(void) { return "rsgrad 0.1.0 sm_100a"; }
+
+rs_status rsgrad_set_host_staging(void *buf, size_t bytes) {
+    if (buf && !is_device_ptr(buf)) return fail(RS_ERR_FLAG, "rsgrad_set_host_staging: not device memory");
+    HostStreams &h = host_streams();
+    if (h.stage && h.stage_used) cudaEventSynchronize(h.stage_free);  // the old buffer is released idle
+    h.stage = (char *)buf;
+    h.stage_bytes = buf ? bytes : 0;
+    h.stage_used = false;
+    return ok();
+}
 
 unsigned long long rsgrad_launch_count(int reset) {
     unsigned long long v = rs::g_launches;
@@ -284,6 +338,7 @@ static rs_status stn_validate(const float *x, const float *theta, int N, int C, 
 
 rs_status stn_fwd(const float *x, const float *theta, int N, int C, int H, int W, int Ho, int Wo,
                   const rs_opts *opts, float *y, rs_stream_t stream) {
+    DeviceGuard dg_((cudaStream_t)stream);
     const rs_opts o = resolve(opts);
     rs_status st = stn_validate(x, theta, N, C, H, W, Ho, Wo, o);
     if (st != RS_OK) return st;
@@ -308,6 +363,7 @@ rs_status stn_fwd(const float *x, const float *theta, int N, int C, int H, int W
 rs_status stn_bwd(const float *x, const float *theta, const float *dy, int N, int C, int H, int W,
                   int Ho, int Wo, const rs_opts *opts, float *dx, float *dtheta, void *workspace,
                   size_t ws_bytes, rs_stream_t stream) {
+    DeviceGuard dg_((cudaStream_t)stream);
     const rs_opts o = resolve(opts);
     rs_status st = stn_validate(x, theta, N, C, H, W, Ho, Wo, o);
     if (st != RS_OK) return st;
@@ -355,6 +411,7 @@ static rs_status warp_validate(const float *x, const float *flow, int N, int C, 
 
 rs_status warp_fwd(const float *x, const float *flow, int N, int C, int H, int W,
                    const rs_opts *opts, float *y, rs_stream_t stream) {
+    DeviceGuard dg_((cudaStream_t)stream);
     const rs_opts o = resolve(opts);
     rs_status st = warp_validate(x, flow, N, C, H, W, o);
     if (st != RS_OK) return st;
@@ -378,6 +435,7 @@ rs_status warp_fwd(const float *x, const float *flow, int N, int C, int H, int W
 rs_status warp_bwd(const float *x, const float *flow, const float *dy, int N, int C, int H, int W,
                    const rs_opts *opts, float *dx, float *dflow, void *workspace, size_t ws_bytes,
                    rs_stream_t stream) {
+    DeviceGuard dg_((cudaStream_t)stream);
     const rs_opts o = resolve(opts);
     rs_status st = warp_validate(x, flow, N, C, H, W, o);
     if (st != RS_OK) return st;
@@ -424,6 +482,7 @@ static rs_status bslice_validate(const float *grid, const float *guide, const fl
 
 rs_status bslice_fwd(const float *grid, const float *guide, const float *x, int N, int H, int W,
                      int D, int Gh, int Gw, const rs_opts *opts, float *y, rs_stream_t stream) {
+    DeviceGuard dg_((cudaStream_t)stream);
     const rs_opts o = resolve(opts);
     rs_status st = bslice_validate(grid, guide, x, N, H, W, D, Gh, Gw, o);
     if (st != RS_OK) return st;
@@ -449,6 +508,7 @@ rs_status bslice_bwd(const float *grid, const float *guide, const float *x, cons
                      int H, int W, int D, int Gh, int Gw, const rs_opts *opts, float *dgrid,
                      float *dguide, float *dx, void *workspace, size_t ws_bytes,
                      rs_stream_t stream) {
+    DeviceGuard dg_((cudaStream_t)stream);
     const rs_opts o = resolve(opts);
     rs_status st = bslice_validate(grid, guide, x, N, H, W, D, Gh, Gw, o);
     if (st != RS_OK) return st;
@@ -502,6 +562,7 @@ static rs_status conv_validate(const float *x, const float *k, int N, int Ci, in
 
 rs_status conv_fwd(const float *x, const float *k, int N, int Ci, int Co, int H, int W, int kh, int kw,
                    const rs_opts *opts, float *y, rs_stream_t stream) {
+    DeviceGuard dg_((cudaStream_t)stream);
     const rs_opts o = resolve(opts);
     rs_status st = conv_validate(x, k, N, Ci, Co, H, W, kh, kw, o);
     if (st != RS_OK) return st;
@@ -516,6 +577,7 @@ rs_status conv_fwd(const float *x, const float *k, int N, int Ci, int Co, int H,
 rs_status conv_bwd(const float *x, const float *k, const float *dy, int N, int Ci, int Co, int H, int W,
                    int kh, int kw, const rs_opts *opts, float *dx, float *dk, void *workspace, size_t ws_bytes,
                    rs_stream_t stream) {
+    DeviceGuard dg_((cudaStream_t)stream);
     const rs_opts o = resolve(opts);
     rs_status st = conv_validate(x, k, N, Ci, Co, H, W, kh, kw, o);
     if (st != RS_OK) return st;
@@ -549,6 +611,7 @@ rs_status conv_bwd(const float *x, const float *k, const float *dy, int N, int C
 rs_status convloss_grad(const float *in, const float *k, const float *target, int N, int H, int W, int kh,
                         int kw, rs_schedule schedule, float *d_in, void *workspace, size_t ws_bytes,
                         rs_stream_t stream) {
+    DeviceGuard dg_((cudaStream_t)stream);
     if (!in || !k || !target || !d_in) return fail(RS_ERR_NULL, "convloss_grad: in, k, target, d_in are required");
     if (!pos(N) || !pos(H) || !pos(W) || !pos(kh) || !pos(kw) || kh > 7 || kw > 7)
         return fail(RS_ERR_SHAPE, "convloss_grad: positive dims, 1 <= kh, kw <= 7 (N=%d H=%d W=%d kh=%d kw=%d)", N,
@@ -581,12 +644,14 @@ static rs_status up4_check(const void *a, const void *b, int N, int C, int H, in
 }
 
 rs_status upsample4_fwd(const float *x, int N, int C, int H, int W, float *y, rs_stream_t stream) {
+    DeviceGuard dg_((cudaStream_t)stream);
     rs_status st = up4_check(x, y, N, C, H, W);
     if (st != RS_OK) return st;
     return launched(rs::upsample4_launch(x, y, N, C, H, W, false, (cudaStream_t)stream), "upsample4_fwd");
 }
 
 rs_status upsample4_bwd(const float *dy, int N, int C, int H, int W, float *dx, rs_stream_t stream) {
+    DeviceGuard dg_((cudaStream_t)stream);
     rs_status st = up4_check(dy, dx, N, C, H, W);
     if (st != RS_OK) return st;
     return launched(rs::upsample4_launch(dy, dx, N, C, H, W, true, (cudaStream_t)stream), "upsample4_bwd");
@@ -627,6 +692,7 @@ rs_status with_ws(size_t need, void *workspace, size_t ws_bytes, cudaStream_t s,
 
 rs_status stn_bicubic_fwd(const float *x, const float *theta, int N, int C, int H, int W, int Ho, int Wo,
                           const rs_opts *opts, float *y, rs_stream_t stream) {
+    DeviceGuard dg_((cudaStream_t)stream);
     const rs_opts o = resolve(opts);
     rs_status st = stn_validate(x, theta, N, C, H, W, Ho, Wo, o);
     if (st != RS_OK) return st;
@@ -641,6 +707,7 @@ rs_status stn_bicubic_fwd(const float *x, const float *theta, int N, int C, int 
 rs_status stn_bicubic_bwd(const float *x, const float *theta, const float *dy, int N, int C, int H, int W, int Ho,
                           int Wo, const rs_opts *opts, float *dx, float *dtheta, void *workspace, size_t ws_bytes,
                           rs_stream_t stream) {
+    DeviceGuard dg_((cudaStream_t)stream);
     const rs_opts o = resolve(opts);
     rs_status st = stn_validate(x, theta, N, C, H, W, Ho, Wo, o);
     if (st != RS_OK) return st;
@@ -673,6 +740,7 @@ static rs_status stn3d_validate(const float *x, const float *theta, int N, int C
 
 rs_status stn3d_fwd(const float *x, const float *theta, int N, int C, int D, int H, int W, int Do, int Ho, int Wo,
                     const rs_opts *opts, float *y, rs_stream_t stream) {
+    DeviceGuard dg_((cudaStream_t)stream);
     const rs_opts o = resolve(opts);
     rs_status st = stn3d_validate(x, theta, N, C, D, H, W, Do, Ho, Wo, o);
     if (st != RS_OK) return st;
@@ -686,6 +754,7 @@ rs_status stn3d_fwd(const float *x, const float *theta, int N, int C, int D, int
 rs_status stn3d_bwd(const float *x, const float *theta, const float *dy, int N, int C, int D, int H, int W, int Do,
                     int Ho, int Wo, const rs_opts *opts, float *dx, float *dtheta, void *workspace, size_t ws_bytes,
                     rs_stream_t stream) {
+    DeviceGuard dg_((cudaStream_t)stream);
     const rs_opts o = resolve(opts);
     rs_status st = stn3d_validate(x, theta, N, C, D, H, W, Do, Ho, Wo, o);
     if (st != RS_OK) return st;
@@ -703,6 +772,7 @@ rs_status stn3d_bwd(const float *x, const float *theta, const float *dy, int N, 
 
 rs_status stn_lanczos_fwd(const float *x, const float *theta, int N, int C, int H, int W, int Ho, int Wo,
                           const rs_opts *opts, float *y, rs_stream_t stream) {
+    DeviceGuard dg_((cudaStream_t)stream);
     const rs_opts o = resolve(opts);
     rs_status st = stn_validate(x, theta, N, C, H, W, Ho, Wo, o);
     if (st != RS_OK) return st;
@@ -717,6 +787,7 @@ rs_status stn_lanczos_fwd(const float *x, const float *theta, int N, int C, int 
 rs_status stn_lanczos_bwd(const float *x, const float *theta, const float *dy, int N, int C, int H, int W, int Ho,
                           int Wo, const rs_opts *opts, float *dx, float *dtheta, void *workspace, size_t ws_bytes,
                           rs_stream_t stream) {
+    DeviceGuard dg_((cudaStream_t)stream);
     const rs_opts o = resolve(opts);
     rs_status st = stn_validate(x, theta, N, C, H, W, Ho, Wo, o);
     if (st != RS_OK) return st;

@@ -718,11 +718,23 @@ size_t bwd_smem(int D) {
            sizeof(float) * kTileXS * kTileYS + 16;
 }
 
+// The tiled backward needs bwd_smem(D) bytes of dynamic shared memory (2056 D + 80740:
+// 212 KB at D = 64); it is used only where the current device's opt-in limit allows.
+bool bwd_smem_fits(int D) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) {
+        cudaGetLastError();
+        optin = 227 * 1024;  // sm_100
+    }
+    return bwd_smem(D) <= (size_t)optin;
+}
+
 }  // namespace
 
 size_t bslice_ws_bytes(int N, int H, int W, int D, int Gh, int Gw) {
     const TileGeom g = tile_geom(N, H, W, D, Gh, Gw);
-    if (!g.ok) return 0;
+    if (!g.ok || !bwd_smem_fits(D)) return 0;
     return sizeof(float) * (size_t)g.blocks * 4 * D * 12 + sizeof(int) * (size_t)(Gh + Gw + 4);
 }
 
@@ -745,16 +757,13 @@ cudaError_t bslice_bwd_launch(const BsliceArgs &a, int algo, int deterministic, 
                               size_t ws_bytes, cudaStream_t s) {
     (void)deterministic;
     const TileGeom g = tile_geom(a.N, a.H, a.W, a.D, a.Gh, a.Gw);
-    const bool tiled = g.ok && algo != 3 /*SCATTER_ATOMIC*/ && a.dgrid &&
+    const bool tiled = g.ok && bwd_smem_fits(a.D) && algo != 3 /*SCATTER_ATOMIC*/ && a.dgrid &&
                        ws_bytes >= bslice_ws_bytes(a.N, a.H, a.W, a.D, a.Gh, a.Gw);
     if (tiled) {
         const size_t sm = bwd_smem(a.D);
-        static thread_local bool attr_set = false;
-        if (!attr_set) {
-            cudaFuncSetAttribute(bslice_bwd_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 200 * 1024);
-            attr_set = true;
-        }
+        // per device and per call (the attribute belongs to the current device's context)
+        cudaError_t ea = cudaFuncSetAttribute(bslice_bwd_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (ea != cudaSuccess) return ea;
         float *partials = (float *)ws;
         int *tab = (int *)(partials + (size_t)g.blocks * 4 * a.D * 12);
         const int nt = (a.Gh > a.Gw ? a.Gh : a.Gw) + 2;

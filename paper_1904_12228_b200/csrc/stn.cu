@@ -44,6 +44,14 @@ namespace {
 
 constexpr int kThreads = 256;
 
+// RS_RACECHECK_SYNC=1 (a sanitizer build only): every mbarrier hand-off of the stage
+// rings is ALSO expressed as cp.async.wait_all + bar.sync, which compute-sanitizer's
+// racecheck models (it does not model mbarrier phases); a clean racecheck of that build
+// shows the rings have no hazard other than the ones the mbarriers order.
+#ifndef RS_RACECHECK_SYNC
+#define RS_RACECHECK_SYNC 0
+#endif
+
 // forward tiles
 constexpr int kFJ = 32;                   // output tile width (px)
 #ifndef RS_FIFWD
@@ -460,6 +468,10 @@ __global__ void __launch_bounds__(FAST ? kOTFast : kThreads, FAST ? kOTFastMinB 
                         issue(kn);
                     }
                     mbar_wait(&full[kc % kNS], (unsigned)((kc / kNS) & 1));
+                    if (RS_RACECHECK_SYNC) {
+                        cp_async_wait<0>();
+                        __syncthreads();
+                    }
                     const float *S = stage + (kc % kNS) * kFSt;
                     const bool fullc = c0 + NC <= a.C;
 #pragma unroll
@@ -492,6 +504,7 @@ __global__ void __launch_bounds__(FAST ? kOTFast : kThreads, FAST ? kOTFastMinB 
                         }
                     }
                     __syncwarp();
+                    if (RS_RACECHECK_SYNC) __syncthreads();
                     if (lane == 0) mbar_arrive(&empty[kc % kNS]);
                 }
             };
@@ -1239,6 +1252,10 @@ __global__ void __launch_bounds__(kThreads, 2)
             issue(stage + ((kc + 1) % kLBufs) * kLStage, c0 + CH, min(CH, a.C - c0 - CH), (kc + 1) & 1);
         if (VEC) {
             mbar_wait(&bars[kc & 1], (unsigned)((kc >> 1) & 1));
+            if (RS_RACECHECK_SYNC) {
+                cp_async_wait<0>();
+                __syncthreads();
+            }
         } else {
             if (kLBufs == 2 && kc + 1 < nch) cp_async_wait<1>();
             else cp_async_wait<0>();

@@ -41,7 +41,9 @@ def lib():
     if _lib is None:
         path = _build.LIB
         try:
-            path = _build.build()
+            # RSGRAD_LIB: an alternative build of the same library (A/B timing, sanitizer
+            # builds); default: the in-tree librsgrad.so, rebuilt if stale
+            path = os.environ.get("RSGRAD_LIB") or _build.build()
         except (OSError, FileNotFoundError, Exception) as e:  # noqa: BLE001
             if not os.path.exists(_build.LIB):
                 raise RsgradError(f"librsgrad.so is missing and could not be built: {e}") from e
@@ -73,6 +75,8 @@ def lib():
         L.rsgrad_bwd_workspace_bytes.restype = S
         L.rsgrad_last_error.restype = ctypes.c_char_p
         L.rsgrad_version.restype = ctypes.c_char_p
+        L.rsgrad_set_host_staging.argtypes = [P, S]
+        L.rsgrad_set_host_staging.restype = ctypes.c_int
         L.rsgrad_launch_count.argtypes = [I]
         L.rsgrad_launch_count.restype = ctypes.c_ulonglong
         _lib = L
@@ -81,6 +85,18 @@ def lib():
 
 def version() -> str:
     return lib().rsgrad_version().decode()
+
+
+def set_host_staging(buf):
+    """Register a caller-owned CUDA uint8 tensor as the host-pointer path's staging
+    buffer on this thread / its device (None: unregister).  Keep the tensor alive while
+    registered."""
+    if buf is None:
+        _check(lib().rsgrad_set_host_staging(None, 0), "rsgrad_set_host_staging")
+        return
+    with torch.cuda.device(buf.device):
+        _check(lib().rsgrad_set_host_staging(ctypes.c_void_p(buf.data_ptr()), buf.numel() * buf.element_size()),
+               "rsgrad_set_host_staging")
 
 
 def launch_count(reset: bool = False) -> int:

@@ -16,7 +16,13 @@ for shape in [(2, 5, 37, 53, 41, 29), (1, 16, 96, 128, 96, 128), (2, 4, 512, 512
         for algo in (("auto", "scatter_priv", "scatter_atomic") if pad == "border" else
                      ("auto", "gather", "scatter_priv", "scatter_atomic")):
             rs.stn_bwd(s["x"], s["theta"], s["dy"], padding=pad, algo=algo)
+        rs.stn_bwd(s["x"], s["theta"], s["dy"], padding=pad, deterministic=True)
+    th = s["theta"].clone()
+    th[0] = torch.tensor([[0.5, 0.5, 0.1], [0.5, 0.5, -0.2]])  # singular: fallback sample
+    rs.stn_bwd(s["x"], th, s["dy"])
+    rs.stn_bwd(s["x"], th, s["dy"], deterministic=True)
     rs.stn_bicubic_fwd(s["x"], s["theta"], Ho, Wo)
+    rs.stn_bicubic_bwd(s["x"], th, s["dy"], deterministic=True)
     rs.stn_lanczos_bwd(s["x"], s["theta"], s["dy"])
     rs.stn_lanczos_fwd(s["x"], s["theta"], Ho, Wo)
     for algo in ("auto", "gather"):
@@ -27,14 +33,20 @@ for flow in ("smooth", "stress"):
         rs.warp_fwd(w["x"], w["flow"], padding=pad)
         for algo in ("auto", "scatter_priv", "scatter_atomic"):
             rs.warp_bwd(w["x"], w["flow"], w["dy"], padding=pad, algo=algo)
-    os.environ["RSGRAD_WARP_BWD"] = "win8,4,4"
+        rs.warp_bwd(w["x"], w["flow"], w["dy"], padding=pad, deterministic=True)
+    for var in ("win8,4,4", "direct"):
+        os.environ["RSGRAD_WARP_BWD"] = var
+        rs.warp_bwd(w["x"], w["flow"], w["dy"])
+        del os.environ["RSGRAD_WARP_BWD"]
+    os.environ["RSGRAD_WARP_R"] = "8"
     rs.warp_bwd(w["x"], w["flow"], w["dy"])
-    del os.environ["RSGRAD_WARP_BWD"]
+    del os.environ["RSGRAD_WARP_R"]
 for dims in [(2, 100, 130, 8, 6, 7), (1, 300, 260, 5, 3, 2), (1, 16, 16, 8, 16, 16)]:
     b = c(synth.bslice_inputs(*dims, cfg=1, grid="iid", guide="wide"))
     rs.bslice_fwd(b["grid"], b["guide"], b["x"])
     for algo in ("auto", "scatter_atomic"):
         rs.bslice_bwd(b["grid"], b["guide"], b["x"], b["dy"], algo=algo)
+    rs.bslice_bwd(b["grid"], b["guide"], b["x"], b["dy"], deterministic=dims[3] * 8 <= dims[1])
 x = torch.randn(2, 9, 37, 45, device=dev)
 k = torch.randn(17, 9, 3, 5, device=dev)
 dy = torch.randn(2, 17, 37, 45, device=dev)

@@ -77,3 +77,40 @@ def test_shard_arithmetic():
     assert [bench.shard(8, r) for r in range(8)] == [(8 * r, 8) for r in range(8)]
     with pytest.raises(AssertionError):
         bench.shard(3, 0)
+
+
+@pytest.mark.timeout(300)
+def test_bench_main_two_ranks_gloo():
+    """bench.py's own rank loop at world size 2 on CPU: `--gpus 2` without torchrun
+    re-execs itself under torch.distributed.run (127.0.0.1), each rank takes its
+    contiguous shard, the per-step timings are reduced as a max over ranks (median over
+    steps) and rank 0 alone prints ONE JSON line (--dry-run: gloo, stand-in calls)."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--dry-run", "--gpus", "2",
+                          "--steps", "3", "--warmup", "3"], capture_output=True, text=True, env=env,
+                         timeout=240, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["steps"] == 3 and d["dry_run"] is True
+    assert d["per_rank_shards"] == [[0, 32], [32, 32]]
+    assert d["config"]["per_rank_batch"] == 32
+    assert d["ms_per_step"] > 0 and d["timing"]["total_ms_k_steps_max_over_ranks"] >= d["ms_per_step"]
+
+
+def test_bench_rejects_world_mismatch():
+    """Under torchrun, --gpus must equal WORLD_SIZE (a silent 1-GPU run is refused)."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--dry-run", "--gpus", "2"],
+                         capture_output=True, text=True, env=env, timeout=120, cwd=root)
+    assert out.returncode != 0 and "WORLD_SIZE" in (out.stderr + out.stdout)

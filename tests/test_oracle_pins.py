@@ -608,6 +608,45 @@ def test_stn_lanczos_identity_and_adjoint():
     np.testing.assert_allclose(dx.ravel(), M.T @ dy.ravel(), rtol=1e-12, atol=1e-12)
 
 
+@pytest.mark.parametrize("ac", [True, False])
+def test_stn_lanczos_fwd_brute_force_all_pixels(ac):
+    """Independent pin of the 6-tap window (R13): the forward
+    equals sum over EVERY image pixel (l, k) of L(iy - l) L(ix - k) X[l, k], with
+    L(t) = numpy sinc(t) sinc(t/3) on |t| < 3 -- no window at all, so an off-by-one tap
+    window (e.g. floor-3 .. floor+2) would drop a nonzero term and fail.  Random theta,
+    zoom and shift: sample points off the integers, partly outside the image (zeros)."""
+    g = np.random.default_rng(45)
+    N, C, H, W, Ho, Wo = 2, 2, 9, 11, 7, 8
+    x = g.standard_normal((N, C, H, W))
+    th = np.array([[[1.0, 0, 0], [0, 1.0, 0]]] * N) + g.normal(0, 0.25, (N, 2, 3))
+
+    def L(t):
+        return np.where(np.abs(t) < 3, np.sinc(t) * np.sinc(t / 3), 0.0)
+
+    if ac:
+        xt = -1 + 2 * np.arange(Wo) / (Wo - 1)
+        yt = -1 + 2 * np.arange(Ho) / (Ho - 1)
+    else:
+        xt = (2 * np.arange(Wo) + 1) / Wo - 1
+        yt = (2 * np.arange(Ho) + 1) / Ho - 1
+    ref = np.zeros((N, C, Ho, Wo))
+    ls, ks = np.arange(H), np.arange(W)
+    offint = []
+    for n in range(N):
+        for i in range(Ho):
+            for j in range(Wo):
+                gx = th[n, 0, 0] * xt[j] + th[n, 0, 1] * yt[i] + th[n, 0, 2]
+                gy = th[n, 1, 0] * xt[j] + th[n, 1, 1] * yt[i] + th[n, 1, 2]
+                ix = (gx + 1) * (W - 1) / 2 if ac else ((gx + 1) * W - 1) / 2
+                iy = (gy + 1) * (H - 1) / 2 if ac else ((gy + 1) * H - 1) / 2
+                offint.append(min(abs(ix - round(ix)), abs(iy - round(iy))) > 1e-3)
+                wgt = np.outer(L(iy - ls), L(ix - ks))  # H x W, every pixel
+                ref[n, :, i, j] = (x[n] * wgt).sum(axis=(1, 2))
+    assert np.mean(offint) > 0.9  # L is continuous; off-integer points see all 6 taps
+    y = oracle.stn_lanczos_fwd(x, th, Ho, Wo, ac)
+    np.testing.assert_allclose(y, ref, rtol=0, atol=1e-12)
+
+
 def test_stn_lanczos_theta_central_fd():
     """d_theta vs central finite differences of <y(theta), dy> with
     sample coordinates kept away from the kernel's kinks (integers)."""

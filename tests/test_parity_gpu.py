@@ -904,3 +904,70 @@ def test_stn_lanczos_parity(cuda_device, dims, ac):
     rdx, rdth = oracle.stn_lanczos_bwd(xn, tn, dn, ac)
     assert_close(_np(dx), rdx, "grad", "dx")
     assert_close(_np(dth), rdth, "grad", "dtheta")
+
+
+# ============================================================================ boundary contract
+@pytest.mark.parametrize("D", [61, 64])
+def test_bslice_many_planes_tiled_backward(cuda_device, D):
+    """D up to 64: the tiled backward's shared memory (2056 D + 80740 B) is set per call
+    from the launch's need (212 KB at D = 64, under the 227 KB opt-in)."""
+    inp = synth.bslice_inputs(1, 96, 128, D, 4, 4, cfg=1, guide="wide")
+    g = _cuda(inp, cuda_device)
+    assert rsgrad.workspace_bytes(2, 1, 3, 96, 128, D=D, Gh=4, Gw=4, opts=rsgrad._opts(deterministic=True)) > 0
+    y = rsgrad.bslice_fwd(g["grid"], g["guide"], g["x"])
+    dgr, dgd, dx = rsgrad.bslice_bwd(g["grid"], g["guide"], g["x"], g["dy"], deterministic=True)
+    gr, gd, x, dy = (inp[k].double().numpy() for k in ("grid", "guide", "x", "dy"))
+    assert_close(_np(y), oracle.bslice_fwd(gr, gd, x), "fwd", "y")
+    rgr, rgd, rdx = oracle.bslice_bwd(gr, gd, x, dy)
+    assert_close(_np(dgr), rgr, "grad", "dgrid")
+    assert_close(_np(dgd), rgd, "grad", "dguide")
+    assert_close(_np(dx), rdx, "grad", "dx")
+
+
+def test_library_workspace_is_not_kept(cuda_device):
+    """ws = NULL: the library takes a stream-ordered temporary from the device's default
+    pool and frees it in stream order; once the stream is synchronised the pool (release
+    threshold 0 by default) holds nothing for the library (SURVEY 8(b) ownership)."""
+    import ctypes
+
+    from cuda.bindings import runtime as cudart
+
+    inp = _cuda(synth.stn_inputs(2, 4, 64, 64, cfg=1), cuda_device)
+    dx, dth = torch.empty_like(inp["x"]), torch.empty(2, 2, 3, device=cuda_device)
+    L = rsgrad.lib()
+    o = rsgrad._opts()
+    s = torch.cuda.current_stream()
+    err, pool = cudart.cudaDeviceGetDefaultMemPool(cuda_device.index or 0)
+    assert err == cudart.cudaError_t.cudaSuccess
+    for _ in range(3):
+        st = L.stn_bwd(rsgrad._ptr(inp["x"]), rsgrad._ptr(inp["theta"]), rsgrad._ptr(inp["dy"]), 2, 4, 64, 64, 64,
+                       64, ctypes.byref(o), rsgrad._ptr(dx), rsgrad._ptr(dth), None, 0, ctypes.c_void_p(s.cuda_stream))
+        assert st == 0
+    s.synchronize()
+    torch.cuda.synchronize()
+    err, reserved = cudart.cudaMemPoolGetAttribute(pool, cudart.cudaMemPoolAttr.cudaMemPoolAttrReservedMemCurrent)
+    assert err == cudart.cudaError_t.cudaSuccess
+    err, thr = cudart.cudaMemPoolGetAttribute(pool, cudart.cudaMemPoolAttr.cudaMemPoolAttrReleaseThreshold)
+    if int(thr) == 0:
+        assert int(reserved) == 0, f"library temporaries still reserved: {int(reserved)} B"
+    ref = rsgrad.stn_bwd(inp["x"], inp["theta"], inp["dy"])
+    assert torch.equal(ref[0], dx) and torch.equal(ref[1], dth)
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two GPUs")
+def test_second_device_same_thread():
+    """Tensors on cuda:1 while cuda:0 is current: every entry point switches to the
+    stream's device (bslice's shared-memory attribute is set for that device too)."""
+    dev1 = torch.device("cuda", 1)
+    torch.cuda.set_device(0)
+    b = _cuda(synth.bslice_inputs(1, 64, 64, 8, 4, 4, cfg=1), torch.device("cuda", 0))
+    rsgrad.bslice_bwd(b["grid"], b["guide"], b["x"], b["dy"])
+    b1 = {k: v.to(dev1) for k, v in b.items()}
+    # the binding passes cuda:1's current stream without making cuda:1 current
+    out = rsgrad.bslice_bwd(b1["grid"], b1["guide"], b1["x"], b1["dy"])
+    torch.cuda.synchronize(dev1)
+    assert torch.cuda.current_device() == 0
+    gr, gd, x, dy = (v.double().cpu().numpy() for v in (b["grid"], b["guide"], b["x"], b["dy"]))
+    rgr, rgd, rdx = oracle.bslice_bwd(gr, gd, x, dy)
+    assert_close(_np(out[0]), rgr, "grad", "dgrid on cuda:1")
+    assert_close(_np(out[2]), rdx, "grad", "dx on cuda:1")
