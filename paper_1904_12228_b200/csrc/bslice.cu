@@ -186,6 +186,33 @@ RS_DEV void stage_corners(float4 *glo, float4 *gdz, const float *grid, const Til
     }
 }
 
+// Backward layout: per (bin, q) the low-plane and plane-difference lerp terms interleaved
+// as float2 pairs {lo, dz}: gi[(b * kQS + q) * 2] = {a_lo, a_dz, b_lo, b_dz},
+// gi[... + 1] = {c_lo, c_dz, d_lo, d_dz}, so one packed FMA (FFMA2) lerps both.
+constexpr int kQS = 12;  // q per bin (the two float4 of a q are adjacent)
+RS_DEV void stage_corners_i(float4 *gi, const float *grid, const Tile &t, int D, int Gh, int Gw) {
+    const int y0 = clampi(t.j, 0, Gh - 1), y1 = clampi(t.j + 1, 0, Gh - 1);
+    const int x0 = clampi(t.k, 0, Gw - 1), x1 = clampi(t.k + 1, 0, Gw - 1);
+    const long long plane = (long long)Gh * Gw;
+    const float *g = grid + (long long)t.n * 12 * D * plane;
+    for (int e = threadIdx.x; e < (D + 1) * 12; e += blockDim.x) {
+        const int b = e / 12, q = e - b * 12;
+        const int zl = clampi(b - 1, 0, D - 1), zh = clampi(b, 0, D - 1);
+        const float *pl = g + ((long long)q * D + zl) * plane;
+        const float *ph = g + ((long long)q * D + zh) * plane;
+        const float l00 = __ldg(pl + y0 * Gw + x0), l01 = __ldg(pl + y0 * Gw + x1);
+        const float l10 = __ldg(pl + y1 * Gw + x0), l11 = __ldg(pl + y1 * Gw + x1);
+        const float h00 = __ldg(ph + y0 * Gw + x0), h01 = __ldg(ph + y0 * Gw + x1);
+        const float h10 = __ldg(ph + y1 * Gw + x0), h11 = __ldg(ph + y1 * Gw + x1);
+        const float4 L = lerp_terms(l00, l01, l10, l11);
+        const float4 Dz = lerp_terms(h00 - l00, h01 - l01, h10 - l10, h11 - l11);
+        gi[(b * kQS + q) * 2] = make_float4(L.x, Dz.x, L.y, Dz.y);
+        gi[(b * kQS + q) * 2 + 1] = make_float4(L.z, Dz.z, L.w, Dz.w);
+    }
+}
+
+RS_DEV float2 f2(float a, float b) { return make_float2(a, b); }
+
 RS_DEV float lerp2(const float4 c, float fx, float fy) {
     return fmaf(fy, fmaf(fx, c.w, c.z), fmaf(fx, c.y, c.x));
 }
@@ -320,9 +347,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     bslice_bwd_tiled(BsliceArgs a, int SY, int SX, float *__restrict__ partials, const int *__restrict__ tab) {
     extern __shared__ float4 smem4[];
     const int D = a.D, NB = D + 1;
-    float4 *glo = smem4;                                    // (D+1)*13 float4
-    float4 *gdz = glo + (D + 1) * kPlaneStride;             // (D+1)*13 float4
-    float *fxt = (float *)(gdz + (D + 1) * kPlaneStride);   // kTileXS
+    float4 *gi = smem4;                                     // (D+1)*12*2 float4 (interleaved lo/dz)
+    float *fxt = (float *)(gi + 2 * (D + 1) * kPlaneStride);  // kTileXS
     float *fyt = fxt + kTileXS;                             // kTileYS
     float *wacc = fyt + kTileYS;                            // kWarps * 4 * D * 12
     int *cnt = (int *)(wacc + kWarps * 4 * D * 12);         // kWarps * NB
@@ -353,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         cp_async_commit();
     }
 
-    stage_corners(glo, gdz, a.grid, t, D, a.Gh, a.Gw);
+    stage_corners_i(gi, a.grid, t, D, a.Gh, a.Gw);
     for (int c = threadIdx.x; c < TW; c += kThreads) {
         const double cx = bs_cx(t.xs + c, a.W, a.Gw);
         fxt[c] = (float)__dsub_rn(cx, floor(cx));
@@ -432,9 +458,27 @@ __global__ void __launch_bounds__(kThreads, 2)
     float *mywacc = wacc + w * 4 * D * 12;
     const int cbeg = (int)(((long long)nchunks * w) / kWarps);
     const int cend = (int)(((long long)nchunks * (w + 1)) / kWarps);
-    float acc[48];
+    // acc2[(pl * 2 + bb) * 6 + qq] = the (corner a = 0, a = 1) pair of plane pl, corner
+    // row bb, coefficient 6 e + qq: the 48 sums of flush_acc's layout as 24 float2 so the
+    // trilinear-weighted updates are packed FMAs (FFMA2)
+    float2 acc2[24];
 #pragma unroll
-    for (int k = 0; k < 48; k++) acc[k] = 0.f;
+    for (int k = 0; k < 24; k++) acc2[k] = f2(0.f, 0.f);
+    auto flush2 = [&](int bin) {
+        float acc[48];
+#pragma unroll
+        for (int pl = 0; pl < 2; pl++)
+#pragma unroll
+            for (int bb = 0; bb < 2; bb++)
+#pragma unroll
+                for (int qq = 0; qq < 6; qq++) {
+                    acc[(pl * 4 + bb * 2 + 0) * 6 + qq] = acc2[(pl * 2 + bb) * 6 + qq].x;
+                    acc[(pl * 4 + bb * 2 + 1) * 6 + qq] = acc2[(pl * 2 + bb) * 6 + qq].y;
+                }
+        flush_acc(acc, mywacc, bin, D, lane);
+#pragma unroll
+        for (int k = 0; k < 24; k++) acc2[k] = f2(0.f, 0.f);
+    };
     const int slot = lane >> 1, e_pl = lane & 1;
     int cur_bin = cbeg < cend ? chunk_bin[cbeg] : 0;
     // software pipeline, distance 2: chunk ch+2's X / dY loads are issued while ch computes
@@ -456,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int ch = cbeg; ch < cend; ch++) {
         const int bin = chunk_bin[ch];
         if (bin != cur_bin) {
-            flush_acc(acc, mywacc, cur_bin, D, lane);
+            flush2(cur_bin);
             cur_bin = bin;
         }
         const unsigned ent = ent_a;
@@ -478,34 +522,40 @@ __global__ void __launch_bounds__(kThreads, 2)
             for (int i = 0; i < 3; i++) { X[i] = 0.f; G[i] = 0.f; }
         }
         // this lane's coefficient half: q = 6 e + qq, (oc, i) = (q / 4, q % 4)
-        const float4 *Lc = glo + bin * kPlaneStride + 6 * e_pl, *Dc = gdz + bin * kPlaneStride + 6 * e_pl;
+        const float4 *Qc = gi + (bin * kQS + 6 * e_pl) * 2;
         const bool e1 = e_pl != 0;
         const float Gq[6] = {e1 ? G[1] : G[0], e1 ? G[1] : G[0], e1 ? G[2] : G[0],
                              e1 ? G[2] : G[0], e1 ? G[2] : G[1], e1 ? G[2] : G[1]};
         const float Xq[6] = {e1 ? X[2] : X[0], e1 ? 1.f : X[1], e1 ? X[0] : X[2],
                              e1 ? X[1] : 1.f, e1 ? X[2] : X[0], e1 ? 1.f : X[1]};
-        float wt[8];  // (plane, corner) trilinear weights
+        float2 wt2[4];  // (plane, corner row) x (corner a = 0, 1) trilinear weights
         {
-            const float wy[2] = {1.f - fy, fy}, wx[2] = {1.f - fx, fx}, wz[2] = {1.f - fz, fz};
+            const float2 wx2 = f2(1.f - fx, fx);
+            const float wy[2] = {1.f - fy, fy}, wz[2] = {1.f - fz, fz};
 #pragma unroll
             for (int pl = 0; pl < 2; pl++)
 #pragma unroll
                 for (int bb = 0; bb < 2; bb++) {
                     const float wzy = wz[pl] * wy[bb];
-                    wt[pl * 4 + bb * 2] = wzy * wx[0];
-                    wt[pl * 4 + bb * 2 + 1] = wzy * wx[1];
+                    wt2[pl * 2 + bb] = __fmul2_rn(f2(wzy, wzy), wx2);
                 }
         }
+        const float2 fx2 = f2(fx, fx), fy2 = f2(fy, fy);
         float u[4] = {0.f, 0.f, 0.f, 0.f}, dgd = 0.f;
 #pragma unroll
         for (int qq = 0; qq < 6; qq++) {
-            const float lo = lerp2(Lc[qq], fx, fy);
-            const float d = lerp2(Dc[qq], fx, fy);
+            const float4 v0 = Qc[2 * qq], v1 = Qc[2 * qq + 1];
+            // {lo, d} = fy (fx w + z) + (fx y + x) for the low plane and the difference
+            const float2 th = __ffma2_rn(fx2, f2(v1.z, v1.w), f2(v1.x, v1.y));
+            const float2 tl = __ffma2_rn(fx2, f2(v0.z, v0.w), f2(v0.x, v0.y));
+            const float2 ld = __ffma2_rn(fy2, th, tl);
+            const float lo = ld.x, d = ld.y;
             const float P = Gq[qq] * Xq[qq];
             u[qq & 3] = fmaf(Gq[qq], fmaf(fz, d, lo), u[qq & 3]);  // A_q G_oc (i = 3 slots unused)
             dgd = fmaf(P, d, dgd);
+            const float2 P2 = f2(P, P);
 #pragma unroll
-            for (int tt = 0; tt < 8; tt++) acc[tt * 6 + qq] = fmaf(wt[tt], P, acc[tt * 6 + qq]);
+            for (int k = 0; k < 4; k++) acc2[k * 6 + qq] = __ffma2_rn(wt2[k], P2, acc2[k * 6 + qq]);
         }
         // dX_i = sum_oc A_{4oc+i} G_oc: this half's slots, then the partner's half
         float dx0 = e1 ? u[2] : u[0], dx1 = e1 ? u[3] : u[1], dx2 = e1 ? u[0] : u[2];
@@ -525,7 +575,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
         }
     }
-    if (cbeg < cend) flush_acc(acc, mywacc, cur_bin, D, lane);
+    if (cbeg < cend) flush2(cur_bin);
     __syncthreads();
     // ---- block partial: fixed-order sum over warps
     float *part = partials + (long long)blockIdx.x * 4 * D * 12;

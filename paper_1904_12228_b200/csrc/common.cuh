@@ -127,6 +127,15 @@ RS_DEV unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_sha
 RS_DEV void cp_async16(void *s, const void *g) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(s)), "l"(g) : "memory");
 }
+// zero-filling variants: ok = false copies 0 source bytes (the 16 / 4 B are zeroed)
+RS_DEV void cp_async16_zfill(void *s, const void *g, bool ok) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(s)), "l"(g), "r"(ok ? 16 : 0)
+                 : "memory");
+}
+RS_DEV void cp_async4_zfill(void *s, const void *g, bool ok) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(s)), "l"(g), "r"(ok ? 4 : 0)
+                 : "memory");
+}
 RS_DEV void cp_async4(void *s, const void *g) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(s)), "l"(g) : "memory");
 }

@@ -6,7 +6,7 @@
 TAG=$1; KR=$2; NB=$3; shift 3
 CMD=${PROF_CMD:-python scripts/bench_layer.py $NB 1}
 MET=$(python -c "import sys; sys.path.insert(0,'scripts'); import ncu_summary; print(ncu_summary.EXTRA_METRICS)")
-env "$@" ncu --set full --metrics $MET --import-source on --clock-control none -k "regex:$KR" -c 4 -f -o gpurun_out/$TAG \
+env "$@" ncu --set full --metrics $MET --import-source on --clock-control none -k "regex:$KR" -c ${PROF_COUNT:-4} -f -o gpurun_out/$TAG \
     $CMD > gpurun_out/$TAG.log 2>&1
 python scripts/ncu_summary.py gpurun_out/$TAG.ncu-rep gpurun_out/$TAG.md >> gpurun_out/$TAG.log 2>&1
 for k in $(ncu -i gpurun_out/$TAG.ncu-rep --page raw --csv 2>/dev/null | python -c "
