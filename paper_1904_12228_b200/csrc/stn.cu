@@ -683,7 +683,6 @@ __global__ void stn_tables_kernel(double *xt, double *yt, int Ho, int Wo, int ac
 
 RS_DEV bool stn_gather_ok(const Affine &A, int Ho, int Wo);
 RS_DEV bool stn_lean_ok(const Affine &A, int Ho, int Wo);
-RS_DEV bool stn_splat_ok(const Affine &A, int Ho, int Wo);
 
 // flags[n] = 1 if sample n takes the gather adjoint (variant 0: cell-owner,
 // 1: per-pixel gather); fb_list = the others.
@@ -696,10 +695,8 @@ __global__ void stn_classify_kernel(StnArgs a, int allow_gather, int variant, in
         const Theta T = load_theta(a.theta, n);
         const Affine A = stn_affine(T, a.H, a.W, a.Ho, a.Wo, a.ac);
         const bool g = allow_gather && !a.border &&
-                       (variant == 1   ? stn_gather_ok(A, a.Ho, a.Wo)
-                        : variant == 2 ? stn_lean_ok(A, a.Ho, a.Wo)
-                        : variant == 4 ? stn_splat_ok(A, a.Ho, a.Wo)
-                                       : stn_gatherable(A, a.Ho, a.Wo));
+                       (variant == 1 ? stn_gather_ok(A, a.Ho, a.Wo)
+                                     : variant == 2 ? stn_lean_ok(A, a.Ho, a.Wo) : stn_gatherable(A, a.Ho, a.Wo));
         flags[n] = g ? 1 : 0;
         if (!g) fb_list[atomicAdd(&cnt, 1)] = n;
     }
@@ -1280,216 +1277,6 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
 }
 
-// ----------------------------------------------------------------- backward: fixed-point splat dX
-// d_input as a scatter privatised per INPUT tile, with integer accumulation.  A block
-// owns a 32 x 32 tile T of input pixels.  The output pixels whose taps can land in T
-// are exactly those whose floor cell lies in [xa0-1, xa0+31] x [yb0-1, yb0+31]: the
-// preimage of that cell range under the affine map (the "bounded footprint" of the
-// scatter-to-gather conversion), enumerated row by row and flattened
-// so every thread gets the same number of output pixels (no per-cell imbalance).  Each
-// output pixel adds w_k * dY to the taps k that fall in T -- taps in a neighbouring
-// tile are added by that tile's block, which enumerates the same output pixel -- so no
-// element is written by two blocks and dX needs no memset and no global atomics.
-// Inside the block the adds go to a shared-memory accumulator per (channel, pixel) by
-// 32-bit integer atomics (native ATOMS.ADD on sm_100, measured 17 lane-ops/clk/SM vs
-// 26 for LDS; float shared atomics are CAS loops): every term is rounded once to a
-// fixed-point integer at a per-(tile, channel) scale 2^S chosen from max|dY| over the
-// tile's preimage and the exact bound Wb on the sum of tap weights an element can
-// receive, so the integer sums cannot overflow and are independent of order
-// (bitwise deterministic).  Resolution: 2^-S <= 2 max|dY| Wb 2^-30 per term.
-// Wb: the output pixels landing in the open 2 x 2 tap square of an element are lattice
-// points of the inverse image of that square (area 4/|det|, perimeter P): at most
-// area + P/2 + 1 of them, each with weight <= 1.
-constexpr int kSX = 32, kSY = 32, kSRQMax = 160, kSFQMax = 2304;
-#ifndef RS_SPLAT_CH
-#define RS_SPLAT_CH 16
-#endif
-constexpr int kSCH = RS_SPLAT_CH;  // channels per pass (shared accumulator: 4 KB each)
-
-RS_DEV bool stn_splat_ok(const Affine &A, int Ho, int Wo) {
-    if (!A.inv || Ho > 65535 || Wo > 65535) return false;
-    const double hq = fabs(A.i10) * (kSX + 1) + fabs(A.i11) * (kSY + 1);
-    const double rq = ceil(hq) + 3.0;
-    const double fq = (double)(kSX + 1) * (kSY + 1) / fabs(A.det) + 8.0 * rq + 64.0;
-    return rq <= kSRQMax && fq <= kSFQMax;
-}
-
-RS_DEV double splat_wbound(const Affine &A) {
-    const double c1 = sqrt(A.i00 * A.i00 + A.i10 * A.i10), c2 = sqrt(A.i01 * A.i01 + A.i11 * A.i11);
-    return 4.0 / fabs(A.det) + 2.0 * (c1 + c2) + 1.0;
-}
-
-template <int CH>
-__global__ void __launch_bounds__(kThreads, 3)
-    stn_bwd_splat(StnArgs a, const double *__restrict__ xtab, const double *__restrict__ ytab,
-                  const int *__restrict__ flags, int tiles_x, int tiles_y) {
-    extern __shared__ __align__(16) float4 sm4[];
-    int *acc = (int *)sm4;                           // CH * 1024
-    uint2 *rec = (uint2 *)(acc + CH * kSX * kSY);     // kSFQMax: cell (rel.) + fractions
-    unsigned *ijs = (unsigned *)(rec + kSFQMax);      // kSFQMax: (i << 16) | j
-    int *qlo = (int *)(ijs + kSFQMax);                // kSRQMax
-    int *qoff = qlo + kSRQMax;                        // kSRQMax + 1
-    __shared__ unsigned mxs[CH];
-    __shared__ float scl[CH], iscl[CH];
-
-    const int n = blockIdx.y;
-    const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
-    const int xa0 = tx * kSX, yb0 = ty * kSY;
-    const long long HW = (long long)a.H * a.W, P = (long long)a.Ho * a.Wo;
-    float *dxn = a.dx + (long long)n * a.C * HW;
-    if (!flags[n]) {  // fallback sample: zero this tile (the atomic scatter adds later)
-        for (int e = threadIdx.x; e < a.C * kSX * kSY; e += kThreads) {
-            const int c = e / (kSX * kSY), l = e - c * (kSX * kSY), y = yb0 + l / kSX, x = xa0 + l % kSX;
-            if (y < a.H && x < a.W) dxn[(long long)c * HW + (long long)y * a.W + x] = 0.f;
-        }
-        return;
-    }
-    const Theta T = load_theta(a.theta, n);
-    const Affine A = stn_affine(T, a.H, a.W, a.Ho, a.Wo, a.ac);
-    // ---- preimage rows of the cells [xa0-1, xa0+kSX-1] x [yb0-1, yb0+kSY-1]
-    const double eps = 1e-3;
-    const double Lx = xa0 - 1 - eps, Ux = xa0 + kSX + eps;
-    const double Ly = yb0 - 1 - eps, Uy = yb0 + kSY + eps;
-    double imin = 1e300, imax = -1e300;
-#pragma unroll
-    for (int c = 0; c < 4; c++) {
-        const double px_ = (c & 1) ? Ux : Lx, py_ = (c & 2) ? Uy : Ly;
-        const double qi = A.i10 * (px_ - A.p0x) + A.i11 * (py_ - A.p0y);
-        imin = fmin(imin, qi);
-        imax = fmax(imax, qi);
-    }
-    const int ilo = max(0, (int)ceil(fmax(imin, -1e9)));
-    const int ihi = min(a.Ho - 1, (int)floor(fmin(imax, 1e9)));
-    const int RQ = min(kSRQMax, max(0, ihi - ilo + 1));
-    for (int r = threadIdx.x; r < RQ; r += kThreads) {
-        const int i = ilo + r;
-        double jl = -1e300, jh = 1e300;
-        const double ax_[2] = {A.m00, A.m10}, bx_[2] = {A.m01 * i + A.p0x, A.m11 * i + A.p0y};
-        const double L_[2] = {Lx, Ly}, U_[2] = {Ux, Uy};
-#pragma unroll
-        for (int d = 0; d < 2; d++) {
-            if (fabs(ax_[d]) < 1e-12) {
-                if (bx_[d] < L_[d] || bx_[d] > U_[d]) { jl = 1e300; jh = -1e300; }
-            } else {
-                double u = (L_[d] - bx_[d]) / ax_[d], v = (U_[d] - bx_[d]) / ax_[d];
-                if (u > v) { const double t = u; u = v; v = t; }
-                jl = fmax(jl, u);
-                jh = fmin(jh, v);
-            }
-        }
-        const int lo = max(0, (int)ceil(fmax(jl, -1e9))), hi = min(a.Wo - 1, (int)floor(fmin(jh, 1e9)));
-        qlo[r] = lo;
-        qoff[r] = hi >= lo ? hi - lo + 1 : 0;  // count, scanned below
-    }
-    for (int e = threadIdx.x; e < CH * kSX * kSY; e += kThreads) acc[e] = 0;
-    if (threadIdx.x < CH) mxs[threadIdx.x] = 0u;
-    __syncthreads();
-    if (threadIdx.x < 32) {  // exclusive scan of the row counts (warp 0)
-        const int lane = threadIdx.x;
-        int run = 0;
-        for (int base = 0; base < RQ; base += 32) {
-            const int r = base + lane;
-            const int v0 = r < RQ ? qoff[r] : 0;
-            int v = v0;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int t = __shfl_up_sync(0xffffffffu, v, o);
-                if (lane >= o) v += t;
-            }
-            if (r < RQ) qoff[r] = run + v - v0;
-            run += __shfl_sync(0xffffffffu, v, 31);
-        }
-        if (lane == 0) qoff[RQ] = run;
-    }
-    __syncthreads();
-    const int FQ = min(qoff[RQ], kSFQMax);
-    // ---- records: exact fp64 floor cell (relative to the tile's cell origin) + fractions
-    for (int e = threadIdx.x; e < FQ; e += kThreads) {
-        int lo = 0, hi = RQ - 1;  // last row with qoff <= e
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (qoff[mid] <= e) lo = mid;
-            else hi = mid - 1;
-        }
-        const int i = ilo + lo, j = qlo[lo] + (e - qoff[lo]);
-        double ix, iy;
-        stn_coord(T, xtab[j], ytab[i], a.H, a.W, a.ac, ix, iy);
-        const Cell cx = cell_of(ix), cy = cell_of(iy);
-        const int rx = cx.i0 - (xa0 - 1), ry = cy.i0 - (yb0 - 1);
-        uint2 R = make_uint2(0xff000000u, 0xff000000u);
-        if (rx >= 0 && rx <= kSX && ry >= 0 && ry <= kSY) R = pack_rec(rx, ry, cx.f, cy.f);
-        rec[e] = R;
-        ijs[e] = ((unsigned)i << 16) | (unsigned)j;
-    }
-    __syncthreads();
-    const float *gbase = a.dy + (long long)n * a.C * P;
-    const double wb = splat_wbound(A);
-    for (int c0 = 0; c0 < a.C; c0 += CH) {
-        const int cn = min(CH, a.C - c0);
-        // ---- pass A: max |dY| per channel over the preimage
-        unsigned m[CH];
-#pragma unroll
-        for (int c = 0; c < CH; c++) m[c] = 0u;
-        for (int e = threadIdx.x; e < FQ; e += kThreads) {
-            if ((rec[e].x >> 24) == 0xffu) continue;
-            const unsigned ij = ijs[e];
-            const float *g = gbase + (long long)c0 * P + (long long)(ij >> 16) * a.Wo + (ij & 0xffffu);
-#pragma unroll
-            for (int c = 0; c < CH; c++)
-                if (c < cn) m[c] = max(m[c], __float_as_uint(fabsf(__ldg(g + (long long)c * P))));
-        }
-#pragma unroll
-        for (int c = 0; c < CH; c++) {
-            const unsigned v = __reduce_max_sync(0xffffffffu, m[c]);
-            if ((threadIdx.x & 31) == 0 && c < cn) atomicMax(&mxs[c], v);
-        }
-        __syncthreads();
-        if (threadIdx.x < cn) {
-            const float mx = __uint_as_float(mxs[threadIdx.x]);
-            int S = 0;
-            if (mx > 0.f && isfinite(mx)) S = 29 - ilogb((double)mx * wb);  // mx * wb * 2^S < 2^30
-            S = max(-120, min(120, S));
-            scl[threadIdx.x] = ldexpf(1.f, S);
-            iscl[threadIdx.x] = ldexpf(1.f, -S);
-            mxs[threadIdx.x] = 0u;
-        }
-        __syncthreads();
-        // ---- pass B: integer splat of w_k * dY into the taps that fall in T
-        for (int e = threadIdx.x; e < FQ; e += kThreads) {
-            const uint2 R = rec[e];
-            const int rx = (int)(R.x >> 24), ry = (int)(R.y >> 24);
-            if (rx == 0xff) continue;
-            const float fx = (float)(R.x & 0xffffffu) * (1.f / 16777216.f);
-            const float fy = (float)(R.y & 0xffffffu) * (1.f / 16777216.f);
-            const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx;
-            const float w10 = fy * (1.f - fx), w11 = fy * fx;
-            // tap (dx, dy) of cell (rx, ry) is tile pixel (rx - 1 + dx, ry - 1 + dy)
-            const bool cx0 = rx >= 1, cx1 = rx <= kSX - 1, cy0 = ry >= 1, cy1 = ry <= kSY - 1;
-            const int l00 = (ry - 1) * kSX + (rx - 1);
-            const unsigned ij = ijs[e];
-            const float *g = gbase + (long long)c0 * P + (long long)(ij >> 16) * a.Wo + (ij & 0xffffu);
-#pragma unroll
-            for (int c = 0; c < CH; c++) {
-                if (c >= cn) break;
-                const float gs = __ldg(g + (long long)c * P) * scl[c];
-                int *ac = acc + c * kSX * kSY + l00;
-                if (cy0 && cx0) atomicAdd(ac, __float2int_rn(w00 * gs));
-                if (cy0 && cx1) atomicAdd(ac + 1, __float2int_rn(w01 * gs));
-                if (cy1 && cx0) atomicAdd(ac + kSX, __float2int_rn(w10 * gs));
-                if (cy1 && cx1) atomicAdd(ac + kSX + 1, __float2int_rn(w11 * gs));
-            }
-        }
-        __syncthreads();
-        // ---- fixed point -> fp32, coalesced rows; re-zero for the next chunk
-        for (int e = threadIdx.x; e < cn * kSX * kSY; e += kThreads) {
-            const int c = e / (kSX * kSY), l = e - c * (kSX * kSY), y = yb0 + l / kSX, x = xa0 + l % kSX;
-            if (y < a.H && x < a.W) dxn[(long long)(c0 + c) * HW + (long long)y * a.W + x] = (float)acc[e] * iscl[c];
-            acc[e] = 0;
-        }
-        __syncthreads();
-    }
-}
-
 // ----------------------------------------------------------------- backward: per-pixel gather
 // Input tile 32 x 16 (thread = column, rows w and w+8).  Each input pixel p walks
 // the preimage window of [p-1, p+1)^2 once, keeping its (<= kGHits) hits — the
@@ -1959,8 +1746,7 @@ int stn_bwd_variant() {
     const char *e = getenv("RSGRAD_STN_BWD");
     if (e && strcmp(e, "gather") == 0) return 1;
     if (e && strcmp(e, "cell") == 0) return 0;
-    if (e && strcmp(e, "lean") == 0) return 2;
-    return 4;  // fixed-point splat dX + staged output-tile d_theta
+    return 2;  // lean dX + staged output-tile d_theta (measured fastest)
 }
 
 struct StnWs {
@@ -2007,11 +1793,6 @@ size_t bwd_lean_smem() {
     return sizeof(float) * kLBufs * kLStage + sizeof(uint2) * kLFQMax + sizeof(int4) * kLRQMax +
            sizeof(int) * (5 * kLRQMax + 8) + sizeof(unsigned short) * 8 * (kLRows + 1) * kLHits * 32 +
            8 * (kLRows + 1) * 32;
-}
-
-size_t splat_smem(int ch) {
-    return sizeof(int) * (size_t)ch * kSX * kSY + (sizeof(uint2) + sizeof(unsigned)) * kSFQMax +
-           sizeof(int) * (2 * kSRQMax + 1);
 }
 
 size_t bwd_gather_smem() {
@@ -2125,16 +1906,7 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
     const bool vin = (a.W % 4 == 0) && aligned16(a.x);
     const bool vout = (a.Wo % 4 == 0) && aligned16(a.dy);
     int tiles_b = g.bx * g.by;
-    if (allow_gather && variant == 4) {
-        // fixed-point splat dX; every sample's d_theta from the output-tile kernel
-        if (a.dx) {
-            const int sx = (a.W + kSX - 1) / kSX, sy = (a.H + kSY - 1) / kSY;
-            const size_t sm = splat_smem(kSCH);
-            set_smem(stn_bwd_splat<kSCH>, sm);
-            stn_bwd_splat<kSCH><<<dim3(sx * sy, a.N), kThreads, sm, s>>>(a, w.xtab, w.ytab, w.flags, sx, sy);
-            note_launch();
-        }
-    } else if (allow_gather && variant == 2) {
+    if (allow_gather && variant == 2) {
         // lean dX kernel; every sample's d_theta comes from the output-tile kernel
         const size_t sm = bwd_lean_smem();
         const int ly = (a.H + kLTY - 1) / kLTY;
@@ -2175,7 +1947,7 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
     }
     // fallback samples (all samples when !allow_gather or the lean dX kernel):
     // d_theta from output tiles ...
-    const bool dth_all = allow_gather && (variant == 2 || variant == 4);
+    const bool dth_all = allow_gather && variant == 2;
     const bool dth_fast = vin && vout && dth_all && !stn_slow_tiles();
     const int fi_df = (a.Ho + kFIdf - 1) / kFIdf;  // d_theta tiles per column, fast path
     // fallback d_input: per-tap global atomics (AUTO, SCATTER_ATOMIC), or block-private
