@@ -204,7 +204,7 @@ template <int MODE, bool VEC, bool FLOW = false, int kFI = (MODE == 0 ? kFIfwd :
 __global__ void __launch_bounds__(FAST ? kOTFast : kThreads, FAST ? kOTFastMinB : 3)
     stn_out_tile(StnArgs a, const double *__restrict__ xtab, const double *__restrict__ ytab,
                  const int *__restrict__ fb_list, const int *__restrict__ fb_count,
-                 double *__restrict__ partials, int tiles_j, int tiles_i) {
+                 double *__restrict__ partials, int tiles_j, int tiles_i, int *__restrict__ ctr = nullptr) {
     constexpr int kOT = FAST ? kOTFast : kThreads, kOW = kOT / 32;  // threads, warps
     constexpr int kFP = kFI / kOW;  // output pixels per thread
     static_assert(kFI % kOW == 0, "every tile row needs a warp: tile rows must be a multiple of the warps");
@@ -669,25 +669,51 @@ __global__ void __launch_bounds__(FAST ? kOTFast : kThreads, FAST ? kOTFastMinB 
                 for (int w = 0; w < kOT / 32; w++) s += (double)red[w][threadIdx.x];
                 partials[((long long)n * tiles_j * tiles_i + blockIdx.x) * 6 + threadIdx.x] = s;
             }
+            if (ctr) {
+                // the last tile block of sample n sums its tiles' partials in tile order
+                // (the fixed order of stn_dtheta_finalize: bitwise the same result) and
+                // writes d_theta -- one launch less per call
+                __shared__ int last;
+                __threadfence();
+                __syncthreads();
+                if (threadIdx.x == 0) last = atomicAdd(ctr + n, 1) == (int)gridDim.x - 1;
+                __syncthreads();
+                if (last) {
+                    __threadfence();
+                    const double *pp = partials + (long long)n * tiles_j * tiles_i * 6;
+                    const int nt = tiles_j * tiles_i;
+                    double sk[6] = {0, 0, 0, 0, 0, 0};
+                    for (int b = threadIdx.x; b < nt; b += kOT)
+#pragma unroll
+                        for (int k = 0; k < 6; k++) sk[k] += __ldcg(pp + (long long)b * 6 + k);
+                    __shared__ double redd[kOT / 32][6];
+#pragma unroll
+                    for (int k = 0; k < 6; k++) {
+                        const double v = warp_sum_d(sk[k]);
+                        if (lane == 0) redd[warp][k] = v;
+                    }
+                    __syncthreads();
+                    if (threadIdx.x < 6) {
+                        double v = 0.0;
+                        for (int w = 0; w < kOT / 32; w++) v += redd[w][threadIdx.x];
+                        a.dtheta[6 * n + threadIdx.x] = (float)v;
+                    }
+                }
+            }
         }
         __syncthreads();
     }
 }
 
 // ----------------------------------------------------------------- backward: tables + classify
-__global__ void stn_tables_kernel(double *xt, double *yt, int Ho, int Wo, int ac) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < Wo) xt[t] = stn_norm(t, Wo, ac);
-    if (t < Ho) yt[t] = stn_norm(t, Ho, ac);
-}
 
 RS_DEV bool stn_gather_ok(const Affine &A, int Ho, int Wo);
 RS_DEV bool stn_lean_ok(const Affine &A, int Ho, int Wo);
 
 // flags[n] = 1 if sample n takes the gather adjoint (variant 0: cell-owner,
-// 1: per-pixel gather); fb_list = the others.
-__global__ void stn_classify_kernel(StnArgs a, int allow_gather, int variant, int *flags, int *fb_list,
-                                    int *fb_count) {
+// 1: per-pixel gather, 2: lean); fb_list = the others.  Called by one whole block.
+RS_DEV void stn_classify_block(const StnArgs &a, int allow_gather, int variant, int *flags, int *fb_list,
+                               int *fb_count) {
     __shared__ int cnt;
     if (threadIdx.x == 0) cnt = 0;
     __syncthreads();
@@ -702,6 +728,19 @@ __global__ void stn_classify_kernel(StnArgs a, int allow_gather, int variant, in
     }
     __syncthreads();
     if (threadIdx.x == 0) *fb_count = cnt;
+}
+
+// One launch for the per-call preparation: the normalised coordinate tables (every
+// block), the per-sample classification and the d_theta tile counters (block 0).
+__global__ void stn_prep_kernel(StnArgs a, int allow_gather, int variant, double *xt, double *yt, int *flags,
+                                int *fb_list, int *fb_count, int *ctr) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < a.Wo) xt[t] = stn_norm(t, a.Wo, a.ac);
+    if (t < a.Ho) yt[t] = stn_norm(t, a.Ho, a.ac);
+    if (blockIdx.x == 0) {
+        for (int n = threadIdx.x; n < a.N; n += blockDim.x) ctr[n] = 0;
+        stn_classify_block(a, allow_gather, variant, flags, fb_list, fb_count);
+    }
 }
 
 // ----------------------------------------------------------------- backward: cell-owner gather
@@ -1751,7 +1790,7 @@ int stn_bwd_variant() {
 
 struct StnWs {
     double *xtab, *ytab, *pb, *pf;
-    int *flags, *fb_list, *fb_count;
+    int *flags, *fb_list, *fb_count, *ctr;
     void *det;  // deterministic fallback scatter (det.cuh), when requested
     size_t bytes;
 };
@@ -1771,6 +1810,7 @@ StnWs stn_ws_layout(void *base, int N, int C, int H, int W, int Ho, int Wo, bool
     w.flags = (int *)take(sizeof(int) * N);
     w.fb_list = (int *)take(sizeof(int) * N);
     w.fb_count = (int *)take(sizeof(int));
+    w.ctr = (int *)take(sizeof(int) * N);
     const size_t tb = (size_t)g.bx * g.by > (size_t)g.gx * g.gy ? (size_t)g.bx * g.by : (size_t)g.gx * g.gy;
     w.pb = (double *)take(sizeof(double) * 6 * (size_t)N * tb);
     w.pf = (double *)take(sizeof(double) * 6 * (size_t)N * g.fj * g.fi);
@@ -1827,7 +1867,7 @@ cudaError_t stn_fwd_launch(const StnArgs &a, cudaStream_t s) {
     if (vec && !stn_slow_tiles()) {
         auto k = stn_out_tile<MODE_FWD, true, false, kFIfwd, true>;
         set_smem(k, sm);
-        k<<<grid, kOTFast, sm, s>>>(a, nullptr, nullptr, nullptr, nullptr, nullptr, g.fj, g.fi_fwd);
+        k<<<grid, kOTFast, sm, s>>>(a, nullptr, nullptr, nullptr, nullptr, nullptr, g.fj, g.fi_fwd, nullptr);
     } else if (vec) {
         set_smem(stn_out_tile<MODE_FWD, true>, sm);
         stn_out_tile<MODE_FWD, true><<<grid, kThreads, sm, s>>>(a, nullptr, nullptr, nullptr, nullptr,
@@ -1862,11 +1902,11 @@ cudaError_t flow_tile_launch(const StnArgs &a, int mode, bool priv, cudaStream_t
         if (vec) {
             auto k = stn_out_tile<MODE_DFLOW, true, true, kFIdth, false, true>;
             set_smem(k, smp);
-            k<<<grid, kThreads, smp, s>>>(a, nullptr, nullptr, nullptr, nullptr, nullptr, g.fj, g.fi);
+            k<<<grid, kThreads, smp, s>>>(a, nullptr, nullptr, nullptr, nullptr, nullptr, g.fj, g.fi, nullptr);
         } else {
             auto k = stn_out_tile<MODE_DFLOW, false, true, kFIdth, false, true>;
             set_smem(k, smp);
-            k<<<grid, kThreads, smp, s>>>(a, nullptr, nullptr, nullptr, nullptr, nullptr, g.fj, g.fi);
+            k<<<grid, kThreads, smp, s>>>(a, nullptr, nullptr, nullptr, nullptr, nullptr, g.fj, g.fi, nullptr);
         }
     } else {
         if (vec) {
@@ -1891,13 +1931,12 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
     const StnWs w = stn_ws_layout(ws, a.N, a.C, a.H, a.W, a.Ho, a.Wo, det);
     const long long HW = (long long)a.H * a.W;
     const int tmax = a.Wo > a.Ho ? a.Wo : a.Ho;
-    stn_tables_kernel<<<(tmax + 255) / 256, 256, 0, s>>>(w.xtab, w.ytab, a.Ho, a.Wo, a.ac);
-    note_launch();
     // AUTO / GATHER: cell-owner gather where the preimage is bounded (zeros padding);
     // SCATTER_ATOMIC or border padding: every sample takes the fallback pair.
     const int allow_gather = (algo == 0 || algo == 1) && !a.border && HW * kBCH < (1LL << 31);
     const int variant = stn_bwd_variant();
-    stn_classify_kernel<<<1, 256, 0, s>>>(a, allow_gather, variant, w.flags, w.fb_list, w.fb_count);
+    stn_prep_kernel<<<(tmax + 255) / 256, 256, 0, s>>>(a, allow_gather, variant, w.xtab, w.ytab, w.flags, w.fb_list,
+                                                       w.fb_count, w.ctr);
     note_launch();
     if (!allow_gather && a.dx && !det) {
         cudaError_t e = cudaMemsetAsync(a.dx, 0, sizeof(float) * (size_t)a.N * a.C * HW, s);
@@ -1962,12 +2001,12 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
             auto k = stn_out_tile<MODE_DTHETA, true, false, kFIdf, true>;
             set_smem(k, sm);
             grid.x = g.fj * fi_df;
-            k<<<grid, kOTFast, sm, s>>>(a, w.xtab, w.ytab, nullptr, w.fb_count, w.pf, g.fj, fi_df);
+            k<<<grid, kOTFast, sm, s>>>(a, w.xtab, w.ytab, nullptr, w.fb_count, w.pf, g.fj, fi_df, w.ctr);
         } else if (priv && !dth_all) {  // fallback samples: d_theta and privatised d_input
             auto k = vin ? stn_out_tile<MODE_DTHETA, true, false, kFIdth, false, true>
                          : stn_out_tile<MODE_DTHETA, false, false, kFIdth, false, true>;
             set_smem(k, smp);
-            k<<<grid, kThreads, smp, s>>>(a, w.xtab, w.ytab, fbl, w.fb_count, w.pf, g.fj, g.fi);
+            k<<<grid, kThreads, smp, s>>>(a, w.xtab, w.ytab, fbl, w.fb_count, w.pf, g.fj, g.fi, nullptr);
         } else if (vin) {
             set_smem(stn_out_tile<MODE_DTHETA, true>, sm);
             stn_out_tile<MODE_DTHETA, true><<<grid, kThreads, sm, s>>>(a, w.xtab, w.ytab, fbl, w.fb_count,
@@ -1986,7 +2025,7 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
         auto k = vin ? stn_out_tile<MODE_DFLOW, true, false, kFIdth, false, true>
                      : stn_out_tile<MODE_DFLOW, false, false, kFIdth, false, true>;
         set_smem(k, smp);
-        k<<<dim3(g.fj * g.fi, 1), kThreads, smp, s>>>(b, w.xtab, w.ytab, w.fb_list, w.fb_count, nullptr, g.fj, g.fi);
+        k<<<dim3(g.fj * g.fi, 1), kThreads, smp, s>>>(b, w.xtab, w.ytab, w.fb_list, w.fb_count, nullptr, g.fj, g.fi, nullptr);
         note_launch();
     } else if (det) {
         // deterministic=1: the fallback samples' d_input by the fixed-point scatter
@@ -1996,13 +2035,14 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
         if (e != cudaSuccess) return e;
     } else if (a.dx && !priv) {
         const long long P = (long long)a.Ho * a.Wo;
+        // grid-stride over the (usually empty) fallback list: a small grid exits at once
         long long blocks = (P + kThreads - 1) / kThreads;
-        if (blocks > 4 * kNumSMs * 8) blocks = 4 * kNumSMs * 8;
+        if (blocks > 2 * kNumSMs) blocks = 2 * kNumSMs;
         stn_dx_scatter<<<(unsigned)blocks, kThreads, 0, s>>>(a, w.fb_list, w.fb_count);
         note_launch();
     }
-    if (a.dtheta) {
-        stn_dtheta_finalize<<<a.N, kThreads, 0, s>>>(w.pb, tiles_b, w.pf, g.fj * (dth_fast ? fi_df : g.fi),
+    if (a.dtheta && !dth_fast) {  // (the FAST d_theta tiles finalize in their last block)
+        stn_dtheta_finalize<<<a.N, kThreads, 0, s>>>(w.pb, tiles_b, w.pf, g.fj * g.fi,
                                                       dth_all ? nullptr : w.flags, a.dtheta);
         note_launch();
     }

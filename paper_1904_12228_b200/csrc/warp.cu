@@ -678,7 +678,7 @@ cudaError_t warp_bwd_launch(const WarpArgs &a, int algo, int deterministic, void
     if (!win && !direct) {
         const int tiles_x = (a.W + 31) / 32;
         int R = 16;
-        if ((long long)tiles_x * ((a.H + 4 * R * kStripW - 1) / (4 * R * kStripW)) * a.N < 8LL * kNumSMs) R = 8;
+        if ((long long)tiles_x * ((a.H + R * kStripW - 1) / (R * kStripW)) * a.N < 8LL * kNumSMs) R = 8;
         const char *er = getenv("RSGRAD_WARP_R");
         if (er) R = atoi(er) == 8 ? 8 : 16;
         const int tiles_y = (a.H + R * kStripW - 1) / (R * kStripW);
