@@ -249,20 +249,28 @@ __global__ void __launch_bounds__(kStripW * 32, RS_STRIP_MINB)
                 }
                 if (same_prev) em[0] = em[1] = em[2] = em[3] = false;
             }
-            // left neighbour's right taps on our left taps (same cell row, one column left)
-            const bool p01 = __shfl_up_sync(0xffffffffu, (int)(em[1] && !same_prev), 1) != 0;
-            const bool p11 = __shfl_up_sync(0xffffffffu, (int)(em[3] && !same_prev), 1) != 0;
-            const bool adj = lane > 0 && ppx + 1 == pcx && ppy == pcy;
+            // the previous emitter's right taps on our left taps (same cell row, one column
+            // left): the previous emitter is the head of the previous run (the left
+            // neighbour lane when there are no runs), the next one takes ours
+            const unsigned heads = runs ? ~runs : 0xffffffffu;
+            const unsigned below = heads & ((1u << lane) - 1u);
+            const int prevh = below ? 31 - __clz(below) : lane;
+            const unsigned above = lane == 31 ? 0u : (heads & (~0u << (lane + 1)));
+            const int nexth = above ? __ffs(above) - 1 : lane;
+            const int qpx = __shfl_sync(0xffffffffu, pcx, prevh), qpy = __shfl_sync(0xffffffffu, pcy, prevh);
+            const bool p01 = __shfl_sync(0xffffffffu, (int)em[1], prevh) != 0;
+            const bool p11 = __shfl_sync(0xffffffffu, (int)em[3], prevh) != 0;
+            const bool adj = prevh != lane && qpx + 1 == pcx && qpy == pcy;
             const bool ab01 = adj && p01 && em[0], ab11 = adj && p11 && em[2];
-            const bool g01 = __shfl_down_sync(0xffffffffu, (int)ab01, 1) != 0 && lane < 31;
-            const bool g11 = __shfl_down_sync(0xffffffffu, (int)ab11, 1) != 0 && lane < 31;
+            const bool g01 = __shfl_sync(0xffffffffu, (int)ab01, nexth) != 0 && nexth != lane;
+            const bool g11 = __shfl_sync(0xffffffffu, (int)ab11, nexth) != 0 && nexth != lane;
             if (g01) em[1] = false;
             if (g11) em[3] = false;
             const int o00 = any ? pcy * a.W + pcx : 0;  // a tap of the cell is in the image
 #pragma unroll
             for (int c = 0; c < CW; c++) {
-                const float r01 = __shfl_up_sync(0xffffffffu, val[c][1], 1);
-                const float r11 = __shfl_up_sync(0xffffffffu, val[c][3], 1);
+                const float r01 = __shfl_sync(0xffffffffu, val[c][1], prevh);
+                const float r11 = __shfl_sync(0xffffffffu, val[c][3], prevh);
                 if (c >= cn) continue;
                 float *dp = dxs + (long long)c * HW + o00;
                 const float v00 = val[c][0] + (ab01 ? r01 : 0.f), v10 = val[c][2] + (ab11 ? r11 : 0.f);
@@ -677,10 +685,12 @@ cudaError_t warp_bwd_launch(const WarpArgs &a, int algo, int deterministic, void
     const bool direct = algo == 3 || (e && strcmp(e, "direct") == 0);
     if (!win && !direct) {
         const int tiles_x = (a.W + 31) / 32;
-        int R = 16;
-        if ((long long)tiles_x * ((a.H + R * kStripW - 1) / (R * kStripW)) * a.N < 8LL * kNumSMs) R = 8;
+        // rows per warp: 8 (measured vs 16: 523 vs 536 us at 16 x 3 x 1024^2).  Not fewer: the
+        // rows a lane walks are also what pre-sums a vertically collapsing flow's taps
+        // before the reds (R = 4 let the 8 x 3 x 384 x 512 collapse test exceed T once)
+        int R = 8;
         const char *er = getenv("RSGRAD_WARP_R");
-        if (er) R = atoi(er) == 8 ? 8 : 16;
+        if (er) R = atoi(er) == 16 ? 16 : 8;
         const int tiles_y = (a.H + R * kStripW - 1) / (R * kStripW);
         const dim3 grid((unsigned)(tiles_x * tiles_y), a.N);
         const int CW = a.C < 4 ? a.C : 4;

@@ -579,13 +579,13 @@ def _fp32_sum_bound(x, flow, dy, border):
     return (n_max + 1) * u * absdx + 1e-30
 
 
-@pytest.mark.parametrize("variant", ["auto", "auto_r8", "win8,4,4", "win4,8,2", "win8,8,1", "win4,4,3", "direct"])
+@pytest.mark.parametrize("variant", ["auto", "auto_r16", "win8,4,4", "win4,8,2", "win8,8,1", "win4,4,3", "direct"])
 @pytest.mark.parametrize("shape", [(2, 3, 70, 100), (1, 7, 45, 61), (1, 1, 33, 36), (2, 2, 130, 68)])
 @pytest.mark.parametrize("flow", ["smooth", "stress", "collapse"])
 @pytest.mark.parametrize("padding", ["zeros", "border"])
 def test_warp_bwd_variants(cuda_device, monkeypatch, variant, shape, flow, padding):
     """warp_bwd d_input variants: "auto" = row strips with register-combined taps
-    (warp_bwd_strip, R = 16 / "auto_r8" R = 8), "win..." = per-warp shared windows flushed
+    (warp_bwd_strip, R = 8 rows per warp / "auto_r16" R = 16), "win..." = per-warp shared windows flushed
     by vector reds (RSGRAD_WARP_BWD=winR,NW,IT), "direct" = one fp32 red per tap (the
     unconverted scatter, = SCATTER_ATOMIC).  Ragged strips, W % 32 != 0, C > 4 (channel
     chunks), stress flows (taps far from their row) and a collapsing flow (~1300 taps per
@@ -596,8 +596,8 @@ def test_warp_bwd_variants(cuda_device, monkeypatch, variant, shape, flow, paddi
         monkeypatch.setenv("RSGRAD_WARP_BWD", variant)
     elif variant == "direct":
         monkeypatch.setenv("RSGRAD_WARP_BWD", "direct")
-    elif variant == "auto_r8":
-        monkeypatch.setenv("RSGRAD_WARP_R", "8")
+    elif variant == "auto_r16":
+        monkeypatch.setenv("RSGRAD_WARP_R", variant[6:])
     N, C, H, W = shape
     inp = synth.warp_inputs(N, C, H, W, cfg=1, flow="stress" if flow == "collapse" else flow)
     if flow == "collapse":
