@@ -145,17 +145,11 @@ RS_DEV void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// ----------------------------------------------------------------- TMA bulk copies (UBLKCP) + mbarrier
+// ----------------------------------------------------------------- mbarrier (cp.async completion)
 RS_DEV void mbar_init(unsigned long long *bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
 RS_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-// order this thread's earlier generic shared accesses before later async-proxy writes
-RS_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-RS_DEV void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
 // arrive on `bar` once all of this thread's earlier cp.async copies have landed
 // (.noinc: the arrival counts against the count the barrier was initialised with)
 RS_DEV void cp_async_arrive(unsigned long long *bar) {
@@ -163,13 +157,6 @@ RS_DEV void cp_async_arrive(unsigned long long *bar) {
 }
 RS_DEV void mbar_arrive(unsigned long long *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-RS_DEV void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
 }
 RS_DEV bool mbar_try_wait(unsigned long long *bar, unsigned parity) {
     unsigned ok;
@@ -198,21 +185,6 @@ RS_DEV void mbar_wait(unsigned long long *bar, unsigned parity) {
 // 16-B cp.async to a shared-window address (no generic->shared conversion per copy)
 RS_DEV void cp_async16_s(unsigned s, const void *g) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(g) : "memory");
-}
-
-// One bulk copy per (channel, row) segment (16-B aligned rows, widths multiple of
-// 16 B).  The caller's thread 0 arms `bar` with mbar_expect_tx(nch * sum(cnt) * 4).
-RS_DEV void stage_rows_bulk(float *dst, int F, const float *base, long long cstride, int nch, int R, int W,
-                            int ybase, const int *xa, const int *off, const int *cnt,
-                            unsigned long long *bar) {
-    fence_proxy_async();
-    for (int p = threadIdx.x; p < nch * R; p += blockDim.x) {
-        const int c = p / R, r = p - c * R;
-        const int w = cnt[r];
-        if (w > 0)
-            bulk_g2s(dst + c * F + off[r], base + c * cstride + (long long)(ybase + r) * W + xa[r],
-                     (unsigned)w * 4u, bar);
-    }
 }
 
 // Compact row layout of a staged footprint: row r holds columns [xa[r], xa[r]+cnt[r])

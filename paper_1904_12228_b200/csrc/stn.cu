@@ -140,10 +140,12 @@ RS_DEV bool stn_gatherable(const Affine &A, int Ho, int Wo) {
 // ----------------------------------------------------------------- output-tile kernel
 // MODE_FWD: y.  MODE_DTHETA: per-tile fp64 partials of d_theta (6 per tile).
 // fb_list (optional): loop over the listed samples instead of blockIdx.y.
-// FAST (x rows 16-B aligned, affine, no fb_list): TMA bulk row copies completing on
-// mbarriers, a compile-time channel-slice stride (immediate smem offsets) with a zero
+// FAST (x rows 16-B aligned, affine, no fb_list): 16-B cp.async row copies completing on
+// per-stage mbarriers, a compile-time channel-slice stride (immediate smem offsets) with a zero
 // slot per slice so every tap is an unpredicated shared load, and for d_theta four
-// per-tap accumulators sum_c dY*V (4 FMAs per channel) combined once at the end.
+// per-tap accumulators sum_c dY*V (4 FMAs per channel) combined once at the end; with
+// ctr (FAST d_theta of every sample) the last tile block of a sample also sums the
+// sample's tile partials in tile order into d_theta (no separate finalize launch).
 // stage ring: 2 stages of 7168 floats (measured vs 3 x 5120: forward 0.590 vs 0.596 ms,
 // backward 1.744 vs 1.774 ms at 16 x 16 x 1024^2; 2 x 9216 drops to 2 blocks per SM)
 #ifndef RS_NS
@@ -1084,10 +1086,6 @@ RS_DEV bool stn_lean_ok(const Affine &A, int Ho, int Wo) {
     return rq <= kLRQMax && fq <= kLFQMax && (wj + 2.0) * (wi + 2.0) <= 16.0;
 }
 
-#ifndef RS_LEAN_CPA
-#define RS_LEAN_CPA 1
-#endif
-constexpr bool kLeanCpa = RS_LEAN_CPA;  // dY rows by cp.async (else TMA bulk copies)
 
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads, 2)
@@ -1105,7 +1103,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     int *ctl = qcnt + kLRQMax;                                  // 8
     unsigned short *hlist = (unsigned short *)(ctl + 8);        // [warp][row][hit][lane]
     unsigned char *hcnt = (unsigned char *)(hlist + 8 * (kLRows + 1) * kLHits * 32);
-    __shared__ unsigned long long bars[2];  // TMA bulk-copy completion, one per stage
+    __shared__ unsigned long long bars[2];  // stage completion (cp.async.mbarrier.arrive), one per stage
 
     const int n = blockIdx.y;
     const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
@@ -1159,8 +1157,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         qhi[r] = min(a.Wo - 1, (int)floor(fmin(jh, 1e9)));
     }
     if (threadIdx.x == 0) {
-        mbar_init(&bars[0], kLeanCpa ? kThreads : 1);
-        mbar_init(&bars[1], kLeanCpa ? kThreads : 1);
+        mbar_init(&bars[0], kThreads);
+        mbar_init(&bars[1], kThreads);
         fence_mbar_init();
     }
     __syncthreads();
@@ -1191,16 +1189,11 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int nch = (a.C + CH - 1) / CH;
     const float *gbase = a.dy + (long long)n * a.C * P;
     __syncthreads();
-    const int Fc = ctl[1];  // floats copied per channel
-    // VEC: one TMA bulk copy per (channel, row) segment; else 4-B LDGSTS
+    // VEC: 16-B cp.async rows completing on the stage's mbarrier; else 4-B cp.async
     auto issue = [&](float *dst, int c0s, int ncp, int slot) {
-        if (VEC && kLeanCpa) {  // 16-B cp.async, completion tracked on the stage's mbarrier
+        if (VEC) {
             if (FQ > 0) stage_rows<true>(dst, FQ, gbase + (long long)c0s * P, P, ncp, RQ, a.Wo, ilo, qxa, qoff, qcnt);
             cp_async_arrive(&bars[slot]);
-        } else if (VEC) {
-            if (threadIdx.x == 0) mbar_expect_tx(&bars[slot], (unsigned)(ncp * Fc) * 4u);
-            if (FQ > 0) stage_rows_bulk(dst, FQ, gbase + (long long)c0s * P, P, ncp, RQ, a.Wo, ilo, qxa, qoff, qcnt,
-                                        &bars[slot]);
         } else {
             if (FQ > 0) stage_rows<VEC>(dst, FQ, gbase + (long long)c0s * P, P, ncp, RQ, a.Wo, ilo, qxa, qoff, qcnt);
             cp_async_commit();
@@ -1299,7 +1292,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (kLBufs == 2 && kc + 1 < nch) cp_async_wait<1>();
             else cp_async_wait<0>();
         }
-        if (!VEC || !kLeanCpa) __syncthreads();
+        if (!VEC) __syncthreads();
         const float *S = stage + (kc % kLBufs) * kLStage;
         switch (cn) {
             case 8: run_chunk(S, c0, std::integral_constant<int, 8>{}); break;
