@@ -453,6 +453,58 @@ def cpu_baseline(s, w, b, budget_s=12.0):
                       f"bslice 16x16x8), fp64 C oracle, OpenMP; host os.cpu_count()={os.cpu_count()}"}
 
 
+def cpu_configs(budget_1t_s=20.0):
+    """the oracle (fp64 fwd + naive scatter adjoint) on the full
+    configs[0..3] (K1 STN 1x3x16^2, K2 STN 4x16x512^2, K3 warp 8x3x384x512, K4 bslice
+    4x1024^2 16x16x8), once with all host threads and once with 1 thread (the 1-thread
+    run stops after the budget; configs not reached are reported as skipped)."""
+    import oracle
+    import synth
+
+    cases = [
+        ("K1_stn_1x3x16x16", 1 * 16 * 16, lambda: synth.stn_inputs(1, 3, 16, 16, cfg=1), "stn"),
+        ("K2_stn_4x16x512x512", 4 * 512 * 512, lambda: synth.stn_inputs(4, 16, 512, 512, cfg=2), "stn"),
+        ("K3_warp_8x3x384x512", 8 * 384 * 512, lambda: synth.warp_inputs(8, 3, 384, 512, cfg=3), "warp"),
+        ("K4_bslice_4x1024x1024_g16x16x8", 4 * 1024 * 1024,
+         lambda: synth.bslice_inputs(4, 1024, 1024, 8, 16, 16, cfg=4), "bslice"),
+    ]
+
+    def run(layer, d):
+        if layer == "stn":
+            oracle.stn_fwd(d["x"], d["theta"])
+            oracle.stn_bwd(d["x"], d["theta"], d["dy"])
+        elif layer == "warp":
+            oracle.warp_fwd(d["x"], d["flow"])
+            oracle.warp_bwd(d["x"], d["flow"], d["dy"])
+        else:
+            oracle.bslice_fwd(d["grid"], d["guide"], d["x"])
+            oracle.bslice_bwd(d["grid"], d["guide"], d["x"], d["dy"])
+
+    nthr = oracle.get_threads()
+    out = {"threads_all": nthr, "host_cpu_count": os.cpu_count(), "cases": {}}
+    spent_1t = 0.0
+    for name, P, make, layer in cases:
+        d = {k: v.double().numpy() for k, v in make().items()}
+        t0 = time.perf_counter()
+        run(layer, d)
+        ta = time.perf_counter() - t0
+        r = {"fwd_bwd_s_all_threads": round(ta, 4), "mpix_s_all_threads": round(P / ta / 1e6, 3)}
+        if spent_1t < budget_1t_s:
+            oracle.set_threads(1)
+            try:
+                t0 = time.perf_counter()
+                run(layer, d)
+                t1 = time.perf_counter() - t0
+            finally:
+                oracle.set_threads(nthr)
+            spent_1t += t1
+            r.update({"fwd_bwd_s_1_thread": round(t1, 4), "mpix_s_1_thread": round(P / t1 / 1e6, 3)})
+        else:
+            r["1_thread"] = "skipped (1-thread budget spent)"
+        out["cases"][name] = r
+    return out
+
+
 # --------------------------------------------------------------------------- reference arm
 def run_reference(args, world, rank):
     if rank != 0:
@@ -660,6 +712,7 @@ def main():
         line["per_rank_shards"] = [list(shard(world, r)) for r in range(world)]
     if world == 1 and not args.no_cpu and not args.dry_run:
         line["cpu_baseline"] = cpu_baseline(s, w, b)
+        line["cpu_baseline"]["configs"] = cpu_configs()
     if world == 1 and not args.no_paper_shapes and not args.dry_run:
         line["paper_shapes"] = paper_shapes(rs, peak)
     if world == 1 and not args.no_next and not args.dry_run:
