@@ -59,8 +59,8 @@
  *             the fixed-point integer scatter: each term w*g rounded once to a 64-bit
  *             integer at a per-sample scale 2^S (S from max|dy|), summed with integer
  *             atomics (order-free), converted once (absolute error <= n 2^-(S+1) for
- *             n terms, n*max|dy|*P*2^-62).  SCATTER_ATOMIC / SCATTER_PRIV with
- *             deterministic=1 => RS_ERR_FLAG; stn3d / lanczos (atomics only) likewise.
+ *             n terms, n*max|dy|*P*2^-62), also for the stn3d / Lanczos adjoints.
+ *             SCATTER_ATOMIC / SCATTER_PRIV with deterministic=1 => RS_ERR_FLAG.
  */
 #ifndef RSGRAD_H
 #define RSGRAD_H
@@ -240,7 +240,8 @@ rs_status upsample4_bwd(const float *dy, int N, int C, int H, int W, float *dx, 
  *                    falls back to reds for that sample, to the fixed-point scatter
  *                    with deterministic=1); AUTO / SCATTER_ATOMIC: memset +
  *                    red.global.add per tap in the d_theta pass (measured faster).
- *   stn3d_bwd        the atomic scatter only (GATHER / deterministic=1 => RS_ERR_FLAG).
+ *   stn3d_bwd        the atomic scatter (GATHER => RS_ERR_FLAG); deterministic=1: the
+ *                    fixed-point scatter (bitwise reproducible).
  * SCATTER_PRIV => RS_ERR_FLAG.
  *   stn_bicubic_*  theta N x 2 x 3, x N x C x H x W, y N x C x Ho x Wo: Keys' cubic
  *                  convolution (A = -0.75) over the 4 x 4 taps floor(i)-1 .. floor(i)+2
@@ -255,8 +256,8 @@ rs_status stn_bicubic_bwd(const float *x, const float *theta, const float *dy, i
                           void *workspace, size_t ws_bytes, rs_stream_t stream);
 /*   stn_lanczos_*  as stn_bicubic_* with 6 x 6 taps floor(i)-2 .. floor(i)+3 and the
  *                  Lanczos-3 kernel L(x) = sinc(x) sinc(x/3), |x| < 3 (R13);
- *                  d_input by the atomic scatter only (GATHER / deterministic=1 =>
- *                  RS_ERR_FLAG); workspace layer 7 (N, Ho, Wo). */
+ *                  d_input by the atomic scatter (GATHER => RS_ERR_FLAG), with
+ *                  deterministic=1 the fixed-point scatter; workspace layer 7. */
 rs_status stn_lanczos_fwd(const float *x, const float *theta, int N, int C, int H, int W, int Ho,
                           int Wo, const rs_opts *opts, float *y, rs_stream_t stream);
 rs_status stn_lanczos_bwd(const float *x, const float *theta, const float *dy, int N, int C, int H,
@@ -272,10 +273,11 @@ rs_status stn3d_bwd(const float *x, const float *theta, const float *dy, int N, 
  * N,C,H,W,Ho,Wo), 1 = warp (N,C,H,W), 2 = bslice (N,H,W,D,Gh,Gw), 3 = conv
  * (N, C = Ci, H, W, D = Co, Gh = kh, Gw = kw), 4 = convloss_grad (N, H, W: the
  * RS_SCHED_ROOT residual), 5 = stn_bicubic (N, Ho, Wo: d_theta partials, coordinate
- * tables, N fallback flags), 6 = stn3d (N, Ho, Wo, D = Do), 7 = stn_lanczos (N, Ho, Wo);
+ * tables, N fallback flags), 6 = stn3d (N, Ho, Wo, D = Do; with deterministic=1 also C, H, W
+ * and Gh = depth of the input volume), 7 = stn_lanczos (N, Ho, Wo; deterministic=1: C, H, W);
  * unused arguments are ignored.
  * opts->deterministic = 1 adds the fixed-point accumulators of one sample
- * (8 * C * H * W bytes) for layers 0, 1 and 5.  Returns 0 for an unknown layer. */
+ * (8 * C * H * W bytes) for layers 0, 1, 5, 6 and 7.  Returns 0 for an unknown layer. */
 size_t rsgrad_bwd_workspace_bytes(int layer, int N, int C, int H, int W, int Ho, int Wo, int D,
                                   int Gh, int Gw, const rs_opts *opts);
 

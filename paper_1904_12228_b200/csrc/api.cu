@@ -311,12 +311,14 @@ size_t rsgrad_bwd_workspace_bytes(int layer, int N, int C, int H, int W, int Ho,
             if (!pos(N) || !pos(Ho) || !pos(Wo)) return 0;
             if (!pos(C) || !pos(H) || !pos(W)) return 0;
             return rs::stn_bicubic_ws_bytes(N, C, H, W, Ho, Wo, det);
-        case 6:
+        case 6:  // stn3d: (N, C, H, W) of the input volume with Gh = its depth; (Ho, Wo, D = Do) of the output
             if (!pos(N) || !pos(Ho) || !pos(Wo) || !pos(D)) return 0;
-            return rs::stn_var_ws_bytes(N, D * Ho * Wo, 12);
+            if (det && (!pos(C) || !pos(H) || !pos(W) || !pos(Gh))) return 0;
+            return rs::stn3d_ws_bytes(N, C, det ? Gh : 1, H, W, D, Ho, Wo, det);
         case 7:
             if (!pos(N) || !pos(Ho) || !pos(Wo)) return 0;
-            return rs::stn_var_ws_bytes(N, Ho * Wo, 6);
+            if (det && (!pos(C) || !pos(H) || !pos(W))) return 0;
+            return rs::stn_lanczos_ws_bytes(N, C, H, W, Ho, Wo, det);
         default:
             return 0;
     }
@@ -665,8 +667,8 @@ static rs_status var_check(const rs_opts &o, bool bwd, bool has_dx, std::initial
     if (o.padding != RS_PAD_ZEROS) return fail(RS_ERR_FLAG, "stn variants: zeros padding only");
     if (bwd && has_dx && o.algo == RS_ALGO_SCATTER_PRIV)
         return fail(RS_ERR_FLAG, "stn variants: SCATTER_PRIV is not implemented");
-    if (bwd && has_dx && !has_gather && (o.algo == RS_ALGO_GATHER || o.deterministic))
-        return fail(RS_ERR_FLAG, "stn3d / lanczos: d_input is the atomic scatter only (not deterministic)");
+    if (bwd && has_dx && !has_gather && o.algo == RS_ALGO_GATHER)
+        return fail(RS_ERR_FLAG, "stn3d / lanczos: no gather form of d_input (scatter only)");
     if (bwd && has_dx && o.algo == RS_ALGO_SCATTER_ATOMIC && o.deterministic)
         return fail(RS_ERR_FLAG, "stn variants: the atomic scatter is not deterministic");
     for (const void *p : ptrs)
@@ -747,7 +749,7 @@ rs_status stn3d_fwd(const float *x, const float *theta, int N, int C, int D, int
     if (!y) return fail(RS_ERR_NULL, "stn3d_fwd: y is required");
     if ((st = var_check(o, false, false, {x, theta, y})) != RS_OK) return st;
     return launched(rs::stn3d_launch(x, theta, nullptr, y, nullptr, nullptr, N, C, D, H, W, Do, Ho, Wo,
-                                     o.align_corners, false, nullptr, (cudaStream_t)stream),
+                                     o.align_corners, false, false, nullptr, (cudaStream_t)stream),
                     "stn3d_fwd");
 }
 
@@ -762,10 +764,11 @@ rs_status stn3d_bwd(const float *x, const float *theta, const float *dy, int N, 
     if ((st = var_check(o, true, dx != nullptr, {x, theta, dy, dx, dtheta})) != RS_OK) return st;
     if (!dx && !dtheta) return ok();
     cudaStream_t s = (cudaStream_t)stream;
-    return with_ws(dtheta ? rs::stn_var_ws_bytes(N, Do * Ho * Wo, 12) : 0, workspace, ws_bytes, s,
+    const bool det = o.deterministic && dx;
+    return with_ws(rs::stn3d_ws_bytes(N, C, D, H, W, Do, Ho, Wo, det), workspace, ws_bytes, s,
                    [&](void *ws) {
                        return rs::stn3d_launch(x, theta, dy, nullptr, dx, dtheta, N, C, D, H, W, Do, Ho, Wo,
-                                               o.align_corners, true, ws, s);
+                                               o.align_corners, true, det, ws, s);
                    },
                    "stn3d_bwd");
 }
@@ -781,7 +784,7 @@ rs_status stn_lanczos_fwd(const float *x, const float *theta, int N, int C, int 
     rs::StnArgs a{};
     a.x = x; a.theta = theta; a.y = y;
     a.N = N; a.C = C; a.H = H; a.W = W; a.Ho = Ho; a.Wo = Wo; a.ac = o.align_corners;
-    return launched(rs::stn_lanczos_launch(a, false, nullptr, (cudaStream_t)stream), "stn_lanczos_fwd");
+    return launched(rs::stn_lanczos_launch(a, false, false, nullptr, (cudaStream_t)stream), "stn_lanczos_fwd");
 }
 
 rs_status stn_lanczos_bwd(const float *x, const float *theta, const float *dy, int N, int C, int H, int W, int Ho,
@@ -798,8 +801,9 @@ rs_status stn_lanczos_bwd(const float *x, const float *theta, const float *dy, i
     a.x = x; a.theta = theta; a.dy = dy; a.dx = dx; a.dtheta = dtheta;
     a.N = N; a.C = C; a.H = H; a.W = W; a.Ho = Ho; a.Wo = Wo; a.ac = o.align_corners;
     cudaStream_t s = (cudaStream_t)stream;
-    return with_ws(dtheta ? rs::stn_var_ws_bytes(N, Ho * Wo, 6) : 0, workspace, ws_bytes, s,
-                   [&](void *ws) { return rs::stn_lanczos_launch(a, true, ws, s); }, "stn_lanczos_bwd");
+    const bool det = o.deterministic && dx;
+    return with_ws(rs::stn_lanczos_ws_bytes(N, C, H, W, Ho, Wo, det), workspace, ws_bytes, s,
+                   [&](void *ws) { return rs::stn_lanczos_launch(a, true, det, ws, s); }, "stn_lanczos_bwd");
 }
 
 }  // extern "C"

@@ -314,8 +314,10 @@ cudaError_t upsample4_launch(const float *src, float *dst, int N, int C, int H, 
 size_t stn_var_ws_bytes(int N, int P, int ne);
 size_t stn_bicubic_ws_bytes(int N, int C, int H, int W, int Ho, int Wo, bool det);
 cudaError_t stn_bicubic_launch(const StnArgs &a, bool bwd, int algo, bool det, void *ws, cudaStream_t s);
-cudaError_t stn_lanczos_launch(const StnArgs &a, bool bwd, void *ws, cudaStream_t s);
+cudaError_t stn_lanczos_launch(const StnArgs &a, bool bwd, bool det, void *ws, cudaStream_t s);
 cudaError_t stn3d_launch(const float *x, const float *theta, const float *dy, float *y, float *dx, float *dtheta,
-                         int N, int C, int D, int H, int W, int Do, int Ho, int Wo, int ac, bool bwd, void *ws,
-                         cudaStream_t s);
+                         int N, int C, int D, int H, int W, int Do, int Ho, int Wo, int ac, bool bwd, bool det,
+                         void *ws, cudaStream_t s);
+size_t stn_lanczos_ws_bytes(int N, int C, int H, int W, int Ho, int Wo, bool det);
+size_t stn3d_ws_bytes(int N, int C, int D, int H, int W, int Do, int Ho, int Wo, bool det);
 }  // namespace rs

@@ -600,6 +600,56 @@ struct BicubicTapSampler {
     }
 };
 
+// Lanczos-3 taps for the fixed-point scatter: the 36 in-image taps of lanczos_bwd with its
+// fp32 weights wy * wx (|L| <= 1, so |w| <= 1 per tap and per element sum_q |w| <= P).
+struct LanczosTapSampler {
+    const float *theta;
+    int H, W, Ho, Wo, ac;
+    static constexpr int kMaxTaps = 36;
+    static constexpr double kWmax = 1.0;
+    RS_DEV int taps(int n, long long q, long long *off, float *w) const {
+        const int i = (int)(q / Wo), j = (int)(q - (long long)i * Wo);
+        const Lz b = lanczos_at(theta, n, i, j, H, W, Ho, Wo, ac);
+        int k = 0;
+#pragma unroll
+        for (int u = 0; u < 6; u++) {
+            const int yy = b.y0 - 2 + u;
+#pragma unroll
+            for (int v = 0; v < 6; v++) {
+                const int xx = b.x0 - 2 + v;
+                if (yy >= 0 && yy < H && xx >= 0 && xx < W) {
+                    off[k] = (long long)yy * W + xx;
+                    w[k++] = b.wy[u] * b.wx[v];
+                }
+            }
+        }
+        return k;
+    }
+};
+
+// Trilinear 3-D taps for the fixed-point scatter: the 8 in-volume taps of stn3d_bwd_k.
+struct Vol3dTapSampler {
+    Vol a;
+    static constexpr int kMaxTaps = 8;
+    static constexpr double kWmax = 1.0;
+    RS_DEV int taps(int n, long long q, long long *off, float *w) const {
+        const int k0 = (int)(q / ((long long)a.Ho * a.Wo));
+        const int rem = (int)(q - (long long)k0 * a.Ho * a.Wo), i = rem / a.Wo, j = rem - i * a.Wo;
+        const Tri r = tri_at(a, n, k0, i, j);
+        int k = 0;
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+            const int ax = e & 1, by = (e >> 1) & 1, dz = e >> 2;
+            const int xx = r.x0 + ax, yy = r.y0 + by, zz = r.z0 + dz;
+            if (xx >= 0 && xx < a.W && yy >= 0 && yy < a.H && zz >= 0 && zz < a.D) {
+                off[k] = ((long long)zz * a.H + yy) * a.W + xx;
+                w[k++] = (ax ? r.f[0] : 1.f - r.f[0]) * (by ? r.f[1] : 1.f - r.f[1]) * (dz ? r.f[2] : 1.f - r.f[2]);
+            }
+        }
+        return k;
+    }
+};
+
 }  // namespace
 
 size_t stn_var_ws_bytes(int N, int P, int ne) {
@@ -668,13 +718,32 @@ cudaError_t stn_bicubic_launch(const StnArgs &a, bool bwd, int algo, bool det, v
     return cudaGetLastError();
 }
 
-cudaError_t stn_lanczos_launch(const StnArgs &a, bool bwd, void *ws, cudaStream_t s) {
+size_t stn_lanczos_ws_bytes(int N, int C, int H, int W, int Ho, int Wo, bool det) {
+    return det_align(stn_var_ws_bytes(N, Ho * Wo, 6)) + (det ? det_ws_bytes(N, (long long)C * H * W) : 0);
+}
+
+size_t stn3d_ws_bytes(int N, int C, int D, int H, int W, int Do, int Ho, int Wo, bool det) {
+    return det_align(stn_var_ws_bytes(N, Do * Ho * Wo, 12)) + (det ? det_ws_bytes(N, (long long)C * D * H * W) : 0);
+}
+
+cudaError_t stn_lanczos_launch(const StnArgs &a, bool bwd, bool det, void *ws, cudaStream_t s) {
     const int P = a.Ho * a.Wo;
     const dim3 grid((P + kVT - 1) / kVT, a.N);
     if (!bwd) {
         lanczos_fwd<<<grid, kVT, 0, s>>>(a);
         note_launch();
         return cudaGetLastError();
+    }
+    if (det && a.dx) {  // deterministic=1: d_theta pass alone, then the fixed-point scatter
+        if (a.dtheta) {
+            StnArgs b = a;
+            b.dx = nullptr;
+            cudaError_t e = stn_lanczos_launch(b, true, false, ws, s);
+            if (e != cudaSuccess) return e;
+        }
+        const LanczosTapSampler smp{a.theta, a.H, a.W, a.Ho, a.Wo, a.ac};
+        return det_scatter_launch(smp, a.dy, a.dx, a.N, a.C, (long long)a.H * a.W, (long long)P, nullptr, nullptr,
+                                  nullptr, (char *)ws + det_align(stn_var_ws_bytes(a.N, P, 6)), s);
     }
     if (a.dx) {
         cudaError_t e = cudaMemsetAsync(a.dx, 0, sizeof(float) * (size_t)a.N * a.C * a.H * a.W, s);
@@ -690,8 +759,8 @@ cudaError_t stn_lanczos_launch(const StnArgs &a, bool bwd, void *ws, cudaStream_
 }
 
 cudaError_t stn3d_launch(const float *x, const float *theta, const float *dy, float *y, float *dx, float *dtheta,
-                         int N, int C, int D, int H, int W, int Do, int Ho, int Wo, int ac, bool bwd, void *ws,
-                         cudaStream_t s) {
+                         int N, int C, int D, int H, int W, int Do, int Ho, int Wo, int ac, bool bwd, bool det,
+                         void *ws, cudaStream_t s) {
     Vol a{N, C, D, H, W, Do, Ho, Wo, ac, x, theta, dy, y, dx, dtheta};
     const int P = Do * Ho * Wo;
     const dim3 grid((P + kVT - 1) / kVT, N);
@@ -699,6 +768,16 @@ cudaError_t stn3d_launch(const float *x, const float *theta, const float *dy, fl
         stn3d_fwd_k<<<grid, kVT, 0, s>>>(a);
         note_launch();
         return cudaGetLastError();
+    }
+    if (det && dx) {  // deterministic=1: d_theta pass alone, then the fixed-point scatter
+        if (dtheta) {
+            cudaError_t e = stn3d_launch(x, theta, dy, y, nullptr, dtheta, N, C, D, H, W, Do, Ho, Wo, ac, true, false,
+                                         ws, s);
+            if (e != cudaSuccess) return e;
+        }
+        const Vol3dTapSampler smp{a};
+        return det_scatter_launch(smp, dy, dx, N, C, (long long)D * H * W, (long long)P, nullptr, nullptr, nullptr,
+                                  (char *)ws + det_align(stn_var_ws_bytes(N, P, 12)), s);
     }
     if (dx) {
         cudaError_t e = cudaMemsetAsync(dx, 0, sizeof(float) * (size_t)N * C * D * H * W, s);

@@ -423,7 +423,7 @@ def stn3d_fwd(x, theta, out_size=None, *, align_corners=True, out=None):
     return y
 
 
-def stn3d_bwd(x, theta, dy, *, align_corners=True, need_dx=True, need_dtheta=True, out=None):
+def stn3d_bwd(x, theta, dy, *, align_corners=True, deterministic=False, need_dx=True, need_dtheta=True, out=None):
     N, C, D, H, W = x.shape
     Do, Ho, Wo = dy.shape[2:]
     if out is not None:
@@ -431,7 +431,7 @@ def stn3d_bwd(x, theta, dy, *, align_corners=True, need_dx=True, need_dtheta=Tru
     else:
         dx = torch.empty_like(x) if need_dx else None
         dth = torch.empty((N, 3, 4), dtype=torch.float32, device=x.device) if need_dtheta else None
-    o = _opts(align_corners, "zeros", "scatter_atomic")
+    o = _opts(align_corners, "zeros", "auto" if deterministic else "scatter_atomic", deterministic)
     _check(lib().stn3d_bwd(_ptr(x), _ptr(theta), _ptr(dy), N, C, D, H, W, Do, Ho, Wo, ctypes.byref(o), _ptr(dx),
                            _ptr(dth), None, 0, _stream(_device_of(x, dy))), "stn3d_bwd")
     return dx, dth
@@ -449,7 +449,8 @@ def stn_lanczos_fwd(x, theta, Ho=None, Wo=None, *, align_corners=True, out=None)
     return y
 
 
-def stn_lanczos_bwd(x, theta, dy, *, align_corners=True, need_dx=True, need_dtheta=True, out=None):
+def stn_lanczos_bwd(x, theta, dy, *, align_corners=True, deterministic=False, need_dx=True, need_dtheta=True,
+                    out=None):
     N, C, H, W = x.shape
     Ho, Wo = dy.shape[2:]
     if out is not None:
@@ -457,7 +458,7 @@ def stn_lanczos_bwd(x, theta, dy, *, align_corners=True, need_dx=True, need_dthe
     else:
         dx = torch.empty_like(x) if need_dx else None
         dth = torch.empty((N, 2, 3), dtype=torch.float32, device=x.device) if need_dtheta else None
-    o = _opts(align_corners, "zeros", "scatter_atomic")
+    o = _opts(align_corners, "zeros", "auto" if deterministic else "scatter_atomic", deterministic)
     _check(lib().stn_lanczos_bwd(_ptr(x), _ptr(theta), _ptr(dy), N, C, H, W, Ho, Wo, ctypes.byref(o), _ptr(dx),
                                  _ptr(dth), None, 0, _stream(_device_of(x, dy))), "stn_lanczos_bwd")
     return dx, dth

@@ -24,6 +24,7 @@ for shape in [(2, 5, 37, 53, 41, 29), (1, 16, 96, 128, 96, 128), (2, 4, 512, 512
     rs.stn_bicubic_fwd(s["x"], s["theta"], Ho, Wo)
     rs.stn_bicubic_bwd(s["x"], th, s["dy"], deterministic=True)
     rs.stn_lanczos_bwd(s["x"], s["theta"], s["dy"])
+    rs.stn_lanczos_bwd(s["x"], s["theta"], s["dy"], deterministic=True)
     rs.stn_lanczos_fwd(s["x"], s["theta"], Ho, Wo)
     for algo in ("auto", "gather"):
         rs.stn_bicubic_bwd(s["x"], s["theta"], s["dy"], algo=algo)
@@ -61,5 +62,6 @@ rs.upsample4_bwd(rs.upsample4_fwd(u))
 x3 = torch.randn(1, 2, 9, 11, 13, device=dev)
 t3 = torch.eye(3, 4, device=dev)[None] + 0.05 * torch.randn(1, 3, 4, device=dev)
 rs.stn3d_bwd(x3, t3, rs.stn3d_fwd(x3, t3))
+rs.stn3d_bwd(x3, t3, rs.stn3d_fwd(x3, t3), deterministic=True)
 torch.cuda.synchronize()
 print("sanitize_all: done")

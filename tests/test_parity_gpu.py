@@ -971,3 +971,30 @@ def test_second_device_same_thread():
     rgr, rgd, rdx = oracle.bslice_bwd(gr, gd, x, dy)
     assert_close(_np(out[0]), rgr, "grad", "dgrid on cuda:1")
     assert_close(_np(out[2]), rdx, "grad", "dx on cuda:1")
+
+
+def test_lanczos_and_3d_deterministic(cuda_device):
+    """deterministic=1 for the atomics-only STN variants: d_theta pass alone,
+    then the fixed-point integer scatter -- bitwise equal reruns, within T of the oracle."""
+    g = torch.Generator().manual_seed(61)
+    N, C, H, W = 2, 3, 30, 34
+    x = torch.randn(N, C, H, W, generator=g, dtype=torch.float64).float()
+    dy = torch.randn(N, C, H, W, generator=g, dtype=torch.float64).float()
+    th = _var_theta(N, 2, 62)
+    xs, ts, ds = (t.to(cuda_device) for t in (x, th, dy))
+    a = rsgrad.stn_lanczos_bwd(xs, ts, ds, deterministic=True)
+    b = rsgrad.stn_lanczos_bwd(xs, ts, ds, deterministic=True)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+    rdx, rdth = oracle.stn_lanczos_bwd(x.double().numpy(), th.double().numpy(), dy.double().numpy())
+    assert_close(_np(a[0]), rdx, "grad", "lanczos dx")
+    assert_close(_np(a[1]), rdth, "grad", "lanczos dtheta")
+    x3 = torch.randn(1, 2, 9, 11, 13, generator=g, dtype=torch.float64).float()
+    d3 = torch.randn(1, 2, 8, 12, 10, generator=g, dtype=torch.float64).float()
+    t3 = _var_theta(1, 3, 63)
+    x3s, d3s, t3s = (t.to(cuda_device) for t in (x3, d3, t3))
+    a3 = rsgrad.stn3d_bwd(x3s, t3s, d3s, deterministic=True)
+    b3 = rsgrad.stn3d_bwd(x3s, t3s, d3s, deterministic=True)
+    assert torch.equal(a3[0], b3[0]) and torch.equal(a3[1], b3[1])
+    r3dx, r3dth = oracle.stn3d_bwd(x3.double().numpy(), t3.double().numpy(), d3.double().numpy())
+    assert_close(_np(a3[0]), r3dx, "grad", "3d dx")
+    assert_close(_np(a3[1]), r3dth, "grad", "3d dtheta")
