@@ -148,6 +148,11 @@ RS_DEV bool stn_gatherable(const Affine &A, int Ho, int Wo) {
 // sample's tile partials in tile order into d_theta (no separate finalize launch).
 // stage ring: 2 stages of 7168 floats (measured vs 3 x 5120: forward 0.590 vs 0.596 ms,
 // backward 1.744 vs 1.774 ms at 16 x 16 x 1024^2; 2 x 9216 drops to 2 blocks per SM)
+// d_theta finalize in the last FAST tile block of each sample (1) or a separate launch (0:
+// measured 6.96 vs 7.04 ms at 64 x 16 x 1024^2, equal at configs[1]: the per-block fence)
+#ifndef RS_DTH_LASTBLOCK
+#define RS_DTH_LASTBLOCK 0
+#endif
 #ifndef RS_NS
 #define RS_NS 2
 #endif
@@ -676,7 +681,7 @@ __global__ void __launch_bounds__(FAST ? kOTFast : kThreads, FAST ? kOTFastMinB 
                 // (the fixed order of stn_dtheta_finalize: bitwise the same result) and
                 // writes d_theta -- one launch less per call
                 __shared__ int last;
-                __threadfence();
+                if (threadIdx.x < 6) __threadfence();  // the partial writers publish
                 __syncthreads();
                 if (threadIdx.x == 0) last = atomicAdd(ctr + n, 1) == (int)gridDim.x - 1;
                 __syncthreads();
@@ -1994,7 +1999,8 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
             auto k = stn_out_tile<MODE_DTHETA, true, false, kFIdf, true>;
             set_smem(k, sm);
             grid.x = g.fj * fi_df;
-            k<<<grid, kOTFast, sm, s>>>(a, w.xtab, w.ytab, nullptr, w.fb_count, w.pf, g.fj, fi_df, w.ctr);
+            k<<<grid, kOTFast, sm, s>>>(a, w.xtab, w.ytab, nullptr, w.fb_count, w.pf, g.fj, fi_df,
+                                        RS_DTH_LASTBLOCK ? w.ctr : nullptr);
         } else if (priv && !dth_all) {  // fallback samples: d_theta and privatised d_input
             auto k = vin ? stn_out_tile<MODE_DTHETA, true, false, kFIdth, false, true>
                          : stn_out_tile<MODE_DTHETA, false, false, kFIdth, false, true>;
@@ -2034,8 +2040,8 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
         stn_dx_scatter<<<(unsigned)blocks, kThreads, 0, s>>>(a, w.fb_list, w.fb_count);
         note_launch();
     }
-    if (a.dtheta && !dth_fast) {  // (the FAST d_theta tiles finalize in their last block)
-        stn_dtheta_finalize<<<a.N, kThreads, 0, s>>>(w.pb, tiles_b, w.pf, g.fj * g.fi,
+    if (a.dtheta && !(dth_fast && RS_DTH_LASTBLOCK)) {  // (else the FAST tiles finalize in their last block)
+        stn_dtheta_finalize<<<a.N, kThreads, 0, s>>>(w.pb, tiles_b, w.pf, g.fj * (dth_fast ? fi_df : g.fi),
                                                       dth_all ? nullptr : w.flags, a.dtheta);
         note_launch();
     }
