@@ -410,19 +410,36 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
     }
     __syncthreads();
-    // ---- scan: bin segments padded to 32, per-(warp, bin) offsets
-    if (threadIdx.x == 0) {
+    // ---- scan: bin segments padded to kChunk, per-(warp, bin) offsets (warp 0: lane = bin,
+    // a warp-wide exclusive scan of the padded bin sizes; the same offsets as a serial
+    // bin-major / warp-minor walk)
+    if (threadIdx.x < 32) {
+        const int lane0 = threadIdx.x;
         int run = 0;
-        for (int b = 0; b < NB; b++) {
-            bstart[b] = run;
-            for (int ww = 0; ww < kWarps; ww++) {
-                const int v = cnt[ww * NB + b];
-                cnt[ww * NB + b] = run;
-                run += v;
+        for (int base = 0; base < NB; base += 32) {
+            const int b = base + lane0;
+            int tot = 0;
+            if (b < NB)
+                for (int ww = 0; ww < kWarps; ww++) tot += cnt[ww * NB + b];
+            const int padded = (tot + kChunk - 1) & ~(kChunk - 1);
+            int v = padded;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t2 = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane0 >= o) v += t2;
             }
-            run = (run + kChunk - 1) & ~(kChunk - 1);
+            if (b < NB) {
+                int off = run + v - padded;
+                bstart[b] = off;
+                for (int ww = 0; ww < kWarps; ww++) {
+                    const int c2 = cnt[ww * NB + b];
+                    cnt[ww * NB + b] = off;
+                    off += c2;
+                }
+            }
+            run += __shfl_sync(0xffffffffu, v, 31);
         }
-        bstart[NB] = run;
+        if (lane0 == 0) bstart[NB] = run;
     }
     __syncthreads();
     const int L = bstart[NB], nchunks = L / kChunk;
