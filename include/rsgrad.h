@@ -107,7 +107,9 @@ typedef enum { RS_PAD_ZEROS = 0, RS_PAD_BORDER = 1 } rs_padding;
  *                     arbitrary flow has no bounded inverse).
  *   bslice_bwd d_grid AUTO, GATHER, SCATTER_PRIV: dual-cell register-privatised
  *                     accumulation + fixed-order partial gather (deterministic;
- *                     cells >= 8 px); SCATTER_ATOMIC: global atomics.
+ *                     cells >= 8 px; finer grids: global atomics, or with
+ *                     deterministic=1 the fixed-point scatter); SCATTER_ATOMIC:
+ *                     global atomics.
  * d_theta, d_flow, d_guide and bslice d_input are always gathers. */
 typedef enum {
     RS_ALGO_AUTO = 0,

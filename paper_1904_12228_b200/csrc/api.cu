@@ -300,7 +300,7 @@ size_t rsgrad_bwd_workspace_bytes(int layer, int N, int C, int H, int W, int Ho,
             return rs::warp_ws_bytes(N, C, H, W, det);
         case 2:
             if (!pos(N) || !pos(H) || !pos(W) || !pos(D) || !pos(Gh) || !pos(Gw)) return 0;
-            return rs::bslice_ws_bytes(N, H, W, D, Gh, Gw);
+            return rs::bslice_bwd_ws_bytes(N, H, W, D, Gh, Gw, det);
         case 3:
             if (!pos(N) || !pos(C) || !pos(H) || !pos(W) || !pos(D) || !pos(Gh) || !pos(Gw)) return 0;
             return rs::conv_ws_bytes(N, C, D, H, W, Gh, Gw);
@@ -517,9 +517,8 @@ rs_status bslice_bwd(const float *grid, const float *guide, const float *x, cons
     if (!dy) return fail(RS_ERR_NULL, "bslice_bwd: dy is required");
     if (dgrid && o.algo == RS_ALGO_SCATTER_ATOMIC && o.deterministic)
         return fail(RS_ERR_FLAG, "bslice_bwd: SCATTER_ATOMIC is not deterministic");
-    if (dgrid && o.deterministic && rs::bslice_ws_bytes(N, H, W, D, Gh, Gw) == 0)
-        return fail(RS_ERR_FLAG, "bslice_bwd: shape needs the atomic d_grid path (cells < 8 px); not deterministic");
     if (!dgrid && !dguide && !dx) return ok();
+    const bool det = o.deterministic && dgrid;
     cudaStream_t s = (cudaStream_t)stream;
     std::vector<TArg> args = {{grid, sizeof(float) * 12 * (size_t)D * Gh * Gw, true, false},
                               {guide, sizeof(float) * (size_t)H * W, true, false},
@@ -529,7 +528,7 @@ rs_status bslice_bwd(const float *grid, const float *guide, const float *x, cons
                               {dguide, sizeof(float) * (size_t)H * W, false, true},
                               {dx, sizeof(float) * 3 * (size_t)H * W, false, true}};
     return run_batched(N, args, s, workspace, ws_bytes,
-                       [&](int n) { return rs::bslice_ws_bytes(n, H, W, D, Gh, Gw); },
+                       [&](int n) { return rs::bslice_bwd_ws_bytes(n, H, W, D, Gh, Gw, det); },
                        [&](int, int nc, void **p, cudaStream_t t, void *ws) {
                            rs::BsliceArgs a{};
                            a.grid = (const float *)p[0];
@@ -541,7 +540,7 @@ rs_status bslice_bwd(const float *grid, const float *guide, const float *x, cons
                            a.dx = (float *)p[6];
                            a.N = nc; a.H = H; a.W = W; a.D = D; a.Gh = Gh; a.Gw = Gw;
                            return rs::bslice_bwd_launch(a, o.algo, o.deterministic, ws,
-                                                        rs::bslice_ws_bytes(nc, H, W, D, Gh, Gw), t);
+                                                        rs::bslice_bwd_ws_bytes(nc, H, W, D, Gh, Gw, det), t);
                        });
 }
 

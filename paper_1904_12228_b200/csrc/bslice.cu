@@ -639,6 +639,15 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ----------------------------------------------------------------- generic (any shape)
+// fixed-point exponent of sample n: |sum| <= max|G| max(1, max|X|) * (sum over pixels of
+// the trilinear weights of a node <= H W) < 2^61 2^-S (non-finite inputs: S = 0)
+RS_DEV int bslice_det_scale(const unsigned *mx, int n, long long HW) {
+    const float mg = __uint_as_float(__ldcg(mx + 2 * n)), mxv = fmaxf(1.f, __uint_as_float(__ldcg(mx + 2 * n + 1)));
+    if (!(mg > 0.f) || !isfinite(mg) || !isfinite(mxv)) return 0;
+    const double bound = (double)mg * (double)mxv * (double)HW;
+    return 61 - ilogb(bound) - 1;
+}
+
 struct Slice8 {
     int xi[2], yi[2], zi[2];
     float wx[2], wy[2], wz[2];
@@ -688,7 +697,13 @@ __global__ void __launch_bounds__(kThreads) bslice_fwd_generic(BsliceArgs a) {
         yp[oc * HW] = fmaf(A[4 * oc], X[0], fmaf(A[4 * oc + 1], X[1], fmaf(A[4 * oc + 2], X[2], A[4 * oc + 3])));
 }
 
-__global__ void __launch_bounds__(kThreads) bslice_bwd_generic(BsliceArgs a) {
+// DET (deterministic=1 on shapes without the tiled path): d_grid by the fixed-point
+// integer scatter of det.cuh, specialised here (a term is w * G_o * X~_i, 96 per pixel):
+// scale 2^S per sample from max|G| and max(1, max|X|) (bslice_absmax) and the bound
+// sum over pixels of w <= H * W, 64-bit integer atomics, one conversion pass.
+template <bool DET>
+__global__ void __launch_bounds__(kThreads)
+    bslice_bwd_generic(BsliceArgs a, unsigned long long *__restrict__ acc, const unsigned *__restrict__ mx) {
     const long long HW = (long long)a.H * a.W;
     const long long idx = (long long)blockIdx.x * kThreads + threadIdx.x;
     if (idx >= (long long)a.N * HW) return;
@@ -739,6 +754,8 @@ __global__ void __launch_bounds__(kThreads) bslice_bwd_generic(BsliceArgs a) {
     }
     if (a.dgrid) {
         float *dg = a.dgrid + (long long)n * 12 * a.D * plane;
+        int S = 0;
+        if (DET) S = bslice_det_scale(mx, n, HW);
         for (int e = 0; e < 2; e++)
             for (int b = 0; b < 2; b++)
                 for (int aa = 0; aa < 2; aa++) {
@@ -747,10 +764,58 @@ __global__ void __launch_bounds__(kThreads) bslice_bwd_generic(BsliceArgs a) {
 #pragma unroll
                     for (int oc = 0; oc < 3; oc++)
 #pragma unroll
-                        for (int i = 0; i < 4; i++)
-                            red_add(dg + (4 * oc + i) * a.D * plane + off, wt * G[oc] * Xt[i]);
+                        for (int i = 0; i < 4; i++) {
+                            const long long gi = (4 * oc + i) * a.D * plane + off;
+                            if (DET) {  // exact fp64 product, one rounding to the fixed point
+                                const double v = ldexp((double)wt * (double)G[oc] * (double)Xt[i], S);
+                                const long long iv = __double2ll_rn(v);
+                                if (iv != 0)
+                                    atomicAdd(acc + (long long)n * 12 * a.D * plane + gi, (unsigned long long)iv);
+                            } else {
+                                red_add(dg + gi, wt * G[oc] * Xt[i]);
+                            }
+                        }
                 }
     }
+}
+
+// max |G| and max |X| per sample (order-free atomicMax on the bit patterns)
+__global__ void __launch_bounds__(kThreads) bslice_absmax(BsliceArgs a, unsigned *mx) {
+    const long long HW = (long long)a.H * a.W;
+    const long long idx = (long long)blockIdx.x * kThreads + threadIdx.x;
+    const bool in = idx < (long long)a.N * HW;
+    const int n = in ? (int)(idx / HW) : 0;
+    const long long o = in ? idx - (long long)n * HW : 0;
+    unsigned mg = 0u, mxx = 0u;
+    if (in)
+        for (int i = 0; i < 3; i++) {
+            mg = max(mg, __float_as_uint(fabsf(__ldg(a.dy + ((long long)n * 3 + i) * HW + o))));
+            mxx = max(mxx, __float_as_uint(fabsf(__ldg(a.x + ((long long)n * 3 + i) * HW + o))));
+        }
+    // a warp may straddle two samples: reduce per sample index
+    const unsigned msk = __match_any_sync(0xffffffffu, in ? n : -1);
+    const int leader = __ffs(msk) - 1;
+    for (int k = 0; k < 32; k++) {  // segmented max over lanes of the same sample
+        const unsigned og = __shfl_sync(0xffffffffu, mg, k), ox = __shfl_sync(0xffffffffu, mxx, k);
+        if ((msk >> k) & 1u) {
+            mg = max(mg, og);
+            mxx = max(mxx, ox);
+        }
+    }
+    if (in && (threadIdx.x & 31) == leader) {
+        atomicMax(mx + 2 * n, mg);
+        atomicMax(mx + 2 * n + 1, mxx);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    bslice_dgrid_convert(BsliceArgs a, const unsigned long long *__restrict__ acc, const unsigned *__restrict__ mx) {
+    const long long per = 12LL * a.D * a.Gh * a.Gw;
+    const long long idx = (long long)blockIdx.x * kThreads + threadIdx.x;
+    if (idx >= (long long)a.N * per) return;
+    const int n = (int)(idx / per);
+    const int S = bslice_det_scale(mx, n, (long long)a.H * a.W);
+    a.dgrid[idx] = (float)ldexp((double)(long long)acc[idx], -S);
 }
 
 // ----------------------------------------------------------------- host-side geometry
@@ -799,6 +864,18 @@ bool bwd_smem_fits(int D) {
 
 }  // namespace
 
+size_t bslice_det_ws_bytes(int N, int D, int Gh, int Gw) {
+    return sizeof(unsigned long long) * (size_t)N * 12 * D * Gh * Gw + sizeof(unsigned) * 2 * (size_t)N + 256;
+}
+
+size_t bslice_ws_bytes(int N, int H, int W, int D, int Gh, int Gw);
+// the workspace a backward call uses: the tiled path's partials, else (deterministic=1)
+// the fixed-point d_grid accumulators
+size_t bslice_bwd_ws_bytes(int N, int H, int W, int D, int Gh, int Gw, bool det) {
+    const size_t t = bslice_ws_bytes(N, H, W, D, Gh, Gw);
+    return t ? t : (det ? bslice_det_ws_bytes(N, D, Gh, Gw) : 0);
+}
+
 size_t bslice_ws_bytes(int N, int H, int W, int D, int Gh, int Gw) {
     const TileGeom g = tile_geom(N, H, W, D, Gh, Gw);
     if (!g.ok || !bwd_smem_fits(D)) return 0;
@@ -822,7 +899,6 @@ cudaError_t bslice_fwd_launch(const BsliceArgs &a, cudaStream_t s) {
 
 cudaError_t bslice_bwd_launch(const BsliceArgs &a, int algo, int deterministic, void *ws,
                               size_t ws_bytes, cudaStream_t s) {
-    (void)deterministic;
     const TileGeom g = tile_geom(a.N, a.H, a.W, a.D, a.Gh, a.Gw);
     const bool tiled = g.ok && bwd_smem_fits(a.D) && algo != 3 /*SCATTER_ATOMIC*/ && a.dgrid &&
                        ws_bytes >= bslice_ws_bytes(a.N, a.H, a.W, a.D, a.Gh, a.Gw);
@@ -842,6 +918,21 @@ cudaError_t bslice_bwd_launch(const BsliceArgs &a, int algo, int deterministic, 
         bslice_dgrid_gather<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(
             a, g.SY, g.SX, partials);
         note_launch();
+    } else if (deterministic && a.dgrid) {
+        // deterministic=1 where the tiled path does not apply: fixed-point d_grid
+        const long long per = 12LL * a.D * a.Gh * a.Gw;
+        unsigned long long *acc = (unsigned long long *)ws;
+        unsigned *mx = (unsigned *)(acc + (size_t)a.N * per);
+        cudaError_t e = cudaMemsetAsync(ws, 0, bslice_det_ws_bytes(a.N, a.D, a.Gh, a.Gw), s);
+        if (e != cudaSuccess) return e;
+        const long long total = (long long)a.N * a.H * a.W;
+        const unsigned nb = (unsigned)((total + kThreads - 1) / kThreads);
+        bslice_absmax<<<nb, kThreads, 0, s>>>(a, mx);
+        note_launch();
+        bslice_bwd_generic<true><<<nb, kThreads, 0, s>>>(a, acc, mx);
+        note_launch();
+        bslice_dgrid_convert<<<(unsigned)((a.N * per + kThreads - 1) / kThreads), kThreads, 0, s>>>(a, acc, mx);
+        note_launch();
     } else {
         if (a.dgrid) {
             cudaError_t e = cudaMemsetAsync(
@@ -849,7 +940,8 @@ cudaError_t bslice_bwd_launch(const BsliceArgs &a, int algo, int deterministic, 
             if (e != cudaSuccess) return e;
         }
         const long long total = (long long)a.N * a.H * a.W;
-        bslice_bwd_generic<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(a);
+        bslice_bwd_generic<false><<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(a, nullptr,
+                                                                                                       nullptr);
         note_launch();
     }
     return cudaGetLastError();

@@ -300,6 +300,8 @@ cudaError_t bslice_fwd_launch(const BsliceArgs &a, cudaStream_t s);
 cudaError_t bslice_bwd_launch(const BsliceArgs &a, int algo, int deterministic, void *ws,
                               size_t ws_bytes, cudaStream_t s);
 size_t bslice_ws_bytes(int N, int H, int W, int D, int Gh, int Gw);
+size_t bslice_det_ws_bytes(int N, int D, int Gh, int Gw);
+size_t bslice_bwd_ws_bytes(int N, int H, int W, int D, int Gh, int Gw, bool det);
 
 bool conv_shape_ok(int Ci, int Co, int kh, int kw);
 cudaError_t conv_fwd_launch(const ConvArgs &a, cudaStream_t s);
