@@ -55,8 +55,9 @@
  *   Determinism: with deterministic=1 every result is bitwise reproducible, for
  *             every sample: gathers and fixed-order partial sums as always, and where
  *             a scatter cannot be converted (STN samples with a singular map or a huge
- *             preimage, STN border padding, warp d_input, bicubic fallback samples)
- *             the fixed-point integer scatter: each term w*g rounded once to a 64-bit
+ *             preimage, STN border padding, warp d_input, bicubic fallback samples,
+ *             bslice d_grid on grids finer than 8 px per cell) the fixed-point
+ *             integer scatter: each term w*g rounded once to a 64-bit
  *             integer at a per-sample scale 2^S (S from max|dy|), summed with integer
  *             atomics (order-free), converted once (absolute error <= n 2^-(S+1) for
  *             n terms, n*max|dy|*P*2^-62), also for the stn3d / Lanczos adjoints.
