@@ -106,11 +106,13 @@ typedef enum { RS_PAD_ZEROS = 0, RS_PAD_BORDER = 1 } rs_padding;
  *                     SCATTER_ATOMIC: one fp32 atomic per tap (the unconverted
  *                     scatter); SCATTER_PRIV as for STN; GATHER -> RS_ERR_FLAG (an
  *                     arbitrary flow has no bounded inverse).
- *   bslice_bwd d_grid AUTO, GATHER, SCATTER_PRIV: dual-cell register-privatised
+ *   bslice_bwd d_grid AUTO, SCATTER_PRIV: dual-cell register-privatised
  *                     accumulation + fixed-order partial gather (deterministic;
  *                     cells >= 8 px; finer grids: global atomics, or with
- *                     deterministic=1 the fixed-point scatter); SCATTER_ATOMIC:
- *                     global atomics.
+ *                     deterministic=1 the fixed-point scatter); GATHER (D <= 16):
+ *                     the pure gather -- every grid node walks the pixels of its
+ *                     2 x 2 dual cells (deterministic; each pixel visited 4 times);
+ *                     SCATTER_ATOMIC: global atomics.
  * d_theta, d_flow, d_guide and bslice d_input are always gathers. */
 typedef enum {
     RS_ALGO_AUTO = 0,

@@ -818,6 +818,76 @@ __global__ void __launch_bounds__(kThreads)
     a.dgrid[idx] = (float)ldexp((double)(long long)acc[idx], -S);
 }
 
+// ----------------------------------------------------------------- d_grid as a pure gather
+// GATHER: every grid node (n, y, x) collects its d_grid values by walking all the pixels
+// whose clamped corners include it -- the pixels of the dual cells (y-1 .. y) x (x-1 .. x),
+// rows [dual_begin(y-1), dual_begin(y+1)) -- and adding w_node * w_z * G_o * X~_i to its
+// (q, z) entries: the converted gather of PAPER.md:700-731 in its plain form, with no
+// per-dual-cell partials (the comparator of the AUTO dual-cell accumulation, row a11).
+// Each pixel is visited by up to 4 nodes.  Per-thread accumulators [q][z][thread] in
+// shared memory (no atomics), summed over the threads in a fixed order: deterministic.
+constexpr int kNGT = 128;   // threads per node block
+constexpr int kNGDMax = 16; // z planes supported (shared memory: 12 * D * kNGT floats)
+
+__global__ void __launch_bounds__(kNGT)
+    bslice_dgrid_node_gather(BsliceArgs a, const int *__restrict__ tab) {
+    extern __shared__ float nacc[];  // [q][z][thread]
+    const int D = a.D;
+    const int node = blockIdx.x, n = blockIdx.y;
+    const int y = node / a.Gw, x = node - y * a.Gw;
+    const int r0 = __ldg(tab + y), r1 = __ldg(tab + y + 2);                      // dual rows y-1 .. y
+    const int c0 = __ldg(tab + a.Gh + 2 + x), c1 = __ldg(tab + a.Gh + 2 + x + 2);  // dual cols x-1 .. x
+    const int RH = r1 - r0, CW = c1 - c0;
+    for (int e = threadIdx.x; e < 12 * D * kNGT; e += kNGT) nacc[e] = 0.f;
+    __syncthreads();
+    const long long HW = (long long)a.H * a.W;
+    const float *gd = a.guide + (long long)n * HW;
+    const float *xp = a.x + (long long)n * 3 * HW;
+    const float *gp = a.dy + (long long)n * 3 * HW;
+    float *my = nacc + threadIdx.x;
+    for (int p = threadIdx.x; p < RH * CW; p += kNGT) {
+        const int py = r0 + p / CW, px = c0 + p % CW;
+        const double cx = bs_cx(px, a.W, a.Gw), cy = bs_cx(py, a.H, a.Gh);
+        const Cell ccx = cell_of(cx), ccy = cell_of(cy);
+        // this node's share of the pixel's spatial taps (both taps when they clamp onto it)
+        const float wx = (clampi(ccx.i0, 0, a.Gw - 1) == x ? 1.f - ccx.f : 0.f) +
+                         (clampi(ccx.i0 + 1, 0, a.Gw - 1) == x ? ccx.f : 0.f);
+        const float wy = (clampi(ccy.i0, 0, a.Gh - 1) == y ? 1.f - ccy.f : 0.f) +
+                         (clampi(ccy.i0 + 1, 0, a.Gh - 1) == y ? ccy.f : 0.f);
+        const float wxy = wy * wx;
+        if (wxy == 0.f) continue;
+        const long long o = (long long)py * a.W + px;
+        const double cz = bs_cz(__ldg(gd + o), D);
+        const Cell ccz = cell_of(cz);
+        const int zl = clampi(ccz.i0, 0, D - 1), zh = clampi(ccz.i0 + 1, 0, D - 1);
+        const float wl = wxy * (1.f - ccz.f), wh = wxy * ccz.f;
+        const float Xt[4] = {__ldg(xp + o), __ldg(xp + HW + o), __ldg(xp + 2 * HW + o), 1.f};
+        const float G[3] = {__ldg(gp + o), __ldg(gp + HW + o), __ldg(gp + 2 * HW + o)};
+#pragma unroll
+        for (int oc = 0; oc < 3; oc++)
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const float P = G[oc] * Xt[i];
+                float *q = my + (4 * oc + i) * D * kNGT;
+                q[zl * kNGT] = fmaf(wl, P, q[zl * kNGT]);
+                q[zh * kNGT] = fmaf(wh, P, q[zh * kNGT]);
+            }
+    }
+    __syncthreads();
+    // fixed-order sum over the threads: warp w sums (q, z) rows w, w + 4, ...
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long long plane = (long long)a.Gh * a.Gw;
+    for (int row = w; row < 12 * D; row += kNGT / 32) {
+        const float *rp = nacc + row * kNGT;
+        float v = rp[lane] + rp[lane + 32] + rp[lane + 64] + rp[lane + 96];
+        v = warp_sum(v);
+        if (lane == 0) {
+            const int q = row / D, z = row - q * D;
+            a.dgrid[(((long long)n * 12 + q) * D + z) * plane + node] = v;
+        }
+    }
+}
+
 // ----------------------------------------------------------------- host-side geometry
 struct TileGeom {
     int SY, SX;
@@ -873,7 +943,9 @@ size_t bslice_ws_bytes(int N, int H, int W, int D, int Gh, int Gw);
 // the fixed-point d_grid accumulators
 size_t bslice_bwd_ws_bytes(int N, int H, int W, int D, int Gh, int Gw, bool det) {
     const size_t t = bslice_ws_bytes(N, H, W, D, Gh, Gw);
-    return t ? t : (det ? bslice_det_ws_bytes(N, D, Gh, Gw) : 0);
+    const size_t g = sizeof(int) * (size_t)(Gh + Gw + 4);  // GATHER: the bounds table
+    const size_t r = t ? t : (det ? bslice_det_ws_bytes(N, D, Gh, Gw) : 0);
+    return r > g ? r : g;
 }
 
 size_t bslice_ws_bytes(int N, int H, int W, int D, int Gh, int Gw) {
@@ -900,7 +972,7 @@ cudaError_t bslice_fwd_launch(const BsliceArgs &a, cudaStream_t s) {
 cudaError_t bslice_bwd_launch(const BsliceArgs &a, int algo, int deterministic, void *ws,
                               size_t ws_bytes, cudaStream_t s) {
     const TileGeom g = tile_geom(a.N, a.H, a.W, a.D, a.Gh, a.Gw);
-    const bool tiled = g.ok && bwd_smem_fits(a.D) && algo != 3 /*SCATTER_ATOMIC*/ && a.dgrid &&
+    const bool tiled = g.ok && bwd_smem_fits(a.D) && algo != 3 /*SCATTER_ATOMIC*/ && (algo != 1 /*GATHER*/ || a.D > kNGDMax) && a.dgrid &&
                        ws_bytes >= bslice_ws_bytes(a.N, a.H, a.W, a.D, a.Gh, a.Gw);
     if (tiled) {
         const size_t sm = bwd_smem(a.D);
@@ -917,6 +989,26 @@ cudaError_t bslice_bwd_launch(const BsliceArgs &a, int algo, int deterministic, 
         const long long total = (long long)a.N * 12 * a.D * a.Gh * a.Gw;
         bslice_dgrid_gather<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(
             a, g.SY, g.SX, partials);
+        note_launch();
+    } else if (algo == 1 /*GATHER*/ && a.dgrid && a.D <= kNGDMax) {
+        // the pure node gather for d_grid; d_input / d_guide from the per-pixel kernel
+        int *tab = (int *)ws;
+        const int nt = (a.Gh > a.Gw ? a.Gh : a.Gw) + 2;
+        bslice_bounds_kernel<<<(nt + 127) / 128, 128, 0, s>>>(tab, a.H, a.W, a.Gh, a.Gw);
+        note_launch();
+        if (a.dx || a.dguide) {
+            BsliceArgs b = a;
+            b.dgrid = nullptr;
+            const long long total = (long long)a.N * a.H * a.W;
+            bslice_bwd_generic<false><<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(b, nullptr,
+                                                                                                           nullptr);
+            note_launch();
+        }
+        const size_t sm = sizeof(float) * 12 * a.D * kNGT;
+        cudaError_t ea = cudaFuncSetAttribute(bslice_dgrid_node_gather, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)sm);
+        if (ea != cudaSuccess) return ea;
+        bslice_dgrid_node_gather<<<dim3(a.Gh * a.Gw, a.N), kNGT, sm, s>>>(a, tab);
         note_launch();
     } else if (deterministic && a.dgrid) {
         // deterministic=1 where the tiled path does not apply: fixed-point d_grid

@@ -2034,9 +2034,11 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
         if (e != cudaSuccess) return e;
     } else if (a.dx && !priv) {
         const long long P = (long long)a.Ho * a.Wo;
-        // grid-stride over the (usually empty) fallback list: a small grid exits at once
+        // grid-stride over the fallback list: when every sample is a fallback (border
+        // padding, SCATTER_ATOMIC) a full grid; else (usually empty) a small one that exits at once
         long long blocks = (P + kThreads - 1) / kThreads;
-        if (blocks > 2 * kNumSMs) blocks = 2 * kNumSMs;
+        const long long cap = allow_gather ? 2 * kNumSMs : 4 * kNumSMs * 8;
+        if (blocks > cap) blocks = cap;
         stn_dx_scatter<<<(unsigned)blocks, kThreads, 0, s>>>(a, w.fb_list, w.fb_count);
         note_launch();
     }

@@ -10,6 +10,7 @@ from paper_1904_12228_b200 import rsgrad as rs
 
 nb = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+only = int(sys.argv[3]) if len(sys.argv) > 3 else -1  # run one variant (per-variant ncu reports)
 dev = torch.device("cuda")
 s, w, b = bench.make_inputs(0, nb, dev)
 o = bench.alloc_outputs(s, w, b)
@@ -43,12 +44,17 @@ variants = [
      lambda: rs.warp_bwd(w["x"], w["flow"], w["dy"], deterministic=True, out=(o["warp_dx"], o["warp_df"]))),
     ("bslice_bwd", "AUTO (dual-cell register accumulation + partial gather)", None,
      lambda: rs.bslice_bwd(b["grid"], b["guide"], b["x"], b["dy"], out=(o["bs_dgr"], o["bs_dgd"], o["bs_dx"]))),
+    ("bslice_bwd", "GATHER (pure node gather: each node walks its 2x2 dual cells)", None,
+     lambda: rs.bslice_bwd(b["grid"], b["guide"], b["x"], b["dy"], algo="gather",
+                           out=(o["bs_dgr"], o["bs_dgd"], o["bs_dx"]))),
     ("bslice_bwd", "SCATTER_ATOMIC (per-pixel global reds into d_grid)", None,
      lambda: rs.bslice_bwd(b["grid"], b["guide"], b["x"], b["dy"], algo="scatter_atomic",
                            out=(o["bs_dgr"], o["bs_dgd"], o["bs_dx"]))),
 ]
 res = []
-for call, name, ev, fn in variants:
+for vi, (call, name, ev, fn) in enumerate(variants):
+    if only >= 0 and vi != only:
+        continue
     if ev:
         os.environ[ev[0]] = ev[1]
     fn()

@@ -100,8 +100,9 @@ def test_workspace_sizes():
     # dual-cell bounds table (Gh + Gw + 4 ints)
     ws = rsgrad.workspace_bytes(2, 4, 3, 1024, 1024, D=8, Gh=16, Gw=16)
     assert ws == 4 * 17 * 17 * 4 * 8 * 12 * 4 + 4 * (16 + 16 + 4)
-    # too-fine grid => atomic path, no workspace; deterministic=1: the fixed-point d_grid
-    assert rsgrad.workspace_bytes(2, 1, 3, 16, 16, D=8, Gh=16, Gw=16) == 0
+    # too-fine grid => atomic path: only the bounds table (GATHER's node walk uses it);
+    # deterministic=1: the fixed-point d_grid
+    assert rsgrad.workspace_bytes(2, 1, 3, 16, 16, D=8, Gh=16, Gw=16) == 4 * (16 + 16 + 4)
     assert rsgrad.workspace_bytes(2, 1, 3, 16, 16, D=8, Gh=16, Gw=16,
                                   opts=rsgrad._opts(deterministic=True)) >= 8 * 12 * 8 * 16 * 16
     assert rsgrad.workspace_bytes(9, 1) == 0

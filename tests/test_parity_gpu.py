@@ -1016,3 +1016,21 @@ def test_bslice_deterministic_fine_grids(cuda_device, dims):
     assert_close(_np(a[0]), rgr, "grad", "dgrid")
     assert_close(_np(a[1]), rgd, "grad", "dguide")
     assert_close(_np(a[2]), rdx, "grad", "dx")
+
+
+@pytest.mark.parametrize("dims", [(2, 100, 130, 8, 6, 7), (1, 64, 64, 8, 4, 4), (2, 16, 16, 8, 16, 16),
+                                  (1, 60, 50, 16, 3, 5)])
+def test_bslice_gather_node_walk(cuda_device, dims):
+    """GATHER: d_grid by the pure node gather (each grid node walks the pixels of its 2 x 2
+    dual cells; clamped border taps count twice onto the border node); bitwise reproducible
+    and within T; d_input / d_guide from the per-pixel kernel."""
+    inp = synth.bslice_inputs(*dims, cfg=1, grid="iid", guide="wide")
+    g = _cuda(inp, cuda_device)
+    a = rsgrad.bslice_bwd(g["grid"], g["guide"], g["x"], g["dy"], algo="gather")
+    b = rsgrad.bslice_bwd(g["grid"], g["guide"], g["x"], g["dy"], algo="gather")
+    assert torch.equal(a[0], b[0])
+    gr, gd, x, dy = (inp[k].double().numpy() for k in ("grid", "guide", "x", "dy"))
+    rgr, rgd, rdx = oracle.bslice_bwd(gr, gd, x, dy)
+    assert_close(_np(a[0]), rgr, "grad", "dgrid")
+    assert_close(_np(a[1]), rgd, "grad", "dguide")
+    assert_close(_np(a[2]), rdx, "grad", "dx")
