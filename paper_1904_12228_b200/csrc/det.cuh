@@ -75,12 +75,13 @@ RS_DEV void det_grid_barrier(unsigned *bar, unsigned nblocks) {
 //     the in-image taps of output pixel q of sample n: element offsets within a
 //     channel plane and the fp32 weights the float path uses.
 // Sample selection: list/count (device list of samples), else flags (flags[n] != 0),
-// else every sample 0..N-1.
+// else every sample 0..N-1.  flags[n] == flag_on selects (a per-call tag lets a flag array
+// be reused without clearing it: stale values only cost a recompute, never correctness).
 template <class S, int kT = 256>
 __global__ void __launch_bounds__(kT)
     det_scatter_kernel(S smp, const float *__restrict__ dy, float *__restrict__ dx, int N, int C, long long HW,
                        long long P, const int *__restrict__ list, const int *__restrict__ count,
-                       const int *__restrict__ flags, DetWs ws) {
+                       const int *__restrict__ flags, int flag_on, DetWs ws) {
     const unsigned nb = gridDim.x;
     const long long tid = (long long)blockIdx.x * kT + threadIdx.x, nthr = (long long)nb * kT;
     const int nsel = list ? *count : N;
@@ -88,7 +89,7 @@ __global__ void __launch_bounds__(kT)
     __shared__ unsigned red[kT / 32];
     for (int f = 0; f < nsel; f++) {
         const int n = list ? list[f] : f;
-        if (!list && flags && !flags[n]) continue;  // uniform over the grid
+        if (!list && flags && flags[n] != flag_on) continue;  // uniform over the grid
         const float *g = dy + (long long)n * CP;
         // (A) zero the accumulator, max |dY| of the sample
         for (long long e = tid; e < CHW; e += nthr) ws.acc[e] = 0ull;
@@ -144,7 +145,8 @@ __global__ void __launch_bounds__(kT)
 // co-resident.
 template <class S>
 cudaError_t det_scatter_launch(const S &smp, const float *dy, float *dx, int N, int C, long long HW, long long P,
-                               const int *list, const int *count, const int *flags, void *ws, cudaStream_t s) {
+                               const int *list, const int *count, const int *flags, void *ws, cudaStream_t s,
+                               int flag_on = 1) {
     constexpr int kT = 256;
     const DetWs w = det_ws_layout(ws, N, (long long)C * HW);
     cudaError_t e = cudaMemsetAsync(w.bar, 0, sizeof(unsigned) * ((size_t)N + 2), s);
@@ -159,9 +161,10 @@ cudaError_t det_scatter_launch(const S &smp, const float *dy, float *dx, int N, 
     const int blocks = nsm * (occ < 4 ? occ : 4);
     S sm = smp;
     long long hw = HW, p = P;
-    int n = N, c = C;
+    int n = N, c = C, fo = flag_on;
     DetWs wk = w;
-    void *args[] = {&sm, (void *)&dy, (void *)&dx, &n, &c, &hw, &p, (void *)&list, (void *)&count, (void *)&flags, &wk};
+    void *args[] = {&sm, (void *)&dy, (void *)&dx, &n, &c, &hw, &p, (void *)&list, (void *)&count, (void *)&flags, &fo,
+                    &wk};
     e = cudaLaunchCooperativeKernel((const void *)kern, dim3(blocks), dim3(kT), args, 0, s);
     note_launch();
     return e;

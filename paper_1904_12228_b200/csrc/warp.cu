@@ -11,6 +11,7 @@
 //   warp_bwd_win      variant (RSGRAD_WARP_BWD=winR,NW,IT): per-warp shared windows
 //                     flushed by red.v4 (measured slower).
 //   SCATTER_PRIV goes through the staged-footprint output tile of stn.cu (flow mode).
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -175,15 +176,25 @@ __global__ void __launch_bounds__(kThreads) warp_bwd_kernel(WarpArgs a, double i
 // (sequential in the order the L2 applies them) inside the tolerance.
 // d_flow is the gather of the same pass; the X taps of a cell one row down reuse the
 // two lower tap values already loaded.
-constexpr int kStripW = 4;  // warps per block (stacked vertically)
+#ifndef RS_STRIP_W
+#define RS_STRIP_W 1
+#endif
+constexpr int kStripW = RS_STRIP_W;  // warps per block (1 measured best: configs[2] smooth 62.5 vs 68.6 us with 4)
 
 #ifndef RS_STRIP_MINB
-#define RS_STRIP_MINB 6
+#define RS_STRIP_MINB (24 / RS_STRIP_W)  // 80 registers
 #endif
+// A run of lanes whose pre-summed emission carries >= kHeavyFanin taps marks the sample
+// "heavy" (heavy[n] = this call's tag): a flow that folds that many pixels onto one cell puts hundreds
+// of taps on an element, where even pre-summed fp32 partials round at the 1e-6 level of
+// T's absolute floor; the launcher then recomputes that sample's d_input with the
+// fixed-point scatter (det.cuh), exact to ~1e-11.  Smooth flows never get there (runs of
+// <= 3 lanes, a row or two per cell).
+constexpr int kHeavyFanin = 32;
+
 template <int CW, int R>
 __global__ void __launch_bounds__(kStripW * 32, RS_STRIP_MINB)
-    warp_bwd_strip(WarpArgs a, int tiles_x, double invW) {
-    (void)invW;
+    warp_bwd_strip(WarpArgs a, int tiles_x, int *__restrict__ heavy, int tag) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int n = blockIdx.y;
     const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
@@ -203,7 +214,7 @@ __global__ void __launch_bounds__(kStripW * 32, RS_STRIP_MINB)
         float *dxs = need_dx ? a.dx + ((long long)n * a.C + c0) * HW : nullptr;
         // pending cell of this lane
         bool have = false;
-        int pcx = 0, pcy = 0;
+        int pcx = 0, pcy = 0, cnt = 0;  // pending cell; cnt: rows pre-summed into it
         bool pk[4] = {false, false, false, false};
         float pend[CW][4], xv[CW][4];
 #pragma unroll
@@ -246,6 +257,15 @@ __global__ void __launch_bounds__(kStripW * 32, RS_STRIP_MINB)
                             const float t = __shfl_down_sync(0xffffffffu, val[c][k], o);
                             if (lane + o <= seg_end) val[c][k] += t;
                         }
+                }
+                if (heavy) {  // taps pre-summed by the run's first lane
+                    int tot = any ? cnt : 0;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int t2 = __shfl_down_sync(0xffffffffu, tot, o);
+                        if (lane + o <= seg_end) tot += t2;
+                    }
+                    if (__ballot_sync(0xffffffffu, !same_prev && tot >= kHeavyFanin) && lane == 0) heavy[n] = tag;
                 }
                 if (same_prev) em[0] = em[1] = em[2] = em[3] = false;
             }
@@ -371,6 +391,7 @@ __global__ void __launch_bounds__(kStripW * 32, RS_STRIP_MINB)
 #pragma unroll
                         for (int k = 0; k < 4; k++) pend[c][k] = nv[c][k];
                 }
+                cnt = (same || down) ? cnt + 1 : 1;
                 have = tany;
                 pcx = t.x0;
                 pcy = t.y0;
@@ -624,8 +645,10 @@ struct WarpTapSampler {
 
 }  // namespace
 
+// AUTO and deterministic=1 both may run the fixed-point scatter (AUTO: for samples the
+// strip kernel marks heavy); AUTO also keeps the per-sample heavy flags after it
 size_t warp_ws_bytes(int N, int C, int H, int W, bool det) {
-    return det ? det_ws_bytes(N, (long long)C * H * W) : 0;
+    return det_align(det_ws_bytes(N, (long long)C * H * W)) + (det ? 0 : det_align(sizeof(int) * (size_t)N));
 }
 
 // Optional tiled path (RSGRAD_WARP=tiled): the staged-footprint output-tile kernel of
@@ -694,12 +717,19 @@ cudaError_t warp_bwd_launch(const WarpArgs &a, int algo, int deterministic, void
         const int tiles_y = (a.H + R * kStripW - 1) / (R * kStripW);
         const dim3 grid((unsigned)(tiles_x * tiles_y), a.N);
         const int CW = a.C < 4 ? a.C : 4;
+        // heavy-sample flags (d_input only; none when the workspace cannot hold the fixed point)
+        const bool rescue = a.dx && ws && ws_bytes >= warp_ws_bytes(a.N, a.C, a.H, a.W, false);
+        int *heavy = rescue ? (int *)((char *)ws + det_align(det_ws_bytes(a.N, (long long)a.C * HW))) : nullptr;
+        // a fresh tag per call instead of clearing the flags (a stale match in reused memory
+        // would only send that sample through the exact recompute)
+        static std::atomic<unsigned> tags{0};
+        const int tag = (int)(tags.fetch_add(1u) % 0x7ffffff0u) + 2;
 #define RS_STRIP(RR)                                                                                        \
     switch (CW) {                                                                                           \
-        case 1: warp_bwd_strip<1, RR><<<grid, kStripW * 32, 0, s>>>(a, tiles_x, 1.0 / a.W); break;          \
-        case 2: warp_bwd_strip<2, RR><<<grid, kStripW * 32, 0, s>>>(a, tiles_x, 1.0 / a.W); break;          \
-        case 3: warp_bwd_strip<3, RR><<<grid, kStripW * 32, 0, s>>>(a, tiles_x, 1.0 / a.W); break;          \
-        default: warp_bwd_strip<4, RR><<<grid, kStripW * 32, 0, s>>>(a, tiles_x, 1.0 / a.W); break;         \
+        case 1: warp_bwd_strip<1, RR><<<grid, kStripW * 32, 0, s>>>(a, tiles_x, heavy, tag); break;              \
+        case 2: warp_bwd_strip<2, RR><<<grid, kStripW * 32, 0, s>>>(a, tiles_x, heavy, tag); break;              \
+        case 3: warp_bwd_strip<3, RR><<<grid, kStripW * 32, 0, s>>>(a, tiles_x, heavy, tag); break;              \
+        default: warp_bwd_strip<4, RR><<<grid, kStripW * 32, 0, s>>>(a, tiles_x, heavy, tag); break;             \
     }
         if (R == 8) {
             RS_STRIP(8)
@@ -708,6 +738,12 @@ cudaError_t warp_bwd_launch(const WarpArgs &a, int algo, int deterministic, void
         }
 #undef RS_STRIP
         note_launch();
+        if (heavy) {  // heavy samples only (the others exit at once): d_input in fixed point
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return e;
+            return det_scatter_launch(WarpTapSampler{a}, a.dy, a.dx, a.N, a.C, HW, HW, nullptr, nullptr, heavy, ws, s,
+                                      tag);
+        }
         return cudaGetLastError();
     }
     if (direct || !win) {

@@ -14,6 +14,8 @@ inp["flow"] = torch.stack([-xx * 0.97 + 3.3, -yy * 0.9 + 2.6]).expand(N, 2, H, W
 g = {k: v.cuda() for k, v in inp.items()}
 for pad in ("zeros", "border"):
     rdx, _ = oracle.warp_bwd(*(inp[k].double().numpy() for k in ("x", "flow", "dy")), pad == "border")
-    for algo in ("auto", "scatter_atomic"):
-        rat = [compare(rs.warp_bwd(g["x"], g["flow"], g["dy"], padding=pad, algo=algo)[0].double().cpu().numpy(), rdx, **GRAD)["max_ratio"] for _ in range(reps)]
+    for algo in ("auto", "scatter_atomic", "deterministic"):
+        kw = {"deterministic": True} if algo == "deterministic" else {"algo": algo}
+        rat = [compare(rs.warp_bwd(g["x"], g["flow"], g["dy"], padding=pad, **kw)[0].double().cpu().numpy(), rdx,
+                       **GRAD)["max_ratio"] for _ in range(reps)]
         print(f"{pad:6s} {algo:15s} max_ratio over {reps} runs: max {max(rat):.3f} min {min(rat):.3f}")

@@ -631,6 +631,22 @@ def test_warp_bwd_auto_collapse_paper_shape(cuda_device, padding):
     assert_close(_np(df), rdf, "grad", "dflow")
 
 
+def test_warp_bwd_heavy_samples_take_fixed_point(cuda_device):
+    """AUTO marks a sample heavy when one pre-summed emission carries >= 32 taps (a
+    collapsing flow) and recomputes its d_input with the fixed-point scatter: that sample
+    is then bitwise equal to deterministic=1; a smooth-flow sample in the same batch stays
+    on the fp32 pre-summed reds (and within T)."""
+    N, C, H, W = 2, 3, 96, 160
+    inp = synth.warp_inputs(N, C, H, W, cfg=1, flow="smooth")
+    inp["flow"][1] = _collapse_flow(1, H, W)[0]
+    g = _cuda(inp, cuda_device)
+    auto, _ = rsgrad.warp_bwd(g["x"], g["flow"], g["dy"])
+    det, _ = rsgrad.warp_bwd(g["x"], g["flow"], g["dy"], deterministic=True)
+    assert torch.equal(auto[1], det[1])
+    rdx, _ = oracle.warp_bwd(*(inp[k].double().numpy() for k in ("x", "flow", "dy")))
+    assert_close(_np(auto), rdx, "grad", "dx")
+
+
 @pytest.mark.parametrize("flow", ["zero", "int", "translate_border"])
 def test_warp_bwd_strip_special_flows(cuda_device, flow):
     """Integer and zero flows put every sample on a kink (fx = fy = 0): the strip kernel's
