@@ -101,7 +101,10 @@ typedef enum { RS_PAD_ZEROS = 0, RS_PAD_BORDER = 1 } rs_padding;
  *   warp_bwd d_input  AUTO: row strips -- each lane walks rows of one column and keeps
  *                     its current cell's 4 tap sums in registers (carried down a
  *                     row, merged with the neighbour lane's shared taps and across
- *                     runs of lanes on one cell) before fp32 global atomics;
+ *                     runs of lanes on one cell) before fp32 global atomics; a
+ *                     sample where one pre-summed emission covers >= 32 taps (a
+ *                     collapsing flow) is then recomputed by the fixed-point
+ *                     scatter (needs the workspace rsgrad_ws_bytes reports);
  *                     deterministic=1: the fixed-point scatter;
  *                     SCATTER_ATOMIC: one fp32 atomic per tap (the unconverted
  *                     scatter); SCATTER_PRIV as for STN; GATHER -> RS_ERR_FLAG (an
