@@ -244,13 +244,11 @@ def flush_l2(buf):
     buf.add_(1.0)
 
 
-def paper_shapes(rs, peak):
-    """configs[1..3] (+ the paper's 32x32x8 grid), each call timed alone after an L2 flush."""
+def paper_cases(rs, dev):
+    """configs[1..3] (+ the paper's 32x32x8 and 2048^2 bslice grids): (name, layer, C, P,
+    fwd thunk, bwd thunk) with inputs and outputs resident on dev."""
     import synth
 
-    dev = torch.device("cuda")
-    fl = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 2x L2
-    out = {}
     cases = [
         ("stn_4x16x512x512", "stn", C_STN, synth.stn_inputs(4, 16, 512, 512, cfg=2, device=dev)),
         ("warp_8x3x384x512_smooth", "warp", 3, synth.warp_inputs(8, 3, 384, 512, cfg=3, device=dev)),
@@ -264,47 +262,79 @@ def paper_shapes(rs, peak):
         ("bslice_4x2048x2048_g64x64x8", "bslice", 3,
          synth.bslice_inputs(4, 2048, 2048, 8, 64, 64, cfg=4, device=dev)),
     ]
+    res = []
     for name, layer, C, i in cases:
         if layer == "stn":
             o = (torch.empty_like(i["x"]), torch.empty_like(i["theta"]))
             y = torch.empty_like(i["dy"])
-            fwd = lambda: rs.stn_fwd(i["x"], i["theta"], out=y)  # noqa: E731
-            bwd = lambda: rs.stn_bwd(i["x"], i["theta"], i["dy"], out=o)  # noqa: E731
+            fwd = lambda i=i, y=y: rs.stn_fwd(i["x"], i["theta"], out=y)  # noqa: E731
+            bwd = lambda i=i, o=o: rs.stn_bwd(i["x"], i["theta"], i["dy"], out=o)  # noqa: E731
             P = i["x"].shape[0] * 512 * 512
         elif layer == "warp":
             o = (torch.empty_like(i["x"]), torch.empty_like(i["flow"]))
             y = torch.empty_like(i["x"])
-            fwd = lambda: rs.warp_fwd(i["x"], i["flow"], out=y)  # noqa: E731
-            bwd = lambda: rs.warp_bwd(i["x"], i["flow"], i["dy"], out=o)  # noqa: E731
+            fwd = lambda i=i, y=y: rs.warp_fwd(i["x"], i["flow"], out=y)  # noqa: E731
+            bwd = lambda i=i, o=o: rs.warp_bwd(i["x"], i["flow"], i["dy"], out=o)  # noqa: E731
             P = 8 * 384 * 512
         else:
             o = (torch.empty_like(i["grid"]), torch.empty_like(i["guide"]), torch.empty_like(i["x"]))
             y = torch.empty_like(i["x"])
-            fwd = lambda: rs.bslice_fwd(i["grid"], i["guide"], i["x"], out=y)  # noqa: E731
-            bwd = lambda: rs.bslice_bwd(i["grid"], i["guide"], i["x"], i["dy"], out=o)  # noqa: E731
+            fwd = lambda i=i, y=y: rs.bslice_fwd(i["grid"], i["guide"], i["x"], out=y)  # noqa: E731
+            bwd = lambda i=i, o=o: rs.bslice_bwd(i["grid"], i["guide"], i["x"], i["dy"], out=o)  # noqa: E731
             P = i["x"].shape[0] * i["x"].shape[2] * i["x"].shape[3]
-        times = {"fwd": [], "bwd": []}
-        for rep in range(25):
-            for kind, fn in (("fwd", fwd), ("bwd", bwd)):
+        res.append((name, layer, C, P, fwd, bwd))
+    return res
+
+
+def capture(fn):
+    """fn's launches captured once into a CUDA graph (the C-ABI calls are capture-safe:
+    stream-ordered work only); returns the replay thunk."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()  # warm: lazy attributes, allocator
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    return g.replay
+
+
+def paper_shapes(rs, peak, reps=25, skip=5):
+    """configs[1..3] (+ the paper's 32x32x8 grid), each call timed alone after an L2 flush,
+    launched eagerly and as one CUDA-graph replay (the per-kernel launch
+    tails of a multi-kernel call at these small shapes)."""
+    dev = torch.device("cuda")
+    fl = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 2x L2
+    out = {}
+    for name, layer, C, P, fwd, bwd in paper_cases(rs, dev):
+        gf, gb = capture(fwd), capture(bwd)
+        times = {k: [] for k in ("fwd", "bwd", "fwd_graph", "bwd_graph")}
+        for rep in range(reps):
+            for kind, fn in (("fwd", fwd), ("bwd", bwd), ("fwd_graph", gf), ("bwd_graph", gb)):
                 flush_l2(fl)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
                 fn()
                 e1.record()
                 torch.cuda.synchronize()
-                if rep >= 5:
+                if rep >= skip:
                     times[kind].append(e0.elapsed_time(e1) * 1e-3)
-        tf, tb = statistics.median(times["fwd"]), statistics.median(times["bwd"])
+        t = {k: statistics.median(v) for k, v in times.items()}
+        tf, tb = min(t["fwd"], t["fwd_graph"]), min(t["bwd"], t["bwd_graph"])
         bf, bb = BYTES[(layer, "fwd")](C) * P, BYTES[(layer, "bwd")](C) * P
         out[name] = {
-            "fwd_us": round(tf * 1e6, 2), "bwd_us": round(tb * 1e6, 2),
+            "fwd_us": round(t["fwd"] * 1e6, 2), "bwd_us": round(t["bwd"] * 1e6, 2),
+            "fwd_us_graph": round(t["fwd_graph"] * 1e6, 2), "bwd_us_graph": round(t["bwd_graph"] * 1e6, 2),
             "fwd_bwd_mpix_s": round(P / (tf + tb) / 1e6, 1),
             "bwd_mpix_s": round(P / tb / 1e6, 1),
             "fwd_roofline_frac": round(bf / tf / 1e9 / peak, 3),
             "bwd_roofline_frac": round(bb / tb / 1e9 / peak, 3),
         }
     del fl
-    return {"l2": "flushed (256 MB write) before every call; median of 20", "cases": out}
+    return {"l2": f"flushed (256 MB write) before every call; median of {reps - skip}; eager and "
+                  "CUDA-graph replay (*_graph), fractions and Mpix/s from the faster of the two",
+            "cases": out}
 
 
 # --------------------------------------------------------------------------- §8(f) NEXT rows

@@ -52,6 +52,12 @@
  *             validation and launch errors (cudaGetLastError) only; kernel
  *             faults surface on the next synchronisation of `stream`.
  *   Threads   re-entrant; concurrent calls on different streams are safe.
+ *   Graphs    with device pointers every entry point is stream-capture safe (only
+ *             kernel launches, memsets and stream-ordered alloc/free on `stream`):
+ *             capture it into a CUDA graph and replay it (the per-kernel launch
+ *             gaps of a multi-kernel call shrink; bench.py paper_shapes *_graph).
+ *             While `stream` is capturing, its device must be the current one.
+ *             The host-pointer path is not capturable.
  *   Determinism: with deterministic=1 every result is bitwise reproducible, for
  *             every sample: gathers and fixed-order partial sums as always, and where
  *             a scatter cannot be converted (STN samples with a singular map or a huge

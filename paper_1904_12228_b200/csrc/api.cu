@@ -79,6 +79,13 @@ struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(cudaStream_t s) {
         if (!s) return;
+        // cudaStreamGetDevice invalidates a stream capture (measured): a capturing stream
+        // belongs to the current device (CUDA-graph capture is set up on it)
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+            cudaGetLastError();
+            return;
+        }
         int d = 0, cur = 0;
         if (cudaStreamGetDevice(s, &d) != cudaSuccess) {
             cudaGetLastError();

@@ -81,7 +81,7 @@ template <class S, int kT = 256>
 __global__ void __launch_bounds__(kT)
     det_scatter_kernel(S smp, const float *__restrict__ dy, float *__restrict__ dx, int N, int C, long long HW,
                        long long P, const int *__restrict__ list, const int *__restrict__ count,
-                       const int *__restrict__ flags, int flag_on, DetWs ws) {
+                       int *__restrict__ flags, int flag_on, DetWs ws) {
     const unsigned nb = gridDim.x;
     const long long tid = (long long)blockIdx.x * kT + threadIdx.x, nthr = (long long)nb * kT;
     const int nsel = list ? *count : N;
@@ -138,6 +138,9 @@ __global__ void __launch_bounds__(kT)
         for (long long e = tid; e < CHW; e += nthr)
             d[e] = finite ? (float)ldexp((double)(long long)__ldcg(ws.acc + e), -Sx) : __int_as_float(0x7fffffff);
         det_grid_barrier(ws.bar, nb);
+        // every block has read flags[n]: clear it, so a CUDA-graph replay (same tag) does
+        // not recompute the sample again unless it is flagged anew
+        if (flags && !list && tid == 0) flags[n] = 0;
     }
 }
 
@@ -145,7 +148,7 @@ __global__ void __launch_bounds__(kT)
 // co-resident.
 template <class S>
 cudaError_t det_scatter_launch(const S &smp, const float *dy, float *dx, int N, int C, long long HW, long long P,
-                               const int *list, const int *count, const int *flags, void *ws, cudaStream_t s,
+                               const int *list, const int *count, int *flags, void *ws, cudaStream_t s,
                                int flag_on = 1) {
     constexpr int kT = 256;
     const DetWs w = det_ws_layout(ws, N, (long long)C * HW);
