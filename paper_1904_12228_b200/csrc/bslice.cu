@@ -604,6 +604,302 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
 }
 
+// ----------------------------------------------------------------- backward, split phases
+// bslice_bwd_split: the same dual-cell ownership, z-bin counting sort and lane-pair
+// register accumulation of d_grid as bslice_bwd_tiled, with the per-pixel work moved
+// out of the accumulation loop:
+//   phase 1 (lane = pixel, raster order, coalesced 32-bit-offset loads and stores):
+//           slice A (12 coefficients, both planes), dX = A^T G and d_guide, and the
+//           pixel's record {G, X, fz, (r, c)} written to its bin-sorted slot in shared
+//           memory (the stable counting-sort placement);
+//   phase 2 (lane pairs over 16-record chunks of one bin): only the 96 trilinear-
+//           weighted products P_q = G_oc Xt_i per pixel into register sums, flushed by
+//           the same reduce-scatter as bslice_bwd_tiled, one partial per (tile, corner).
+// Sub-tiles are at most kV2TX x kV2TY px so two blocks fit per SM.  (PAPER.md:36-42
+// slice-apply; PAPER.md:700-731 bounded-footprint gather for d_grid.)
+constexpr int kV2TX = 64, kV2TY = 32;                 // nominal max sub-tile (px)
+constexpr int kV2PX = (kV2TX + 2) * (kV2TY + 2);      // per-tile pixel capacity (+1 rounding slack per axis)
+constexpr int kBinS = 25;                             // float4 per bin in gi (24 + 1: lanes on different bins hit different banks)
+
+RS_DEV int v2_maxch(int NB) { return kV2PX / kChunk + NB + 1; }
+
+RS_DEV void stage_corners_b(float4 *gi, const float *grid, const Tile &t, int D, int Gh, int Gw) {
+    const int y0 = clampi(t.j, 0, Gh - 1), y1 = clampi(t.j + 1, 0, Gh - 1);
+    const int x0 = clampi(t.k, 0, Gw - 1), x1 = clampi(t.k + 1, 0, Gw - 1);
+    const long long plane = (long long)Gh * Gw;
+    const float *g = grid + (long long)t.n * 12 * D * plane;
+    for (int e = threadIdx.x; e < (D + 1) * 12; e += blockDim.x) {
+        const int b = e / 12, q = e - b * 12;
+        const int zl = clampi(b - 1, 0, D - 1), zh = clampi(b, 0, D - 1);
+        const float *pl = g + ((long long)q * D + zl) * plane;
+        const float *ph = g + ((long long)q * D + zh) * plane;
+        const float l00 = __ldg(pl + y0 * Gw + x0), l01 = __ldg(pl + y0 * Gw + x1);
+        const float l10 = __ldg(pl + y1 * Gw + x0), l11 = __ldg(pl + y1 * Gw + x1);
+        const float h00 = __ldg(ph + y0 * Gw + x0), h01 = __ldg(ph + y0 * Gw + x1);
+        const float h10 = __ldg(ph + y1 * Gw + x0), h11 = __ldg(ph + y1 * Gw + x1);
+        const float4 L = lerp_terms(l00, l01, l10, l11);
+        const float4 Dz = lerp_terms(h00 - l00, h01 - l01, h10 - l10, h11 - l11);
+        gi[b * kBinS + 2 * q] = make_float4(L.x, Dz.x, L.y, Dz.y);
+        gi[b * kBinS + 2 * q + 1] = make_float4(L.z, Dz.z, L.w, Dz.w);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 2)
+    bslice_bwd_split(BsliceArgs a, int SY, int SX, float *__restrict__ partials, const int *__restrict__ tab) {
+    extern __shared__ float4 smem4[];
+    const int D = a.D, NB = D + 1;
+    const int maxch = v2_maxch(NB);
+    float4 *rec = smem4;                                   // maxch * kChunk * 2 (32-B records)
+    float4 *gi = rec + maxch * kChunk * 2;                 // NB * kBinS
+    float *fzv = (float *)(gi + NB * kBinS);               // kV2PX: guide, then fz in place
+    float *fxt = fzv + kV2PX;                              // kV2TX + 4
+    float *fyt = fxt + kV2TX + 4;                          // kV2TY + 4
+    float *wacc = fyt + kV2TY + 4;                         // kWarps * 4 * D * 12
+    int *cnt = (int *)(wacc + kWarps * 4 * D * 12);        // kWarps * NB
+    int *bstart = cnt + kWarps * NB;                       // NB + 1
+    int *chunk_bin = bstart + NB + 1;                      // maxch
+    unsigned char *binv = (unsigned char *)(chunk_bin + maxch);  // kV2PX
+
+    const Tile t = tile_of_tab(blockIdx.x, a.Gh, a.Gw, SY, SX, tab);
+    const int TW = t.xe - t.xs, TH = t.ye - t.ys;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long long HW = (long long)a.H * a.W;
+    const long long tbase = (long long)t.ys * a.W + t.xs;  // tile origin within a plane
+    {  // guide tile -> smem (cp.async; overlaps the corner staging below)
+        const float *gd = a.guide + (long long)t.n * HW + tbase;
+        const bool vec = (TW % 4 == 0) && (a.W % 4 == 0) && (t.xs % 4 == 0) && (((uintptr_t)a.guide & 15u) == 0);
+        const int wq = vec ? TW / 4 : TW;
+        for (int e = threadIdx.x; e < TH * wq; e += kThreads) {
+            const int r = e / wq, q = e - r * wq;
+            const float *src = gd + (long long)r * a.W;
+            if (vec) cp_async16(fzv + r * TW + 4 * q, src + 4 * q);
+            else cp_async4(fzv + r * TW + q, src + q);
+        }
+        cp_async_commit();
+    }
+    stage_corners_b(gi, a.grid, t, D, a.Gh, a.Gw);
+    for (int c = threadIdx.x; c < TW; c += kThreads) {
+        const double cx = bs_cx(t.xs + c, a.W, a.Gw);
+        fxt[c] = (float)__dsub_rn(cx, floor(cx));
+    }
+    for (int r = threadIdx.x; r < TH; r += kThreads) {
+        const double cy = bs_cx(t.ys + r, a.H, a.Gh);
+        fyt[r] = (float)__dsub_rn(cy, floor(cy));
+    }
+    for (int e = threadIdx.x; e < kWarps * 4 * D * 12; e += kThreads) wacc[e] = 0.f;
+    for (int e = threadIdx.x; e < kWarps * NB; e += kThreads) cnt[e] = 0;
+    cp_async_wait<0>();
+    __syncthreads();
+
+    // ---- phase 0: z-bin of every pixel, per-warp counts (warp w: rows w, w+8, ...)
+    for (int r = w; r < TH; r += kWarps) {
+        for (int c0 = 0; c0 < TW; c0 += 32) {
+            const int c = c0 + lane;
+            int bin = -1;
+            if (c < TW) {
+                float fz;
+                z_cell(fzv[r * TW + c], D, bin, fz);
+                binv[r * TW + c] = (unsigned char)bin;
+                fzv[r * TW + c] = fz;
+            }
+            const unsigned m = __match_any_sync(0xffffffffu, bin);
+            if (bin >= 0 && lane == __ffs(m) - 1) cnt[w * NB + bin] += __popc(m);
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    // ---- scan (warp 0, lane = bin): bin segments padded to kChunk, per-(warp, bin)
+    // offsets; the padding slots get zero records (G = X = 0: no contribution)
+    if (threadIdx.x < 32) {
+        int run = 0;
+        for (int base = 0; base < NB; base += 32) {
+            const int b = base + lane;
+            int tot = 0;
+            if (b < NB)
+                for (int ww = 0; ww < kWarps; ww++) tot += cnt[ww * NB + b];
+            const int padded = (tot + kChunk - 1) & ~(kChunk - 1);
+            int v = padded;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t2 = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += t2;
+            }
+            if (b < NB) {
+                int off = run + v - padded;
+                bstart[b] = off;
+                for (int ww = 0; ww < kWarps; ww++) {
+                    const int c2 = cnt[ww * NB + b];
+                    cnt[ww * NB + b] = off;
+                    off += c2;
+                }
+                for (int e = off; e < run + v; e++) {
+                    rec[2 * e] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    rec[2 * e + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+            run += __shfl_sync(0xffffffffu, v, 31);
+        }
+        if (lane == 0) bstart[NB] = run;
+    }
+    __syncthreads();
+    const int nchunks = bstart[NB] / kChunk;
+    for (int c = threadIdx.x; c < nchunks; c += kThreads) {
+        int b = 0;
+        while (bstart[b + 1] <= c * kChunk) b++;
+        chunk_bin[c] = b;
+    }
+
+    // ---- phase 1: lane = pixel (same walk order as phase 0: stable placement)
+    {
+        const long long nb3 = (long long)t.n * 3 * HW + tbase;
+        const float *x0p = a.x + nb3, *x1p = x0p + HW, *x2p = x1p + HW;
+        const float *g0p = a.dy + nb3, *g1p = g0p + HW, *g2p = g1p + HW;
+        float *d0p = a.dx ? a.dx + nb3 : nullptr;
+        float *dgp = a.dguide ? a.dguide + (long long)t.n * HW + tbase : nullptr;
+        const float Df = (float)D;
+        // the warp's (row, 32-column segment) items in phase-0 order; the next item's six
+        // global loads are issued before the current one is processed (pipeline depth 1)
+        const int ncx = (TW + 31) >> 5;
+        float Xn[3] = {0.f, 0.f, 0.f}, Gn[3] = {0.f, 0.f, 0.f};
+        auto fetch = [&](int r, int c) {
+            if (r < TH && c < TW) {
+                const int o = r * a.W + c;
+                Xn[0] = ldg_stream(x0p + o); Xn[1] = ldg_stream(x1p + o); Xn[2] = ldg_stream(x2p + o);
+                Gn[0] = ldg_stream(g0p + o); Gn[1] = ldg_stream(g1p + o); Gn[2] = ldg_stream(g2p + o);
+            }
+        };
+        fetch(w, lane);
+        int r = w, cx = 0;
+        while (r < TH) {
+            const int c = cx * 32 + lane;
+            float X[3], G[3];
+#pragma unroll
+            for (int i = 0; i < 3; i++) { X[i] = Xn[i]; G[i] = Gn[i]; }
+            const int cx1 = cx + 1 < ncx ? cx + 1 : 0, r1 = cx + 1 < ncx ? r : r + kWarps;
+            fetch(r1, cx1 * 32 + lane);
+            const bool ok = c < TW;
+            const int o = r * a.W + c;
+            const float2 fy2 = f2(fyt[r], fyt[r]);
+            const int bin = ok ? (int)binv[r * TW + c] : -1;
+            const unsigned m = __match_any_sync(0xffffffffu, bin);
+            if (ok) {
+                const float fz = fzv[r * TW + c];
+                const float fx = fxt[c];
+                const float2 fx2 = f2(fx, fx);
+                const float4 *Qb = gi + bin * kBinS;
+                float A[12], dq[12];
+#pragma unroll
+                for (int q = 0; q < 12; q++) {
+                    const float4 v0 = Qb[2 * q], v1 = Qb[2 * q + 1];
+                    const float2 th = __ffma2_rn(fx2, f2(v1.z, v1.w), f2(v1.x, v1.y));
+                    const float2 tl = __ffma2_rn(fx2, f2(v0.z, v0.w), f2(v0.x, v0.y));
+                    const float2 ld = __ffma2_rn(fy2, th, tl);
+                    A[q] = fmaf(fz, ld.y, ld.x);
+                    dq[q] = ld.y;
+                }
+                // dX_i = sum_oc A_{4 oc + i} G_oc, d_guide = D sum_q G_oc Xt_i dA_q/dz
+                // (the summation order of bslice_bwd_tiled's lane pairs)
+                const float Xt[4] = {X[0], X[1], X[2], 1.f};
+                float dlo = 0.f, dhi = 0.f;
+#pragma unroll
+                for (int q = 0; q < 6; q++) dlo = fmaf(G[q >> 2] * Xt[q & 3], dq[q], dlo);
+#pragma unroll
+                for (int q = 6; q < 12; q++) dhi = fmaf(G[q >> 2] * Xt[q & 3], dq[q], dhi);
+                if (d0p) {
+                    // (explicit _rn: no contraction of the final sums into FMAs)
+                    const float dx0 = __fadd_rn(fmaf(G[1], A[4], fmaf(G[0], A[0], 0.f)), __fmul_rn(G[2], A[8]));
+                    const float dx1 = __fadd_rn(fmaf(G[1], A[5], fmaf(G[0], A[1], 0.f)), __fmul_rn(G[2], A[9]));
+                    const float dx2 = __fadd_rn(__fmul_rn(G[0], A[2]), fmaf(G[2], A[10], fmaf(G[1], A[6], 0.f)));
+                    d0p[o] = dx0;
+                    d0p[HW + o] = dx1;
+                    d0p[2 * HW + o] = dx2;
+                }
+                if (dgp) dgp[o] = Df * (dlo + dhi);
+                const int pos = cnt[w * NB + bin] + __popc(m & ((1u << lane) - 1u));
+                rec[2 * pos] = make_float4(G[0], G[1], G[2], X[0]);
+                rec[2 * pos + 1] = make_float4(X[1], X[2], fz, __uint_as_float(((unsigned)r << 16) | (unsigned)c));
+            }
+            __syncwarp();
+            if (ok && lane == __ffs(m) - 1) cnt[w * NB + bin] += __popc(m);
+            __syncwarp();
+            r = r1;
+            cx = cx1;
+        }
+    }
+    __syncthreads();
+
+    // ---- phase 2: d_grid, lane pairs over the bin-sorted records (warp w: a contiguous
+    // chunk range); lane 2s+e owns record slot s and coefficient half q = 6e .. 6e+5
+    float *mywacc = wacc + w * 4 * D * 12;
+    const int cbeg = (int)(((long long)nchunks * w) / kWarps);
+    const int cend = (int)(((long long)nchunks * (w + 1)) / kWarps);
+    float2 acc2[24];
+#pragma unroll
+    for (int k = 0; k < 24; k++) acc2[k] = f2(0.f, 0.f);
+    auto flush2 = [&](int bin) {
+        float acc[48];
+#pragma unroll
+        for (int pl = 0; pl < 2; pl++)
+#pragma unroll
+            for (int bb = 0; bb < 2; bb++)
+#pragma unroll
+                for (int qq = 0; qq < 6; qq++) {
+                    acc[(pl * 4 + bb * 2 + 0) * 6 + qq] = acc2[(pl * 2 + bb) * 6 + qq].x;
+                    acc[(pl * 4 + bb * 2 + 1) * 6 + qq] = acc2[(pl * 2 + bb) * 6 + qq].y;
+                }
+        flush_acc(acc, mywacc, bin, D, lane);
+#pragma unroll
+        for (int k = 0; k < 24; k++) acc2[k] = f2(0.f, 0.f);
+    };
+    const int slot = lane >> 1;
+    const bool e1 = (lane & 1) != 0;
+    int cur_bin = cbeg < cend ? chunk_bin[cbeg] : 0;
+    for (int ch = cbeg; ch < cend; ch++) {
+        const int bin = chunk_bin[ch];
+        if (bin != cur_bin) {
+            flush2(cur_bin);
+            cur_bin = bin;
+        }
+        const float4 r0 = rec[2 * (ch * kChunk + slot)], r1 = rec[2 * (ch * kChunk + slot) + 1];
+        const unsigned rc = __float_as_uint(r1.w);
+        const float fx = fxt[rc & 0xffffu], fy = fyt[rc >> 16], fz = r1.z;
+        // this lane's half: P_q = G_oc Xt_i for q = 6e .. 6e+5 (q = 4 oc + i)
+        const float Gq[6] = {e1 ? r0.y : r0.x, e1 ? r0.y : r0.x, e1 ? r0.z : r0.x,
+                             e1 ? r0.z : r0.x, e1 ? r0.z : r0.y, e1 ? r0.z : r0.y};
+        const float Xq[6] = {e1 ? r1.y : r0.w, e1 ? 1.f : r1.x, e1 ? r0.w : r1.y,
+                             e1 ? r1.x : 1.f, e1 ? r1.y : r0.w, e1 ? 1.f : r1.x};
+        float2 wt2[4];
+        {
+            const float2 wx2 = f2(1.f - fx, fx);
+            const float wy[2] = {1.f - fy, fy}, wz[2] = {1.f - fz, fz};
+#pragma unroll
+            for (int pl = 0; pl < 2; pl++)
+#pragma unroll
+                for (int bb = 0; bb < 2; bb++) {
+                    const float wzy = wz[pl] * wy[bb];
+                    wt2[pl * 2 + bb] = __fmul2_rn(f2(wzy, wzy), wx2);
+                }
+        }
+#pragma unroll
+        for (int qq = 0; qq < 6; qq++) {
+            const float P = Gq[qq] * Xq[qq];
+            const float2 P2 = f2(P, P);
+#pragma unroll
+            for (int k = 0; k < 4; k++) acc2[k * 6 + qq] = __ffma2_rn(wt2[k], P2, acc2[k * 6 + qq]);
+        }
+    }
+    if (cbeg < cend) flush2(cur_bin);
+    __syncthreads();
+    // ---- block partial: fixed-order sum over warps
+    float *part = partials + (long long)blockIdx.x * 4 * D * 12;
+    for (int e = threadIdx.x; e < 4 * D * 12; e += kThreads) {
+        float s = 0.f;
+#pragma unroll
+        for (int ww = 0; ww < kWarps; ww++) s += wacc[ww * 4 * D * 12 + e];
+        part[e] = s;
+    }
+}
+
 // dgrid[n,q,z,y,x] = fixed-order sum of the partials of the dual cells whose
 // clamped corners are (y, x).  partial layout: [block][corner][z][q].
 __global__ void __launch_bounds__(kThreads)
@@ -920,6 +1216,41 @@ size_t bwd_smem(int D) {
            sizeof(float) * kTileXS * kTileYS + 16;
 }
 
+size_t split_smem(int D) {
+    const int NB = D + 1, maxch = kV2PX / kChunk + NB + 1;
+    return sizeof(float4) * ((size_t)maxch * kChunk * 2 + (size_t)NB * kBinS) +
+           sizeof(float) * ((size_t)kV2PX + kV2TX + 4 + kV2TY + 4 + (size_t)kWarps * 4 * D * 12) +
+           sizeof(int) * ((size_t)kWarps * NB + NB + 1 + maxch) + kV2PX + 16;
+}
+
+// Backward kernel choice.  bslice_bwd_split where its tile is a whole dual cell (cells of
+// <= kV2TX x kV2TY px, two blocks per SM: D <= 9) -- measured 238.6 vs 267.3 us at
+// 4 x 1024^2 / 32x32x8 and 855 vs 970 us at 4 x 2048^2 / 64x64x8; for larger cells
+// (split into sub-tiles, more d_grid flushes per pixel) bslice_bwd_tiled: 2.52 vs 2.59 ms
+// at 64 x 1024^2 / 16x16x8, 193.5 vs 191.5 us at 4 x 1024^2.  RSGRAD_BSLICE_BWD=split|tiled
+// forces one (A/B measurements and tests; read per call).
+bool use_split(int H, int W, int D, int Gh, int Gw) {
+    if (split_smem(D) > 113 * 1024) return false;
+    const char *e = getenv("RSGRAD_BSLICE_BWD");
+    if (e && strcmp(e, "tiled") == 0) return false;
+    if (e && strcmp(e, "split") == 0) return true;
+    const int maxw = (W + Gw - 1) / Gw, maxh = (H + Gh - 1) / Gh;
+    return maxw <= kV2TX && maxh <= kV2TY;
+}
+
+TileGeom tile_geom_split(int N, int H, int W, int D, int Gh, int Gw) {
+    TileGeom g = tile_geom(N, H, W, D, Gh, Gw);
+    const int maxw = (W + Gw - 1) / Gw, maxh = (H + Gh - 1) / Gh;
+    g.SX = (maxw + kV2TX - 1) / kV2TX;
+    g.SY = (maxh + kV2TY - 1) / kV2TY;
+    g.blocks = (long long)N * (Gh + 1) * (Gw + 1) * g.SY * g.SX;
+    return g;
+}
+
+TileGeom bwd_geom(int N, int H, int W, int D, int Gh, int Gw) {
+    return use_split(H, W, D, Gh, Gw) ? tile_geom_split(N, H, W, D, Gh, Gw) : tile_geom(N, H, W, D, Gh, Gw);
+}
+
 // The tiled backward needs bwd_smem(D) bytes of dynamic shared memory (2056 D + 80740:
 // 212 KB at D = 64); it is used only where the current device's opt-in limit allows.
 bool bwd_smem_fits(int D) {
@@ -949,7 +1280,7 @@ size_t bslice_bwd_ws_bytes(int N, int H, int W, int D, int Gh, int Gw, bool det)
 }
 
 size_t bslice_ws_bytes(int N, int H, int W, int D, int Gh, int Gw) {
-    const TileGeom g = tile_geom(N, H, W, D, Gh, Gw);
+    const TileGeom g = bwd_geom(N, H, W, D, Gh, Gw);
     if (!g.ok || !bwd_smem_fits(D)) return 0;
     return sizeof(float) * (size_t)g.blocks * 4 * D * 12 + sizeof(int) * (size_t)(Gh + Gw + 4);
 }
@@ -971,20 +1302,23 @@ cudaError_t bslice_fwd_launch(const BsliceArgs &a, cudaStream_t s) {
 
 cudaError_t bslice_bwd_launch(const BsliceArgs &a, int algo, int deterministic, void *ws,
                               size_t ws_bytes, cudaStream_t s) {
-    const TileGeom g = tile_geom(a.N, a.H, a.W, a.D, a.Gh, a.Gw);
+    const TileGeom g = bwd_geom(a.N, a.H, a.W, a.D, a.Gh, a.Gw);
+    const bool split = use_split(a.H, a.W, a.D, a.Gh, a.Gw);
     const bool tiled = g.ok && bwd_smem_fits(a.D) && algo != 3 /*SCATTER_ATOMIC*/ && (algo != 1 /*GATHER*/ || a.D > kNGDMax) && a.dgrid &&
                        ws_bytes >= bslice_ws_bytes(a.N, a.H, a.W, a.D, a.Gh, a.Gw);
     if (tiled) {
-        const size_t sm = bwd_smem(a.D);
+        const size_t sm = split ? split_smem(a.D) : bwd_smem(a.D);
         // per device and per call (the attribute belongs to the current device's context)
-        cudaError_t ea = cudaFuncSetAttribute(bslice_bwd_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaError_t ea = cudaFuncSetAttribute(split ? bslice_bwd_split : bslice_bwd_tiled,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (ea != cudaSuccess) return ea;
         float *partials = (float *)ws;
         int *tab = (int *)(partials + (size_t)g.blocks * 4 * a.D * 12);
         const int nt = (a.Gh > a.Gw ? a.Gh : a.Gw) + 2;
         bslice_bounds_kernel<<<(nt + 127) / 128, 128, 0, s>>>(tab, a.H, a.W, a.Gh, a.Gw);
         note_launch();
-        bslice_bwd_tiled<<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX, partials, tab);
+        if (split) bslice_bwd_split<<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX, partials, tab);
+        else bslice_bwd_tiled<<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX, partials, tab);
         note_launch();
         const long long total = (long long)a.N * 12 * a.D * a.Gh * a.Gw;
         bslice_dgrid_gather<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(

@@ -288,6 +288,27 @@ def test_bslice_parity(cuda_device, shape, guide):
     assert_close(_np(dgr), rgr, "grad", "dgrid")
 
 
+@pytest.mark.parametrize("shape", BS_SHAPES[:3] + [(2, 256, 192, 8, 4, 3), (1, 128, 128, 9, 4, 4)])
+@pytest.mark.parametrize("guide", ["uniform", "smooth"])
+def test_bslice_bwd_split_vs_tiled(cuda_device, monkeypatch, shape, guide):
+    """Both dual-cell backward kernels (RSGRAD_BSLICE_BWD=split|tiled) match the oracle;
+    their dX / d_guide share one summation order (bitwise equal), d_grid differs only
+    in how the pixel sums are split (sub-tiles, lane ranges)."""
+    N, H, W, D, Gh, Gw = shape
+    inp = synth.bslice_inputs(N, H, W, D, Gh, Gw, cfg=1, grid="iid", guide=guide)
+    g = _cuda(inp, cuda_device)
+    gr, gd, x, dy = (inp[k].double().numpy() for k in ("grid", "guide", "x", "dy"))
+    rgr, rgd, rdx = oracle.bslice_bwd(gr, gd, x, dy)
+    res = {}
+    for kern in ("split", "tiled"):
+        monkeypatch.setenv("RSGRAD_BSLICE_BWD", kern)
+        dgr, dgd, dx = res[kern] = rsgrad.bslice_bwd(g["grid"], g["guide"], g["x"], g["dy"])
+        assert_close(_np(dx), rdx, "grad", f"dx[{kern}]")
+        assert_close(_np(dgd), rgd, "grad", f"dguide[{kern}]")
+        assert_close(_np(dgr), rgr, "grad", f"dgrid[{kern}]")
+    assert torch.equal(res["split"][1], res["tiled"][1]) and torch.equal(res["split"][2], res["tiled"][2])
+
+
 def test_bslice_atomic_algo_and_determinism(cuda_device):
     inp = synth.bslice_inputs(2, 128, 96, 8, 8, 6, cfg=1)
     g = _cuda(inp, cuda_device)
