@@ -149,11 +149,14 @@ __global__ void __launch_bounds__(kT)
 template <class S>
 cudaError_t det_scatter_launch(const S &smp, const float *dy, float *dx, int N, int C, long long HW, long long P,
                                const int *list, const int *count, int *flags, void *ws, cudaStream_t s,
-                               int flag_on = 1) {
+                               int flag_on = 1, bool zero_slots = true, int max_blocks_per_sm = 4) {
     constexpr int kT = 256;
     const DetWs w = det_ws_layout(ws, N, (long long)C * HW);
-    cudaError_t e = cudaMemsetAsync(w.bar, 0, sizeof(unsigned) * ((size_t)N + 2), s);
-    if (e != cudaSuccess) return e;
+    cudaError_t e = cudaSuccess;
+    if (zero_slots) {  // (else the caller's previous kernel on s zeroed them)
+        e = cudaMemsetAsync(w.bar, 0, sizeof(unsigned) * ((size_t)N + 2), s);
+        if (e != cudaSuccess) return e;
+    }
     int dev = 0, nsm = 0, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -161,7 +164,7 @@ cudaError_t det_scatter_launch(const S &smp, const float *dy, float *dx, int N, 
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kT, 0);
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
-    const int blocks = nsm * (occ < 4 ? occ : 4);
+    const int blocks = nsm * (occ < max_blocks_per_sm ? occ : max_blocks_per_sm);
     S sm = smp;
     long long hw = HW, p = P;
     int n = N, c = C, fo = flag_on;

@@ -1092,8 +1092,11 @@ RS_DEV bool stn_lean_ok(const Affine &A, int Ho, int Wo) {
 }
 
 
+#ifndef RS_LMINB
+#define RS_LMINB 2
+#endif
 template <bool VEC>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, RS_LMINB)
     stn_bwd_lean(StnArgs a, const double *__restrict__ xtab, const double *__restrict__ ytab,
                  const int *__restrict__ flags, int tiles_x, int tiles_y) {
     extern __shared__ __align__(16) float4 sm4[];

@@ -267,9 +267,14 @@ constexpr int kHeavyFanin = 32;
 
 template <int CW, int R>
 __global__ void __launch_bounds__(kStripW * 32, RS_STRIP_MINB)
-    warp_bwd_strip(WarpArgs a, int tiles_x, int *__restrict__ heavy, int tag) {
+    warp_bwd_strip(WarpArgs a, int tiles_x, int *__restrict__ heavy, int tag, unsigned *__restrict__ det_zero = nullptr,
+                   int nzero = 0) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int n = blockIdx.y;
+    // the heavy-sample recompute's barrier / max slots, zeroed here instead of by a
+    // separate memset on the stream (the recompute kernel runs after this one)
+    if (det_zero && blockIdx.x == 0 && blockIdx.y == 0)
+        for (int e = threadIdx.x; e < nzero; e += blockDim.x) det_zero[e] = 0u;
     const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
     const int x = tx * 32 + lane;
     const bool xin = x < a.W;
@@ -803,16 +808,18 @@ cudaError_t warp_bwd_launch(const WarpArgs &a, int algo, int deterministic, void
         // heavy-sample flags (d_input only; none when the workspace cannot hold the fixed point)
         const bool rescue = a.dx && ws && ws_bytes >= warp_ws_bytes(a.N, a.C, a.H, a.W, false);
         int *heavy = rescue ? (int *)((char *)ws + det_align(det_ws_bytes(a.N, (long long)a.C * HW))) : nullptr;
+        unsigned *dz = rescue ? det_ws_layout(ws, a.N, (long long)a.C * HW).bar : nullptr;
+        const int nz = a.N + 2;
         // a fresh tag per call instead of clearing the flags (a stale match in reused memory
         // would only send that sample through the exact recompute)
         static std::atomic<unsigned> tags{0};
         const int tag = (int)(tags.fetch_add(1u) % 0x7ffffff0u) + 2;
 #define RS_STRIP(RR)                                                                                        \
     switch (CW) {                                                                                           \
-        case 1: warp_bwd_strip<1, RR><<<grid, kStripW * 32, 0, s>>>(a, tiles_x, heavy, tag); break;              \
-        case 2: warp_bwd_strip<2, RR><<<grid, kStripW * 32, 0, s>>>(a, tiles_x, heavy, tag); break;              \
-        case 3: warp_bwd_strip<3, RR><<<grid, kStripW * 32, 0, s>>>(a, tiles_x, heavy, tag); break;              \
-        default: warp_bwd_strip<4, RR><<<grid, kStripW * 32, 0, s>>>(a, tiles_x, heavy, tag); break;             \
+        case 1: warp_bwd_strip<1, RR><<<grid, kStripW * 32, 0, s>>>(a, tiles_x, heavy, tag, dz, nz); break;              \
+        case 2: warp_bwd_strip<2, RR><<<grid, kStripW * 32, 0, s>>>(a, tiles_x, heavy, tag, dz, nz); break;              \
+        case 3: warp_bwd_strip<3, RR><<<grid, kStripW * 32, 0, s>>>(a, tiles_x, heavy, tag, dz, nz); break;              \
+        default: warp_bwd_strip<4, RR><<<grid, kStripW * 32, 0, s>>>(a, tiles_x, heavy, tag, dz, nz); break;             \
     }
         if (R == 8) {
             RS_STRIP(8)
@@ -824,8 +831,9 @@ cudaError_t warp_bwd_launch(const WarpArgs &a, int algo, int deterministic, void
         if (heavy) {  // heavy samples only (the others exit at once): d_input in fixed point
             cudaError_t e = cudaGetLastError();
             if (e != cudaSuccess) return e;
+            // (slots zeroed by the strip kernel; one block per SM: the grid mostly exits at once)
             return det_scatter_launch(WarpTapSampler{a}, a.dy, a.dx, a.N, a.C, HW, HW, nullptr, nullptr, heavy, ws, s,
-                                      tag);
+                                      tag, false, 1);
         }
         return cudaGetLastError();
     }
