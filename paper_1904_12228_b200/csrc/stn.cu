@@ -1082,6 +1082,13 @@ constexpr int kLTY = kLRows * 8;          // 32 px rows per block
 constexpr int kLBufs = RS_LBUFS;  // dY stage buffers (1: the other block on the SM overlaps)
 constexpr int kLRQMax = 160, kLFQMax = 2304, kLStage = RS_LSTAGE, kLCH = RS_LCH;
 constexpr int kLCells = (kBX + 1) * (kLTY + 1);  // the block's floor cells: 32 columns x 33 rows
+#ifndef RS_LEAN_FXY
+#define RS_LEAN_FXY 1
+#endif
+#ifndef RS_LEAN_ROWMAX
+#define RS_LEAN_ROWMAX 1
+#endif
+constexpr int kLRTot = 8 * (kLRows + 1) > kLTY + 3 ? 8 * (kLRows + 1) : kLTY + 3;
 
 RS_DEV bool stn_lean_ok(const Affine &A, int Ho, int Wo) {
     if (!A.inv || Ho > 65535 || Wo > 65535) return false;
@@ -1114,8 +1121,8 @@ __global__ void __launch_bounds__(kThreads, RS_LMINB)
     int *ctl = qcnt + kLRQMax;                                  // 8
     int *cstart = ctl + 8;                                      // kLCells: first hit of each cell
     int *cfill = cstart + kLCells;                              // kLCells: hit counts, then fill ends
-    int *rtot = cfill + kLCells;                                // kLTY + 1 (+ pad): per cell row totals
-    unsigned short *hits = (unsigned short *)(rtot + kLTY + 3); // kLFQMax: record indices, by cell
+    int *rtot = cfill + kLCells;                                // kLRTot: cell row totals, then warp row hit maxima
+    unsigned short *hits = (unsigned short *)(rtot + kLRTot);   // kLFQMax: record indices, by cell
     __shared__ unsigned long long bars[2];  // stage completion (cp.async.mbarrier.arrive), one per stage
 
     const int n = blockIdx.y;
@@ -1247,7 +1254,7 @@ __global__ void __launch_bounds__(kThreads, RS_LMINB)
         }
         __syncwarp();
         rtot[lane] = t - v0;
-        if (lane == 31) rtot[32] += t;  // row 32 starts after rows 0..31
+        if (lane == 31) rtot[32] = t;  // row 32 starts after rows 0..31
     }
     __syncthreads();
     for (int c = threadIdx.x; c < kLCells; c += kThreads) {
@@ -1275,6 +1282,38 @@ __global__ void __launch_bounds__(kThreads, RS_LMINB)
         }
     }
     __syncthreads();
+    // the walk reads a hit's fractions in list order: (fx, fy) as float2 at its list
+    // position, over the records (no longer needed), and each warp row's maximum hit
+    // count once (the walk runs every cell row once per channel chunk)
+    {
+        const int nh = cfill[kLCells - 1];
+        float2 fr[(kLFQMax + kThreads - 1) / kThreads];
+#pragma unroll
+        for (int k = 0; k < (kLFQMax + kThreads - 1) / kThreads; k++) {
+            const int pos = threadIdx.x + k * kThreads;
+            if (pos < nh) {
+                const uint2 R = rec[hits[pos]];
+                fr[k] = make_float2((float)(R.x & 0xffffffu) * (1.f / 16777216.f),
+                                    (float)(R.y & 0xffffffu) * (1.f / 16777216.f));
+            }
+        }
+        for (int rr = 0; rr <= kLRows; rr++) {
+            const int cell = (kLRows * warp + rr) * (kBX + 1) + lane;
+            const int m = __reduce_max_sync(0xffffffffu, cfill[cell] - cstart[cell]);
+            if (lane == 0) rtot[warp * (kLRows + 1) + rr] = m;  // (row totals no longer needed)
+        }
+        __syncthreads();
+        float2 *fxy = (float2 *)rec;
+#pragma unroll
+        for (int k = 0; k < (kLFQMax + kThreads - 1) / kThreads; k++) {
+            const int pos = threadIdx.x + k * kThreads;
+            if (RS_LEAN_FXY && pos < nh) fxy[pos] = fr[k];
+        }
+    }
+    __syncthreads();
+    const float2 *fxy = (const float2 *)rec;
+    const uint2 *recs = rec;
+    const int *rowmax = rtot + warp * (kLRows + 1);
 
     // every warp walks its own halo cell row: rows wy0-1 .. wy0+kLRows-1 (cell rows
     // 4 warp .. 4 warp + 4 of the block; lane = cell column)
@@ -1292,10 +1331,16 @@ __global__ void __launch_bounds__(kThreads, RS_LMINB)
             const int y0 = wy0 - 1 + rr;
 #pragma unroll
             for (int c = 0; c < NC; c++) { L[c] = NL[c]; Rr[c] = NR[c]; NL[c] = 0.f; NR[c] = 0.f; }
-            auto process = [&](int e) {
-                const uint2 R = rec[e];
+            auto process = [&](int pos) {
+                const int e = hits[pos];
+#if RS_LEAN_FXY
+                const float2 f = fxy[pos];
+                const float fx = f.x, fy = f.y;
+#else
+                const uint2 R = recs[e];
                 const float fx = (float)(R.x & 0xffffffu) * (1.f / 16777216.f);
                 const float fy = (float)(R.y & 0xffffffu) * (1.f / 16777216.f);
+#endif
                 const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx;
                 const float w10 = fy * (1.f - fx), w11 = fy * fx;
                 const float *Se = S + e;
@@ -1310,9 +1355,13 @@ __global__ void __launch_bounds__(kThreads, RS_LMINB)
             };
             const int cell = (kLRows * warp + rr) * (kBX + 1) + lane;
             const int hb = cstart[cell], hn = cfill[cell] - hb;
+#if RS_LEAN_ROWMAX
+            const int hmax = rowmax[rr];
+#else
             const int hmax = __reduce_max_sync(0xffffffffu, hn);
+#endif
             for (int h = 0; h < hmax; h++)
-                if (h < hn) process(hits[hb + h]);
+                if (h < hn) process(hb + h);
             if (rr > 0) {  // row 0 is the halo: it only seeds the carry
                 const bool wr = pxin && y0 < a.H;
 #pragma unroll
@@ -1870,7 +1919,7 @@ size_t out_tile_smem() {
 }
 size_t bwd_lean_smem() {
     return sizeof(float) * kLBufs * kLStage + sizeof(uint2) * kLFQMax + sizeof(int4) * kLRQMax +
-           sizeof(int) * (5 * kLRQMax + 8 + 2 * kLCells + kLTY + 3) + sizeof(unsigned short) * kLFQMax;
+           sizeof(int) * (5 * kLRQMax + 8 + 2 * kLCells + kLRTot) + sizeof(unsigned short) * kLFQMax;
 }
 
 size_t bwd_gather_smem() {
