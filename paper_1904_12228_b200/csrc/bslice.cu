@@ -249,52 +249,74 @@ __global__ void __launch_bounds__(kThreads)
     // plane and of the plane difference, for every (bin, q), bins kPlaneStride float4
     // apart (conflict-free across bins): one LDS.128 per coefficient and pixel
     float4 *rt = (float4 *)(fyt + kTileYS) + w * kPlaneStride * NB;
-    for (int r = w; r < TH; r += kWarps) {
-        const float fy = fyt[r];
-        __syncwarp();
-        for (int e = lane; e < 12 * NB; e += 32) {
-            const int b = e / 12, q = e - b * 12;
-            const float4 L = glo[b * kPlaneStride + q], Dz = gdz[b * kPlaneStride + q];
-            rt[b * kPlaneStride + q] = make_float4(fmaf(fy, L.z, L.x), fmaf(fy, L.w, L.y), fmaf(fy, Dz.z, Dz.x),
-                                                   fmaf(fy, Dz.w, Dz.y));
-        }
-        __syncwarp();
+    // the warp's items: (row r, 64-column pair segment cx), two pixels per lane; the next
+    // item's guide and X loads are issued before the current item is computed (a small
+    // dual cell has one item per row: without the prefetch every row waits a round trip)
+    const int ncx = (TW + 63) >> 6;
+    float gn[2] = {0.f, 0.f}, xn[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
+    auto fetch = [&](int r, int cx) {
+        if (r >= TH) return;
         const long long rowoff = (long long)(t.ys + r) * a.W + t.xs;
-        // two pixels per lane per step, their loads issued together
-        for (int c0 = lane; c0 < TW; c0 += 64) {
-            float gv[2], xv[2][3];
-            bool ok[2];
 #pragma unroll
-            for (int k = 0; k < 2; k++) {
-                const int c = c0 + 32 * k;
-                ok[k] = c < TW;
-                const long long o = rowoff + (ok[k] ? c : 0);
-                gv[k] = ok[k] ? ldg_stream(gd + o) : 0.f;
+        for (int k = 0; k < 2; k++) {
+            const int c = cx * 64 + lane + 32 * k;
+            const bool ok = c < TW;
+            const long long o = rowoff + (ok ? c : 0);
+            gn[k] = ok ? ldg_stream(gd + o) : 0.f;
 #pragma unroll
-                for (int i = 0; i < 3; i++) xv[k][i] = ok[k] ? ldg_stream(xp + i * HW + o) : 0.f;
+            for (int i = 0; i < 3; i++) xn[k][i] = ok ? ldg_stream(xp + i * HW + o) : 0.f;
+        }
+    };
+    fetch(w, 0);
+    int r = w, cx = 0;
+    while (r < TH) {
+        float gv[2], xv[2][3];
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+            gv[k] = gn[k];
+#pragma unroll
+            for (int i = 0; i < 3; i++) xv[k][i] = xn[k][i];
+        }
+        const int cx1 = cx + 1 < ncx ? cx + 1 : 0, r1 = cx + 1 < ncx ? r : r + kWarps;
+        fetch(r1, cx1);
+        if (cx == 0) {
+            // per-warp row table: for the row's fy, (a + fy c, b + fy d) of the low plane
+            // and of the plane difference, for every (bin, q), bins kPlaneStride float4
+            // apart (conflict-free across bins): one LDS.128 per coefficient and pixel
+            const float fy = fyt[r];
+            __syncwarp();
+            for (int e = lane; e < 12 * NB; e += 32) {
+                const int b = e / 12, q = e - b * 12;
+                const float4 L = glo[b * kPlaneStride + q], Dz = gdz[b * kPlaneStride + q];
+                rt[b * kPlaneStride + q] = make_float4(fmaf(fy, L.z, L.x), fmaf(fy, L.w, L.y), fmaf(fy, Dz.z, Dz.x),
+                                                       fmaf(fy, Dz.w, Dz.y));
             }
+            __syncwarp();
+        }
+        const long long rowoff = (long long)(t.ys + r) * a.W + t.xs;
 #pragma unroll
-            for (int k = 0; k < 2; k++) {
-                if (!ok[k]) continue;
-                const int c = c0 + 32 * k;
-                const long long o = rowoff + c;
-                const float fx = fxt[c];
-                int bin;
-                float fz;
-                z_cell(gv[k], a.D, bin, fz);
-                const float4 *T = rt + bin * kPlaneStride;
+        for (int k = 0; k < 2; k++) {
+            const int c = cx * 64 + lane + 32 * k;
+            if (c >= TW) continue;
+            const long long o = rowoff + c;
+            const float fx = fxt[c];
+            int bin;
+            float fz;
+            z_cell(gv[k], a.D, bin, fz);
+            const float4 *T = rt + bin * kPlaneStride;
 #pragma unroll
-                for (int oc = 0; oc < 3; oc++) {
-                    float A[4];
+            for (int oc = 0; oc < 3; oc++) {
+                float A[4];
 #pragma unroll
-                    for (int i = 0; i < 4; i++) {
-                        const float4 v = T[4 * oc + i];
-                        A[i] = fmaf(fz, fmaf(fx, v.w, v.z), fmaf(fx, v.y, v.x));
-                    }
-                    yp[oc * HW + o] = fmaf(A[0], xv[k][0], fmaf(A[1], xv[k][1], fmaf(A[2], xv[k][2], A[3])));
+                for (int i = 0; i < 4; i++) {
+                    const float4 v = T[4 * oc + i];
+                    A[i] = fmaf(fz, fmaf(fx, v.w, v.z), fmaf(fx, v.y, v.x));
                 }
+                yp[oc * HW + o] = fmaf(A[0], xv[k][0], fmaf(A[1], xv[k][1], fmaf(A[2], xv[k][2], A[3])));
             }
         }
+        r = r1;
+        cx = cx1;
     }
 }
 
@@ -617,7 +639,13 @@ __global__ void __launch_bounds__(kThreads, 2)
 //           the same reduce-scatter as bslice_bwd_tiled, one partial per (tile, corner).
 // Sub-tiles are at most kV2TX x kV2TY px so two blocks fit per SM.  (PAPER.md:36-42
 // slice-apply; PAPER.md:700-731 bounded-footprint gather for d_grid.)
-constexpr int kV2TX = 64, kV2TY = 32;                 // nominal max sub-tile (px)
+#ifndef RS_V2TY
+#define RS_V2TY 32
+#endif
+#ifndef RS_V2MINB
+#define RS_V2MINB 2
+#endif
+constexpr int kV2TX = 64, kV2TY = RS_V2TY;            // nominal max sub-tile (px)
 constexpr int kV2PX = (kV2TX + 2) * (kV2TY + 2);      // per-tile pixel capacity (+1 rounding slack per axis)
 constexpr int kBinS = 25;                             // float4 per bin in gi (24 + 1: lanes on different bins hit different banks)
 
@@ -644,7 +672,7 @@ RS_DEV void stage_corners_b(float4 *gi, const float *grid, const Tile &t, int D,
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, RS_V2MINB)
     bslice_bwd_split(BsliceArgs a, int SY, int SX, float *__restrict__ partials, const int *__restrict__ tab) {
     extern __shared__ float4 smem4[];
     const int D = a.D, NB = D + 1;
@@ -1230,7 +1258,7 @@ size_t split_smem(int D) {
 // at 64 x 1024^2 / 16x16x8, 193.5 vs 191.5 us at 4 x 1024^2.  RSGRAD_BSLICE_BWD=split|tiled
 // forces one (A/B measurements and tests; read per call).
 bool use_split(int H, int W, int D, int Gh, int Gw) {
-    if (split_smem(D) > 113 * 1024) return false;
+    if (split_smem(D) > (RS_V2MINB >= 2 ? 113 : 226) * 1024) return false;
     const char *e = getenv("RSGRAD_BSLICE_BWD");
     if (e && strcmp(e, "tiled") == 0) return false;
     if (e && strcmp(e, "split") == 0) return true;
