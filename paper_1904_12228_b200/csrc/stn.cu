@@ -2010,6 +2010,37 @@ cudaError_t flow_tile_launch(const StnArgs &a, int mode, bool priv, cudaStream_t
     return cudaGetLastError();
 }
 
+// Side stream + fork/join events for running the d_theta tiles beside the lean d_input
+// kernel, once per (host thread, device): no sharing between threads, so concurrent
+// calls stay re-entrant; stream-capture safe (the side stream joins a capture through
+// the fork event).  Released with the CUDA context.
+struct StnFork {
+    bool made = false;
+    cudaStream_t side;
+    cudaEvent_t fork, join;
+};
+StnFork *stn_fork() {
+    static thread_local StnFork f[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    StnFork &x = f[dev];
+    if (!x.made) {
+        if (cudaStreamCreateWithFlags(&x.side, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming);
+        x.made = true;
+    }
+    return &x;
+}
+
+// Concurrent d_theta tiles and lean d_input when the lean grid is at most this many blocks
+// (small batches: both grids end in a partial wave, which the other kernel fills; a
+// large batch fills the GPU with either alone -- measured no gain at 64 x 1024^2)
+int stn_fork_blocks() {
+    const char *e = getenv("RSGRAD_STN_FORK");
+    return e ? atoi(e) : 4096;
+}
+
 cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *ws, size_t ws_bytes,
                            cudaStream_t s) {
     (void)ws_bytes;
@@ -2032,11 +2063,21 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
     const bool vin = (a.W % 4 == 0) && aligned16(a.x);
     const bool vout = (a.Wo % 4 == 0) && aligned16(a.dy);
     int tiles_b = g.bx * g.by;
+    cudaStream_t sdt = s;  // stream of the d_theta tiles
+    StnFork *fk = nullptr;
     if (allow_gather && variant == 2) {
         // lean dX kernel; every sample's d_theta comes from the output-tile kernel
         const size_t sm = bwd_lean_smem();
         const int ly = (a.H + kLTY - 1) / kLTY;
         dim3 grid(g.bx * ly, a.N);
+        const bool fast_dth = a.dtheta && (a.W % 4 == 0) && aligned16(a.x) && (a.Wo % 4 == 0) && aligned16(a.dy) &&
+                              !stn_slow_tiles();
+        if (a.dx && fast_dth && (long long)grid.x * grid.y <= stn_fork_blocks() && (fk = stn_fork()) != nullptr) {
+            cudaError_t e = cudaEventRecord(fk->fork, s);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(fk->side, fk->fork, 0);
+            if (e != cudaSuccess) return e;
+            sdt = fk->side;
+        }
         if (a.dx) {
             if (vout) {
                 set_smem(stn_bwd_lean<true>, sm);
@@ -2088,8 +2129,13 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
             auto k = stn_out_tile<MODE_DTHETA, true, false, kFIdf, true>;
             set_smem(k, sm);
             grid.x = g.fj * fi_df;
-            k<<<grid, kOTFast, sm, s>>>(a, w.xtab, w.ytab, nullptr, w.fb_count, w.pf, g.fj, fi_df,
-                                        RS_DTH_LASTBLOCK ? w.ctr : nullptr);
+            k<<<grid, kOTFast, sm, sdt>>>(a, w.xtab, w.ytab, nullptr, w.fb_count, w.pf, g.fj, fi_df,
+                                          RS_DTH_LASTBLOCK ? w.ctr : nullptr);
+            if (sdt != s) {  // join: the finalize (and the caller) see the tiles' partials
+                cudaError_t e = cudaEventRecord(fk->join, sdt);
+                if (e == cudaSuccess) e = cudaStreamWaitEvent(s, fk->join, 0);
+                if (e != cudaSuccess) return e;
+            }
         } else if (priv && !dth_all) {  // fallback samples: d_theta and privatised d_input
             auto k = vin ? stn_out_tile<MODE_DTHETA, true, false, kFIdth, false, true>
                          : stn_out_tile<MODE_DTHETA, false, false, kFIdth, false, true>;
