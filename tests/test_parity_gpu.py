@@ -98,6 +98,25 @@ def test_stn_fallback_samples_priv_and_atomic(cuda_device):
         assert_close(_np(dth), rdth, "grad", f"dtheta [{algo}]")
 
 
+@pytest.mark.parametrize("fork", ["0", "100000"])
+def test_stn_bwd_fork(cuda_device, monkeypatch, fork):
+    """The d_theta tiles on the library side stream beside the lean d_input kernel, or
+    after it on the caller's stream: both match the oracle and agree bitwise."""
+    monkeypatch.setenv("RSGRAD_STN_FORK", fork)
+    inp = synth.stn_inputs(3, 16, 80, 96, cfg=1)
+    g = _cuda(inp, cuda_device)
+    y = rsgrad.stn_fwd(g["x"], g["theta"])
+    dx, dth = rsgrad.stn_bwd(g["x"], g["theta"], g["dy"])
+    x, th, dy = (inp[k].double().numpy() for k in ("x", "theta", "dy"))
+    assert_close(_np(y), oracle.stn_fwd(x, th), "fwd", "y")
+    rdx, rdth = oracle.stn_bwd(x, th, dy)
+    assert_close(_np(dx), rdx, "grad", "dx")
+    assert_close(_np(dth), rdth, "grad", "dtheta")
+    monkeypatch.setenv("RSGRAD_STN_FORK", "0" if fork != "0" else "100000")
+    dx2, dth2 = rsgrad.stn_bwd(g["x"], g["theta"], g["dy"])
+    assert torch.equal(dx, dx2) and torch.equal(dth, dth2)
+
+
 def test_stn_singular_theta_falls_back(cuda_device):
     """A rank-deficient theta has no bounded preimage: AUTO must take the atomic scatter."""
     inp = synth.stn_inputs(3, 4, 20, 24, cfg=1)
