@@ -98,6 +98,26 @@ def test_stn_fallback_samples_priv_and_atomic(cuda_device):
         assert_close(_np(dth), rdth, "grad", f"dtheta [{algo}]")
 
 
+@pytest.mark.parametrize("scale", [0.79, 0.85])
+def test_stn_lean_near_record_cap(cuda_device, scale):
+    """Zoomed-in affine maps (scale < 1: ~1/s^2 output pixels per input cell) fill the lean
+    kernel's per-tile record and hit-list buffers close to their caps (2304 records) at
+    every rotation; d_input is still the gather (no fallback) and matches the oracle."""
+    import math
+    N = 4
+    inp = synth.stn_inputs(N, 4, 96, 128, cfg=1)
+    for n in range(N):
+        a = math.radians(15.0 * n)
+        inp["theta"][n] = torch.tensor([[scale * math.cos(a), -scale * math.sin(a), 0.05],
+                                        [scale * math.sin(a), scale * math.cos(a), -0.03]])
+    g = _cuda(inp, cuda_device)
+    dx, dth = rsgrad.stn_bwd(g["x"], g["theta"], g["dy"], deterministic=True)
+    x, th, dy = (inp[k].double().numpy() for k in ("x", "theta", "dy"))
+    rdx, rdth = oracle.stn_bwd(x, th, dy)
+    assert_close(_np(dx), rdx, "grad", "dx")
+    assert_close(_np(dth), rdth, "grad", "dtheta")
+
+
 @pytest.mark.parametrize("fork", ["0", "100000"])
 def test_stn_bwd_fork(cuda_device, monkeypatch, fork):
     """The d_theta tiles on the library side stream beside the lean d_input kernel, or
