@@ -104,22 +104,12 @@ __global__ void __launch_bounds__(kThreads) warp_fwd_kernel(WarpArgs a, double i
     }
 }
 
-// PX pixels per thread (rem0 + k * kThreads, k < PX): every flow load, then every tap
-// load of a channel for all PX pixels, are issued before their first use (memory-level
-// parallelism for the latency-bound gather).
+// One group of PX pixels per thread (base + k * kThreads, k < PX) of sample n, flow values
+// already loaded: every tap load of a channel for all PX pixels is issued before its
+// first use (memory-level parallelism for the latency-bound gather).
 template <int PX>
-__global__ void __launch_bounds__(kThreads) warp_fwd_px(WarpArgs a, double invW) {
+RS_DEV void warp_fwd_group(const WarpArgs &a, double invW, int n, int base, const float *u, const float *v) {
     const int HW = a.H * a.W;
-    const int base = blockIdx.x * kThreads * PX + threadIdx.x;
-    const int n = blockIdx.y;
-    const float *fp = a.flow + (long long)n * 2 * HW;
-    float u[PX], v[PX];
-#pragma unroll
-    for (int k = 0; k < PX; k++) {
-        const int rem = min(base + k * kThreads, HW - 1);
-        u[k] = ldg_stream(fp + rem);
-        v[k] = ldg_stream(fp + HW + rem);
-    }
     int o[PX];
     float w[PX][4];
 #pragma unroll
@@ -173,6 +163,54 @@ __global__ void __launch_bounds__(kThreads) warp_fwd_px(WarpArgs a, double invW)
         }
         xp += HW;
         yp += HW;
+    }
+}
+
+// PX pixels per thread, one group per thread
+template <int PX>
+__global__ void __launch_bounds__(kThreads) warp_fwd_px(WarpArgs a, double invW) {
+    const int HW = a.H * a.W;
+    const int base = blockIdx.x * kThreads * PX + threadIdx.x;
+    const int n = blockIdx.y;
+    const float *fp = a.flow + (long long)n * 2 * HW;
+    float u[PX], v[PX];
+#pragma unroll
+    for (int k = 0; k < PX; k++) {
+        const int rem = min(base + k * kThreads, HW - 1);
+        u[k] = ldg_stream(fp + rem);
+        v[k] = ldg_stream(fp + HW + rem);
+    }
+    warp_fwd_group<PX>(a, invW, n, base, u, v);
+}
+
+// G consecutive groups of PX pixels per thread; the next group's flow loads are issued
+// before the current group's taps (the flow -> coordinate -> tap dependency otherwise
+// exposes one full memory round trip per group)
+template <int PX, int G>
+__global__ void __launch_bounds__(kThreads) warp_fwd_pipe(WarpArgs a, double invW) {
+    const int HW = a.H * a.W;
+    const int per = kThreads * PX;
+    const int b0 = blockIdx.x * per * G;
+    const int n = blockIdx.y;
+    const float *fp = a.flow + (long long)n * 2 * HW;
+    float un[PX], vn[PX];
+    auto fetch = [&](int g) {
+#pragma unroll
+        for (int k = 0; k < PX; k++) {
+            const int rem = min(b0 + g * per + k * kThreads + (int)threadIdx.x, HW - 1);
+            un[k] = ldg_stream(fp + rem);
+            vn[k] = ldg_stream(fp + HW + rem);
+        }
+    };
+    fetch(0);
+#pragma unroll 1
+    for (int g = 0; g < G; g++) {
+        if (b0 + g * per >= HW) break;  // block-uniform
+        float u[PX], v[PX];
+#pragma unroll
+        for (int k = 0; k < PX; k++) { u[k] = un[k]; v[k] = vn[k]; }
+        if (g + 1 < G) fetch(g + 1);
+        warp_fwd_group<PX>(a, invW, n, b0 + g * per + (int)threadIdx.x, u, v);
     }
 }
 
@@ -754,7 +792,18 @@ cudaError_t warp_fwd_launch(const WarpArgs &a, cudaStream_t s) {
         const char *e = getenv("RSGRAD_WARP_FWD_PX");
         return e ? atoi(e) : 2;  // 2 px per thread: 0.703 vs 0.768 ms at 64 x 1024^2 (4: 1.01)
     }();
-    if (px == 2 || px == 4) {
+    // four pixel pairs per thread with the flow of the next pair prefetched (0.70 -> 0.64 ms
+    // at 64 x 1024^2) when the grid stays many waves deep; small batches keep one pair per
+    // thread (configs[2]: 26.6 vs 32.8 us with four -- a quarter of the blocks)
+    const char *eg = getenv("RSGRAD_WARP_FWD_G");  // (read per call: tests switch it)
+    const int groups = eg ? atoi(eg) : ((long long)a.N * HW >= (16LL << 20) ? 4 : 1);
+    if (px == 2 && groups == 4) {
+        const int per = kThreads * 2 * 4;
+        warp_fwd_pipe<2, 4><<<dim3((HW + per - 1) / per, a.N), kThreads, 0, s>>>(a, 1.0 / a.W);
+    } else if (px == 2 && groups == 2) {
+        const int per = kThreads * 2 * 2;
+        warp_fwd_pipe<2, 2><<<dim3((HW + per - 1) / per, a.N), kThreads, 0, s>>>(a, 1.0 / a.W);
+    } else if (px == 2 || px == 4) {
         const int per = kThreads * px;
         if (px == 2) warp_fwd_px<2><<<dim3((HW + per - 1) / per, a.N), kThreads, 0, s>>>(a, 1.0 / a.W);
         else warp_fwd_px<4><<<dim3((HW + per - 1) / per, a.N), kThreads, 0, s>>>(a, 1.0 / a.W);

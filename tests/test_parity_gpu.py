@@ -118,6 +118,18 @@ def test_stn_lean_near_record_cap(cuda_device, scale):
     assert_close(_np(dth), rdth, "grad", "dtheta")
 
 
+@pytest.mark.parametrize("groups", ["1", "2", "4"])
+@pytest.mark.parametrize("flow", ["smooth", "stress"])
+def test_warp_fwd_pixel_groups(cuda_device, monkeypatch, groups, flow):
+    """warp_fwd with 1, 2 or 4 pixel pairs per thread (the pipelined kernel prefetches the
+    next pair's flow), ragged sizes so the last block's groups run past the image."""
+    monkeypatch.setenv("RSGRAD_WARP_FWD_G", groups)
+    inp = synth.warp_inputs(3, 3, 37, 101, cfg=1, flow=flow)
+    g = _cuda(inp, cuda_device)
+    y = rsgrad.warp_fwd(g["x"], g["flow"])
+    assert_close(_np(y), oracle.warp_fwd(inp["x"].double().numpy(), inp["flow"].double().numpy()), "fwd", "y")
+
+
 @pytest.mark.parametrize("fork", ["0", "100000"])
 def test_stn_bwd_fork(cuda_device, monkeypatch, fork):
     """The d_theta tiles on the library side stream beside the lean d_input kernel, or
