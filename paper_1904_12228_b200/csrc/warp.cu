@@ -417,26 +417,34 @@ __global__ void __launch_bounds__(kStripW * 32, RS_STRIP_MINB)
             }
         };
 
-        float un = 0.f, vn = 0.f;
+        float un = 0.f, vn = 0.f, gn[CW];
+#pragma unroll
+        for (int c = 0; c < CW; c++) gn[c] = 0.f;
         if (xin) {
             un = ldg_stream(fs + ybeg * a.W + x);
             vn = ldg_stream(fs + HW + ybeg * a.W + x);
+#pragma unroll
+            for (int c = 0; c < CW; c++)
+                if (c < cn) gn[c] = ldg_stream(gs + (long long)c * HW + ybeg * a.W + x);
         }
 #pragma unroll 1
         for (int y = ybeg; y < yend; y++) {
             const float u = un, v = vn;
-            if (xin && y + 1 < yend) {  // prefetch the next row's flow
+            float g[CW];
+#pragma unroll
+            for (int c = 0; c < CW; c++) g[c] = gn[c];
+            if (xin && y + 1 < yend) {  // prefetch the next row's flow and dY
                 un = ldg_stream(fs + (y + 1) * a.W + x);
                 vn = ldg_stream(fs + HW + (y + 1) * a.W + x);
+#pragma unroll
+                for (int c = 0; c < CW; c++)
+                    if (c < cn) gn[c] = ldg_stream(gs + (long long)c * HW + (y + 1) * a.W + x);
             }
             float cgx, cgy;
             Tap t = warp_tap(a, xin ? x : 0, y, u, v, cgx, cgy);
             if (!xin) t.k00 = t.k01 = t.k10 = t.k11 = false;
             const bool tany = t.k00 || t.k01 || t.k10 || t.k11;
             const int rem = y * a.W + (xin ? x : 0);
-            float g[CW];
-#pragma unroll
-            for (int c = 0; c < CW; c++) g[c] = (xin && c < cn) ? ldg_stream(gs + (long long)c * HW + rem) : 0.f;
             // relation of this row's cell to the pending one
             const bool same = have && t.x0 == pcx && t.y0 == pcy;
             const bool down = have && t.x0 == pcx && t.y0 == pcy + 1;
