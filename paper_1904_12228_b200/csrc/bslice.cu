@@ -672,6 +672,7 @@ RS_DEV void stage_corners_b(float4 *gi, const float *grid, const Tile &t, int D,
     }
 }
 
+template <bool kMulti>
 __global__ void __launch_bounds__(kThreads, RS_V2MINB)
     bslice_bwd_split(BsliceArgs a, int SY, int SX, float *__restrict__ partials, const int *__restrict__ tab) {
     extern __shared__ float4 smem4[];
@@ -688,11 +689,48 @@ __global__ void __launch_bounds__(kThreads, RS_V2MINB)
     int *chunk_bin = bstart + NB + 1;                      // maxch
     unsigned char *binv = (unsigned char *)(chunk_bin + maxch);  // kV2PX
 
-    const Tile t = tile_of_tab(blockIdx.x, a.Gh, a.Gw, SY, SX, tab);
-    const int TW = t.xe - t.xs, TH = t.ye - t.ys;
+    // the block owns a whole dual cell (column split SX); its rows are walked as
+    // sub-tiles of <= kV2TY rows (the records hold 32 B per pixel)
+    const Tile tc = tile_of_tab(blockIdx.x, a.Gh, a.Gw, SY, SX, tab);
+    const int TW = tc.xe - tc.xs, THc = tc.ye - tc.ys;
+    const int nsub = (THc + kV2TY - 1) / kV2TY;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const long long HW = (long long)a.H * a.W;
+    stage_corners_b(gi, a.grid, tc, D, a.Gh, a.Gw);
+    for (int c = threadIdx.x; c < TW; c += kThreads) {
+        const double cx = bs_cx(tc.xs + c, a.W, a.Gw);
+        fxt[c] = (float)__dsub_rn(cx, floor(cx));
+    }
+    for (int e = threadIdx.x; e < kWarps * 4 * D * 12; e += kThreads) wacc[e] = 0.f;
+    float *mywacc = wacc + w * 4 * D * 12;
+    float2 acc2[24];
+#pragma unroll
+    for (int k = 0; k < 24; k++) acc2[k] = f2(0.f, 0.f);
+    auto flush2 = [&](int bin) {
+        float acc[48];
+#pragma unroll
+        for (int pl = 0; pl < 2; pl++)
+#pragma unroll
+            for (int bb = 0; bb < 2; bb++)
+#pragma unroll
+                for (int qq = 0; qq < 6; qq++) {
+                    acc[(pl * 4 + bb * 2 + 0) * 6 + qq] = acc2[(pl * 2 + bb) * 6 + qq].x;
+                    acc[(pl * 4 + bb * 2 + 1) * 6 + qq] = acc2[(pl * 2 + bb) * 6 + qq].y;
+                }
+        flush_acc(acc, mywacc, bin, D, lane);
+#pragma unroll
+        for (int k = 0; k < 24; k++) acc2[k] = f2(0.f, 0.f);
+    };
+    const int slot = lane >> 1;
+    const bool e1 = (lane & 1) != 0;
+    int cur_bin = -1;  // bin of the pending register sums (-1: none)
+    for (int sub = 0; sub < nsub; sub++) {
+    Tile t = tc;
+    t.ys = tc.ys + (int)(((long long)THc * sub) / nsub);
+    t.ye = tc.ys + (int)(((long long)THc * (sub + 1)) / nsub);
+    const int TH = t.ye - t.ys;
     const long long tbase = (long long)t.ys * a.W + t.xs;  // tile origin within a plane
+    __syncthreads();  // the previous sub-tile's records, bins and counts are consumed
     {  // guide tile -> smem (cp.async; overlaps the corner staging below)
         const float *gd = a.guide + (long long)t.n * HW + tbase;
         const bool vec = (TW % 4 == 0) && (a.W % 4 == 0) && (t.xs % 4 == 0) && (((uintptr_t)a.guide & 15u) == 0);
@@ -705,16 +743,10 @@ __global__ void __launch_bounds__(kThreads, RS_V2MINB)
         }
         cp_async_commit();
     }
-    stage_corners_b(gi, a.grid, t, D, a.Gh, a.Gw);
-    for (int c = threadIdx.x; c < TW; c += kThreads) {
-        const double cx = bs_cx(t.xs + c, a.W, a.Gw);
-        fxt[c] = (float)__dsub_rn(cx, floor(cx));
-    }
     for (int r = threadIdx.x; r < TH; r += kThreads) {
         const double cy = bs_cx(t.ys + r, a.H, a.Gh);
         fyt[r] = (float)__dsub_rn(cy, floor(cy));
     }
-    for (int e = threadIdx.x; e < kWarps * 4 * D * 12; e += kThreads) wacc[e] = 0.f;
     for (int e = threadIdx.x; e < kWarps * NB; e += kThreads) cnt[e] = 0;
     cp_async_wait<0>();
     __syncthreads();
@@ -857,66 +889,57 @@ __global__ void __launch_bounds__(kThreads, RS_V2MINB)
     __syncthreads();
 
     // ---- phase 2: d_grid, lane pairs over the bin-sorted records (warp w: a contiguous
-    // chunk range); lane 2s+e owns record slot s and coefficient half q = 6e .. 6e+5
-    float *mywacc = wacc + w * 4 * D * 12;
-    const int cbeg = (int)(((long long)nchunks * w) / kWarps);
-    const int cend = (int)(((long long)nchunks * (w + 1)) / kWarps);
-    float2 acc2[24];
+    // chunk range); lane 2s+e owns record slot s and coefficient half q = 6e .. 6e+5.
+    // The register sums persist across sub-tiles; odd sub-tiles walk the range backwards,
+    // so a warp starts a sub-tile in (about) the bin it ended the previous one with.
+    {
+        const int cbeg = (int)(((long long)nchunks * w) / kWarps);
+        const int cend = (int)(((long long)nchunks * (w + 1)) / kWarps);
+        const bool back = kMulti && (sub & 1) != 0;
+        if (!kMulti) {  // one sub-tile: the sums start here (not live across phases 0-1)
 #pragma unroll
-    for (int k = 0; k < 24; k++) acc2[k] = f2(0.f, 0.f);
-    auto flush2 = [&](int bin) {
-        float acc[48];
-#pragma unroll
-        for (int pl = 0; pl < 2; pl++)
-#pragma unroll
-            for (int bb = 0; bb < 2; bb++)
-#pragma unroll
-                for (int qq = 0; qq < 6; qq++) {
-                    acc[(pl * 4 + bb * 2 + 0) * 6 + qq] = acc2[(pl * 2 + bb) * 6 + qq].x;
-                    acc[(pl * 4 + bb * 2 + 1) * 6 + qq] = acc2[(pl * 2 + bb) * 6 + qq].y;
-                }
-        flush_acc(acc, mywacc, bin, D, lane);
-#pragma unroll
-        for (int k = 0; k < 24; k++) acc2[k] = f2(0.f, 0.f);
-    };
-    const int slot = lane >> 1;
-    const bool e1 = (lane & 1) != 0;
-    int cur_bin = cbeg < cend ? chunk_bin[cbeg] : 0;
-    for (int ch = cbeg; ch < cend; ch++) {
-        const int bin = chunk_bin[ch];
-        if (bin != cur_bin) {
-            flush2(cur_bin);
-            cur_bin = bin;
+            for (int k = 0; k < 24; k++) acc2[k] = f2(0.f, 0.f);
+            cur_bin = -1;
         }
-        const float4 r0 = rec[2 * (ch * kChunk + slot)], r1 = rec[2 * (ch * kChunk + slot) + 1];
-        const unsigned rc = __float_as_uint(r1.w);
-        const float fx = fxt[rc & 0xffffu], fy = fyt[rc >> 16], fz = r1.z;
-        // this lane's half: P_q = G_oc Xt_i for q = 6e .. 6e+5 (q = 4 oc + i)
-        const float Gq[6] = {e1 ? r0.y : r0.x, e1 ? r0.y : r0.x, e1 ? r0.z : r0.x,
-                             e1 ? r0.z : r0.x, e1 ? r0.z : r0.y, e1 ? r0.z : r0.y};
-        const float Xq[6] = {e1 ? r1.y : r0.w, e1 ? 1.f : r1.x, e1 ? r0.w : r1.y,
-                             e1 ? r1.x : 1.f, e1 ? r1.y : r0.w, e1 ? 1.f : r1.x};
-        float2 wt2[4];
-        {
-            const float2 wx2 = f2(1.f - fx, fx);
-            const float wy[2] = {1.f - fy, fy}, wz[2] = {1.f - fz, fz};
+        for (int it = cbeg; it < cend; it++) {
+            const int ch = back ? cend - 1 - (it - cbeg) : it;
+            const int bin = chunk_bin[ch];
+            if (bin != cur_bin) {
+                if (cur_bin >= 0) flush2(cur_bin);
+                cur_bin = bin;
+            }
+            const float4 r0 = rec[2 * (ch * kChunk + slot)], r1 = rec[2 * (ch * kChunk + slot) + 1];
+            const unsigned rc = __float_as_uint(r1.w);
+            const float fx = fxt[rc & 0xffffu], fy = fyt[rc >> 16], fz = r1.z;
+            // this lane's half: P_q = G_oc Xt_i for q = 6e .. 6e+5 (q = 4 oc + i)
+            const float Gq[6] = {e1 ? r0.y : r0.x, e1 ? r0.y : r0.x, e1 ? r0.z : r0.x,
+                                 e1 ? r0.z : r0.x, e1 ? r0.z : r0.y, e1 ? r0.z : r0.y};
+            const float Xq[6] = {e1 ? r1.y : r0.w, e1 ? 1.f : r1.x, e1 ? r0.w : r1.y,
+                                 e1 ? r1.x : 1.f, e1 ? r1.y : r0.w, e1 ? 1.f : r1.x};
+            float2 wt2[4];
+            {
+                const float2 wx2 = f2(1.f - fx, fx);
+                const float wy[2] = {1.f - fy, fy}, wz[2] = {1.f - fz, fz};
 #pragma unroll
-            for (int pl = 0; pl < 2; pl++)
+                for (int pl = 0; pl < 2; pl++)
 #pragma unroll
-                for (int bb = 0; bb < 2; bb++) {
-                    const float wzy = wz[pl] * wy[bb];
-                    wt2[pl * 2 + bb] = __fmul2_rn(f2(wzy, wzy), wx2);
-                }
-        }
+                    for (int bb = 0; bb < 2; bb++) {
+                        const float wzy = wz[pl] * wy[bb];
+                        wt2[pl * 2 + bb] = __fmul2_rn(f2(wzy, wzy), wx2);
+                    }
+            }
 #pragma unroll
-        for (int qq = 0; qq < 6; qq++) {
-            const float P = Gq[qq] * Xq[qq];
-            const float2 P2 = f2(P, P);
+            for (int qq = 0; qq < 6; qq++) {
+                const float P = Gq[qq] * Xq[qq];
+                const float2 P2 = f2(P, P);
 #pragma unroll
-            for (int k = 0; k < 4; k++) acc2[k * 6 + qq] = __ffma2_rn(wt2[k], P2, acc2[k * 6 + qq]);
+                for (int k = 0; k < 4; k++) acc2[k * 6 + qq] = __ffma2_rn(wt2[k], P2, acc2[k * 6 + qq]);
+            }
         }
     }
-    if (cbeg < cend) flush2(cur_bin);
+        if (!kMulti && cur_bin >= 0) flush2(cur_bin);
+    }  // sub-tiles
+    if (kMulti && cur_bin >= 0) flush2(cur_bin);
     __syncthreads();
     // ---- block partial: fixed-order sum over warps
     float *part = partials + (long long)blockIdx.x * 4 * D * 12;
@@ -1263,14 +1286,15 @@ bool use_split(int H, int W, int D, int Gh, int Gw) {
     if (e && strcmp(e, "tiled") == 0) return false;
     if (e && strcmp(e, "split") == 0) return true;
     const int maxw = (W + Gw - 1) / Gw, maxh = (H + Gh - 1) / Gh;
-    return maxw <= kV2TX && maxh <= kV2TY;
+    return maxw <= kV2TX && maxh <= 2 * kV2TY;
 }
 
 TileGeom tile_geom_split(int N, int H, int W, int D, int Gh, int Gw) {
     TileGeom g = tile_geom(N, H, W, D, Gh, Gw);
     const int maxw = (W + Gw - 1) / Gw, maxh = (H + Gh - 1) / Gh;
     g.SX = (maxw + kV2TX - 1) / kV2TX;
-    g.SY = (maxh + kV2TY - 1) / kV2TY;
+    g.SY = 1;  // (the kernel walks a cell's rows in sub-tiles of <= kV2TY)
+    (void)maxh;
     g.blocks = (long long)N * (Gh + 1) * (Gw + 1) * g.SY * g.SX;
     return g;
 }
@@ -1337,7 +1361,8 @@ cudaError_t bslice_bwd_launch(const BsliceArgs &a, int algo, int deterministic, 
     if (tiled) {
         const size_t sm = split ? split_smem(a.D) : bwd_smem(a.D);
         // per device and per call (the attribute belongs to the current device's context)
-        cudaError_t ea = cudaFuncSetAttribute(split ? bslice_bwd_split : bslice_bwd_tiled,
+        const bool multi = split && (a.H + a.Gh - 1) / a.Gh > kV2TY;  // cells of several sub-tiles
+        cudaError_t ea = cudaFuncSetAttribute(!split ? bslice_bwd_tiled : multi ? bslice_bwd_split<true> : bslice_bwd_split<false>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (ea != cudaSuccess) return ea;
         float *partials = (float *)ws;
@@ -1345,7 +1370,8 @@ cudaError_t bslice_bwd_launch(const BsliceArgs &a, int algo, int deterministic, 
         const int nt = (a.Gh > a.Gw ? a.Gh : a.Gw) + 2;
         bslice_bounds_kernel<<<(nt + 127) / 128, 128, 0, s>>>(tab, a.H, a.W, a.Gh, a.Gw);
         note_launch();
-        if (split) bslice_bwd_split<<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX, partials, tab);
+        if (split && multi) bslice_bwd_split<true><<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX, partials, tab);
+        else if (split) bslice_bwd_split<false><<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX, partials, tab);
         else bslice_bwd_tiled<<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX, partials, tab);
         note_launch();
         const long long total = (long long)a.N * 12 * a.D * a.Gh * a.Gw;
