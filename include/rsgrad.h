@@ -31,7 +31,8 @@
  *   Ownership the caller owns every buffer; the library allocates nothing that
  *             outlives a call.  Its only state: the thread-local error string and,
  *             per (thread, device), the internal streams/events of the host-pointer
- *             path (created on first use, reused, released with the CUDA context).
+ *             path and of stn_bwd's side stream (created on first use, reused,
+ *             released with the CUDA context).
  *   Workspace *_bwd take an optional device workspace of
  *             rsgrad_bwd_workspace_bytes(...) bytes (same opts: deterministic=1
  *             adds the fixed-point accumulators).  NULL / ws_bytes too small (e.g.
@@ -53,7 +54,11 @@
  *             faults surface on the next synchronisation of `stream`.
  *   Threads   re-entrant; concurrent calls on different streams are safe.
  *   Graphs    with device pointers every entry point is stream-capture safe (only
- *             kernel launches, memsets and stream-ordered alloc/free on `stream`):
+ *             kernel launches, memsets and stream-ordered alloc/free on `stream`;
+ *             stn_bwd on a small batch also forks its d_theta kernel onto a library
+ *             side stream with an event recorded on `stream` and joins it back with
+ *             an event wait before its last kernel -- ordered like `stream`, and part
+ *             of a capture of `stream`):
  *             capture it into a CUDA graph and replay it (the per-kernel launch
  *             gaps of a multi-kernel call shrink; bench.py paper_shapes *_graph).
  *             While `stream` is capturing, its device must be the current one.
