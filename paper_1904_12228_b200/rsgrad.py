@@ -21,6 +21,7 @@ from . import _build
 _PADDING = {"zeros": 0, "border": 1}
 _ALGO = {"auto": 0, "gather": 1, "scatter_priv": 2, "scatter_atomic": 3}
 LAYER_STN, LAYER_WARP, LAYER_BSLICE, LAYER_CONV = 0, 1, 2, 3
+LAYER_BICUBIC, LAYER_STN3D, LAYER_LANCZOS = 5, 6, 7  # rsgrad_bwd_workspace_bytes layer ids
 
 
 class RsOpts(ctypes.Structure):
@@ -155,6 +156,10 @@ def _workspace(dev, nbytes):
         return None, 0
     d = dev if dev is not None else torch.device("cuda", torch.cuda.current_device())
     return torch.empty(nbytes, dtype=torch.uint8, device=d), nbytes
+
+
+def _wsp(ws):
+    return None if ws is None else ctypes.c_void_p(ws.data_ptr())
 
 
 def workspace_bytes(layer, N, C=0, H=0, W=0, Ho=0, Wo=0, D=0, Gh=0, Gw=0, opts=None):
@@ -407,8 +412,10 @@ def stn_bicubic_bwd(x, theta, dy, *, align_corners=True, algo="auto", determinis
         dx = torch.empty_like(x) if need_dx else None
         dth = torch.empty((N, 2, 3), dtype=torch.float32, device=x.device) if need_dtheta else None
     o = _opts(align_corners, "zeros", algo, deterministic)
+    dev = _device_of(x, dy)
+    ws, nws = _workspace(dev, workspace_bytes(LAYER_BICUBIC, N, C, H, W, Ho, Wo, opts=o))
     _check(lib().stn_bicubic_bwd(_ptr(x), _ptr(theta), _ptr(dy), N, C, H, W, Ho, Wo, ctypes.byref(o), _ptr(dx),
-                                 _ptr(dth), None, 0, _stream(_device_of(x, dy))), "stn_bicubic_bwd")
+                                 _ptr(dth), _wsp(ws), nws, _stream(dev)), "stn_bicubic_bwd")
     return dx, dth
 
 
@@ -432,8 +439,11 @@ def stn3d_bwd(x, theta, dy, *, align_corners=True, deterministic=False, need_dx=
         dx = torch.empty_like(x) if need_dx else None
         dth = torch.empty((N, 3, 4), dtype=torch.float32, device=x.device) if need_dtheta else None
     o = _opts(align_corners, "zeros", "auto" if deterministic else "scatter_atomic", deterministic)
+    dev = _device_of(x, dy)
+    # (the stn3d query: (N, C, H, W) of the input volume with Gh = its depth, (Ho, Wo, D = Do) of the output)
+    ws, nws = _workspace(dev, workspace_bytes(LAYER_STN3D, N, C, H, W, Ho, Wo, D=Do, Gh=D, opts=o))
     _check(lib().stn3d_bwd(_ptr(x), _ptr(theta), _ptr(dy), N, C, D, H, W, Do, Ho, Wo, ctypes.byref(o), _ptr(dx),
-                           _ptr(dth), None, 0, _stream(_device_of(x, dy))), "stn3d_bwd")
+                           _ptr(dth), _wsp(ws), nws, _stream(dev)), "stn3d_bwd")
     return dx, dth
 
 
@@ -459,6 +469,8 @@ def stn_lanczos_bwd(x, theta, dy, *, align_corners=True, deterministic=False, ne
         dx = torch.empty_like(x) if need_dx else None
         dth = torch.empty((N, 2, 3), dtype=torch.float32, device=x.device) if need_dtheta else None
     o = _opts(align_corners, "zeros", "auto" if deterministic else "scatter_atomic", deterministic)
+    dev = _device_of(x, dy)
+    ws, nws = _workspace(dev, workspace_bytes(LAYER_LANCZOS, N, C, H, W, Ho, Wo, opts=o))
     _check(lib().stn_lanczos_bwd(_ptr(x), _ptr(theta), _ptr(dy), N, C, H, W, Ho, Wo, ctypes.byref(o), _ptr(dx),
-                                 _ptr(dth), None, 0, _stream(_device_of(x, dy))), "stn_lanczos_bwd")
+                                 _ptr(dth), _wsp(ws), nws, _stream(dev)), "stn_lanczos_bwd")
     return dx, dth
