@@ -340,6 +340,9 @@ RS_DEV void rs_stage(float *v, int lane, int m) {
 // Reduce-scatter across the 16 lanes of the same half (xor 16, 8, 4, 2: 45
 // shuffles); lane then owns 3 sums, base = 24 b4 + 12 b3 + 6 b2 + 3 b1.
 // wacc (warp slot): [corner(4)][z(D)][q(12)]
+// kQmap: false -> lane e holds q = 6e + qq; true (split kernel) -> q = 4e + qq (qq < 4),
+// 8 + 2e + (qq - 4) (qq >= 4): both halves then read G and Xt in the same pattern
+template <bool kQmap = false>
 RS_DEV void flush_acc(float *acc, float *wacc, int bin, int D, int lane) {
     rs_stage<24>(acc, lane, 16);
     rs_stage<12>(acc, lane, 8);
@@ -355,7 +358,8 @@ RS_DEV void flush_acc(float *acc, float *wacc, int bin, int D, int lane) {
 #pragma unroll
             for (int t = 0; t < 3; t++) {
                 const int idx = (base + t) % 24;  // (corner, qq) within the plane
-                const int corner = idx / 6, q = 6 * e + idx % 6;
+                const int qq = idx % 6, corner = idx / 6;
+                const int q = kQmap ? (qq < 4 ? 4 * e + qq : 8 + 2 * e + (qq - 4)) : 6 * e + qq;
                 wacc[(corner * D + z) * 12 + q] += acc[t];
             }
         }
@@ -717,7 +721,7 @@ __global__ void __launch_bounds__(kThreads, RS_V2MINB)
                     acc[(pl * 4 + bb * 2 + 0) * 6 + qq] = acc2[(pl * 2 + bb) * 6 + qq].x;
                     acc[(pl * 4 + bb * 2 + 1) * 6 + qq] = acc2[(pl * 2 + bb) * 6 + qq].y;
                 }
-        flush_acc(acc, mywacc, bin, D, lane);
+        flush_acc<true>(acc, mywacc, bin, D, lane);
 #pragma unroll
         for (int k = 0; k < 24; k++) acc2[k] = f2(0.f, 0.f);
     };
@@ -911,11 +915,11 @@ __global__ void __launch_bounds__(kThreads, RS_V2MINB)
             const float4 r0 = rec[2 * (ch * kChunk + slot)], r1 = rec[2 * (ch * kChunk + slot) + 1];
             const unsigned rc = __float_as_uint(r1.w);
             const float fx = fxt[rc & 0xffffu], fy = fyt[rc >> 16], fz = r1.z;
-            // this lane's half: P_q = G_oc Xt_i for q = 6e .. 6e+5 (q = 4 oc + i)
-            const float Gq[6] = {e1 ? r0.y : r0.x, e1 ? r0.y : r0.x, e1 ? r0.z : r0.x,
-                                 e1 ? r0.z : r0.x, e1 ? r0.z : r0.y, e1 ? r0.z : r0.y};
-            const float Xq[6] = {e1 ? r1.y : r0.w, e1 ? 1.f : r1.x, e1 ? r0.w : r1.y,
-                                 e1 ? r1.x : 1.f, e1 ? r1.y : r0.w, e1 ? 1.f : r1.x};
+            // this lane's half (q = 4 oc + i): e = 0 owns oc 0 (i = 0..3) and q 8, 9; e = 1 owns
+            // oc 1 and q 10, 11 -- the same G / Xt pattern in both halves, three selects
+            const float Ga = e1 ? r0.y : r0.x;
+            const float Gq[6] = {Ga, Ga, Ga, Ga, r0.z, r0.z};
+            const float Xq[6] = {r0.w, r1.x, r1.y, 1.f, e1 ? r1.y : r0.w, e1 ? 1.f : r1.x};
             float2 wt2[4];
             {
                 const float2 wx2 = f2(1.f - fx, fx);
