@@ -1082,6 +1082,12 @@ constexpr int kLTY = kLRows * 8;          // 32 px rows per block
 constexpr int kLBufs = RS_LBUFS;  // dY stage buffers (1: the other block on the SM overlaps)
 constexpr int kLRQMax = 160, kLFQMax = 2304, kLStage = RS_LSTAGE, kLCH = RS_LCH;
 constexpr int kLCells = (kBX + 1) * (kLTY + 1);  // the block's floor cells: 32 columns x 33 rows
+// stage completion: 1 = the stage mbarrier (try_wait spin: ~11% of the kernel's
+// instructions, but not of its time), 0 = cp.async groups + a block barrier (measured
+// equal: 6.566 vs 6.562 ms for stn_bwd at 64 x 16 x 1024^2)
+#ifndef RS_LEAN_MBAR
+#define RS_LEAN_MBAR 1
+#endif
 #ifndef RS_LEAN_FXY
 #define RS_LEAN_FXY 1
 #endif
@@ -1212,7 +1218,7 @@ __global__ void __launch_bounds__(kThreads, RS_LMINB)
     __syncthreads();
     // VEC: 16-B cp.async rows completing on the stage's mbarrier; else 4-B cp.async
     auto issue = [&](float *dst, int c0s, int ncp, int slot) {
-        if (VEC) {
+        if (VEC && RS_LEAN_MBAR) {
             if (FQ > 0) stage_rows<true>(dst, FQ, gbase + (long long)c0s * P, P, ncp, RQ, a.Wo, ilo, qxa, qoff, qcnt);
             cp_async_arrive(&bars[slot]);
         } else {
@@ -1377,7 +1383,7 @@ __global__ void __launch_bounds__(kThreads, RS_LMINB)
         const int c0 = kc * CH, cn = min(CH, a.C - c0);
         if (kLBufs == 2 && kc + 1 < nch)
             issue(stage + ((kc + 1) % kLBufs) * kLStage, c0 + CH, min(CH, a.C - c0 - CH), (kc + 1) & 1);
-        if (VEC) {
+        if (VEC && RS_LEAN_MBAR) {
             mbar_wait(&bars[kc & 1], (unsigned)((kc >> 1) & 1));
             if (RS_RACECHECK_SYNC) {
                 cp_async_wait<0>();
@@ -1387,7 +1393,7 @@ __global__ void __launch_bounds__(kThreads, RS_LMINB)
             if (kLBufs == 2 && kc + 1 < nch) cp_async_wait<1>();
             else cp_async_wait<0>();
         }
-        if (!VEC) __syncthreads();
+        if (!(VEC && RS_LEAN_MBAR)) __syncthreads();
         const float *S = stage + (kc % kLBufs) * kLStage;
         switch (cn) {
             case 8: run_chunk(S, c0, std::integral_constant<int, 8>{}); break;
