@@ -219,7 +219,7 @@ RS_DEV float lerp2(const float4 c, float fx, float fy) {
 
 // ----------------------------------------------------------------- forward, tiled
 __global__ void __launch_bounds__(kThreads)
-    bslice_fwd_tiled(BsliceArgs a, int SY, int SX) {
+    bslice_fwd_tiled(BsliceArgs a, int SY, int SX, int ntab) {
     extern __shared__ float4 smem4[];
     float4 *glo = smem4;                                       // (D+1) * 13
     float4 *gdz = glo + (a.D + 1) * kPlaneStride;              // (D+1) * 13
@@ -248,25 +248,29 @@ __global__ void __launch_bounds__(kThreads)
     // per-warp row table: for the current row's fy, (a + fy c, b + fy d) of the low
     // plane and of the plane difference, for every (bin, q), bins kPlaneStride float4
     // apart (conflict-free across bins): one LDS.128 per coefficient and pixel
-    float4 *rt = (float4 *)(fyt + kTileYS) + w * kPlaneStride * NB;
-    // the warp's items: (row r, 64-column pair segment cx), two pixels per lane; the next
-    // item's guide and X loads are issued before the current item is computed (a small
-    // dual cell has one item per row: without the prefetch every row waits a round trip)
-    const int ncx = (TW + 63) >> 6;
+    float4 *rt = (float4 *)(fyt + kTileYS) + w * ntab * kPlaneStride * NB;  // ntab (1 or 2) tables per warp
+    // the warp's items, two pixels per lane: (row r, 64-column segment cx) -- or, for a dual
+    // cell at most 32 px wide, rows r and r + kWarps at column lane (a second row table),
+    // so both pixels are live; the next item's guide and X loads are issued before the
+    // current item is computed (a small dual cell has one item per row: without the
+    // prefetch every row waits a round trip)
+    const bool pairs = ntab == 2 && TW <= 32;
+    const int ncx = pairs ? 1 : (TW + 63) >> 6;
+    auto row_of = [&](int r, int k) { return pairs ? r + k * kWarps : r; };
+    auto col_of = [&](int cx, int k) { return pairs ? lane : cx * 64 + lane + 32 * k; };
     float gn[2] = {0.f, 0.f}, xn[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
     auto fetch = [&](int r, int cx) {
-        if (r >= TH) return;
-        const long long rowoff = (long long)(t.ys + r) * a.W + t.xs;
 #pragma unroll
         for (int k = 0; k < 2; k++) {
-            const int c = cx * 64 + lane + 32 * k;
-            const bool ok = c < TW;
-            const long long o = rowoff + (ok ? c : 0);
+            const int rk = row_of(r, k), c = col_of(cx, k);
+            const bool ok = rk < TH && c < TW;
+            const long long o = ok ? (long long)(t.ys + rk) * a.W + t.xs + c : 0;
             gn[k] = ok ? ldg_stream(gd + o) : 0.f;
 #pragma unroll
             for (int i = 0; i < 3; i++) xn[k][i] = ok ? ldg_stream(xp + i * HW + o) : 0.f;
         }
     };
+    const int rstep = pairs ? 2 * kWarps : kWarps;
     fetch(w, 0);
     int r = w, cx = 0;
     while (r < TH) {
@@ -277,33 +281,37 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
             for (int i = 0; i < 3; i++) xv[k][i] = xn[k][i];
         }
-        const int cx1 = cx + 1 < ncx ? cx + 1 : 0, r1 = cx + 1 < ncx ? r : r + kWarps;
+        const int cx1 = cx + 1 < ncx ? cx + 1 : 0, r1 = cx + 1 < ncx ? r : r + rstep;
         fetch(r1, cx1);
         if (cx == 0) {
-            // per-warp row table: for the row's fy, (a + fy c, b + fy d) of the low plane
+            // per-warp row table(s): for the row's fy, (a + fy c, b + fy d) of the low plane
             // and of the plane difference, for every (bin, q), bins kPlaneStride float4
             // apart (conflict-free across bins): one LDS.128 per coefficient and pixel
-            const float fy = fyt[r];
             __syncwarp();
-            for (int e = lane; e < 12 * NB; e += 32) {
-                const int b = e / 12, q = e - b * 12;
-                const float4 L = glo[b * kPlaneStride + q], Dz = gdz[b * kPlaneStride + q];
-                rt[b * kPlaneStride + q] = make_float4(fmaf(fy, L.z, L.x), fmaf(fy, L.w, L.y), fmaf(fy, Dz.z, Dz.x),
-                                                       fmaf(fy, Dz.w, Dz.y));
+#pragma unroll
+            for (int k = 0; k < 2; k++) {
+                if (k == 1 && !(pairs && r + kWarps < TH)) break;
+                const float fy = fyt[row_of(r, k)];
+                float4 *tk = rt + k * kPlaneStride * NB;
+                for (int e = lane; e < 12 * NB; e += 32) {
+                    const int b = e / 12, q = e - b * 12;
+                    const float4 L = glo[b * kPlaneStride + q], Dz = gdz[b * kPlaneStride + q];
+                    tk[b * kPlaneStride + q] = make_float4(fmaf(fy, L.z, L.x), fmaf(fy, L.w, L.y),
+                                                           fmaf(fy, Dz.z, Dz.x), fmaf(fy, Dz.w, Dz.y));
+                }
             }
             __syncwarp();
         }
-        const long long rowoff = (long long)(t.ys + r) * a.W + t.xs;
 #pragma unroll
         for (int k = 0; k < 2; k++) {
-            const int c = cx * 64 + lane + 32 * k;
-            if (c >= TW) continue;
-            const long long o = rowoff + c;
+            const int rk = row_of(r, k), c = col_of(cx, k);
+            if (rk >= TH || c >= TW) continue;
+            const long long o = (long long)(t.ys + rk) * a.W + t.xs + c;
             const float fx = fxt[c];
             int bin;
             float fz;
             z_cell(gv[k], a.D, bin, fz);
-            const float4 *T = rt + bin * kPlaneStride;
+            const float4 *T = rt + (pairs ? k : 0) * kPlaneStride * NB + bin * kPlaneStride;
 #pragma unroll
             for (int oc = 0; oc < 3; oc++) {
                 float A[4];
@@ -1257,9 +1265,9 @@ TileGeom tile_geom(int N, int H, int W, int D, int Gh, int Gw) {
     return g;
 }
 
-size_t fwd_smem(int D) {
+size_t fwd_smem(int D, int ntab = 1) {
     return sizeof(float4) * 2 * (D + 1) * kPlaneStride + sizeof(float) * (kTileXS + kTileYS) +
-           sizeof(float4) * kWarps * kPlaneStride * (D + 1) + 16;
+           sizeof(float4) * kWarps * ntab * kPlaneStride * (D + 1) + 16;
 }
 
 size_t bwd_smem(int D) {
@@ -1344,10 +1352,15 @@ size_t bslice_ws_bytes(int N, int H, int W, int D, int Gh, int Gw) {
 cudaError_t bslice_fwd_launch(const BsliceArgs &a, cudaStream_t s) {
     const TileGeom g = tile_geom(a.N, a.H, a.W, a.D, a.Gh, a.Gw);
     if (g.ok) {
-        const size_t sm = fwd_smem(a.D);
-        if (sm > 48 * 1024)
-            cudaFuncSetAttribute(bslice_fwd_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        bslice_fwd_tiled<<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX);
+        // a second row table per warp (narrow dual cells take two rows per item) where it
+        // costs little shared memory (D <= ~25)
+        const int ntab = fwd_smem(a.D, 2) <= 100 * 1024 ? 2 : 1;
+        const size_t sm = fwd_smem(a.D, ntab);
+        if (sm > 48 * 1024) {
+            cudaError_t ea = cudaFuncSetAttribute(bslice_fwd_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            if (ea != cudaSuccess) return ea;
+        }
+        bslice_fwd_tiled<<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX, ntab);
     } else {
         const long long total = (long long)a.N * a.H * a.W;
         bslice_fwd_generic<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(a);
