@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(FAST ? kOTFast : kThreads, FAST ? kOTFastMinB 
         const bool col = threadIdx.x < kFJ;
         const int idx = col ? tj * kFJ + threadIdx.x : ti * kFI + threadIdx.x - kFJ;
         const int L = col ? a.Wo : a.Ho;
-        ntab[threadIdx.x] = idx < L ? (MODE == MODE_DTHETA ? (col ? xtab[idx] : ytab[idx]) : stn_norm(idx, L, a.ac)) : 0.0;
+        ntab[threadIdx.x] = idx < L ? ((MODE == MODE_DTHETA && xtab) ? (col ? xtab[idx] : ytab[idx]) : stn_norm(idx, L, a.ac)) : 0.0;
     }
     __syncthreads();
     const int nloop = fb_list ? *fb_count : 1;
@@ -1094,6 +1094,7 @@ constexpr int kLCells = (kBX + 1) * (kLTY + 1);  // the block's floor cells: 32 
 #ifndef RS_LEAN_ROWMAX
 #define RS_LEAN_ROWMAX 1
 #endif
+constexpr int kLXT = 256;  // lean: per-block table of the preimage columns' normalised coordinates
 constexpr int kLRTot = 8 * (kLRows + 1) > kLTY + 3 ? 8 * (kLRows + 1) : kLTY + 3;
 
 RS_DEV bool stn_lean_ok(const Affine &A, int Ho, int Wo) {
@@ -1111,7 +1112,7 @@ RS_DEV bool stn_lean_ok(const Affine &A, int Ho, int Wo) {
 #ifndef RS_LMINB
 #define RS_LMINB 3
 #endif
-template <bool VEC>
+template <bool VEC, bool SELF = false>
 __global__ void __launch_bounds__(kThreads, RS_LMINB)
     stn_bwd_lean(StnArgs a, const double *__restrict__ xtab, const double *__restrict__ ytab,
                  const int *__restrict__ flags, int tiles_x, int tiles_y) {
@@ -1129,6 +1130,7 @@ __global__ void __launch_bounds__(kThreads, RS_LMINB)
     int *cfill = cstart + kLCells;                              // kLCells: hit counts, then fill ends
     int *rtot = cfill + kLCells;                                // kLRTot: cell row totals, then warp row hit maxima
     unsigned short *hits = (unsigned short *)(rtot + kLRTot);   // kLFQMax: record indices, by cell
+    double *xts = (double *)(((uintptr_t)(hits + kLFQMax) + 7) & ~(uintptr_t)7);  // kLXT column coordinates
     __shared__ unsigned long long bars[2];  // stage completion (cp.async.mbarrier.arrive), one per stage
 
     const int n = blockIdx.y;
@@ -1138,7 +1140,10 @@ __global__ void __launch_bounds__(kThreads, RS_LMINB)
     const long long HW = (long long)a.H * a.W, P = (long long)a.Ho * a.Wo;
     const int px = xa0 - 1 + lane;
     float *dxn = a.dx + (long long)n * a.C * HW;
-    if (!flags[n]) {  // fallback sample: zero this tile (the atomic scatter adds later)
+    const Theta T = load_theta(a.theta, n);
+    const Affine A = stn_affine(T, a.H, a.W, a.Ho, a.Wo, a.ac);
+    // SELF (no prep launch): the block classifies its sample itself (the same test stn_prep makes)
+    if (SELF ? !stn_lean_ok(A, a.Ho, a.Wo) : !flags[n]) {  // fallback sample: zero this tile (the atomic scatter adds later)
         if (lane >= 1 && px < a.W)
             for (int r = warp; r < kLTY; r += 8) {
                 const int y = yb0 + r;
@@ -1147,22 +1152,34 @@ __global__ void __launch_bounds__(kThreads, RS_LMINB)
             }
         return;
     }
-    const Theta T = load_theta(a.theta, n);
-    const Affine A = stn_affine(T, a.H, a.W, a.Ho, a.Wo, a.ac);
     const double eps = 1e-3;
     const double Lx = xa0 - 1 - eps, Ux = xa0 + kBX + eps;
     const double Ly = yb0 - 1 - eps, Uy = yb0 + kLTY + eps;
-    double imin = 1e300, imax = -1e300;
+    double imin = 1e300, imax = -1e300, jmin = 1e300, jmax = -1e300;
 #pragma unroll
     for (int c = 0; c < 4; c++) {
         const double px_ = (c & 1) ? Ux : Lx, py_ = (c & 2) ? Uy : Ly;
         const double qi = A.i10 * (px_ - A.p0x) + A.i11 * (py_ - A.p0y);
         imin = fmin(imin, qi);
         imax = fmax(imax, qi);
+        if (SELF) {
+            const double qj = A.i00 * (px_ - A.p0x) + A.i01 * (py_ - A.p0y);
+            jmin = fmin(jmin, qj);
+            jmax = fmax(jmax, qj);
+        }
     }
     const int ilo = max(0, (int)ceil(fmax(imin, -1e9)));
     const int ihi = min(a.Ho - 1, (int)floor(fmin(imax, 1e9)));
     const int RQ = min(kLRQMax, max(0, ihi - ilo + 1));
+    // SELF: the normalised coordinates of the preimage's columns once per block (one
+    // division each) instead of a table from the prep launch
+    int jlo = 0, jn = 0;
+    if (SELF) {
+        jlo = max(0, (int)floor(fmax(jmin, -1e9)) - 4);
+        jn = min(a.Wo - 1, (int)ceil(fmin(jmax, 1e9)) + 4) - jlo + 1;
+        if (jn > kLXT) jn = 0;  // (then stn_norm per record)
+        for (int q = threadIdx.x; q < jn; q += kThreads) xts[q] = stn_norm(jlo + q, a.Wo, a.ac);
+    }
     for (int r = threadIdx.x; r < RQ; r += kThreads) {
         const int i = ilo + r;
         double jl = -1e300, jh = 1e300;
@@ -1196,7 +1213,7 @@ __global__ void __launch_bounds__(kThreads, RS_LMINB)
     for (int r = threadIdx.x; r < RQ; r += kThreads) rowt[r] = make_int4(qlo[r], qhi[r], qoff[r] - qxa[r], 0);
     for (int r = warp; r < RQ; r += 8) {
         const int i = ilo + r;
-        const double yt = ytab[i];
+        const double yt = SELF ? stn_norm(i, a.Ho, a.ac) : ytab[i];
         const int wr = (qcnt[r] + 3) & ~3;
         for (int col = lane; col < wr; col += 32) {
             const int j = qxa[r] + col, e = qoff[r] + col;
@@ -1204,7 +1221,8 @@ __global__ void __launch_bounds__(kThreads, RS_LMINB)
             uint2 R = make_uint2(0xff000000u, 0xff000000u);
             if (col < qcnt[r] && j >= qlo[r] && j <= qhi[r]) {
                 double ix, iy;
-                stn_coord(T, xtab[j], yt, a.H, a.W, a.ac, ix, iy);
+                const double xt = !SELF ? xtab[j] : (j - jlo >= 0 && j - jlo < jn) ? xts[j - jlo] : stn_norm(j, a.Wo, a.ac);
+                stn_coord(T, xt, yt, a.H, a.W, a.ac, ix, iy);
                 const Cell cx = cell_of(ix), cy = cell_of(iy);
                 const int rx = cx.i0 - (xa0 - 1), ry = cy.i0 - (yb0 - 1);
                 if (rx >= 0 && rx <= kBX && ry >= 0 && ry <= kLTY) R = pack_rec(rx, ry, cx.f, cy.f);
@@ -1850,6 +1868,77 @@ struct StnTapSampler {
     }
 };
 
+// ----------------------------------------------------------------- lean path tail
+// The last launch of the lean backward when no prep kernel ran: blocks [0, N) sum sample
+// n's d_theta tile partials in fixed order (stn_dtheta_finalize, every sample from the
+// output tiles); blocks [N, grid) classify every sample as stn_bwd_lean did and add the
+// atomic scatter of the fallback samples (singular / huge preimage: their dX tiles were
+// zeroed by the lean kernel) -- one launch instead of prep + scatter + finalize.
+__global__ void __launch_bounds__(kThreads)
+    stn_bwd_tail(StnArgs a, const double *__restrict__ pf, int nf) {
+    const int n = blockIdx.x;
+    if (n < a.N) {
+        if (!a.dtheta) return;
+        const double *p = pf + (long long)n * nf * 6;
+        __shared__ double red[kThreads / 32][6];
+        double sk[6] = {0, 0, 0, 0, 0, 0};
+        for (int b = threadIdx.x; b < nf; b += kThreads)
+#pragma unroll
+            for (int k = 0; k < 6; k++) sk[k] += p[(long long)b * 6 + k];
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+        for (int k = 0; k < 6; k++) {
+            const double v = warp_sum_d(sk[k]);
+            if (lane == 0) red[wid][k] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < 6) {
+            double v = 0.0;
+            for (int w = 0; w < kThreads / 32; w++) v += red[w][threadIdx.x];
+            a.dtheta[6 * n + threadIdx.x] = (float)v;
+        }
+        return;
+    }
+    if (!a.dx) return;
+    const long long P = (long long)a.Ho * a.Wo, HW = (long long)a.H * a.W;
+    const long long b0 = blockIdx.x - a.N, nbk = gridDim.x - a.N;
+    __shared__ int fb[kThreads], nfb;
+    for (int m0 = 0; m0 < a.N; m0 += kThreads) {
+        // classify kThreads samples at once (thread = sample), then walk the fallback ones
+        __syncthreads();
+        if (threadIdx.x == 0) nfb = 0;
+        __syncthreads();
+        const int mm = m0 + threadIdx.x;
+        if (mm < a.N && !stn_lean_ok(stn_affine(load_theta(a.theta, mm), a.H, a.W, a.Ho, a.Wo, a.ac), a.Ho, a.Wo))
+            fb[atomicAdd(&nfb, 1)] = mm;
+        __syncthreads();
+        for (int f = 0; f < nfb; f++) {
+        const int m = fb[f];
+        const Theta T = load_theta(a.theta, m);
+        for (long long rem = b0 * kThreads + threadIdx.x; rem < P; rem += nbk * kThreads) {
+            const int i = (int)(rem / a.Wo), j = (int)(rem - (long long)i * a.Wo);
+            double ix, iy;
+            stn_coord(T, stn_norm(j, a.Wo, a.ac), stn_norm(i, a.Ho, a.ac), a.H, a.W, a.ac, ix, iy);
+            const Cell cx = cell_of(ix), cy = cell_of(iy);
+            const bool x0ok = cx.i0 >= 0 && cx.i0 < a.W, x1ok = cx.i0 + 1 >= 0 && cx.i0 + 1 < a.W;
+            const bool y0ok = cy.i0 >= 0 && cy.i0 < a.H, y1ok = cy.i0 + 1 >= 0 && cy.i0 + 1 < a.H;
+            if (!((x0ok || x1ok) && (y0ok || y1ok))) continue;
+            const float w00 = (1.f - cy.f) * (1.f - cx.f), w01 = (1.f - cy.f) * cx.f;
+            const float w10 = cy.f * (1.f - cx.f), w11 = cy.f * cx.f;
+            const long long o00 = (long long)cy.i0 * a.W + cx.i0;
+            for (int c = 0; c < a.C; c++) {
+                const float g = ldg_stream(a.dy + ((long long)m * a.C + c) * P + rem);
+                float *q = a.dx + ((long long)m * a.C + c) * HW + o00;
+                if (y0ok && x0ok) red_add(q, w00 * g);
+                if (y0ok && x1ok) red_add(q + 1, w01 * g);
+                if (y1ok && x0ok) red_add(q + a.W, w10 * g);
+                if (y1ok && x1ok) red_add(q + a.W + 1, w11 * g);
+            }
+        }
+        }
+    }
+}
+
 // ----------------------------------------------------------------- host helpers
 size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
@@ -1925,7 +2014,8 @@ size_t out_tile_smem() {
 }
 size_t bwd_lean_smem() {
     return sizeof(float) * kLBufs * kLStage + sizeof(uint2) * kLFQMax + sizeof(int4) * kLRQMax +
-           sizeof(int) * (5 * kLRQMax + 8 + 2 * kLCells + kLRTot) + sizeof(unsigned short) * kLFQMax;
+           sizeof(int) * (5 * kLRQMax + 8 + 2 * kLCells + kLRTot) + sizeof(unsigned short) * kLFQMax + 8 +
+           sizeof(double) * kLXT;
 }
 
 size_t bwd_gather_smem() {
@@ -2059,6 +2149,50 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
     // SCATTER_ATOMIC or border padding: every sample takes the fallback pair.
     const int allow_gather = (algo == 0 || algo == 1) && !a.border && HW * kBCH < (1LL << 31);
     const int variant = stn_bwd_variant();
+    const bool vin0 = (a.W % 4 == 0) && aligned16(a.x), vout0 = (a.Wo % 4 == 0) && aligned16(a.dy);
+    const long long lean_blocks = (long long)g.bx * ((a.H + kLTY - 1) / kLTY) * a.N;
+    if (allow_gather && variant == 2 && !det && vin0 && vout0 && !stn_slow_tiles() && !RS_DTH_LASTBLOCK &&
+        lean_blocks <= stn_fork_blocks() && !getenv("RSGRAD_STN_PREP")) {
+        // Lean path in three launches: stn_bwd_lean (classifies its sample and computes the
+        // normalised coordinates itself), the FAST d_theta tiles (on the side stream for
+        // small grids), stn_bwd_tail (d_theta finalize + the fallback samples' scatter)
+        const int ly = (a.H + kLTY - 1) / kLTY;
+        const dim3 lgrid(g.bx * ly, a.N);
+        const int fi_df = (a.Ho + kFIdf - 1) / kFIdf;
+        cudaStream_t sdt = s;
+        StnFork *fk = nullptr;
+        if (a.dx && a.dtheta && (long long)lgrid.x * lgrid.y <= stn_fork_blocks() && (fk = stn_fork()) != nullptr) {
+            cudaError_t e = cudaEventRecord(fk->fork, s);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(fk->side, fk->fork, 0);
+            if (e != cudaSuccess) return e;
+            sdt = fk->side;
+        }
+        if (a.dx) {
+            const size_t sm = bwd_lean_smem();
+            set_smem(stn_bwd_lean<true, true>, sm);
+            stn_bwd_lean<true, true><<<lgrid, kThreads, sm, s>>>(a, nullptr, nullptr, nullptr, g.bx, ly);
+            note_launch();
+        }
+        if (a.dtheta) {
+            auto k = stn_out_tile<MODE_DTHETA, true, false, kFIdf, true>;
+            const size_t sm = out_tile_smem();
+            set_smem(k, sm);
+            k<<<dim3(g.fj * fi_df, a.N), kOTFast, sm, sdt>>>(a, nullptr, nullptr, nullptr, w.fb_count, w.pf, g.fj,
+                                                              fi_df, nullptr);
+            note_launch();
+            if (sdt != s) {
+                cudaError_t e = cudaEventRecord(fk->join, sdt);
+                if (e == cudaSuccess) e = cudaStreamWaitEvent(s, fk->join, 0);
+                if (e != cudaSuccess) return e;
+            }
+        }
+        const long long P = (long long)a.Ho * a.Wo;
+        long long sb = a.dx ? (P + kThreads - 1) / kThreads : 0;
+        if (sb > 2 * kNumSMs) sb = 2 * kNumSMs;
+        stn_bwd_tail<<<(unsigned)(a.N + sb), kThreads, 0, s>>>(a, w.pf, g.fj * fi_df);
+        note_launch();
+        return cudaGetLastError();
+    }
     stn_prep_kernel<<<(tmax + 255) / 256, 256, 0, s>>>(a, allow_gather, variant, w.xtab, w.ytab, w.flags, w.fb_list,
                                                        w.fb_count, w.ctr);
     note_launch();

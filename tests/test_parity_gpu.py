@@ -130,6 +130,34 @@ def test_warp_fwd_pixel_groups(cuda_device, monkeypatch, groups, flow):
     assert_close(_np(y), oracle.warp_fwd(inp["x"].double().numpy(), inp["flow"].double().numpy()), "fwd", "y")
 
 
+def test_stn_bwd_three_launches(cuda_device, monkeypatch):
+    """The lean backward path runs as three launches (lean d_input with its own sample
+    classification and coordinates, d_theta tiles, finalize + fallback scatter) and agrees
+    bitwise with the path that prepares tables and classes in a separate kernel
+    (RSGRAD_STN_PREP); with fallback samples (singular / huge preimage) both match the oracle."""
+    inp = synth.stn_inputs(3, 8, 64, 96, cfg=1)
+    g = _cuda(inp, cuda_device)
+    rsgrad.launch_count(reset=True)
+    dx, dth = rsgrad.stn_bwd(g["x"], g["theta"], g["dy"])
+    assert rsgrad.launch_count() == 3
+    monkeypatch.setenv("RSGRAD_STN_PREP", "1")
+    dx2, dth2 = rsgrad.stn_bwd(g["x"], g["theta"], g["dy"])
+    assert torch.equal(dx, dx2) and torch.equal(dth, dth2)
+    monkeypatch.delenv("RSGRAD_STN_PREP")
+    inp["theta"][1] = torch.tensor([[0.5, 0.5, 0.1], [0.5, 0.5, -0.2]])   # det = 0
+    inp["theta"][2] = torch.tensor([[0.02, 0.0, 0.1], [0.0, 0.03, 0.0]])  # huge preimage
+    g = _cuda(inp, cuda_device)
+    x, th, dy = (inp[k].double().numpy() for k in ("x", "theta", "dy"))
+    rdx, rdth = oracle.stn_bwd(x, th, dy)
+    for need_dtheta in (True, False):
+        dx, dth = rsgrad.stn_bwd(g["x"], g["theta"], g["dy"], need_dtheta=need_dtheta)
+        assert_close(_np(dx), rdx, "grad", "dx")
+        if need_dtheta:
+            assert_close(_np(dth), rdth, "grad", "dtheta")
+    _, dth = rsgrad.stn_bwd(g["x"], g["theta"], g["dy"], need_dx=False)
+    assert_close(_np(dth), rdth, "grad", "dtheta only")
+
+
 @pytest.mark.parametrize("fork", ["0", "100000"])
 def test_stn_bwd_fork(cuda_device, monkeypatch, fork):
     """The d_theta tiles on the library side stream beside the lean d_input kernel, or
