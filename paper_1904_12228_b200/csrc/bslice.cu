@@ -703,7 +703,9 @@ __global__ void __launch_bounds__(kThreads, RS_V2MINB)
 
     // the block owns a whole dual cell (column split SX); its rows are walked as
     // sub-tiles of <= kV2TY rows (the records hold 32 B per pixel)
-    const Tile tc = tile_of_tab(blockIdx.x, a.Gh, a.Gw, SY, SX, tab);
+    __shared__ int tsh[4];  // (tab == nullptr: the block searches its dual cell's bounds itself)
+    const Tile tc = tab ? tile_of_tab(blockIdx.x, a.Gh, a.Gw, SY, SX, tab)
+                        : tile_of_block(blockIdx.x, a.Gh, a.Gw, SY, SX, a.H, a.W, tsh);
     const int TW = tc.xe - tc.xs, THc = tc.ye - tc.ys;
     const int nsub = (THc + kV2TY - 1) / kV2TY;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1385,10 +1387,17 @@ cudaError_t bslice_bwd_launch(const BsliceArgs &a, int algo, int deterministic, 
         float *partials = (float *)ws;
         int *tab = (int *)(partials + (size_t)g.blocks * 4 * a.D * 12);
         const int nt = (a.Gh > a.Gw ? a.Gh : a.Gw) + 2;
-        bslice_bounds_kernel<<<(nt + 127) / 128, 128, 0, s>>>(tab, a.H, a.W, a.Gh, a.Gw);
-        note_launch();
-        if (split && multi) bslice_bwd_split<true><<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX, partials, tab);
-        else if (split) bslice_bwd_split<false><<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX, partials, tab);
+        // few blocks: the split kernel's blocks search their cell bounds themselves (one launch
+        // less: configs[3] 189.4 -> 185.3 us); many small cells: the bounds table (the fp64
+        // searches per block cost more: 32x32x8 238.6 vs 246.8 us)
+        const bool self_bounds = split && g.blocks <= 2048;
+        if (!self_bounds) {
+            bslice_bounds_kernel<<<(nt + 127) / 128, 128, 0, s>>>(tab, a.H, a.W, a.Gh, a.Gw);
+            note_launch();
+        }
+        int *stab = self_bounds ? nullptr : tab;
+        if (split && multi) bslice_bwd_split<true><<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX, partials, stab);
+        else if (split) bslice_bwd_split<false><<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX, partials, stab);
         else bslice_bwd_tiled<<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX, partials, tab);
         note_launch();
         const long long total = (long long)a.N * 12 * a.D * a.Gh * a.Gw;
