@@ -967,18 +967,16 @@ __global__ void __launch_bounds__(kThreads, RS_V2MINB)
 
 // dgrid[n,q,z,y,x] = fixed-order sum of the partials of the dual cells whose
 // clamped corners are (y, x).  partial layout: [block][corner][z][q].
+// grid (ceil(Gw / 21), Gh D, N): thread t = (q = t % 12, x = 21 blockIdx.x + t / 12) of row y,
+// plane z, sample n -- the 12 q of a node are adjacent in a partial, so a warp reads a few
+// 48-B runs instead of 32 scattered words (the summation order of every node is fixed).
+constexpr int kGX = kThreads / 12;  // 21 grid columns per block
 __global__ void __launch_bounds__(kThreads)
     bslice_dgrid_gather(BsliceArgs a, int SY, int SX, const float *__restrict__ partials) {
-    const long long total = (long long)a.N * 12 * a.D * a.Gh * a.Gw;
-    const long long idx = (long long)blockIdx.x * kThreads + threadIdx.x;
-    if (idx >= total) return;
-    long long r = idx;
-    const int x = (int)(r % a.Gw); r /= a.Gw;
-    const int y = (int)(r % a.Gh); r /= a.Gh;
-    const int z = (int)(r % a.D); r /= a.D;
-    const int q = (int)(r % 12);
-    const int n = (int)(r / 12);
-    const int D = a.D;
+    const int t = threadIdx.x, q = t % 12, x = blockIdx.x * kGX + t / 12;
+    if (t >= 12 * kGX || x >= a.Gw) return;
+    const int D = a.D, y = blockIdx.y / D, z = blockIdx.y - y * D, n = blockIdx.z;
+    const int per = 4 * D * 12, S = SY * SX;
     float s = 0.f;
     for (int jj = y; jj <= y + 1 && jj <= a.Gh; jj++) {
         for (int b = 0; b < 2; b++) {
@@ -986,17 +984,14 @@ __global__ void __launch_bounds__(kThreads)
             for (int kk = x; kk <= x + 1 && kk <= a.Gw; kk++) {
                 for (int aa = 0; aa < 2; aa++) {
                     if (clampi(kk - 1 + aa, 0, a.Gw - 1) != x) continue;
-                    const long long blk0 =
-                        ((((long long)n * (a.Gh + 1) + jj) * (a.Gw + 1) + kk) * SY) * SX;
-                    for (int st = 0; st < SY * SX; st++) {
-                        const float *p = partials + (blk0 + st) * 4 * D * 12;
-                        s += p[((b * 2 + aa) * D + z) * 12 + q];
-                    }
+                    const long long blk0 = (((long long)n * (a.Gh + 1) + jj) * (a.Gw + 1) + kk) * S;
+                    const float *p = partials + blk0 * per + ((b * 2 + aa) * D + z) * 12 + q;
+                    for (int st = 0; st < S; st++) s += __ldg(p + (long long)st * per);
                 }
             }
         }
     }
-    a.dgrid[idx] = s;
+    a.dgrid[((((long long)n * 12 + q) * D + z) * a.Gh + y) * a.Gw + x] = s;
 }
 
 // ----------------------------------------------------------------- generic (any shape)
@@ -1400,8 +1395,7 @@ cudaError_t bslice_bwd_launch(const BsliceArgs &a, int algo, int deterministic, 
         else if (split) bslice_bwd_split<false><<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX, partials, stab);
         else bslice_bwd_tiled<<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX, partials, tab);
         note_launch();
-        const long long total = (long long)a.N * 12 * a.D * a.Gh * a.Gw;
-        bslice_dgrid_gather<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(
+        bslice_dgrid_gather<<<dim3((unsigned)((a.Gw + kGX - 1) / kGX), a.Gh * a.D, a.N), kThreads, 0, s>>>(
             a, g.SY, g.SX, partials);
         note_launch();
     } else if (algo == 1 /*GATHER*/ && a.dgrid && a.D <= kNGDMax) {
