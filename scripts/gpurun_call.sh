@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -k "bslice" > gpurun_out/pytest_bs.log 2>&1; tail -2 gpurun_out/pytest_bs.log
-python scripts/bench_layer.py 64 10 bslice_bwd; python scripts/bench_paper.py bslice
+timeout 900 python -m pytest tests/test_graph_gpu.py -q -p no:cacheprovider 2>&1 | tail -2

@@ -37,9 +37,14 @@ def _load(bufs, inp):
         b.copy_(inp[k])
 
 
-@pytest.mark.parametrize("padding", ["zeros", "border"])
-def test_stn_graph_replay(cuda_device, padding):
-    N, C, H, W = 3, 5, 61, 70
+@pytest.mark.parametrize("padding,W,mode", [("zeros", 70, "auto"), ("border", 70, "auto"), ("zeros", 72, "auto"),
+                                            ("zeros", 72, "prep")])
+def test_stn_graph_replay(cuda_device, monkeypatch, padding, W, mode):
+    """W = 72 (rows 16-B aligned): the three-launch path with the d_theta tiles forked onto
+    the library side stream inside the capture; mode prep: the prep / finalize kernels."""
+    if mode == "prep":
+        monkeypatch.setenv("RSGRAD_STN_PREP", "1")
+    N, C, H = 3, 5, 61
     mk = lambda n0: synth.stn_inputs(N, C, H, W, cfg=1, n0=n0)  # noqa: E731
     bufs = {k: v.to(cuda_device).contiguous() for k, v in mk(0).items()}
     y = torch.empty_like(bufs["dy"])
