@@ -684,22 +684,24 @@ RS_DEV void stage_corners_b(float4 *gi, const float *grid, const Tile &t, int D,
     }
 }
 
-template <bool kMulti>
-__global__ void __launch_bounds__(kThreads, RS_V2MINB)
+// NW warps per block; CAP pixels of record capacity (NW = 4: cells of at most 33 x 33 px)
+template <bool kMulti, int NW = 8>
+__global__ void __launch_bounds__(NW * 32, NW == 4 ? 4 : RS_V2MINB)
     bslice_bwd_split(BsliceArgs a, int SY, int SX, float *__restrict__ partials, const int *__restrict__ tab) {
     extern __shared__ float4 smem4[];
     const int D = a.D, NB = D + 1;
-    const int maxch = v2_maxch(NB);
+    constexpr int kNT = NW * 32, CAP = NW == 4 ? 34 * 34 : kV2PX;
+    const int maxch = CAP / kChunk + NB + 1;
     float4 *rec = smem4;                                   // maxch * kChunk * 2 (32-B records)
     float4 *gi = rec + maxch * kChunk * 2;                 // NB * kBinS
-    float *fzv = (float *)(gi + NB * kBinS);               // kV2PX: guide, then fz in place
-    float *fxt = fzv + kV2PX;                              // kV2TX + 4
+    float *fzv = (float *)(gi + NB * kBinS);               // CAP: guide, then fz in place
+    float *fxt = fzv + CAP;                              // kV2TX + 4
     float *fyt = fxt + kV2TX + 4;                          // kV2TY + 4
-    float *wacc = fyt + kV2TY + 4;                         // kWarps * 4 * D * 12
-    int *cnt = (int *)(wacc + kWarps * 4 * D * 12);        // kWarps * NB
-    int *bstart = cnt + kWarps * NB;                       // NB + 1
+    float *wacc = fyt + kV2TY + 4;                         // NW * 4 * D * 12
+    int *cnt = (int *)(wacc + NW * 4 * D * 12);        // NW * NB
+    int *bstart = cnt + NW * NB;                       // NB + 1
     int *chunk_bin = bstart + NB + 1;                      // maxch
-    unsigned char *binv = (unsigned char *)(chunk_bin + maxch);  // kV2PX
+    unsigned char *binv = (unsigned char *)(chunk_bin + maxch);  // CAP
 
     // the block owns a whole dual cell (column split SX); its rows are walked as
     // sub-tiles of <= kV2TY rows (the records hold 32 B per pixel)
@@ -711,11 +713,11 @@ __global__ void __launch_bounds__(kThreads, RS_V2MINB)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const long long HW = (long long)a.H * a.W;
     stage_corners_b(gi, a.grid, tc, D, a.Gh, a.Gw);
-    for (int c = threadIdx.x; c < TW; c += kThreads) {
+    for (int c = threadIdx.x; c < TW; c += kNT) {
         const double cx = bs_cx(tc.xs + c, a.W, a.Gw);
         fxt[c] = (float)__dsub_rn(cx, floor(cx));
     }
-    for (int e = threadIdx.x; e < kWarps * 4 * D * 12; e += kThreads) wacc[e] = 0.f;
+    for (int e = threadIdx.x; e < NW * 4 * D * 12; e += kNT) wacc[e] = 0.f;
     float *mywacc = wacc + w * 4 * D * 12;
     float2 acc2[24];
 #pragma unroll
@@ -749,7 +751,7 @@ __global__ void __launch_bounds__(kThreads, RS_V2MINB)
         const float *gd = a.guide + (long long)t.n * HW + tbase;
         const bool vec = (TW % 4 == 0) && (a.W % 4 == 0) && (t.xs % 4 == 0) && (((uintptr_t)a.guide & 15u) == 0);
         const int wq = vec ? TW / 4 : TW;
-        for (int e = threadIdx.x; e < TH * wq; e += kThreads) {
+        for (int e = threadIdx.x; e < TH * wq; e += kNT) {
             const int r = e / wq, q = e - r * wq;
             const float *src = gd + (long long)r * a.W;
             if (vec) cp_async16(fzv + r * TW + 4 * q, src + 4 * q);
@@ -757,16 +759,16 @@ __global__ void __launch_bounds__(kThreads, RS_V2MINB)
         }
         cp_async_commit();
     }
-    for (int r = threadIdx.x; r < TH; r += kThreads) {
+    for (int r = threadIdx.x; r < TH; r += kNT) {
         const double cy = bs_cx(t.ys + r, a.H, a.Gh);
         fyt[r] = (float)__dsub_rn(cy, floor(cy));
     }
-    for (int e = threadIdx.x; e < kWarps * NB; e += kThreads) cnt[e] = 0;
+    for (int e = threadIdx.x; e < NW * NB; e += kNT) cnt[e] = 0;
     cp_async_wait<0>();
     __syncthreads();
 
     // ---- phase 0: z-bin of every pixel, per-warp counts (warp w: rows w, w+8, ...)
-    for (int r = w; r < TH; r += kWarps) {
+    for (int r = w; r < TH; r += NW) {
         for (int c0 = 0; c0 < TW; c0 += 32) {
             const int c = c0 + lane;
             int bin = -1;
@@ -790,7 +792,7 @@ __global__ void __launch_bounds__(kThreads, RS_V2MINB)
             const int b = base + lane;
             int tot = 0;
             if (b < NB)
-                for (int ww = 0; ww < kWarps; ww++) tot += cnt[ww * NB + b];
+                for (int ww = 0; ww < NW; ww++) tot += cnt[ww * NB + b];
             const int padded = (tot + kChunk - 1) & ~(kChunk - 1);
             int v = padded;
 #pragma unroll
@@ -801,7 +803,7 @@ __global__ void __launch_bounds__(kThreads, RS_V2MINB)
             if (b < NB) {
                 int off = run + v - padded;
                 bstart[b] = off;
-                for (int ww = 0; ww < kWarps; ww++) {
+                for (int ww = 0; ww < NW; ww++) {
                     const int c2 = cnt[ww * NB + b];
                     cnt[ww * NB + b] = off;
                     off += c2;
@@ -817,7 +819,7 @@ __global__ void __launch_bounds__(kThreads, RS_V2MINB)
     }
     __syncthreads();
     const int nchunks = bstart[NB] / kChunk;
-    for (int c = threadIdx.x; c < nchunks; c += kThreads) {
+    for (int c = threadIdx.x; c < nchunks; c += kNT) {
         int b = 0;
         while (bstart[b + 1] <= c * kChunk) b++;
         chunk_bin[c] = b;
@@ -849,7 +851,7 @@ __global__ void __launch_bounds__(kThreads, RS_V2MINB)
             float X[3], G[3];
 #pragma unroll
             for (int i = 0; i < 3; i++) { X[i] = Xn[i]; G[i] = Gn[i]; }
-            const int cx1 = cx + 1 < ncx ? cx + 1 : 0, r1 = cx + 1 < ncx ? r : r + kWarps;
+            const int cx1 = cx + 1 < ncx ? cx + 1 : 0, r1 = cx + 1 < ncx ? r : r + NW;
             fetch(r1, cx1 * 32 + lane);
             const bool ok = c < TW;
             const int o = r * a.W + c;
@@ -907,8 +909,8 @@ __global__ void __launch_bounds__(kThreads, RS_V2MINB)
     // The register sums persist across sub-tiles; odd sub-tiles walk the range backwards,
     // so a warp starts a sub-tile in (about) the bin it ended the previous one with.
     {
-        const int cbeg = (int)(((long long)nchunks * w) / kWarps);
-        const int cend = (int)(((long long)nchunks * (w + 1)) / kWarps);
+        const int cbeg = (int)(((long long)nchunks * w) / NW);
+        const int cend = (int)(((long long)nchunks * (w + 1)) / NW);
         const bool back = kMulti && (sub & 1) != 0;
         if (!kMulti) {  // one sub-tile: the sums start here (not live across phases 0-1)
 #pragma unroll
@@ -957,10 +959,10 @@ __global__ void __launch_bounds__(kThreads, RS_V2MINB)
     __syncthreads();
     // ---- block partial: fixed-order sum over warps
     float *part = partials + (long long)blockIdx.x * 4 * D * 12;
-    for (int e = threadIdx.x; e < 4 * D * 12; e += kThreads) {
+    for (int e = threadIdx.x; e < 4 * D * 12; e += kNT) {
         float s = 0.f;
 #pragma unroll
-        for (int ww = 0; ww < kWarps; ww++) s += wacc[ww * 4 * D * 12 + e];
+        for (int ww = 0; ww < NW; ww++) s += wacc[ww * 4 * D * 12 + e];
         part[e] = s;
     }
 }
@@ -1276,11 +1278,20 @@ size_t bwd_smem(int D) {
            sizeof(float) * kTileXS * kTileYS + 16;
 }
 
-size_t split_smem(int D) {
-    const int NB = D + 1, maxch = kV2PX / kChunk + NB + 1;
+size_t split_smem(int D, int NW = kWarps) {
+    const int cap = NW == 4 ? 34 * 34 : kV2PX;
+    const int NB = D + 1, maxch = cap / kChunk + NB + 1;
     return sizeof(float4) * ((size_t)maxch * kChunk * 2 + (size_t)NB * kBinS) +
-           sizeof(float) * ((size_t)kV2PX + kV2TX + 4 + kV2TY + 4 + (size_t)kWarps * 4 * D * 12) +
-           sizeof(int) * ((size_t)kWarps * NB + NB + 1 + maxch) + kV2PX + 16;
+           sizeof(float) * ((size_t)cap + kV2TX + 4 + kV2TY + 4 + (size_t)NW * 4 * D * 12) +
+           sizeof(int) * ((size_t)NW * NB + NB + 1 + maxch) + cap + 16;
+}
+
+// four-warp blocks for dual cells of at most 32 x 32 px (half the d_grid flushes per pixel,
+// four blocks per SM); RSGRAD_BSLICE_NW=8 forces the eight-warp form
+int split_warps(int H, int W, int Gh, int Gw) {
+    const char *e = getenv("RSGRAD_BSLICE_NW");
+    if (e && atoi(e) == 8) return 8;
+    return ((W + Gw - 1) / Gw <= 32 && (H + Gh - 1) / Gh <= 32) ? 4 : 8;
 }
 
 // Backward kernel choice.  bslice_bwd_split where its tile is a whole dual cell (cells of
@@ -1376,8 +1387,12 @@ cudaError_t bslice_bwd_launch(const BsliceArgs &a, int algo, int deterministic, 
         const size_t sm = split ? split_smem(a.D) : bwd_smem(a.D);
         // per device and per call (the attribute belongs to the current device's context)
         const bool multi = split && (a.H + a.Gh - 1) / a.Gh > kV2TY;  // cells of several sub-tiles
-        cudaError_t ea = cudaFuncSetAttribute(!split ? bslice_bwd_tiled : multi ? bslice_bwd_split<true> : bslice_bwd_split<false>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        const int nw = split && !multi ? split_warps(a.H, a.W, a.Gh, a.Gw) : 8;
+        const size_t smw = split ? split_smem(a.D, nw) : sm;
+        cudaError_t ea = cudaFuncSetAttribute(!split ? bslice_bwd_tiled : multi ? bslice_bwd_split<true>
+                                                                          : nw == 4 ? bslice_bwd_split<false, 4>
+                                                                                    : bslice_bwd_split<false>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw);
         if (ea != cudaSuccess) return ea;
         float *partials = (float *)ws;
         int *tab = (int *)(partials + (size_t)g.blocks * 4 * a.D * 12);
@@ -1391,8 +1406,10 @@ cudaError_t bslice_bwd_launch(const BsliceArgs &a, int algo, int deterministic, 
             note_launch();
         }
         int *stab = self_bounds ? nullptr : tab;
-        if (split && multi) bslice_bwd_split<true><<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX, partials, stab);
-        else if (split) bslice_bwd_split<false><<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX, partials, stab);
+        if (split && multi) bslice_bwd_split<true><<<(unsigned)g.blocks, kThreads, smw, s>>>(a, g.SY, g.SX, partials, stab);
+        else if (split && nw == 4)
+            bslice_bwd_split<false, 4><<<(unsigned)g.blocks, 128, smw, s>>>(a, g.SY, g.SX, partials, stab);
+        else if (split) bslice_bwd_split<false><<<(unsigned)g.blocks, kThreads, smw, s>>>(a, g.SY, g.SX, partials, stab);
         else bslice_bwd_tiled<<<(unsigned)g.blocks, kThreads, sm, s>>>(a, g.SY, g.SX, partials, tab);
         note_launch();
         bslice_dgrid_gather<<<dim3((unsigned)((a.Gw + kGX - 1) / kGX), a.Gh * a.D, a.N), kThreads, 0, s>>>(
