@@ -1,7 +1,3 @@
-# scratch: the command list of the most recent gpurun call (see DESIGN.md 9a for the reproducible commands)
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
-timeout 900 python bench.py > gpurun_out/bench_r2h.json 2> gpurun_out/bench_r2h.err; tail -c 300 gpurun_out/bench_r2h.json
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/paper_r2h.csv python scripts/bench_paper.py --launches gpurun_out/paper_r2h.csv.order > gpurun_out/pl.log 2>&1
-python scripts/bench_paper.py --parse gpurun_out/paper_r2h.csv > gpurun_out/paper_breakdown_r2h.md 2>&1
-python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')"
+RSGRAD_BSLICE_NW=4 timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -k "bslice" 2>&1 | tail -1
+for nw in 8 4; do echo nw=$nw; RSGRAD_BSLICE_NW=$nw python scripts/bench_layer.py 64 10 bslice_bwd; RSGRAD_BSLICE_NW=$nw python scripts/bench_paper.py g16x16; done
