@@ -87,6 +87,14 @@ __global__ void __launch_bounds__(kT)
     const int nsel = list ? *count : N;
     const long long CHW = (long long)C * HW, CP = (long long)C * P;
     __shared__ unsigned red[kT / 32];
+    if (!list && flags) {
+        // flag-selected samples (the AUTO warp rescue, usually none): one parallel pass over
+        // the flags first, so a call without a selected sample exits after one load
+        // latency instead of N dependent ones
+        int any = 0;
+        for (int n = threadIdx.x; n < N; n += kT) any |= flags[n] == flag_on;
+        if (!__syncthreads_or(any)) return;
+    }
     for (int f = 0; f < nsel; f++) {
         const int n = list ? list[f] : f;
         if (!list && flags && flags[n] != flag_on) continue;  // uniform over the grid

@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-RSGRAD_BSLICE_NW=4 timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -k "bslice" 2>&1 | tail -1
-for nw in 8 4; do echo nw=$nw; RSGRAD_BSLICE_NW=$nw python scripts/bench_layer.py 64 10 bslice_bwd; RSGRAD_BSLICE_NW=$nw python scripts/bench_paper.py g16x16; done
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -k "warp or graph" > gpurun_out/pytest_w.log 2>&1; tail -1 gpurun_out/pytest_w.log
+python scripts/bench_paper.py warp; python scripts/bench_layer.py 64 10 warp_bwd
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv -k regex:det_scatter python scripts/bench_paper.py warp 2>/dev/null | grep det_scatter | head -3 | cut -c1-200
