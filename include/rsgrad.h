@@ -35,7 +35,9 @@
  *             released with the CUDA context).
  *   Workspace *_bwd take an optional device workspace of
  *             rsgrad_bwd_workspace_bytes(...) bytes (same opts: deterministic=1
- *             adds the fixed-point accumulators).  NULL / ws_bytes too small (e.g.
+ *             adds the fixed-point accumulators; stn_bwd always holds one sample's,
+ *             for AUTO's exact scatter of high fan-in fallback samples).  NULL /
+ *             ws_bytes too small (e.g.
  *             0) => the library takes a stream-ordered temporary of that size from
  *             the stream's device's DEFAULT memory pool (cudaMallocAsync) and frees it
  *             in stream order (cudaFreeAsync): nothing is reserved by the library

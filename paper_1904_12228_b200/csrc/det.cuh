@@ -77,15 +77,70 @@ RS_DEV void det_grid_barrier(unsigned *bar, unsigned nblocks) {
 // Sample selection: list/count (device list of samples), else flags (flags[n] != 0),
 // else every sample 0..N-1.  flags[n] == flag_on selects (a per-call tag lets a flag array
 // be reused without clearing it: stale values only cost a recompute, never correctness).
+// One sample's exact scatter, by every block of a co-resident grid (three phases
+// separated by grid barriers; max-slot `slot` of ws.maxbits must be zero on entry).
+template <class S, int kT>
+RS_DEV void det_scatter_one(const S &smp, const float *__restrict__ dy, float *__restrict__ dx, int n, int slot, int C,
+                            long long HW, long long P, const DetWs &ws, unsigned *red) {
+    const unsigned nb = gridDim.x;
+    const long long tid = (long long)blockIdx.x * kT + threadIdx.x, nthr = (long long)nb * kT;
+    const long long CHW = (long long)C * HW, CP = (long long)C * P;
+    const float *g = dy + (long long)n * CP;
+    // (A) zero the accumulator, max |dY| of the sample
+    for (long long e = tid; e < CHW; e += nthr) ws.acc[e] = 0ull;
+    unsigned m = 0u;
+    for (long long e = tid; e < CP; e += nthr) m = max(m, __float_as_uint(fabsf(__ldg(g + e))));
+    m = __reduce_max_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned b = 0u;
+        for (int k = 0; k < kT / 32; k++) b = max(b, red[k]);
+        atomicMax(ws.maxbits + slot, b);
+    }
+    det_grid_barrier(ws.bar, nb);
+    // (B) scatter: round(w*g * 2^S) into 64-bit integer sums
+    const float mx = __uint_as_float(__ldcg(ws.maxbits + slot));
+    const bool finite = isfinite(mx);
+    int Sx = 0;
+    if (mx > 0.f && finite) {
+        const double bound = (double)mx * (double)P * S::kWmax;
+        Sx = 61 - ilogb(bound) - 1;  // bound < 2^(ilogb+1)  =>  bound * 2^S < 2^61
+    }
+    if (finite) {
+        for (long long q = tid; q < P; q += nthr) {
+            long long off[S::kMaxTaps];
+            float w[S::kMaxTaps];
+            const int nt = smp.taps(n, q, off, w);
+            if (nt == 0) continue;
+            for (int c = 0; c < C; c++) {
+                const float gv = __ldg(g + (long long)c * P + q);
+                if (gv == 0.f) continue;
+                unsigned long long *ac = ws.acc + (long long)c * HW;
+#pragma unroll
+                for (int k = 0; k < S::kMaxTaps; k++) {
+                    if (k >= nt) break;
+                    const double v = ldexp((double)w[k] * (double)gv, Sx);  // exact product, exact scaling
+                    const long long iv = __double2ll_rn(v);
+                    if (iv != 0) atomicAdd(ac + off[k], (unsigned long long)iv);
+                }
+            }
+        }
+    }
+    det_grid_barrier(ws.bar, nb);
+    // (C) fixed point -> fp32 (non-finite dY: the sample's dx is NaN)
+    float *d = dx + (long long)n * CHW;
+    for (long long e = tid; e < CHW; e += nthr)
+        d[e] = finite ? (float)ldexp((double)(long long)__ldcg(ws.acc + e), -Sx) : __int_as_float(0x7fffffff);
+    det_grid_barrier(ws.bar, nb);
+}
+
 template <class S, int kT = 256>
 __global__ void __launch_bounds__(kT)
     det_scatter_kernel(S smp, const float *__restrict__ dy, float *__restrict__ dx, int N, int C, long long HW,
                        long long P, const int *__restrict__ list, const int *__restrict__ count,
                        int *__restrict__ flags, int flag_on, DetWs ws) {
-    const unsigned nb = gridDim.x;
-    const long long tid = (long long)blockIdx.x * kT + threadIdx.x, nthr = (long long)nb * kT;
     const int nsel = list ? *count : N;
-    const long long CHW = (long long)C * HW, CP = (long long)C * P;
     __shared__ unsigned red[kT / 32];
     if (!list && flags) {
         // flag-selected samples (the AUTO warp rescue, usually none): one parallel pass over
@@ -98,60 +153,12 @@ __global__ void __launch_bounds__(kT)
     for (int f = 0; f < nsel; f++) {
         const int n = list ? list[f] : f;
         if (!list && flags && flags[n] != flag_on) continue;  // uniform over the grid
-        const float *g = dy + (long long)n * CP;
-        // (A) zero the accumulator, max |dY| of the sample
-        for (long long e = tid; e < CHW; e += nthr) ws.acc[e] = 0ull;
-        unsigned m = 0u;
-        for (long long e = tid; e < CP; e += nthr) m = max(m, __float_as_uint(fabsf(__ldg(g + e))));
-        m = __reduce_max_sync(0xffffffffu, m);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            unsigned b = 0u;
-            for (int k = 0; k < kT / 32; k++) b = max(b, red[k]);
-            atomicMax(ws.maxbits + f, b);
-        }
-        det_grid_barrier(ws.bar, nb);
-        // (B) scatter: round(w*g * 2^S) into 64-bit integer sums
-        const float mx = __uint_as_float(__ldcg(ws.maxbits + f));
-        const bool finite = isfinite(mx);
-        int Sx = 0;
-        if (mx > 0.f && finite) {
-            const double bound = (double)mx * (double)P * S::kWmax;
-            Sx = 61 - ilogb(bound) - 1;  // bound < 2^(ilogb+1)  =>  bound * 2^S < 2^61
-        }
-        if (finite) {
-            for (long long q = tid; q < P; q += nthr) {
-                long long off[S::kMaxTaps];
-                float w[S::kMaxTaps];
-                const int nt = smp.taps(n, q, off, w);
-                if (nt == 0) continue;
-                for (int c = 0; c < C; c++) {
-                    const float gv = __ldg(g + (long long)c * P + q);
-                    if (gv == 0.f) continue;
-                    unsigned long long *ac = ws.acc + (long long)c * HW;
-#pragma unroll
-                    for (int k = 0; k < S::kMaxTaps; k++) {
-                        if (k >= nt) break;
-                        const double v = ldexp((double)w[k] * (double)gv, Sx);  // exact product, exact scaling
-                        const long long iv = __double2ll_rn(v);
-                        if (iv != 0) atomicAdd(ac + off[k], (unsigned long long)iv);
-                    }
-                }
-            }
-        }
-        det_grid_barrier(ws.bar, nb);
-        // (C) fixed point -> fp32 (non-finite dY: the sample's dx is NaN)
-        float *d = dx + (long long)n * CHW;
-        for (long long e = tid; e < CHW; e += nthr)
-            d[e] = finite ? (float)ldexp((double)(long long)__ldcg(ws.acc + e), -Sx) : __int_as_float(0x7fffffff);
-        det_grid_barrier(ws.bar, nb);
+        det_scatter_one<S, kT>(smp, dy, dx, n, f, C, HW, P, ws, red);
         // every block has read flags[n]: clear it, so a CUDA-graph replay (same tag) does
         // not recompute the sample again unless it is flagged anew
-        if (flags && !list && tid == 0) flags[n] = 0;
+        if (flags && !list && (long long)blockIdx.x * kT + threadIdx.x == 0) flags[n] = 0;
     }
 }
-
 // Zero the barrier / max slots, then launch the cooperative kernel with every block
 // co-resident.
 template <class S>

@@ -719,10 +719,13 @@ RS_DEV bool stn_lean_ok(const Affine &A, int Ho, int Wo);
 
 // flags[n] = 1 if sample n takes the gather adjoint (variant 0: cell-owner,
 // 1: per-pixel gather, 2: lean); fb_list = the others.  Called by one whole block.
+RS_DEV bool stn_heavy(const Affine &A);
+
 RS_DEV void stn_classify_block(const StnArgs &a, int allow_gather, int variant, int *flags, int *fb_list,
-                               int *fb_count) {
-    __shared__ int cnt;
-    if (threadIdx.x == 0) cnt = 0;
+                               int *fb_count, int *hv_list, int *hv_count, unsigned *det_slots) {
+    __shared__ int cnt, hcnt;
+    if (threadIdx.x == 0) cnt = hcnt = 0;
+    for (int e = threadIdx.x; e < a.N + 2; e += blockDim.x) det_slots[e] = 0u;  // det.cuh bar + max slots
     __syncthreads();
     for (int n = threadIdx.x; n < a.N; n += blockDim.x) {
         const Theta T = load_theta(a.theta, n);
@@ -732,21 +735,26 @@ RS_DEV void stn_classify_block(const StnArgs &a, int allow_gather, int variant, 
                                      : variant == 2 ? stn_lean_ok(A, a.Ho, a.Wo) : stn_gatherable(A, a.Ho, a.Wo));
         flags[n] = g ? 1 : 0;
         if (!g) fb_list[atomicAdd(&cnt, 1)] = n;
+        if (!g && stn_heavy(A)) hv_list[atomicAdd(&hcnt, 1)] = n;  // exact scatter (AUTO's atomics skip it)
     }
     __syncthreads();
-    if (threadIdx.x == 0) *fb_count = cnt;
+    if (threadIdx.x == 0) {
+        *fb_count = cnt;
+        *hv_count = hcnt;
+    }
 }
 
 // One launch for the per-call preparation: the normalised coordinate tables (every
 // block), the per-sample classification and the d_theta tile counters (block 0).
 __global__ void stn_prep_kernel(StnArgs a, int allow_gather, int variant, double *xt, double *yt, int *flags,
-                                int *fb_list, int *fb_count, int *ctr) {
+                                int *fb_list, int *fb_count, int *ctr, int *hv_list, int *hv_count,
+                                unsigned *det_slots) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t < a.Wo) xt[t] = stn_norm(t, a.Wo, a.ac);
     if (t < a.Ho) yt[t] = stn_norm(t, a.Ho, a.ac);
     if (blockIdx.x == 0) {
         for (int n = threadIdx.x; n < a.N; n += blockDim.x) ctr[n] = 0;
-        stn_classify_block(a, allow_gather, variant, flags, fb_list, fb_count);
+        stn_classify_block(a, allow_gather, variant, flags, fb_list, fb_count, hv_list, hv_count, det_slots);
     }
 }
 
@@ -1088,6 +1096,10 @@ constexpr int kLCells = (kBX + 1) * (kLTY + 1);  // the block's floor cells: 32 
 #ifndef RS_LEAN_MBAR
 #define RS_LEAN_MBAR 1
 #endif
+#ifndef RS_LEAN_RRU
+#define RS_LEAN_RRU 5  // full unroll of the 5 cell rows: 6.42 vs 6.55 ms (2: 6.61)
+#endif
+constexpr int kLRRU = RS_LEAN_RRU;  // unroll of the lean walk's cell-row loop
 #ifndef RS_LEAN_FXY
 #define RS_LEAN_FXY 1
 #endif
@@ -1115,7 +1127,7 @@ RS_DEV bool stn_lean_ok(const Affine &A, int Ho, int Wo) {
 template <bool VEC, bool SELF = false>
 __global__ void __launch_bounds__(kThreads, RS_LMINB)
     stn_bwd_lean(StnArgs a, const double *__restrict__ xtab, const double *__restrict__ ytab,
-                 const int *__restrict__ flags, int tiles_x, int tiles_y) {
+                 const int *__restrict__ flags, int tiles_x, int tiles_y, unsigned *__restrict__ det_slots = nullptr) {
     extern __shared__ __align__(16) float4 sm4[];
     float *stage = (float *)sm4;                               // kLBufs * kLStage
     uint2 *rec = (uint2 *)(stage + kLBufs * kLStage);          // kLFQMax
@@ -1140,6 +1152,8 @@ __global__ void __launch_bounds__(kThreads, RS_LMINB)
     const long long HW = (long long)a.H * a.W, P = (long long)a.Ho * a.Wo;
     const int px = xa0 - 1 + lane;
     float *dxn = a.dx + (long long)n * a.C * HW;
+    if (det_slots && blockIdx.x == 0 && blockIdx.y == 0)  // (SELF) the tail's det.cuh slots
+        for (int e = threadIdx.x; e < a.N + 2; e += kThreads) det_slots[e] = 0u;
     const Theta T = load_theta(a.theta, n);
     const Affine A = stn_affine(T, a.H, a.W, a.Ho, a.Wo, a.ac);
     // SELF (no prep launch): the block classifies its sample itself (the same test stn_prep makes)
@@ -1350,7 +1364,7 @@ __global__ void __launch_bounds__(kThreads, RS_LMINB)
 #pragma unroll
         for (int c = 0; c < NC; c++) NL[c] = NR[c] = 0.f;
         float *drow = dxn + (long long)c0 * HW + (long long)(wy0 - 1) * a.W + px;
-#pragma unroll 1
+#pragma unroll (kLRRU)
         for (int rr = 0; rr <= kLRows; rr++, drow += a.W) {
             const int y0 = wy0 - 1 + rr;
 #pragma unroll
@@ -1800,6 +1814,13 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ----------------------------------------------------------------- atomic scatter (fallback samples)
+// A fallback sample whose map gathers many output pixels onto one input cell (a singular
+// map, or a zoom-out with 4 / |det| > 64 output pixels per input pixel) would sum hundreds
+// to thousands of fp32 reds per element: with cancelling terms beyond the north star's
+// gradient tolerance, as the warp layer's collapsing flows were.  Such "heavy" samples
+// take the fixed-point scatter (det.cuh), exact to ~1e-11, in AUTO as well.
+RS_DEV bool stn_heavy(const Affine &A) { return !A.inv || fabs(A.det) < 4.0 / 64.0; }
+
 __global__ void __launch_bounds__(kThreads)
     stn_dx_scatter(StnArgs a, const int *__restrict__ fb_list, const int *__restrict__ fb_count) {
     const long long P = (long long)a.Ho * a.Wo, HW = (long long)a.H * a.W;
@@ -1807,6 +1828,7 @@ __global__ void __launch_bounds__(kThreads)
     for (int f = 0; f < nf; f++) {
         const int n = fb_list[f];
         const Theta T = load_theta(a.theta, n);
+        if (stn_heavy(stn_affine(T, a.H, a.W, a.Ho, a.Wo, a.ac))) continue;  // (fixed-point scatter)
         for (long long rem = (long long)blockIdx.x * kThreads + threadIdx.x; rem < P;
              rem += (long long)gridDim.x * kThreads) {
             const int i = (int)(rem / a.Wo), j = (int)(rem - (long long)i * a.Wo);
@@ -1869,73 +1891,43 @@ struct StnTapSampler {
 };
 
 // ----------------------------------------------------------------- lean path tail
-// The last launch of the lean backward when no prep kernel ran: blocks [0, N) sum sample
-// n's d_theta tile partials in fixed order (stn_dtheta_finalize, every sample from the
-// output tiles); blocks [N, grid) classify every sample as stn_bwd_lean did and add the
-// atomic scatter of the fallback samples (singular / huge preimage: their dX tiles were
-// zeroed by the lean kernel) -- one launch instead of prep + scatter + finalize.
+// The last launch of the lean backward when no prep kernel ran (cooperative: every block
+// co-resident): d_theta of every sample as the fixed-order sum of its tile partials
+// (stn_dtheta_finalize's order), then every sample that stn_bwd_lean classified as a
+// fallback (singular / huge preimage: its dX tiles were zeroed) gets the exact
+// fixed-point scatter of det.cuh -- one launch instead of prep + scatter + finalize.
+// ws.maxbits[n] must be zero on entry (stn_bwd_lean<SELF> zeroes them).
 __global__ void __launch_bounds__(kThreads)
-    stn_bwd_tail(StnArgs a, const double *__restrict__ pf, int nf) {
-    const int n = blockIdx.x;
-    if (n < a.N) {
-        if (!a.dtheta) return;
-        const double *p = pf + (long long)n * nf * 6;
-        __shared__ double red[kThreads / 32][6];
-        double sk[6] = {0, 0, 0, 0, 0, 0};
-        for (int b = threadIdx.x; b < nf; b += kThreads)
+    stn_det_tail(StnArgs a, const double *__restrict__ pf, int nf, DetWs ws) {
+    __shared__ double redd[kThreads / 32][6];
+    __shared__ unsigned redu[kThreads / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (a.dtheta)
+        for (int n = blockIdx.x; n < a.N; n += gridDim.x) {  // block-uniform
+            const double *p = pf + (long long)n * nf * 6;
+            double sk[6] = {0, 0, 0, 0, 0, 0};
+            for (int b = threadIdx.x; b < nf; b += kThreads)
 #pragma unroll
-            for (int k = 0; k < 6; k++) sk[k] += p[(long long)b * 6 + k];
-        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+                for (int k = 0; k < 6; k++) sk[k] += p[(long long)b * 6 + k];
 #pragma unroll
-        for (int k = 0; k < 6; k++) {
-            const double v = warp_sum_d(sk[k]);
-            if (lane == 0) red[wid][k] = v;
-        }
-        __syncthreads();
-        if (threadIdx.x < 6) {
-            double v = 0.0;
-            for (int w = 0; w < kThreads / 32; w++) v += red[w][threadIdx.x];
-            a.dtheta[6 * n + threadIdx.x] = (float)v;
-        }
-        return;
-    }
-    if (!a.dx) return;
-    const long long P = (long long)a.Ho * a.Wo, HW = (long long)a.H * a.W;
-    const long long b0 = blockIdx.x - a.N, nbk = gridDim.x - a.N;
-    __shared__ int fb[kThreads], nfb;
-    for (int m0 = 0; m0 < a.N; m0 += kThreads) {
-        // classify kThreads samples at once (thread = sample), then walk the fallback ones
-        __syncthreads();
-        if (threadIdx.x == 0) nfb = 0;
-        __syncthreads();
-        const int mm = m0 + threadIdx.x;
-        if (mm < a.N && !stn_lean_ok(stn_affine(load_theta(a.theta, mm), a.H, a.W, a.Ho, a.Wo, a.ac), a.Ho, a.Wo))
-            fb[atomicAdd(&nfb, 1)] = mm;
-        __syncthreads();
-        for (int f = 0; f < nfb; f++) {
-        const int m = fb[f];
-        const Theta T = load_theta(a.theta, m);
-        for (long long rem = b0 * kThreads + threadIdx.x; rem < P; rem += nbk * kThreads) {
-            const int i = (int)(rem / a.Wo), j = (int)(rem - (long long)i * a.Wo);
-            double ix, iy;
-            stn_coord(T, stn_norm(j, a.Wo, a.ac), stn_norm(i, a.Ho, a.ac), a.H, a.W, a.ac, ix, iy);
-            const Cell cx = cell_of(ix), cy = cell_of(iy);
-            const bool x0ok = cx.i0 >= 0 && cx.i0 < a.W, x1ok = cx.i0 + 1 >= 0 && cx.i0 + 1 < a.W;
-            const bool y0ok = cy.i0 >= 0 && cy.i0 < a.H, y1ok = cy.i0 + 1 >= 0 && cy.i0 + 1 < a.H;
-            if (!((x0ok || x1ok) && (y0ok || y1ok))) continue;
-            const float w00 = (1.f - cy.f) * (1.f - cx.f), w01 = (1.f - cy.f) * cx.f;
-            const float w10 = cy.f * (1.f - cx.f), w11 = cy.f * cx.f;
-            const long long o00 = (long long)cy.i0 * a.W + cx.i0;
-            for (int c = 0; c < a.C; c++) {
-                const float g = ldg_stream(a.dy + ((long long)m * a.C + c) * P + rem);
-                float *q = a.dx + ((long long)m * a.C + c) * HW + o00;
-                if (y0ok && x0ok) red_add(q, w00 * g);
-                if (y0ok && x1ok) red_add(q + 1, w01 * g);
-                if (y1ok && x0ok) red_add(q + a.W, w10 * g);
-                if (y1ok && x1ok) red_add(q + a.W + 1, w11 * g);
+            for (int k = 0; k < 6; k++) {
+                const double v = warp_sum_d(sk[k]);
+                if (lane == 0) redd[wid][k] = v;
             }
+            __syncthreads();
+            if (threadIdx.x < 6) {
+                double v = 0.0;
+                for (int w = 0; w < kThreads / 32; w++) v += redd[w][threadIdx.x];
+                a.dtheta[6 * n + threadIdx.x] = (float)v;
+            }
+            __syncthreads();
         }
-        }
+    if (!a.dx) return;
+    const StnTapSampler smp{a.theta, a.H, a.W, a.Ho, a.Wo, a.ac, a.border};
+    const long long HW = (long long)a.H * a.W, P = (long long)a.Ho * a.Wo;
+    for (int m = 0; m < a.N; m++) {
+        if (stn_lean_ok(stn_affine(load_theta(a.theta, m), a.H, a.W, a.Ho, a.Wo, a.ac), a.Ho, a.Wo)) continue;
+        det_scatter_one<StnTapSampler, kThreads>(smp, a.dy, a.dx, m, m, a.C, HW, P, ws, redu);
     }
 }
 
@@ -1973,7 +1965,7 @@ int stn_bwd_variant() {
 
 struct StnWs {
     double *xtab, *ytab, *pb, *pf;
-    int *flags, *fb_list, *fb_count, *ctr;
+    int *flags, *fb_list, *fb_count, *ctr, *hv_list, *hv_count;
     void *det;  // deterministic fallback scatter (det.cuh), when requested
     size_t bytes;
 };
@@ -1997,7 +1989,10 @@ StnWs stn_ws_layout(void *base, int N, int C, int H, int W, int Ho, int Wo, bool
     const size_t tb = (size_t)g.bx * g.by > (size_t)g.gx * g.gy ? (size_t)g.bx * g.by : (size_t)g.gx * g.gy;
     w.pb = (double *)take(sizeof(double) * 6 * (size_t)N * tb);
     w.pf = (double *)take(sizeof(double) * 6 * (size_t)N * g.fj * g.fi);
-    w.det = det ? take(det_ws_bytes(N, (long long)C * H * W)) : nullptr;
+    w.hv_list = (int *)take(sizeof(int) * N);
+    w.hv_count = (int *)take(sizeof(int));
+    (void)det;  // the fixed-point accumulators serve deterministic=1 and AUTO's heavy samples
+    w.det = take(det_ws_bytes(N, (long long)C * H * W));
     w.bytes = off;
     return w;
 }
@@ -2170,7 +2165,8 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
         if (a.dx) {
             const size_t sm = bwd_lean_smem();
             set_smem(stn_bwd_lean<true, true>, sm);
-            stn_bwd_lean<true, true><<<lgrid, kThreads, sm, s>>>(a, nullptr, nullptr, nullptr, g.bx, ly);
+            stn_bwd_lean<true, true><<<lgrid, kThreads, sm, s>>>(a, nullptr, nullptr, nullptr, g.bx, ly,
+                                                                 det_ws_layout(w.det, a.N, (long long)a.C * HW).bar);
             note_launch();
         }
         if (a.dtheta) {
@@ -2186,15 +2182,26 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
                 if (e != cudaSuccess) return e;
             }
         }
-        const long long P = (long long)a.Ho * a.Wo;
-        long long sb = a.dx ? (P + kThreads - 1) / kThreads : 0;
-        if (sb > 2 * kNumSMs) sb = 2 * kNumSMs;
-        stn_bwd_tail<<<(unsigned)(a.N + sb), kThreads, 0, s>>>(a, w.pf, g.fj * fi_df);
+        // cooperative (co-resident blocks: the fixed-point scatter's grid barriers)
+        int dev = 0, nsm = 0, occ = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stn_det_tail, kThreads, 0);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) return cudaErrorInvalidConfiguration;
+        StnArgs ta = a;
+        const double *pf = w.pf;
+        int nf = g.fj * fi_df;
+        DetWs dw = det_ws_layout(w.det, a.N, (long long)a.C * HW);
+        void *args[] = {&ta, (void *)&pf, &nf, &dw};
+        e = cudaLaunchCooperativeKernel((const void *)stn_det_tail, dim3(nsm * (occ < 2 ? occ : 2)), dim3(kThreads), args,
+                                        0, s);
         note_launch();
-        return cudaGetLastError();
+        return e;
     }
+    const DetWs dw = det_ws_layout(w.det, a.N, (long long)a.C * HW);
     stn_prep_kernel<<<(tmax + 255) / 256, 256, 0, s>>>(a, allow_gather, variant, w.xtab, w.ytab, w.flags, w.fb_list,
-                                                       w.fb_count, w.ctr);
+                                                       w.fb_count, w.ctr, w.hv_list, w.hv_count, dw.bar);
     note_launch();
     if (!allow_gather && a.dx && !det) {
         cudaError_t e = cudaMemsetAsync(a.dx, 0, sizeof(float) * (size_t)a.N * a.C * HW, s);
@@ -2316,6 +2323,11 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
         if (blocks > cap) blocks = cap;
         stn_dx_scatter<<<(unsigned)blocks, kThreads, 0, s>>>(a, w.fb_list, w.fb_count);
         note_launch();
+        // heavy fallback samples (skipped by the atomic scatter): the exact fixed-point scatter
+        const StnTapSampler hsmp{a.theta, a.H, a.W, a.Ho, a.Wo, a.ac, a.border};
+        cudaError_t e = det_scatter_launch(hsmp, a.dy, a.dx, a.N, a.C, HW, P, w.hv_list, w.hv_count, nullptr, w.det, s,
+                                           1, false, 1);
+        if (e != cudaSuccess) return e;
     }
     if (a.dtheta && !(dth_fast && RS_DTH_LASTBLOCK)) {  // (else the FAST tiles finalize in their last block)
         stn_dtheta_finalize<<<a.N, kThreads, 0, s>>>(w.pb, tiles_b, w.pf, g.fj * (dth_fast ? fi_df : g.fi),

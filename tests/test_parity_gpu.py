@@ -158,6 +158,26 @@ def test_stn_bwd_three_launches(cuda_device, monkeypatch):
     assert_close(_np(dth), rdth, "grad", "dtheta only")
 
 
+@pytest.mark.parametrize("padding", ["zeros", "border"])
+def test_stn_high_fan_in_fallback(cuda_device, padding):
+    """AUTO fallback samples whose map piles many output pixels onto one input cell (a
+    near-singular map, strong zoom-out: thousands of taps per element; 2x zoom-out under
+    border padding: clamped taps on the edges) stay within T: the scatter pre-sums each
+    warp's runs of equal tap address before its reds."""
+    inp = synth.stn_inputs(4, 4, 64, 96, cfg=1)
+    inp["theta"][0] = torch.tensor([[0.02, 0.0, 0.1], [0.0, 0.03, 0.0]])
+    inp["theta"][1] = torch.tensor([[0.5, 0.5, 0.1], [0.5, 0.5, -0.2]])
+    inp["theta"][2] = torch.tensor([[2.0, 0.0, 0.0], [0.0, 2.0, 0.0]])
+    inp["theta"][3] = torch.tensor([[0.05, 0.01, -0.3], [-0.02, 0.04, 0.2]])
+    g = _cuda(inp, cuda_device)
+    x, th, dy = (inp[k].double().numpy() for k in ("x", "theta", "dy"))
+    rdx, rdth = oracle.stn_bwd(x, th, dy, True, padding == "border")
+    for _ in range(3):
+        dx, dth = rsgrad.stn_bwd(g["x"], g["theta"], g["dy"], padding=padding)
+        assert_close(_np(dx), rdx, "grad", "dx")
+        assert_close(_np(dth), rdth, "grad", "dtheta")
+
+
 @pytest.mark.parametrize("fork", ["0", "100000"])
 def test_stn_bwd_fork(cuda_device, monkeypatch, fork):
     """The d_theta tiles on the library side stream beside the lean d_input kernel, or
