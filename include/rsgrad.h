@@ -35,8 +35,8 @@
  *             released with the CUDA context).
  *   Workspace *_bwd take an optional device workspace of
  *             rsgrad_bwd_workspace_bytes(...) bytes (same opts: deterministic=1
- *             adds the fixed-point accumulators; stn_bwd always holds one sample's,
- *             for AUTO's exact scatter of high fan-in fallback samples).  NULL /
+ *             adds the fixed-point accumulators; stn_bwd always holds one channel
+ *             plane's, for AUTO's exact scatter of high fan-in fallback samples).  NULL /
  *             ws_bytes too small (e.g.
  *             0) => the library takes a stream-ordered temporary of that size from
  *             the stream's device's DEFAULT memory pool (cudaMallocAsync) and frees it
@@ -298,8 +298,9 @@ rs_status stn3d_bwd(const float *x, const float *theta, const float *dy, int N, 
  * and Gh = depth of the input volume), 7 = stn_lanczos (N, Ho, Wo; deterministic=1: C, H, W);
  * unused arguments are ignored.
  * opts->deterministic = 1 adds the fixed-point accumulators of one sample
- * (8 * C * H * W bytes) for layers 1, 5, 6 and 7; layer 0 (stn) always includes them
- * (AUTO's exact scatter of high fan-in fallback samples).  Returns 0 for an unknown layer. */
+ * (8 * C * H * W bytes) for layers 0, 1, 5, 6 and 7; layer 0 (stn) always includes one
+ * channel plane (8 * H * W bytes: AUTO's exact scatter of high fan-in fallback samples).
+ * Returns 0 for an unknown layer. */
 size_t rsgrad_bwd_workspace_bytes(int layer, int N, int C, int H, int W, int Ho, int Wo, int D,
                                   int Gh, int Gw, const rs_opts *opts);
 

@@ -79,15 +79,17 @@ RS_DEV void det_grid_barrier(unsigned *bar, unsigned nblocks) {
 // be reused without clearing it: stale values only cost a recompute, never correctness).
 // One sample's exact scatter, by every block of a co-resident grid (three phases
 // separated by grid barriers; max-slot `slot` of ws.maxbits must be zero on entry).
+// cpp > 0: the accumulator holds cpp channel planes and the channels are walked in groups
+// of cpp (zero / scatter / convert per group: a small workspace for rare samples).
 template <class S, int kT>
 RS_DEV void det_scatter_one(const S &smp, const float *__restrict__ dy, float *__restrict__ dx, int n, int slot, int C,
-                            long long HW, long long P, const DetWs &ws, unsigned *red) {
+                            long long HW, long long P, const DetWs &ws, unsigned *red, int cpp = 0) {
     const unsigned nb = gridDim.x;
     const long long tid = (long long)blockIdx.x * kT + threadIdx.x, nthr = (long long)nb * kT;
-    const long long CHW = (long long)C * HW, CP = (long long)C * P;
+    const long long CP = (long long)C * P;
     const float *g = dy + (long long)n * CP;
-    // (A) zero the accumulator, max |dY| of the sample
-    for (long long e = tid; e < CHW; e += nthr) ws.acc[e] = 0ull;
+    if (cpp <= 0 || cpp > C) cpp = C;
+    // max |dY| of the sample
     unsigned m = 0u;
     for (long long e = tid; e < CP; e += nthr) m = max(m, __float_as_uint(fabsf(__ldg(g + e))));
     m = __reduce_max_sync(0xffffffffu, m);
@@ -99,7 +101,6 @@ RS_DEV void det_scatter_one(const S &smp, const float *__restrict__ dy, float *_
         atomicMax(ws.maxbits + slot, b);
     }
     det_grid_barrier(ws.bar, nb);
-    // (B) scatter: round(w*g * 2^S) into 64-bit integer sums
     const float mx = __uint_as_float(__ldcg(ws.maxbits + slot));
     const bool finite = isfinite(mx);
     int Sx = 0;
@@ -107,39 +108,47 @@ RS_DEV void det_scatter_one(const S &smp, const float *__restrict__ dy, float *_
         const double bound = (double)mx * (double)P * S::kWmax;
         Sx = 61 - ilogb(bound) - 1;  // bound < 2^(ilogb+1)  =>  bound * 2^S < 2^61
     }
-    if (finite) {
-        for (long long q = tid; q < P; q += nthr) {
-            long long off[S::kMaxTaps];
-            float w[S::kMaxTaps];
-            const int nt = smp.taps(n, q, off, w);
-            if (nt == 0) continue;
-            for (int c = 0; c < C; c++) {
-                const float gv = __ldg(g + (long long)c * P + q);
-                if (gv == 0.f) continue;
-                unsigned long long *ac = ws.acc + (long long)c * HW;
+    for (int c0 = 0; c0 < C; c0 += cpp) {
+        const int cn = min(cpp, C - c0);
+        const long long GHW = (long long)cn * HW;
+        // (A) zero the accumulator of this channel group
+        for (long long e = tid; e < GHW; e += nthr) ws.acc[e] = 0ull;
+        det_grid_barrier(ws.bar, nb);
+        // (B) scatter: round(w*g * 2^S) into 64-bit integer sums
+        if (finite) {
+            for (long long q = tid; q < P; q += nthr) {
+                long long off[S::kMaxTaps];
+                float w[S::kMaxTaps];
+                const int nt = smp.taps(n, q, off, w);
+                if (nt == 0) continue;
+                for (int c = 0; c < cn; c++) {
+                    const float gv = __ldg(g + (long long)(c0 + c) * P + q);
+                    if (gv == 0.f) continue;
+                    unsigned long long *ac = ws.acc + (long long)c * HW;
 #pragma unroll
-                for (int k = 0; k < S::kMaxTaps; k++) {
-                    if (k >= nt) break;
-                    const double v = ldexp((double)w[k] * (double)gv, Sx);  // exact product, exact scaling
-                    const long long iv = __double2ll_rn(v);
-                    if (iv != 0) atomicAdd(ac + off[k], (unsigned long long)iv);
+                    for (int k = 0; k < S::kMaxTaps; k++) {
+                        if (k >= nt) break;
+                        const double v = ldexp((double)w[k] * (double)gv, Sx);  // exact product, exact scaling
+                        const long long iv = __double2ll_rn(v);
+                        if (iv != 0) atomicAdd(ac + off[k], (unsigned long long)iv);
+                    }
                 }
             }
         }
+        det_grid_barrier(ws.bar, nb);
+        // (C) fixed point -> fp32 (non-finite dY: the sample's dx is NaN)
+        float *d = dx + ((long long)n * C + c0) * HW;
+        for (long long e = tid; e < GHW; e += nthr)
+            d[e] = finite ? (float)ldexp((double)(long long)__ldcg(ws.acc + e), -Sx) : __int_as_float(0x7fffffff);
+        det_grid_barrier(ws.bar, nb);
     }
-    det_grid_barrier(ws.bar, nb);
-    // (C) fixed point -> fp32 (non-finite dY: the sample's dx is NaN)
-    float *d = dx + (long long)n * CHW;
-    for (long long e = tid; e < CHW; e += nthr)
-        d[e] = finite ? (float)ldexp((double)(long long)__ldcg(ws.acc + e), -Sx) : __int_as_float(0x7fffffff);
-    det_grid_barrier(ws.bar, nb);
 }
 
 template <class S, int kT = 256>
 __global__ void __launch_bounds__(kT)
     det_scatter_kernel(S smp, const float *__restrict__ dy, float *__restrict__ dx, int N, int C, long long HW,
                        long long P, const int *__restrict__ list, const int *__restrict__ count,
-                       int *__restrict__ flags, int flag_on, DetWs ws) {
+                       int *__restrict__ flags, int flag_on, DetWs ws, int cpp = 0) {
     const int nsel = list ? *count : N;
     __shared__ unsigned red[kT / 32];
     if (!list && flags) {
@@ -153,7 +162,7 @@ __global__ void __launch_bounds__(kT)
     for (int f = 0; f < nsel; f++) {
         const int n = list ? list[f] : f;
         if (!list && flags && flags[n] != flag_on) continue;  // uniform over the grid
-        det_scatter_one<S, kT>(smp, dy, dx, n, f, C, HW, P, ws, red);
+        det_scatter_one<S, kT>(smp, dy, dx, n, f, C, HW, P, ws, red, cpp);
         // every block has read flags[n]: clear it, so a CUDA-graph replay (same tag) does
         // not recompute the sample again unless it is flagged anew
         if (flags && !list && (long long)blockIdx.x * kT + threadIdx.x == 0) flags[n] = 0;
@@ -164,9 +173,9 @@ __global__ void __launch_bounds__(kT)
 template <class S>
 cudaError_t det_scatter_launch(const S &smp, const float *dy, float *dx, int N, int C, long long HW, long long P,
                                const int *list, const int *count, int *flags, void *ws, cudaStream_t s,
-                               int flag_on = 1, bool zero_slots = true, int max_blocks_per_sm = 4) {
+                               int flag_on = 1, bool zero_slots = true, int max_blocks_per_sm = 4, int cpp = 0) {
     constexpr int kT = 256;
-    const DetWs w = det_ws_layout(ws, N, (long long)C * HW);
+    const DetWs w = det_ws_layout(ws, N, (long long)(cpp > 0 && cpp < C ? cpp : C) * HW);
     cudaError_t e = cudaSuccess;
     if (zero_slots) {  // (else the caller's previous kernel on s zeroed them)
         e = cudaMemsetAsync(w.bar, 0, sizeof(unsigned) * ((size_t)N + 2), s);
@@ -182,10 +191,10 @@ cudaError_t det_scatter_launch(const S &smp, const float *dy, float *dx, int N, 
     const int blocks = nsm * (occ < max_blocks_per_sm ? occ : max_blocks_per_sm);
     S sm = smp;
     long long hw = HW, p = P;
-    int n = N, c = C, fo = flag_on;
+    int n = N, c = C, fo = flag_on, cp = cpp;
     DetWs wk = w;
     void *args[] = {&sm, (void *)&dy, (void *)&dx, &n, &c, &hw, &p, (void *)&list, (void *)&count, (void *)&flags, &fo,
-                    &wk};
+                    &wk, &cp};
     e = cudaLaunchCooperativeKernel((const void *)kern, dim3(blocks), dim3(kT), args, 0, s);
     note_launch();
     return e;

@@ -719,7 +719,7 @@ RS_DEV bool stn_lean_ok(const Affine &A, int Ho, int Wo);
 
 // flags[n] = 1 if sample n takes the gather adjoint (variant 0: cell-owner,
 // 1: per-pixel gather, 2: lean); fb_list = the others.  Called by one whole block.
-RS_DEV bool stn_heavy(const Affine &A);
+RS_DEV bool stn_heavy(const Affine &A, int border, int H, int W, int Ho, int Wo);
 
 RS_DEV void stn_classify_block(const StnArgs &a, int allow_gather, int variant, int *flags, int *fb_list,
                                int *fb_count, int *hv_list, int *hv_count, unsigned *det_slots) {
@@ -735,7 +735,7 @@ RS_DEV void stn_classify_block(const StnArgs &a, int allow_gather, int variant, 
                                      : variant == 2 ? stn_lean_ok(A, a.Ho, a.Wo) : stn_gatherable(A, a.Ho, a.Wo));
         flags[n] = g ? 1 : 0;
         if (!g) fb_list[atomicAdd(&cnt, 1)] = n;
-        if (!g && stn_heavy(A)) hv_list[atomicAdd(&hcnt, 1)] = n;  // exact scatter (AUTO's atomics skip it)
+        if (!g && stn_heavy(A, a.border, a.H, a.W, a.Ho, a.Wo)) hv_list[atomicAdd(&hcnt, 1)] = n;  // exact scatter (AUTO's atomics skip it)
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1819,7 +1819,18 @@ __global__ void __launch_bounds__(kThreads)
 // to thousands of fp32 reds per element: with cancelling terms beyond the north star's
 // gradient tolerance, as the warp layer's collapsing flows were.  Such "heavy" samples
 // take the fixed-point scatter (det.cuh), exact to ~1e-11, in AUTO as well.
-RS_DEV bool stn_heavy(const Affine &A) { return !A.inv || fabs(A.det) < 4.0 / 64.0; }
+RS_DEV bool stn_heavy(const Affine &A, int border = 0, int H = 0, int W = 0, int Ho = 0, int Wo = 0) {
+    if (!A.inv || fabs(A.det) < 4.0 / 64.0) return true;
+    if (!border) return false;
+    // border padding clamps every tap outside the image onto its edge (a corner pixel
+    // collects the whole region beyond both edges): heavy once the output reaches outside
+    for (int c = 0; c < 4; c++) {
+        const double qx = (c & 1) ? Wo - 1 : 0, qy = (c & 2) ? Ho - 1 : 0;
+        const double px = A.p0x + A.m00 * qx + A.m01 * qy, py = A.p0y + A.m10 * qx + A.m11 * qy;
+        if (px < -1.0 || px > W || py < -1.0 || py > H) return true;
+    }
+    return false;
+}
 
 __global__ void __launch_bounds__(kThreads)
     stn_dx_scatter(StnArgs a, const int *__restrict__ fb_list, const int *__restrict__ fb_count) {
@@ -1828,7 +1839,7 @@ __global__ void __launch_bounds__(kThreads)
     for (int f = 0; f < nf; f++) {
         const int n = fb_list[f];
         const Theta T = load_theta(a.theta, n);
-        if (stn_heavy(stn_affine(T, a.H, a.W, a.Ho, a.Wo, a.ac))) continue;  // (fixed-point scatter)
+        if (stn_heavy(stn_affine(T, a.H, a.W, a.Ho, a.Wo, a.ac), a.border, a.H, a.W, a.Ho, a.Wo)) continue;  // (fixed-point scatter)
         for (long long rem = (long long)blockIdx.x * kThreads + threadIdx.x; rem < P;
              rem += (long long)gridDim.x * kThreads) {
             const int i = (int)(rem / a.Wo), j = (int)(rem - (long long)i * a.Wo);
@@ -1927,7 +1938,7 @@ __global__ void __launch_bounds__(kThreads)
     const long long HW = (long long)a.H * a.W, P = (long long)a.Ho * a.Wo;
     for (int m = 0; m < a.N; m++) {
         if (stn_lean_ok(stn_affine(load_theta(a.theta, m), a.H, a.W, a.Ho, a.Wo, a.ac), a.Ho, a.Wo)) continue;
-        det_scatter_one<StnTapSampler, kThreads>(smp, a.dy, a.dx, m, m, a.C, HW, P, ws, redu);
+        det_scatter_one<StnTapSampler, kThreads>(smp, a.dy, a.dx, m, m, a.C, HW, P, ws, redu, 1);
     }
 }
 
@@ -1991,8 +2002,9 @@ StnWs stn_ws_layout(void *base, int N, int C, int H, int W, int Ho, int Wo, bool
     w.pf = (double *)take(sizeof(double) * 6 * (size_t)N * g.fj * g.fi);
     w.hv_list = (int *)take(sizeof(int) * N);
     w.hv_count = (int *)take(sizeof(int));
-    (void)det;  // the fixed-point accumulators serve deterministic=1 and AUTO's heavy samples
-    w.det = take(det_ws_bytes(N, (long long)C * H * W));
+    // fixed-point accumulators: every channel for deterministic=1, one channel plane for
+    // AUTO's heavy samples (walked a channel at a time: det_scatter_one's cpp = 1)
+    w.det = take(det_ws_bytes(N, (det ? (long long)C : 1LL) * H * W));
     w.bytes = off;
     return w;
 }
@@ -2166,7 +2178,7 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
             const size_t sm = bwd_lean_smem();
             set_smem(stn_bwd_lean<true, true>, sm);
             stn_bwd_lean<true, true><<<lgrid, kThreads, sm, s>>>(a, nullptr, nullptr, nullptr, g.bx, ly,
-                                                                 det_ws_layout(w.det, a.N, (long long)a.C * HW).bar);
+                                                                 det_ws_layout(w.det, a.N, HW).bar);
             note_launch();
         }
         if (a.dtheta) {
@@ -2192,14 +2204,14 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
         StnArgs ta = a;
         const double *pf = w.pf;
         int nf = g.fj * fi_df;
-        DetWs dw = det_ws_layout(w.det, a.N, (long long)a.C * HW);
+        DetWs dw = det_ws_layout(w.det, a.N, HW);  // one channel plane (cpp = 1)
         void *args[] = {&ta, (void *)&pf, &nf, &dw};
         e = cudaLaunchCooperativeKernel((const void *)stn_det_tail, dim3(nsm * (occ < 2 ? occ : 2)), dim3(kThreads), args,
                                         0, s);
         note_launch();
         return e;
     }
-    const DetWs dw = det_ws_layout(w.det, a.N, (long long)a.C * HW);
+    const DetWs dw = det_ws_layout(w.det, a.N, (det ? (long long)a.C : 1LL) * HW);
     stn_prep_kernel<<<(tmax + 255) / 256, 256, 0, s>>>(a, allow_gather, variant, w.xtab, w.ytab, w.flags, w.fb_list,
                                                        w.fb_count, w.ctr, w.hv_list, w.hv_count, dw.bar);
     note_launch();
@@ -2326,7 +2338,7 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
         // heavy fallback samples (skipped by the atomic scatter): the exact fixed-point scatter
         const StnTapSampler hsmp{a.theta, a.H, a.W, a.Ho, a.Wo, a.ac, a.border};
         cudaError_t e = det_scatter_launch(hsmp, a.dy, a.dx, a.N, a.C, HW, P, w.hv_list, w.hv_count, nullptr, w.det, s,
-                                           1, false, 1);
+                                           1, false, 1, 1);
         if (e != cudaSuccess) return e;
     }
     if (a.dtheta && !(dth_fast && RS_DTH_LASTBLOCK)) {  // (else the FAST tiles finalize in their last block)

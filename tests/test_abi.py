@@ -88,16 +88,16 @@ def test_validation_flags():
 
 
 def test_workspace_sizes():
-    # STN: per-block fp64 d_theta partials + coordinate tables + one sample of 64-bit
+    # STN: per-block fp64 d_theta partials + coordinate tables + one channel plane of 64-bit
     # fixed-point accumulators (AUTO's exact scatter of high fan-in fallback samples)
-    assert rsgrad.workspace_bytes(0, 4, 16, 512, 512, 512, 512) >= 8 * 16 * 512 * 512
+    assert rsgrad.workspace_bytes(0, 4, 16, 512, 512, 512, 512) >= 8 * 512 * 512
     # warp AUTO: room for the fixed-point recompute of heavy (collapsing) samples + flags
     assert rsgrad.workspace_bytes(1, 8, 3, 384, 512) >= 8 * 3 * 384 * 512 + 4 * 8
     # deterministic=1: + one sample of 64-bit fixed-point accumulators (det.cuh)
     det = rsgrad._opts(deterministic=True)
     assert rsgrad.workspace_bytes(1, 8, 3, 384, 512, opts=det) >= 8 * 3 * 384 * 512
     assert (rsgrad.workspace_bytes(0, 4, 16, 512, 512, 512, 512, opts=det)
-            >= rsgrad.workspace_bytes(0, 4, 16, 512, 512, 512, 512))
+            >= rsgrad.workspace_bytes(0, 4, 16, 512, 512, 512, 512) + 8 * 15 * 512 * 512)
     # bslice tiled path: one partial per (dual cell, corner, z, q) + the per-call
     # dual-cell bounds table (Gh + Gw + 4 ints)
     ws = rsgrad.workspace_bytes(2, 4, 3, 1024, 1024, D=8, Gh=16, Gw=16)
