@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-python scripts/bench_layer.py 64 10 stn_bwd
-for t in b2a b2b; do echo $t; python scripts/ab_lib.py paper_1904_12228_b200/ab_$t.so 64 10 stn_bwd; done
+for i in 1 2; do timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider 2>&1 | tail -1; done
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')"
