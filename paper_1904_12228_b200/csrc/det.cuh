@@ -181,12 +181,18 @@ cudaError_t det_scatter_launch(const S &smp, const float *dy, float *dx, int N, 
         e = cudaMemsetAsync(w.bar, 0, sizeof(unsigned) * ((size_t)N + 2), s);
         if (e != cudaSuccess) return e;
     }
-    int dev = 0, nsm = 0, occ = 0;
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     auto kern = det_scatter_kernel<S, kT>;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kT, 0);
-    if (e != cudaSuccess) return e;
+    // SM count and occupancy per (kernel instantiation, device), queried once per thread
+    static thread_local int cache_nsm[64], cache_occ[64];
+    const int slot = dev >= 0 && dev < 64 ? dev : 0;
+    if (cache_occ[slot] <= 0) {
+        cudaDeviceGetAttribute(&cache_nsm[slot], cudaDevAttrMultiProcessorCount, dev);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cache_occ[slot], kern, kT, 0);
+        if (e != cudaSuccess) return e;
+    }
+    const int nsm = cache_nsm[slot], occ = cache_occ[slot];
     if (occ < 1) return cudaErrorInvalidConfiguration;
     const int blocks = nsm * (occ < max_blocks_per_sm ? occ : max_blocks_per_sm);
     S sm = smp;

@@ -2195,11 +2195,17 @@ cudaError_t stn_bwd_launch(const StnArgs &a, int algo, int deterministic, void *
             }
         }
         // cooperative (co-resident blocks: the fixed-point scatter's grid barriers)
-        int dev = 0, nsm = 0, occ = 0;
+        int dev = 0;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stn_det_tail, kThreads, 0);
-        if (e != cudaSuccess) return e;
+        static thread_local int cache_nsm[64], cache_occ[64];  // per device, queried once per thread
+        const int slot = dev >= 0 && dev < 64 ? dev : 0;
+        cudaError_t e = cudaSuccess;
+        if (cache_occ[slot] <= 0) {
+            cudaDeviceGetAttribute(&cache_nsm[slot], cudaDevAttrMultiProcessorCount, dev);
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cache_occ[slot], stn_det_tail, kThreads, 0);
+            if (e != cudaSuccess) return e;
+        }
+        const int nsm = cache_nsm[slot], occ = cache_occ[slot];
         if (occ < 1) return cudaErrorInvalidConfiguration;
         StnArgs ta = a;
         const double *pf = w.pf;

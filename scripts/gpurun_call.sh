@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-for i in 1 2; do timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider 2>&1 | tail -1; done
-python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')"
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -k "stn or warp or graph" 2>&1 | tail -1
+python scripts/bench_paper.py stn; python scripts/bench_paper.py warp
