@@ -19,6 +19,20 @@ namespace {
 
 constexpr int kVT = 256;
 
+// Output pixel of this thread.  When the output tiles exactly into 32 x 8 blocks, each
+// warp covers an 8 x 4 patch: under a rotation the 32 lanes of one tap load then touch
+// ~6 input rows instead of up to 16 (a 32-pixel row run), so each load costs fewer L1
+// wavefronts.  Otherwise (ragged shapes) row-major runs of 256.  Either way a block owns
+// 256 output pixels and the grid has P / 256 blocks per sample (d_theta partial slots).
+RS_DEV int out_pixel(int Ho, int Wo) {
+    if ((Wo & 31) == 0 && (Ho & 7) == 0) {
+        const int tw = Wo >> 5, ty = blockIdx.x / tw, tx = blockIdx.x - ty * tw;
+        const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+        return (ty * 8 + (w >> 2) * 4 + (l >> 3)) * Wo + tx * 32 + (w & 3) * 8 + (l & 7);
+    }
+    return blockIdx.x * kVT + threadIdx.x;
+}
+
 RS_DEV void cubic_w(double t, float w[4], float dw[4]) {
     const double A = -0.75;
     auto c1 = [&](double x) { return __dadd_rn(__dmul_rn(__dmul_rn(__dsub_rn(__dmul_rn(A + 2.0, x), A + 3.0), x), x), 1.0); };
@@ -60,7 +74,7 @@ RS_DEV Bicubic bicubic_at(const float *theta, int n, int i, int j, int H, int W,
 
 __global__ void __launch_bounds__(kVT) bicubic_fwd(StnArgs a) {
     const int P = a.Ho * a.Wo, HW = a.H * a.W;
-    const int q = blockIdx.x * kVT + threadIdx.x;
+    const int q = out_pixel(a.Ho, a.Wo);
     if (q >= P) return;
     const int n = blockIdx.y, i = q / a.Wo, j = q - i * a.Wo;
     const Bicubic b = bicubic_at(a.theta, n, i, j, a.H, a.W, a.Ho, a.Wo, a.ac);
@@ -219,7 +233,7 @@ __global__ void __launch_bounds__(kVT)
 
 __global__ void __launch_bounds__(kVT, 3) bicubic_bwd(StnArgs a, double *part, const int *flags) {
     const int P = a.Ho * a.Wo, HW = a.H * a.W;
-    const int q = blockIdx.x * kVT + threadIdx.x;
+    const int q = out_pixel(a.Ho, a.Wo);
     const int n = blockIdx.y;
     if (flags && !flags[n]) a.dx = nullptr;  // d_input came from the gather
     float dth[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -344,9 +358,12 @@ RS_DEV Lz lanczos_at(const float *theta, int n, int i, int j, int H, int W, int 
     return b;
 }
 
-__global__ void __launch_bounds__(kVT) lanczos_fwd(StnArgs a) {
+#ifndef RS_LZ_MINB
+#define RS_LZ_MINB 2
+#endif
+__global__ void __launch_bounds__(kVT, RS_LZ_MINB) lanczos_fwd(StnArgs a) {
     const int P = a.Ho * a.Wo, HW = a.H * a.W;
-    const int q = blockIdx.x * kVT + threadIdx.x;
+    const int q = out_pixel(a.Ho, a.Wo);
     if (q >= P) return;
     const int n = blockIdx.y, i = q / a.Wo, j = q - i * a.Wo;
     const Lz b = lanczos_at(a.theta, n, i, j, a.H, a.W, a.Ho, a.Wo, a.ac);
@@ -377,9 +394,12 @@ __global__ void __launch_bounds__(kVT) lanczos_fwd(StnArgs a) {
     }
 }
 
-__global__ void __launch_bounds__(kVT) lanczos_bwd(StnArgs a, double *part) {
+#ifndef RS_LZ_BWD_MINB
+#define RS_LZ_BWD_MINB 1
+#endif
+__global__ void __launch_bounds__(kVT, RS_LZ_BWD_MINB) lanczos_bwd(StnArgs a, double *part) {
     const int P = a.Ho * a.Wo, HW = a.H * a.W;
-    const int q = blockIdx.x * kVT + threadIdx.x;
+    const int q = out_pixel(a.Ho, a.Wo);
     const int n = blockIdx.y;
     float dth[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if (q < P) {
@@ -420,10 +440,12 @@ __global__ void __launch_bounds__(kVT) lanczos_bwd(StnArgs a, double *part) {
             if (a.dx) {
                 float *d = a.dx + ((long long)n * a.C + c) * HW;
 #pragma unroll
-                for (int u = 0; u < 6; u++)
+                for (int u = 0; u < 6; u++) {
+                    const float gw = g * b.wy[u];
 #pragma unroll
                     for (int v = 0; v < 6; v++)
-                        if (vy[u] && vx[v]) red_add_nc(d + ro[u] + co[v], g * (b.wy[u] * b.wx[v]));
+                        if (vy[u] && vx[v]) red_add_nc(d + ro[u] + co[v], gw * b.wx[v]);
+                }
             }
         }
         const float sx = a.ac ? 0.5f * (a.W - 1) : 0.5f * a.W, sy = a.ac ? 0.5f * (a.H - 1) : 0.5f * a.H;

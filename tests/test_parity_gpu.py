@@ -1048,6 +1048,24 @@ def test_stn_lanczos_parity(cuda_device, dims, ac):
     assert_close(_np(dth), rdth, "grad", "dtheta")
 
 
+def test_stn_lanczos_tiled_zoom_and_edge(cuda_device):
+    """Ho, Wo multiples of 8 and 32: the 32 x 8 block tiles with 8 x 4 warp patches
+    (out_pixel) under a 5x zoom-in (sample 0), a 5x zoom-out (sample 1: every output
+    pixel's taps are disjoint from its neighbours') and a map whose taps are clipped by
+    two image edges (sample 2)."""
+    g = torch.Generator().manual_seed(47)
+    N, C, H, W, Ho, Wo = 3, 2, 320, 320, 64, 64
+    x = torch.randn(N, C, H, W, generator=g, dtype=torch.float64).float()
+    dy = torch.randn(N, C, Ho, Wo, generator=g, dtype=torch.float64).float()
+    th = torch.tensor([[[0.21, 0.03, 0.02], [-0.02, 0.19, 0.05]],
+                       [[1.0, 0.0, 0.0], [0.0, 1.0, 0.0]],
+                       [[0.15, 0.05, 0.93], [-0.04, 0.16, -0.9]]])
+    dx, dth = rsgrad.stn_lanczos_bwd(x.to(cuda_device), th.to(cuda_device), dy.to(cuda_device))
+    rdx, rdth = oracle.stn_lanczos_bwd(x.double().numpy(), th.double().numpy(), dy.double().numpy())
+    assert_close(_np(dx), rdx, "grad", "dx")
+    assert_close(_np(dth), rdth, "grad", "dtheta")
+
+
 # ============================================================================ boundary contract
 @pytest.mark.parametrize("D", [61, 64])
 def test_bslice_many_planes_tiled_backward(cuda_device, D):
