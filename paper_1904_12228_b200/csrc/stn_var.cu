@@ -20,15 +20,19 @@ namespace {
 constexpr int kVT = 256;
 
 // Output pixel of this thread.  When the output tiles exactly into 32 x 8 blocks, each
-// warp covers an 8 x 4 patch: under a rotation the 32 lanes of one tap load then touch
-// ~6 input rows instead of up to 16 (a 32-pixel row run), so each load costs fewer L1
-// wavefronts.  Otherwise (ragged shapes) row-major runs of 256.  Either way a block owns
+// warp covers a 16 x 2 patch: under a rotation the 32 lanes of one tap load then touch
+// fewer input rows than a 32-pixel row run (up to 16 rows at 30 degrees), so each load
+// costs fewer L1 wavefronts (measured: 16 x 2 < 8 x 4 < 4 x 8 in time).  Otherwise (ragged shapes) row-major runs of 256.  Either way a block owns
 // 256 output pixels and the grid has P / 256 blocks per sample (d_theta partial slots).
+#ifndef RS_PATCH_W
+#define RS_PATCH_W 16
+#endif
 RS_DEV int out_pixel(int Ho, int Wo) {
     if ((Wo & 31) == 0 && (Ho & 7) == 0) {
         const int tw = Wo >> 5, ty = blockIdx.x / tw, tx = blockIdx.x - ty * tw;
+        constexpr int PW = RS_PATCH_W, PH = 32 / PW, WA = 32 / PW;  // warp patch PW x PH
         const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-        return (ty * 8 + (w >> 2) * 4 + (l >> 3)) * Wo + tx * 32 + (w & 3) * 8 + (l & 7);
+        return (ty * 8 + (w / WA) * PH + l / PW) * Wo + tx * 32 + (w % WA) * PW + l % PW;
     }
     return blockIdx.x * kVT + threadIdx.x;
 }
