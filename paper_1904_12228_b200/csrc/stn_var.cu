@@ -235,7 +235,10 @@ __global__ void __launch_bounds__(kVT)
     }
 }
 
-__global__ void __launch_bounds__(kVT, 3) bicubic_bwd(StnArgs a, double *part, const int *flags) {
+#ifndef RS_BC_BWD_MINB
+#define RS_BC_BWD_MINB 2  // 128 registers, no spills (3: 80 + 244 B spills, 662 vs 568 us)
+#endif
+__global__ void __launch_bounds__(kVT, RS_BC_BWD_MINB) bicubic_bwd(StnArgs a, double *part, const int *flags) {
     const int P = a.Ho * a.Wo, HW = a.H * a.W;
     const int q = out_pixel(a.Ho, a.Wo);
     const int n = blockIdx.y;
