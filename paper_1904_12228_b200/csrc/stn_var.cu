@@ -184,7 +184,10 @@ __global__ void norm_tables(double *xt, double *yt, int Ho, int Wo, int ac) {
     if (t < Ho) yt[t] = stn_norm(t, Ho, ac);
 }
 
-__global__ void __launch_bounds__(kVT)
+#ifndef RS_BC_GATHER_MINB
+#define RS_BC_GATHER_MINB 2  // 128 registers (unbounded: 148, 1 block/SM; 930 vs 691 us)
+#endif
+__global__ void __launch_bounds__(kVT, RS_BC_GATHER_MINB)
     bicubic_dx_gather(StnArgs a, int *flags, const double *__restrict__ xtab, const double *__restrict__ ytab) {
     const int HW = a.H * a.W, P = a.Ho * a.Wo;
     const int n = blockIdx.y;
